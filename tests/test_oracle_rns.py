@@ -1,0 +1,184 @@
+"""Known-answer tests pinning the C RNS-CKKS oracle (oracle/ckks_oracle.c).
+
+Residue-level: NTT == schoolbook negacyclic product; NTT index j evaluates
+at psi^(2 brv(j) + 1); mul_i is X^(N/2); automorphisms match coefficient
+maps.  Slot-level: every op decrypts to the emulator's slot semantics
+(emulator.py:195-273) within CKKS noise; restated schedules over the oracle
+reproduce the reference's golden ledgers exactly and its values within the
+stated tolerance.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import rns as R
+from oracle import slots as S
+from paper_2403_14111_b200 import workloads as wl
+
+OPS = S.OP_KINDS
+TOL = 1e-6        # per-op decrypt tolerance (CKKS noise at Delta = 2^40..2^42)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return R.RnsParams("tiny", seed=7)
+
+
+@pytest.fixture(scope="module")
+def small():
+    return R.RnsParams("small12", seed=11)
+
+
+def brv(x, bits):
+    return int(format(x, f"0{bits}b")[::-1], 2)
+
+
+def negacyclic(a, b, q):
+    n = len(a)
+    out = [0] * n
+    for i in range(n):
+        if a[i] == 0:
+            continue
+        for j in range(n):
+            k = i + j
+            if k < n:
+                out[k] = (out[k] + a[i] * b[j]) % q
+            else:
+                out[k - n] = (out[k - n] - a[i] * b[j]) % q
+    return out
+
+
+def test_primes_and_scales(tiny, small):
+    for p in (tiny, small):
+        q = [int(x) for x in p.moduli]
+        assert len(set(q)) == len(q)
+        assert all((x - 1) % (2 * p.N) == 0 for x in q)
+        for x, psi in zip(q, p.psis):
+            assert pow(int(psi), p.N, x) == x - 1
+    assert [int(x).bit_length() for x in small.moduli] == [58] + [42] * 12 + [60] * 3
+    assert small.scales[-1] == 2.0 ** 42
+
+
+def test_ntt_matches_schoolbook(tiny):
+    rng = np.random.default_rng(0)
+    q = int(tiny.moduli[1])
+    a = rng.integers(0, q, tiny.N, dtype=np.uint64)
+    b = rng.integers(0, 5, tiny.N, dtype=np.uint64)
+    fa, fb = tiny.ntt(1, a), tiny.ntt(1, b)
+    prod = np.array([(int(x) * int(y)) % q for x, y in zip(fa, fb)], dtype=np.uint64)
+    got = tiny.ntt(1, prod, inverse=True)
+    want = negacyclic([int(x) for x in a], [int(x) for x in b], q)
+    assert [int(x) for x in got] == want
+    # evaluation-point convention of the spec
+    psi = int(tiny.psis[1])
+    for j in (0, 1, 5, tiny.N - 1):
+        e = 2 * brv(j, tiny.logN) + 1
+        val = sum(int(a[i]) * pow(psi, e * i, q) for i in range(tiny.N)) % q
+        assert int(fa[j]) == val
+    np.testing.assert_array_equal(tiny.ntt(1, fa, inverse=True), a)
+
+
+def test_encode_decode_roundtrip(tiny):
+    rng = np.random.default_rng(1)
+    z = rng.uniform(-1, 1, tiny.slots) + 1j * rng.uniform(-1, 1, tiny.slots)
+    ct = tiny.encrypt(z, tiny.L, nonce=3)
+    got = tiny.decrypt(ct, tiny.L)
+    assert np.max(np.abs(got - z)) < TOL
+    # deterministic: same nonce, same residues
+    np.testing.assert_array_equal(ct, tiny.encrypt(z, tiny.L, nonce=3))
+    assert not np.array_equal(ct, tiny.encrypt(z, tiny.L, nonce=4))
+
+
+def test_secret_is_ternary_hw(tiny):
+    s = tiny.secret()
+    assert set(np.unique(s)) <= {-1, 0, 1}
+    assert int(np.count_nonzero(s)) == 32
+
+
+def test_per_op_slot_semantics(small):
+    rng = np.random.default_rng(2)
+    n, L = small.slots, small.L
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    cx, cy = small.encrypt(x, L, 0), small.encrypt(y, L, 1)
+    dec = small.decrypt
+    assert np.max(np.abs(dec(small.add(cx, cy, L), L) - (x + y))) < TOL
+    assert np.max(np.abs(dec(small.add(cx, cy, L, negate=True), L) - (x - y))) < TOL
+    assert np.max(np.abs(dec(small.mult(cx, cy, L), L - 1) - x * y)) < TOL
+    assert np.max(np.abs(dec(small.mul_const(cx, L, 0.3 - 0.2j), L - 1) - x * (0.3 - 0.2j))) < TOL
+    assert np.max(np.abs(dec(small.add_const(cx, L, 1.5 + 2j), L) - (x + 1.5 + 2j))) < TOL
+    assert np.max(np.abs(dec(small.mul_i(cx, L), L) - 1j * x)) < TOL
+    pt = small.encode_ntt(y, L)
+    assert np.max(np.abs(dec(small.mul_pt(cx, pt, L), L - 1) - x * y)) < TOL
+    for r in (1, 5, n - 3):
+        got = dec(small.automorph(cx, L, small.galois(r)), L)
+        assert np.max(np.abs(got - np.roll(x, -r))) < TOL
+    got = dec(small.automorph(cx, L, 2 * small.N - 1), L)
+    assert np.max(np.abs(got - np.conj(x))) < TOL
+    lo = small.level_adjust(cx, L, 3)
+    assert np.max(np.abs(dec(lo, 3) - x)) < TOL
+    fresh = small.refresh(lo, 3, 99)
+    assert np.max(np.abs(dec(fresh, L) - x)) < TOL
+    c0 = small.level_adjust(cx, L, 0)
+    assert np.max(np.abs(dec(small.refresh(c0, 0, 100), L) - x)) < TOL
+
+
+def test_mul_i_is_monomial(tiny):
+    # X^(N/2) encodes i in every slot: its NTT is (+I, ..., -I, ...)
+    N = tiny.N
+    q = int(tiny.moduli[0])
+    m = np.zeros(N, np.uint64)
+    m[N // 2] = 1
+    f = tiny.ntt(0, m)
+    I = pow(int(tiny.psis[0]), N // 2, q)
+    assert all(int(v) == I for v in f[: N // 2])
+    assert all(int(v) == q - I for v in f[N // 2:])
+
+
+def test_restated_diag_abt_config0_over_oracle(golden):
+    A, B = wl.config0()
+    ctx = R.OracleCKKSContext("cfg0", 64, seed=5)
+    r = S.diag_abt(S.encode(ctx, A), S.encode(ctx, B, "vertical"))
+    led = np.array([ctx.ledger.counts()[k] for k in OPS])
+    np.testing.assert_array_equal(led, golden["cfg0_led"])
+    assert r.level == 1
+    out = S.decode(r, tol=1e-4)
+    assert np.max(np.abs(out - golden["cfg0_out"])) < 1e-4
+    assert ctx.extra["KeySwitch"] == 8 + 104 + 1
+
+
+def test_restated_softmax_small12(golden):
+    ctx = R.OracleCKKSContext("small12", 16, auto_bootstrap=True, seed=6)
+    r = S.a_softmax(S.encode(ctx, golden["small_sm_in"], "horizontal"))
+    led = np.array([ctx.ledger.counts()[k] for k in OPS])
+    np.testing.assert_array_equal(led, golden["small_sm_led"])
+    assert r.level == golden["small_sm_level"]
+    out = S.decode(r, tol=1e-3)
+    assert np.max(np.abs(out - golden["small_sm_out"])) < 1e-3
+
+
+def test_restated_diag_atb_small12(golden):
+    for branch, alev in (("rl", None), ("pru", 11)):
+        ctx = R.OracleCKKSContext("small12", 16, seed=8)
+        r = S.diag_atb(S.encode(ctx, golden["small_atb_A"], "horizontal", level=alev),
+                       S.encode(ctx, golden["small_atb_B"]), scale=2.0)
+        led = np.array([ctx.ledger.counts()[k] for k in OPS])
+        np.testing.assert_array_equal(led, golden[f"small_atb_{branch}_led"])
+        out = S.decode(r, tol=1e-4)
+        assert np.max(np.abs(out - golden[f"small_atb_{branch}_out"])) < 1e-4
+
+
+def test_restated_training_small12(golden):
+    x, y = golden["small_train_x"], golden["small_train_y"]
+    ctx = R.OracleCKKSContext("small12", 16, auto_bootstrap=True, seed=9)
+    W = S.encode(ctx, S.init_weights(3, x.shape[1], 7), "vertical")
+    st = S.State(W, W)
+    Y = S.one_hot(y, 3)
+    snaps = []
+    for step in range(3):
+        sl = slice((step % 2) * 16, (step % 2) * 16 + 16)
+        S.nag_step(st, S.encode(ctx, x[sl]), S.encode(ctx, Y[sl], "horizontal"), 0.3, 16)
+        snaps.append(S.decode(st.weights, tol=1e-3))
+    led = np.array([ctx.ledger.counts()[k] for k in OPS])
+    np.testing.assert_array_equal(led, golden["small_train_led"])
+    assert np.max(np.abs(np.stack(snaps) - golden["small_train_snaps"])) < 1e-4

@@ -1,0 +1,138 @@
+/*
+ * hc.h — C-ABI of the B200-native RNS-CKKS backend for the HETAL hot path.
+ *
+ * The reference (hefit) ships no FFI: its backend seam is the Python
+ * `EmulatorContext` duck type (pkg/src/hefit/emulator.py:111-281), declared
+ * as "a backend interface a real HE library could later satisfy"
+ * (SPEC.md:19).  Each entry point below replaces one method of that
+ * interface (or one layer-2 schedule built on it); the comment names the
+ * reference line it stands in for.  Plain pointers and sizes only: no torch
+ * types cross this boundary.
+ *
+ * Conventions
+ *   - Every function returns 0 on success or a negative status:
+ *       HC_EPARAM (-1) bad argument        HC_ECUDA  (-2) CUDA failure
+ *       HC_EDEPTH (-3) level exhausted     -> hefit.errors.DepthExhausted (errors.py:14-17)
+ *       HC_ELEVEL (-4) layout/level misuse HC_EENCODE (-5) encoding overflow
+ *     hc_last_error() returns the message of the last failure on this thread.
+ *   - Ciphertext residues are [2][level+1][N] uint64 in NTT form.
+ *   - Slot vectors are N/2 complex values passed as separate re/im doubles.
+ *   - Handles are owned by the caller and released with hc_*_free.
+ *   - Ops are asynchronous on the context's CUDA stream; download / decrypt
+ *     and hc_sync synchronise.
+ */
+#ifndef HC_H
+#define HC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_EPARAM -1
+#define HC_ECUDA -2
+#define HC_EDEPTH -3
+#define HC_ELEVEL -4
+#define HC_EENCODE -5
+
+typedef struct hc_ctx hc_ctx;
+typedef struct hc_ct hc_ct;
+typedef struct hc_pt hc_pt;
+
+/* ledger slots of hc_ctx_counts: the reference's OP_KINDS (emulator.py:29)
+ * followed by two CKKS-only counters that the reference ledger never sees */
+enum { HC_ADD = 0, HC_CMULT, HC_MULT, HC_ROT, HC_CONJ, HC_BOOTSTRAP, HC_LEVEL_ADJUST, HC_KEYSWITCH, HC_NCOUNTS };
+
+const char *hc_last_error(void);
+
+/* EmulatorContext.__init__ (emulator.py:124-148): ring, modulus chain and keys.
+ * qbits[nq] (q0 first), pbits[np]; alpha primes per key-switching digit. */
+int hc_ctx_create(int log_n, int nq, const int *qbits, int np, const int *pbits, int alpha, int log_scale,
+                  int hamming_weight, double sigma, uint64_t seed, int device, hc_ctx **out);
+int hc_ctx_destroy(hc_ctx *ctx);
+/* moduli[nq+np]; scales[nq] canonical scale per level */
+int hc_ctx_info(hc_ctx *ctx, uint64_t *moduli, double *scales);
+/* EmulatorContext.grid_rows (emulator.py:144): s0 of the s0 x s1 slot grid */
+int hc_set_grid_rows(hc_ctx *ctx, int grid_rows);
+/* EmulatorContext.auto_bootstrap (emulator.py:132) */
+int hc_set_auto_bootstrap(hc_ctx *ctx, int on);
+/* OpLedger.counts / reset (emulator.py:88-108); counts[HC_NCOUNTS] */
+int hc_ctx_counts(hc_ctx *ctx, int64_t *counts, int reset);
+/* encryption-randomness counter (shared with the oracle's nonce sequence) */
+int hc_ctx_nonce(hc_ctx *ctx, uint64_t *get, const uint64_t *set);
+int hc_sync(hc_ctx *ctx);
+/* pre-generate the switching key of galois element g (0 = relinearisation) */
+int hc_keygen(hc_ctx *ctx, int g);
+int hc_key_download(hc_ctx *ctx, int g, uint64_t *out); /* [dnum][2][nq+np][N] */
+uint64_t hc_galois_rot(hc_ctx *ctx, int64_t r);
+
+/* ciphertext handles (CipherBlock, emulator.py:49-67) */
+int hc_ct_free(hc_ct *ct);
+int hc_ct_level(const hc_ct *ct);
+int hc_ct_download(const hc_ct *ct, uint64_t *out);
+int hc_ct_upload(hc_ctx *ctx, const uint64_t *in, int level, hc_ct **out);
+int hc_ct_device_ptr(const hc_ct *ct, uint64_t **dptr);
+
+/* plaintexts: encoded at scales[level] in NTT form */
+int hc_pt_free(hc_pt *pt);
+int hc_encode_pt(hc_ctx *ctx, const double *re, const double *im, int level, hc_pt **out);
+int hc_pt_download(const hc_pt *pt, uint64_t *out);
+/* host encoder KAT: slots -> N integer coefficients at `scale` */
+int hc_encode_coef(hc_ctx *ctx, const double *re, const double *im, double scale, int64_t *coef);
+
+/* EmulatorContext.encrypt (emulator.py:160-164) with an explicit nonce */
+int hc_encrypt(hc_ctx *ctx, const double *re, const double *im, int level, uint64_t nonce, hc_ct **out);
+/* CipherBlock.slots read by encoding.decode (encoding.py:202): audited client decrypt */
+int hc_decrypt(hc_ctx *ctx, const hc_ct *ct, double *re, double *im);
+
+/* ---- EmulatorContext ops with the reference's ledger / level semantics ---- */
+/* add / sub (emulator.py:195-210): ct +- ct */
+int hc_op_add(hc_ctx *ctx, const hc_ct *a, const hc_ct *b, int sub, hc_ct **out);
+/* ct + s (mode 0), ct - s (mode 1), s - ct (mode 2) for a complex scalar */
+int hc_op_add_scalar(hc_ctx *ctx, const hc_ct *a, double re, double im, int mode, hc_ct **out);
+/* same with a slot-vector plaintext; `key` content-addresses the encoding cache */
+int hc_op_add_plain(hc_ctx *ctx, const hc_ct *a, const double *re, const double *im, const char *key, int mode,
+                    hc_ct **out);
+/* mult (emulator.py:212-229): ct x ct -> Mult (+ per-operand auto-bootstrap) */
+int hc_op_mult(hc_ctx *ctx, const hc_ct *a, const hc_ct *b, hc_ct **out);
+/* cmult (emulator.py:231-235): ct x scalar / ct x plaintext -> CMult */
+int hc_op_mult_scalar(hc_ctx *ctx, const hc_ct *a, double re, double im, hc_ct **out);
+int hc_op_mult_plain(hc_ctx *ctx, const hc_ct *a, const double *re, const double *im, const char *key, hc_ct **out);
+/* lrot (emulator.py:237-247); r mod slots must be non-zero (r == 0 is the caller's no-op) */
+int hc_op_lrot(hc_ctx *ctx, const hc_ct *a, int64_t r, hc_ct **out);
+/* conj (emulator.py:253-257), mul_i (emulator.py:259-265, unledgered) */
+int hc_op_conj(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
+int hc_op_mul_i(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
+/* bootstrap (emulator.py:267-273): refresh surrogate, NOT CKKS bootstrapping */
+int hc_op_bootstrap(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
+
+/* ---- exact CKKS primitives (no ledger), for residue-level parity ---- */
+int hc_rescale(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
+int hc_level_adjust(hc_ctx *ctx, const hc_ct *a, int level, hc_ct **out);
+
+/* ---- layer-2 schedules (native, same op order and ledger as the reference) ---- */
+/* diag_abt (matmul.py:74-110): A[m][n] untiled blocks (row-major handles),
+ * B[n] the single block row of the vertically tiled operand, period c.
+ * out[m]: the horizontally tiled result column.  counts[HC_NCOUNTS] += delta. */
+int hc_diag_abt(hc_ctx *ctx, const hc_ct *const *A, int m, int n, const hc_ct *const *B, int c, double scale,
+                hc_ct **out, int64_t *counts);
+/* diag_atb (matmul.py:113-154): A[m] (one block column, horizontally tiled,
+ * period c), B[m][n]; out[n].  The row_sums pre-add (encoding.py:375-377) is
+ * the cross-rank reduction point: with nranks > 1 the caller provides
+ * `reduce_fn(user, cts, count)` which must replace each ciphertext's residues
+ * by the modular sum over ranks (see hc_mod_reduce). */
+typedef int (*hc_reduce_fn)(void *user, hc_ct **cts, int count);
+int hc_diag_atb(hc_ctx *ctx, const hc_ct *const *A, int m, const hc_ct *const *B, int n, int c, double scale,
+                hc_ct **out, int64_t *counts, hc_reduce_fn reduce_fn, void *user);
+/* a_softmax (approx.py:312-344) on one horizontally tiled block column A[m] */
+int hc_softmax(hc_ctx *ctx, const hc_ct *const *A, int m, int classes, int period, const double *cfg, hc_ct **out,
+               int64_t *counts);
+
+/* finish a cross-rank uint64 sum: residues mod q_i in place (K8) */
+int hc_mod_reduce(hc_ctx *ctx, hc_ct *ct);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,320 @@
+// extern "C" boundary (include/hc.h): handle wrappers, error mapping.
+#include <cstring>
+
+#include "../../include/hc.h"
+#include "evaluator.h"
+#include "kernels.cuh"
+#include "schedules.h"
+
+struct hc_ctx {
+    hc::Ctx* c;
+    bool auto_boot = false;
+};
+struct hc_ct {
+    hc::CtP p;
+};
+struct hc_pt {
+    hc::PtP p;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const hc::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+static hc_ct* wrap(hc::CtP p) { return new hc_ct{std::move(p)}; }
+
+extern "C" {
+
+const char* hc_last_error(void) { return g_err.c_str(); }
+
+int hc_ctx_create(int log_n, int nq, const int* qbits, int np, const int* pbits, int alpha, int log_scale,
+                  int hamming_weight, double sigma, uint64_t seed, int device, hc_ctx** out) {
+    return guard([&] {
+        hc::Ctx* c = hc::ctx_create(log_n, nq, qbits, np, pbits, alpha, log_scale, hamming_weight, sigma, seed,
+                                    device);
+        *out = new hc_ctx{c, false};
+    });
+}
+
+int hc_ctx_destroy(hc_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        hc::ctx_destroy(ctx->c);
+        delete ctx;
+    });
+}
+
+int hc_ctx_info(hc_ctx* ctx, uint64_t* moduli, double* scales) {
+    return guard([&] {
+        for (int i = 0; i < ctx->c->nall; i++) moduli[i] = ctx->c->pr[i].q;
+        for (int l = 0; l <= ctx->c->L; l++) scales[l] = ctx->c->scale[l];
+    });
+}
+
+int hc_set_grid_rows(hc_ctx* ctx, int grid_rows) {
+    const int S = ctx->c->N / 2;
+    if (grid_rows < 1 || grid_rows > S || (grid_rows & (grid_rows - 1))) {
+        g_err = "grid_rows must be a power of two <= slot count";
+        return HC_EPARAM;
+    }
+    ctx->c->grid_rows = grid_rows;
+    return 0;
+}
+
+int hc_set_auto_bootstrap(hc_ctx* ctx, int on) {
+    ctx->auto_boot = on != 0;
+    return 0;
+}
+
+int hc_ctx_counts(hc_ctx* ctx, int64_t* counts, int reset) {
+    std::lock_guard<std::mutex> g(ctx->c->mu);
+    for (int i = 0; i < HC_NCOUNTS; i++) {
+        if (counts) counts[i] = ctx->c->counts[i];
+        if (reset) ctx->c->counts[i] = 0;
+    }
+    return 0;
+}
+
+int hc_ctx_nonce(hc_ctx* ctx, uint64_t* get, const uint64_t* set) {
+    std::lock_guard<std::mutex> g(ctx->c->mu);
+    if (get) *get = ctx->c->nonce;
+    if (set) ctx->c->nonce = *set;
+    return 0;
+}
+
+int hc_sync(hc_ctx* ctx) { return guard([&] { HC_CUDA(cudaStreamSynchronize(ctx->c->stream)); }); }
+
+int hc_keygen(hc_ctx* ctx, int g) { return guard([&] { hc::get_key(*ctx->c, g); }); }
+
+int hc_key_download(hc_ctx* ctx, int g, uint64_t* out) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        const hc::Key& k = hc::get_key(c, g);
+        const size_t words = (size_t)c.dnum * 2 * c.nall * c.N;
+        HC_CUDA(cudaMemcpyAsync(out, k.d, words * 8, cudaMemcpyDeviceToHost, c.stream));
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+uint64_t hc_galois_rot(hc_ctx* ctx, int64_t r) { return hc::galois_rot(*ctx->c, r); }
+
+int hc_ct_free(hc_ct* ct) {
+    return guard([&] { delete ct; });
+}
+int hc_ct_level(const hc_ct* ct) { return ct->p->level; }
+
+int hc_ct_download(const hc_ct* ct, uint64_t* out) {
+    return guard([&] {
+        hc::Ctx& c = *ct->p->ctx;
+        HC_CUDA(cudaMemcpyAsync(out, ct->p->d, ct->p->words() * 8, cudaMemcpyDeviceToHost, c.stream));
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int hc_ct_upload(hc_ctx* ctx, const uint64_t* in, int level, hc_ct** out) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (level < 0 || level > c.L) throw hc::Error(HC_EPARAM, "level out of range");
+        hc::CtP p = hc::new_ct(c, level);
+        HC_CUDA(cudaMemcpyAsync(p->d, in, p->words() * 8, cudaMemcpyHostToDevice, c.stream));
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+        *out = wrap(p);
+    });
+}
+
+int hc_ct_device_ptr(const hc_ct* ct, uint64_t** dptr) {
+    *dptr = ct->p->d;
+    return 0;
+}
+
+int hc_pt_free(hc_pt* pt) {
+    return guard([&] { delete pt; });
+}
+
+int hc_encode_pt(hc_ctx* ctx, const double* re, const double* im, int level, hc_pt** out) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (level < 0 || level > c.L) throw hc::Error(HC_EPARAM, "level out of range");
+        *out = new hc_pt{hc::encode_pt(c, re, im, level, c.scale[level])};
+    });
+}
+
+int hc_pt_download(const hc_pt* pt, uint64_t* out) {
+    return guard([&] {
+        hc::Ctx& c = *pt->p->ctx;
+        HC_CUDA(cudaMemcpyAsync(out, pt->p->d, (size_t)(pt->p->level + 1) * c.N * 8, cudaMemcpyDeviceToHost,
+                                c.stream));
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int hc_encode_coef(hc_ctx* ctx, const double* re, const double* im, double scale, int64_t* coef) {
+    return guard([&] {
+        if (hc::encode_host(*ctx->c, re, im, scale, coef)) throw hc::Error(HC_EENCODE, "encode overflow");
+    });
+}
+
+int hc_encrypt(hc_ctx* ctx, const double* re, const double* im, int level, uint64_t nonce, hc_ct** out) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (level < 0 || level > c.L) throw hc::Error(HC_EPARAM, "level out of range");
+        *out = wrap(hc::encrypt(c, re, im, level, nonce));
+    });
+}
+
+int hc_decrypt(hc_ctx* ctx, const hc_ct* ct, double* re, double* im) {
+    return guard([&] { hc::decrypt(*ctx->c, *ct->p, re, im); });
+}
+
+static hc::Pattern pattern_of(hc_ctx* ctx, const double* re, const double* im, const char* key) {
+    hc::Pattern p;
+    p.key = std::string("py:") + (key ? key : "");
+    const int S = ctx->c->N / 2;
+    p.vals.resize(S);
+    for (int i = 0; i < S; i++) p.vals[i] = {re[i], im ? im[i] : 0.0};
+    return p;
+}
+
+int hc_op_add(hc_ctx* ctx, const hc_ct* a, const hc_ct* b, int sub, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).add(a->p, b->p, sub != 0)); });
+}
+
+int hc_op_add_scalar(hc_ctx* ctx, const hc_ct* a, double re, double im, int mode, hc_ct** out) {
+    return guard([&] {
+        *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).add_c(a->p, {re, im}, mode == 1, mode == 2));
+    });
+}
+
+int hc_op_add_plain(hc_ctx* ctx, const hc_ct* a, const double* re, const double* im, const char* key, int mode,
+                    hc_ct** out) {
+    return guard([&] {
+        hc::Pattern p = pattern_of(ctx, re, im, key);
+        *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).add_p(a->p, p, mode == 1, mode == 2));
+    });
+}
+
+int hc_op_mult(hc_ctx* ctx, const hc_ct* a, const hc_ct* b, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).mult(a->p, b->p)); });
+}
+
+int hc_op_mult_scalar(hc_ctx* ctx, const hc_ct* a, double re, double im, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).mult_c(a->p, {re, im})); });
+}
+
+int hc_op_mult_plain(hc_ctx* ctx, const hc_ct* a, const double* re, const double* im, const char* key,
+                     hc_ct** out) {
+    return guard([&] {
+        hc::Pattern p = pattern_of(ctx, re, im, key);
+        *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).mult_p(a->p, p));
+    });
+}
+
+int hc_op_lrot(hc_ctx* ctx, const hc_ct* a, int64_t r, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).lrot(a->p, r)); });
+}
+
+int hc_op_conj(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).conj(a->p)); });
+}
+
+int hc_op_mul_i(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).mul_i(a->p)); });
+}
+
+int hc_op_bootstrap(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).bootstrap(a->p)); });
+}
+
+int hc_rescale(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::ev_rescale(*ctx->c, *a->p)); });
+}
+
+int hc_level_adjust(hc_ctx* ctx, const hc_ct* a, int level, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::ev_level_adjust(*ctx->c, *a->p, level)); });
+}
+
+int hc_mod_reduce(hc_ctx* ctx, hc_ct* ct) {
+    return guard([&] { hc::k_mod_reduce(*ctx->c, ct->p->d, ct->p->level + 1, ct->p->npoly); });
+}
+
+// ---- schedules ----
+
+static std::vector<hc::CtP> unwrap(const hc_ct* const* a, int n) {
+    std::vector<hc::CtP> v(n);
+    for (int i = 0; i < n; i++) v[i] = a[i]->p;
+    return v;
+}
+
+static void add_counts(hc_ctx* ctx, const int64_t* before, int64_t* counts) {
+    if (!counts) return;
+    std::lock_guard<std::mutex> g(ctx->c->mu);
+    for (int i = 0; i < HC_NCOUNTS; i++) counts[i] += ctx->c->counts[i] - before[i];
+}
+
+static void snap(hc_ctx* ctx, int64_t* b) {
+    std::lock_guard<std::mutex> g(ctx->c->mu);
+    for (int i = 0; i < HC_NCOUNTS; i++) b[i] = ctx->c->counts[i];
+}
+
+int hc_diag_abt(hc_ctx* ctx, const hc_ct* const* A, int m, int n, const hc_ct* const* B, int c, double scale,
+                hc_ct** out, int64_t* counts) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        std::vector<hc::CtP> res = hc::sched_diag_abt(ev, unwrap(A, m * n), m, n, unwrap(B, n), c, scale);
+        for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
+int hc_diag_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B, int n, int c, double scale,
+                hc_ct** out, int64_t* counts, hc_reduce_fn reduce_fn, void* user) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        hc::Reducer red;
+        if (reduce_fn) {
+            red = [&](std::vector<hc::CtP>& cts) {
+                std::vector<hc_ct*> hs(cts.size());
+                for (size_t i = 0; i < cts.size(); i++) hs[i] = wrap(cts[i]);
+                HC_CUDA(cudaStreamSynchronize(ctx->c->stream));
+                const int rc = reduce_fn(user, hs.data(), (int)hs.size());
+                for (size_t i = 0; i < cts.size(); i++) { cts[i] = hs[i]->p; delete hs[i]; }
+                if (rc) throw hc::Error(HC_ECUDA, "cross-rank reduction failed");
+            };
+        }
+        std::vector<hc::CtP> res = hc::sched_diag_atb(ev, unwrap(A, m), m, unwrap(B, m * n), n, c, scale, red);
+        for (int i = 0; i < n; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
+int hc_softmax(hc_ctx* ctx, const hc_ct* const* A, int m, int classes, int period, const double* cfg, hc_ct** out,
+               int64_t* counts) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        hc::SoftmaxCfg sc;
+        if (cfg) sc = hc::SoftmaxCfg::from(cfg);
+        std::vector<hc::CtP> res = hc::sched_softmax(ev, unwrap(A, m), classes, period, sc);
+        for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
+}  // extern "C"

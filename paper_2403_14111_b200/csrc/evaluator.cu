@@ -1,0 +1,349 @@
+// Exact RNS-CKKS ciphertext operations on the device, and the
+// reference-semantics policy layer (Eval) shared by the per-op C-ABI and the
+// native schedules.
+//
+// Hybrid key switching (K5):
+//   INTT(d) -> ModUp fast base conversion per digit -> NTT of new limbs ->
+//   key inner product (128-bit lazy accumulation, one Barrett reduction) ->
+//   INTT of the P limbs -> ModDown conversion -> NTT -> (acc - conv) * P^-1
+//   with the automorphism's c0 / the tensor's (d0, d1) added in the same pass.
+#include <cmath>
+
+#include "evaluator.h"
+#include "kernels.cuh"
+
+namespace hc {
+
+typedef unsigned __int128 u128;
+
+static u64 mulm(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+static u64 shoup_of(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+static u64 from_i64_h(int64_t v, u64 q) {
+    if (v >= 0) return (u64)v % q;
+    u64 m = (u64)(-(v + 1)) % q;
+    return q - 1 - m;
+}
+
+static void check_same(const Ct& a, const Ct& b) {
+    if (a.level != b.level) throw Error(-4, "level mismatch in low-level op");
+}
+
+// (cr + ci I, cr - ci I) per limb with Shoup companions
+static void const_pairs(const Ctx& c, int64_t cr, int64_t ci, int nl, ConstTab& t) {
+    for (int i = 0; i < nl; i++) {
+        const u64 q = c.pr[i].q;
+        const u64 r = from_i64_h(cr, q), im = mulm(from_i64_h(ci, q), c.pr[i].I, q);
+        const u64 lo = (r + im) % q, hi = (r + q - im) % q;
+        t.v[4 * i] = lo;
+        t.v[4 * i + 1] = shoup_of(lo, q);
+        t.v[4 * i + 2] = hi;
+        t.v[4 * i + 3] = shoup_of(hi, q);
+    }
+}
+
+CtP ev_add(Ctx& c, const Ct& a, const Ct& b, bool sub) {
+    check_same(a, b);
+    CtP o = new_ct(c, a.level);
+    k_elementwise(c, sub ? EWP_SUB : EWP_ADD, o->d, a.d, b.d, nullptr, a.level + 1, 2, 2);
+    return o;
+}
+
+CtP ev_neg(Ctx& c, const Ct& a) {
+    CtP o = new_ct(c, a.level);
+    k_elementwise(c, EWP_NEG, o->d, a.d, nullptr, nullptr, a.level + 1, 2, 0);
+    return o;
+}
+
+CtP ev_add_pt(Ctx& c, const Ct& a, const Pt& p, bool sub, bool pt_minus_ct) {
+    if (p.level < a.level) throw Error(-4, "plaintext level too low");
+    CtP o = new_ct(c, a.level);
+    int op = pt_minus_ct ? EWP_PT_RSUB : (sub ? EWP_PT_SUB : EWP_PT_ADD);
+    k_elementwise(c, op, o->d, a.d, p.d, nullptr, a.level + 1, 2, 1);
+    return o;
+}
+
+CtP ev_add_const(Ctx& c, const Ct& a, double re, double im, bool negate_ct) {
+    const double s = c.scale[a.level];
+    ConstTab t;
+    const_pairs(c, std::llrint(re * s), std::llrint(im * s), a.level + 1, t);
+    CtP o = new_ct(c, a.level);
+    k_elementwise(c, negate_ct ? EWP_CONST_RADD : EWP_CONST_ADD, o->d, a.d, nullptr, &t, a.level + 1, 2, 0);
+    return o;
+}
+
+// rescale [npoly][level+1][N] at `a` into [npoly][level][N] at `out`
+static void rescale_raw(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+    const int N = c.N;
+    u64* X = c.alloc((size_t)npoly * N);
+    JobList j;
+    j.n = npoly;
+    for (int s = 0; s < npoly; s++) {
+        j.prime[s] = level;
+        j.ptr[s] = X + (size_t)s * N;
+        j.src[s] = a + ((size_t)s * (level + 1) + level) * N;
+    }
+    ntt_inverse(c, j);
+    u64* Y = c.alloc((size_t)npoly * level * N);
+    k_rescale_bcast(c, Y, X, level, npoly);
+    JobList f;
+    f.n = 0;
+    for (int s = 0; s < npoly; s++)
+        for (int i = 0; i < level; i++) {
+            f.prime[f.n] = i;
+            f.ptr[f.n] = Y + ((size_t)s * level + i) * N;
+            f.src[f.n] = nullptr;
+            f.n++;
+        }
+    ntt_forward(c, f);
+    k_rescale_combine(c, out, a, Y, level, npoly);
+    c.free(X);
+    c.free(Y);
+}
+
+CtP ev_rescale(Ctx& c, const Ct& a) {
+    if (a.level < 1) throw Error(-3, "rescale at level 0");
+    CtP o = new_ct(c, a.level - 1);
+    rescale_raw(c, a.d, a.level, 2, o->d);
+    return o;
+}
+
+static CtP mul_int_rescale(Ctx& c, const u64* a, int level, int64_t cr, int64_t ci) {
+    ConstTab t;
+    const_pairs(c, cr, ci, level + 1, t);
+    u64* T = c.alloc((size_t)2 * (level + 1) * c.N);
+    k_elementwise(c, EWP_CONST_MUL, T, a, nullptr, &t, level + 1, 2, 0);
+    CtP o = new_ct(c, level - 1);
+    rescale_raw(c, T, level, 2, o->d);
+    c.free(T);
+    return o;
+}
+
+CtP ev_mul_const(Ctx& c, const Ct& a, double re, double im) {
+    if (a.level < 1) throw Error(-3, "multiply at level 0");
+    const double s = c.scale[a.level];
+    return mul_int_rescale(c, a.d, a.level, std::llrint(re * s), std::llrint(im * s));
+}
+
+CtP ev_mul_pt(Ctx& c, const Ct& a, const Pt& p) {
+    if (a.level < 1) throw Error(-3, "multiply at level 0");
+    if (p.level != a.level) throw Error(-4, "plaintext level must equal ciphertext level");
+    u64* T = c.alloc((size_t)2 * (a.level + 1) * c.N);
+    k_elementwise(c, EWP_PT_MUL, T, a.d, p.d, nullptr, a.level + 1, 2, 1);
+    CtP o = new_ct(c, a.level - 1);
+    rescale_raw(c, T, a.level, 2, o->d);
+    c.free(T);
+    return o;
+}
+
+CtP ev_mul_i(Ctx& c, const Ct& a) {
+    ConstTab t;
+    const_pairs(c, 0, 1, a.level + 1, t);
+    CtP o = new_ct(c, a.level);
+    k_elementwise(c, EWP_CONST_MUL, o->d, a.d, nullptr, &t, a.level + 1, 2, 0);
+    return o;
+}
+
+CtP ev_drop(Ctx& c, const Ct& a, int to) {
+    if (to > a.level) throw Error(-4, "drop to a higher level");
+    CtP o = new_ct(c, to);
+    for (int s = 0; s < 2; s++)
+        HC_CUDA(cudaMemcpyAsync(o->poly(s), a.poly(s), sizeof(u64) * (size_t)(to + 1) * c.N,
+                                cudaMemcpyDeviceToDevice, c.stream));
+    return o;
+}
+
+CtP ev_level_adjust(Ctx& c, const Ct& a, int to) {
+    if (to >= a.level) throw Error(-4, "level adjust needs a lower target");
+    CtP d = ev_drop(c, a, to + 1);
+    const double s1 = c.scale[to + 1];
+    const int64_t cst = std::llrint(s1 * (s1 / c.scale[a.level]));
+    return mul_int_rescale(c, d->d, to + 1, cst, 0);
+}
+
+// ---------------------------------------------------------------------------
+// hybrid key switching
+// ---------------------------------------------------------------------------
+
+static inline int tprime(const Ctx& c, int level, int t) { return t <= level ? t : c.L + 1 + (t - level - 1); }
+
+// d: [level+1][N] (NTT).  out [2][level+1][N] = KS(d) + addend (first add_npoly polys)
+void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+    const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
+    const int beta = (nl + c.alpha - 1) / c.alpha;
+    u64* X = c.alloc((size_t)nl * N);
+    ntt_limbs(c, X, 0, nl, true, d);
+    u64* UP = c.alloc((size_t)beta * nt * N);
+    k_modup(c, UP, X, d, level, beta);
+    {
+        JobList j;
+        j.n = 0;
+        for (int dj = 0; dj < beta; dj++) {
+            const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
+            for (int t = 0; t < nt; t++) {
+                if (t >= lo && t < hi) continue;
+                if (j.n == MAXJ) { ntt_forward(c, j); j.n = 0; }
+                j.prime[j.n] = tprime(c, level, t);
+                j.ptr[j.n] = UP + ((size_t)dj * nt + t) * N;
+                j.src[j.n] = nullptr;
+                j.n++;
+            }
+        }
+        ntt_forward(c, j);
+    }
+    u64* ACC = c.alloc((size_t)2 * nt * N);
+    k_keyprod(c, ACC, UP, key.d, level, beta);
+    c.free(UP);
+    {
+        JobList j;
+        j.n = 0;
+        for (int s = 0; s < 2; s++)
+            for (int t = nl; t < nt; t++) {
+                j.prime[j.n] = tprime(c, level, t);
+                j.ptr[j.n] = ACC + ((size_t)s * nt + t) * N;
+                j.src[j.n] = nullptr;
+                j.n++;
+            }
+        ntt_inverse(c, j);
+    }
+    c.free(X);
+    u64* W = c.alloc((size_t)2 * nl * N);
+    k_moddown_conv(c, W, ACC, level);
+    ntt_limbs(c, W, 0, nl, false);
+    ntt_limbs(c, W + (size_t)nl * N, 0, nl, false);
+    k_moddown_combine(c, out, ACC, W, addend, add_npoly, level);
+    c.free(W);
+    c.free(ACC);
+    c.counts[OP_KS]++;
+}
+
+CtP ev_automorph(Ctx& c, const Ct& a, u64 g) {
+    const Key& key = get_key(c, (int)g);
+    const int nl = a.level + 1;
+    u64* S = c.alloc((size_t)2 * nl * c.N);
+    k_automorph(c, S, a.d, 2 * nl, g);
+    CtP o = new_ct(c, a.level);
+    keyswitch(c, S + (size_t)nl * c.N, a.level, key, o->d, S, 1);
+    c.free(S);
+    return o;
+}
+
+CtP ev_mult(Ctx& c, const Ct& a, const Ct& b) {
+    check_same(a, b);
+    if (a.level < 1) throw Error(-3, "multiply at level 0");
+    const Key& key = get_key(c, 0);
+    const int nl = a.level + 1;
+    const size_t poly = (size_t)nl * c.N;
+    u64* D = c.alloc(3 * poly);
+    k_tensor(c, D, a.d, b.d, nl);
+    u64* T = c.alloc(2 * poly);
+    keyswitch(c, D + 2 * poly, a.level, key, T, D, 2);
+    c.free(D);
+    CtP o = new_ct(c, a.level - 1);
+    rescale_raw(c, T, a.level, 2, o->d);
+    c.free(T);
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// Eval: the reference backend semantics (emulator.py:160-273) over CKKS
+// ---------------------------------------------------------------------------
+
+void Eval::rec(int k, int n) {
+    std::lock_guard<std::mutex> g(c.mu);
+    c.counts[k] += n;
+}
+
+u64 Eval::next_nonce() {
+    std::lock_guard<std::mutex> g(c.mu);
+    return c.nonce++;
+}
+
+CtP Eval::at(const CtP& a, int level) {
+    if (a->level == level) return a;
+    rec(OP_ADJUST);
+    return ev_level_adjust(c, *a, level);
+}
+
+CtP Eval::ready(const CtP& a) {
+    if (a->level >= 1) return a;
+    if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
+    rec(OP_BOOT);
+    return refresh(c, *a, next_nonce());
+}
+
+CtP Eval::add(const CtP& a, const CtP& b, bool sub) {
+    rec(OP_ADD);
+    const int l = std::min(a->level, b->level);
+    return ev_add(c, *at(a, l), *at(b, l), sub);
+}
+
+CtP Eval::add_c(const CtP& a, std::complex<double> s, bool sub, bool reversed) {
+    rec(OP_ADD);
+    // ct + s, ct - s, s - ct
+    if (reversed) return ev_add_const(c, *a, s.real(), s.imag(), true);
+    if (sub) s = -s;
+    return ev_add_const(c, *a, s.real(), s.imag(), false);
+}
+
+CtP Eval::add_p(const CtP& a, const Pattern& p, bool sub, bool reversed) {
+    rec(OP_ADD);
+    PtP pt = encoded(p, a->level);
+    return ev_add_pt(c, *a, *pt, sub, reversed);
+}
+
+CtP Eval::mult(const CtP& x, const CtP& y) {
+    CtP a = ready(x), b = ready(y);
+    rec(OP_MULT);
+    const int l = std::min(a->level, b->level);
+    return ev_mult(c, *at(a, l), *at(b, l));
+}
+
+CtP Eval::mult_c(const CtP& x, std::complex<double> s) {
+    CtP a = ready(x);
+    rec(OP_CMULT);
+    return ev_mul_const(c, *a, s.real(), s.imag());
+}
+
+CtP Eval::mult_p(const CtP& x, const Pattern& p) {
+    CtP a = ready(x);
+    rec(OP_CMULT);
+    PtP pt = encoded(p, a->level);
+    return ev_mul_pt(c, *a, *pt);
+}
+
+CtP Eval::lrot(const CtP& a, int64_t r) {
+    const int64_t S = c.N / 2;
+    r = ((r % S) + S) % S;
+    if (r == 0) return a;
+    rec(OP_ROT);
+    return ev_automorph(c, *a, galois_rot(c, r));
+}
+
+CtP Eval::conj(const CtP& a) {
+    rec(OP_CONJ);
+    return ev_automorph(c, *a, 2 * (u64)c.N - 1);
+}
+
+CtP Eval::mul_i(const CtP& a) { return ev_mul_i(c, *a); }
+
+CtP Eval::bootstrap(const CtP& a) {
+    rec(OP_BOOT);
+    return refresh(c, *a, next_nonce());
+}
+
+PtP Eval::encoded(const Pattern& p, int level) {
+    std::string key = p.key + "@" + std::to_string(level);
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto it = c.pt_cache.find(key);
+        if (it != c.pt_cache.end()) return it->second;
+    }
+    std::vector<double> zr(p.vals.size()), zi(p.vals.size());
+    for (size_t i = 0; i < p.vals.size(); i++) { zr[i] = p.vals[i].real(); zi[i] = p.vals[i].imag(); }
+    PtP pt = encode_pt(c, zr.data(), zi.data(), level, c.scale[level]);
+    std::lock_guard<std::mutex> g(c.mu);
+    c.pt_cache[key] = pt;
+    return pt;
+}
+
+}  // namespace hc

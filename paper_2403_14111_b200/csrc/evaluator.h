@@ -1,0 +1,48 @@
+// Policy layer with the reference backend's semantics (emulator.py:160-273):
+// ledger increments, per-operand auto-bootstrap at level 0, result level =
+// min(levels) (- 1 for products), lrot by 0 is free and returns its input.
+// CKKS-specific: operands at different levels are first brought to the
+// lower level by an unledgered level adjustment (counted under OP_ADJUST).
+#pragma once
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "hc_internal.h"
+
+namespace hc {
+
+void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const u64* addend, int add_npoly);
+
+// a plaintext slot pattern with a cache key (content-addressed by the caller)
+struct Pattern {
+    std::string key;
+    std::vector<std::complex<double>> vals;
+};
+
+struct Eval {
+    Ctx& c;
+    bool auto_boot;
+    Eval(Ctx& ctx, bool ab) : c(ctx), auto_boot(ab) {}
+
+    void rec(int kind, int n = 1);
+    u64 next_nonce();
+    CtP at(const CtP& a, int level);
+    CtP ready(const CtP& a);
+
+    CtP add(const CtP& a, const CtP& b, bool sub = false);
+    CtP sub(const CtP& a, const CtP& b) { return add(a, b, true); }
+    CtP add_c(const CtP& a, std::complex<double> s, bool sub = false, bool reversed = false);
+    CtP add_p(const CtP& a, const Pattern& p, bool sub = false, bool reversed = false);
+    CtP mult(const CtP& a, const CtP& b);
+    CtP mult_c(const CtP& a, std::complex<double> s);
+    CtP mult_p(const CtP& a, const Pattern& p);
+    CtP lrot(const CtP& a, int64_t r);
+    CtP rrot(const CtP& a, int64_t r) { return lrot(a, -r); }
+    CtP conj(const CtP& a);
+    CtP mul_i(const CtP& a);
+    CtP bootstrap(const CtP& a);
+    PtP encoded(const Pattern& p, int level);
+};
+
+}  // namespace hc

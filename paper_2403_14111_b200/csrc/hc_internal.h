@@ -1,0 +1,150 @@
+// Internal declarations of the B200 RNS-CKKS library (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "modarith.cuh"
+
+namespace hc {
+
+constexpr int MAXP = 48;       // max primes in Q u P
+constexpr int MAXJ = 96;       // max limb jobs in one batched launch
+
+#define HC_CUDA(x)                                                                     \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw hc::Error(-2, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " \
+                                    + __FILE__ + ":" + std::to_string(__LINE__));      \
+    } while (0)
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// one limb job for a batched launch: a pointer to N words and its prime
+struct JobList {
+    int n;
+    int prime[MAXJ];
+    u64* ptr[MAXJ];
+    const u64* src[MAXJ];   // optional out-of-place source (nullptr = in place)
+};
+
+// host-side view of one prime with its precomputation
+struct PrimeHost {
+    u64 q, mu_hi, mu_lo, psi, ipsi, ninv, I;
+};
+
+struct Ctx;
+
+// device ciphertext: residues [npoly][level+1][N] in NTT form
+struct Ct {
+    Ctx* ctx = nullptr;
+    u64* d = nullptr;
+    int level = 0;
+    int npoly = 2;
+    size_t words() const;
+    u64* poly(int s) const;
+};
+using CtP = std::shared_ptr<Ct>;
+
+// device plaintext: residues [level+1][N] in NTT form, encoded at scale[level]
+struct Pt {
+    Ctx* ctx = nullptr;
+    u64* d = nullptr;
+    int level = 0;
+};
+using PtP = std::shared_ptr<Pt>;
+
+struct Key {
+    int id;                       // galois element, 0 = relinearisation
+    u64* d;                       // [dnum][2][nall][N]
+};
+
+enum OpKind { OP_ADD = 0, OP_CMULT, OP_MULT, OP_ROT, OP_CONJ, OP_BOOT, OP_ADJUST, OP_KS, OP_NKIND };
+
+struct Ctx {
+    int logN, N, L, K, alpha, dnum, nall, hw;
+    double sigma;
+    u64 seed;
+    int device;
+    int grid_rows = 0;            // s0 of the slot grid (EmulatorContext.grid_rows)
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    PrimeHost pr[MAXP];
+    double scale[MAXP];
+    // device tables
+    PrimeDev* d_primes = nullptr;
+    u64 *d_tw = nullptr, *d_tws = nullptr, *d_itw = nullptr, *d_itws = nullptr;   // [nall][N]
+    u64* d_cdt = nullptr;
+    int cdt_n = 0, cdt_b = 0;
+    u64 cdt_host[128];
+    u64* d_sk = nullptr;          // [nall][N] NTT form
+    std::vector<int64_t> sk_coef;
+    // host encoder tables
+    std::vector<double> tw_re, tw_im, zt_re, zt_im;
+    std::vector<int> slot_t;
+    // keys (lazy, by galois element)
+    std::map<int, Key> keys;
+    // base-conversion tables (device), see context.cu
+    u64* d_modup = nullptr;       // [L+1 levels][dnum][alpha][nall] (value, shoup) pairs
+    u64* d_modup_inv = nullptr;   // [L+1][dnum][alpha] (value, shoup)
+    u64* d_moddown = nullptr;     // [K][nall] (value, shoup) phat_{p->i}
+    u64* d_moddown_inv = nullptr; // [K] (value, shoup)
+    u64* d_pinv = nullptr;        // [nall] (value, shoup) P^-1 mod q_i
+    u64* d_rescale = nullptr;     // [L+1 (dropped prime l)][nall] (q_l^-1 mod q_i, shoup, q_l mod q_i)
+    // counters
+    uint64_t nonce = 0;
+    int64_t counts[OP_NKIND] = {0};
+    std::mutex mu;
+    // encoded-mask cache used by the native schedules
+    std::map<std::string, PtP> pt_cache;
+
+    // workspace stream-ordered allocation
+    u64* alloc(size_t words);
+    void free(u64* p);
+};
+
+// ---- kernels / launchers (ntt.cu, kernels.cu) ----
+void ntt_forward(Ctx& c, const JobList& jobs);
+void ntt_inverse(Ctx& c, const JobList& jobs);
+
+// ---- context (context.cu) ----
+Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, int alpha,
+                int log_scale, int hw, double sigma, u64 seed, int device);
+void ctx_destroy(Ctx* c);
+Key& get_key(Ctx& c, int gid);
+int encode_host(const Ctx& c, const double* zr, const double* zi, double scale, int64_t* coef);
+void decode_host(const Ctx& c, const double* m, double* zr, double* zi);
+CtP new_ct(Ctx& c, int level, int npoly = 2);
+PtP new_pt(Ctx& c, int level);
+PtP encode_pt(Ctx& c, const double* zr, const double* zi, int level, double scale);
+CtP encrypt_coef_dev(Ctx& c, const int64_t* d_m, int level, u64 nonce);
+CtP encrypt(Ctx& c, const double* zr, const double* zi, int level, u64 nonce);
+void decrypt(Ctx& c, const Ct& a, double* zr, double* zi);
+CtP refresh(Ctx& c, const Ct& a, u64 nonce);
+u64 galois_rot(const Ctx& c, int64_t r);
+
+// ---- evaluator (evaluator.cu): exact CKKS ops, DESIGN.md §3 ----
+CtP ev_add(Ctx& c, const Ct& a, const Ct& b, bool sub);
+CtP ev_add_pt(Ctx& c, const Ct& a, const Pt& p, bool sub, bool pt_minus_ct);
+CtP ev_add_const(Ctx& c, const Ct& a, double re, double im, bool negate_ct);
+CtP ev_neg(Ctx& c, const Ct& a);
+CtP ev_mul_pt(Ctx& c, const Ct& a, const Pt& p);
+CtP ev_mul_const(Ctx& c, const Ct& a, double re, double im);
+CtP ev_mult(Ctx& c, const Ct& a, const Ct& b);
+CtP ev_automorph(Ctx& c, const Ct& a, u64 g);
+CtP ev_mul_i(Ctx& c, const Ct& a);
+CtP ev_rescale(Ctx& c, const Ct& a);
+CtP ev_level_adjust(Ctx& c, const Ct& a, int to);
+CtP ev_drop(Ctx& c, const Ct& a, int to);
+
+}  // namespace hc

@@ -1,0 +1,499 @@
+// Element-wise, base-conversion, key-product and sampling kernels (sm_100a).
+//
+// All kernels work on limb-major residue arrays [poly][limb][N] (uint64) in
+// HBM.  Element-wise kernels move two words per thread (16-byte vector
+// accesses) and use a grid sized in multiples of the SM count; they are
+// HBM-bound by construction.  Base conversion (ModUp / ModDown) and the key
+// inner product are the integer-heavy parts of key switching.
+#include "kernels.cuh"
+
+namespace hc {
+
+static inline int nblocks(size_t work, int threads) {
+    size_t b = (work + threads - 1) / threads;
+    const size_t cap = 148 * 16;
+    return (int)(b < cap ? b : cap);
+}
+
+// ---------------------------------------------------------------------------
+// element-wise ciphertext ops; prime of limb i is i (Q basis)
+// ---------------------------------------------------------------------------
+
+enum EwOp { EW_ADD, EW_SUB, EW_NEG, EW_PT_ADD, EW_PT_SUB, EW_PT_RSUB, EW_PT_MUL, EW_CONST_MUL, EW_CONST_ADD,
+            EW_CONST_RADD };
+
+// consts: per limb {lo, lo_shoup, hi, hi_shoup}
+__global__ void ew_kernel(int op, u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
+                          const ConstTab consts, const PrimeDev* __restrict__ primes, int nl, int npoly,
+                          int N, int bpoly) {
+    const size_t half = (size_t)N / 2;
+    const size_t total = (size_t)npoly * nl * half;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        const size_t e = v * 2;
+        const int limb = (int)((e / N) % nl);
+        const int s = (int)(e / ((size_t)N * nl));
+        const size_t k = e % N;
+        const u64 q = primes[limb].q;
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + e);
+        u64 r0, r1;
+        switch (op) {
+            case EW_ADD:
+            case EW_SUB: {
+                ulonglong2 y = (s < bpoly) ? *reinterpret_cast<const ulonglong2*>(b + e) : make_ulonglong2(0, 0);
+                if (op == EW_ADD) { r0 = add_mod(x.x, y.x, q); r1 = add_mod(x.y, y.y, q); }
+                else { r0 = sub_mod(x.x, y.x, q); r1 = sub_mod(x.y, y.y, q); }
+                break;
+            }
+            case EW_NEG: r0 = neg_mod(x.x, q); r1 = neg_mod(x.y, q); break;
+            case EW_PT_ADD:
+            case EW_PT_SUB:
+            case EW_PT_RSUB: {
+                ulonglong2 y = (s == 0) ? *reinterpret_cast<const ulonglong2*>(b + (size_t)limb * N + k)
+                                        : make_ulonglong2(0, 0);
+                if (op == EW_PT_ADD) { r0 = add_mod(x.x, y.x, q); r1 = add_mod(x.y, y.y, q); }
+                else if (op == EW_PT_SUB) { r0 = sub_mod(x.x, y.x, q); r1 = sub_mod(x.y, y.y, q); }
+                else { r0 = sub_mod(y.x, x.x, q); r1 = sub_mod(y.y, x.y, q); }
+                break;
+            }
+            case EW_PT_MUL: {
+                const PrimeDev P = primes[limb];
+                ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b + (size_t)limb * N + k);
+                r0 = mul_mod(x.x, y.x, P);
+                r1 = mul_mod(x.y, y.y, P);
+                break;
+            }
+            case EW_CONST_MUL: {
+                const u64* cc = consts.v + 4 * limb + (k < half ? 0 : 2);
+                r0 = mul_shoup(x.x, cc[0], cc[1], q);
+                r1 = mul_shoup(x.y, cc[0], cc[1], q);
+                break;
+            }
+            case EW_CONST_ADD:
+            case EW_CONST_RADD: {
+                u64 cv = (s == 0) ? consts.v[4 * limb + (k < half ? 0 : 2)] : 0;
+                u64 x0 = x.x, x1 = x.y;
+                if (op == EW_CONST_RADD) { x0 = neg_mod(x0, q); x1 = neg_mod(x1, q); }
+                r0 = add_mod(x0, cv, q);
+                r1 = add_mod(x1, cv, q);
+                break;
+            }
+            default: r0 = r1 = 0;
+        }
+        *reinterpret_cast<ulonglong2*>(out + e) = make_ulonglong2(r0, r1);
+    }
+}
+
+void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const ConstTab* consts, int nl, int npoly,
+                   int bpoly) {
+    const size_t work = (size_t)npoly * nl * c.N / 2;
+    static const ConstTab zero = {};
+    ew_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(op, out, a, b, consts ? *consts : zero, c.d_primes, nl, npoly,
+                                                        c.N, bpoly);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// tensor product: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
+// ---------------------------------------------------------------------------
+
+__global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, const u64* __restrict__ b,
+                              const PrimeDev* __restrict__ primes, int nl, int N) {
+    const size_t poly = (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        const u64 a0 = a[e], a1 = a[poly + e], b0 = b[e], b1 = b[poly + e];
+        d[e] = mul_mod(a0, b0, P);
+        U128 acc = {0, 0};
+        mac128(acc, a0, b1);
+        mac128(acc, a1, b0);
+        d[poly + e] = reduce128(acc.hi, acc.lo, P);
+        d[2 * poly + e] = mul_mod(a1, b1, P);
+    }
+}
+
+void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl) {
+    tensor_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(d, a, b, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Galois automorphism in the NTT domain: out[j] = in[src(j)]
+// ---------------------------------------------------------------------------
+
+__global__ void automorph_kernel(u64* __restrict__ out, const u64* __restrict__ in, int nlimbs, int logN, u64 g) {
+    const int N = 1 << logN;
+    const u64 mask = 2 * (u64)N - 1;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nlimbs * N;
+         e += (size_t)gridDim.x * blockDim.x) {
+        const unsigned j = (unsigned)(e & (N - 1));
+        const size_t base = e - j;
+        const u64 ex = 2 * (u64)(__brev(j) >> (32 - logN)) + 1;
+        const u64 e2 = (ex * g) & mask;
+        const unsigned src = __brev((unsigned)((e2 - 1) >> 1)) >> (32 - logN);
+        out[e] = in[base + src];
+    }
+}
+
+void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g) {
+    automorph_kernel<<<nblocks((size_t)nlimbs * c.N, 256), 256, 0, c.stream>>>(out, in, nlimbs, c.logN, g);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// ModUp fast base conversion for all active digits of a level.
+//   X   : [level+1][N] coefficient form of the input (INTT of d)
+//   D   : [level+1][N] NTT form of the input (copied into in-digit limbs)
+//   UP  : [beta][nt][N], nt = level+1+K; limb t <-> prime (t <= level ? t : L+1+t-(level+1))
+// Non-digit limbs are written in coefficient form (NTT'd afterwards).
+// ---------------------------------------------------------------------------
+
+__global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, const u64* __restrict__ D,
+                             const u64* __restrict__ tab, const u64* __restrict__ tab_inv,
+                             const PrimeDev* __restrict__ primes, int level, int L, int K, int alpha, int dnum,
+                             int nall, int N) {
+    const int j = blockIdx.y;
+    const int lo = j * alpha;
+    int hi = lo + alpha;
+    if (hi > level + 1) hi = level + 1;
+    const int na = hi - lo;
+    const int nt = level + 1 + K;
+    const u64* inv = tab_inv + ((size_t)(level * dnum + j) * alpha) * 2;
+    const u64* cf = tab + ((size_t)(level * dnum + j) * alpha) * nall * 2;
+    u64* out = up + (size_t)j * nt * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        u64 y[8];
+        for (int a = 0; a < na; a++) {
+            const u64 q = primes[lo + a].q;
+            y[a] = mul_shoup(X[(size_t)(lo + a) * N + k], inv[2 * a], inv[2 * a + 1], q);
+        }
+        for (int t = 0; t < nt; t++) {
+            const int pi = t <= level ? t : L + 1 + (t - level - 1);
+            if (t >= lo && t < hi) {
+                out[(size_t)t * N + k] = D[(size_t)t * N + k];
+                continue;
+            }
+            const u64 p = primes[pi].q;
+            u64 acc = 0;
+            for (int a = 0; a < na; a++) {
+                const u64* c2 = cf + ((size_t)a * nall + pi) * 2;
+                acc += mul_shoup_lazy(y[a], c2[0], c2[1], p);
+            }
+            // acc < 2 * na * p <= 8p
+            if (acc >= 4 * p) acc -= 4 * p;
+            if (acc >= 2 * p) acc -= 2 * p;
+            if (acc >= p) acc -= p;
+            out[(size_t)t * N + k] = acc;
+        }
+    }
+}
+
+void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
+    dim3 grid((c.N + 255) / 256, beta);
+    modup_kernel<<<grid, 256, 0, c.stream>>>(up, X, D, c.d_modup, c.d_modup_inv, c.d_primes, level, c.L, c.K,
+                                              c.alpha, c.dnum, c.nall, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// key inner product: acc[s][t] = sum_j UP[j][t] * key[j][s][prime(t)]
+// ---------------------------------------------------------------------------
+
+__global__ void keyprod_kernel(u64* __restrict__ acc, const u64* __restrict__ up, const u64* __restrict__ key,
+                               const PrimeDev* __restrict__ primes, int level, int L, int K, int beta, int nall,
+                               int N) {
+    const int nt = level + 1 + K;
+    const size_t poly = (size_t)nt * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e / N);
+        const size_t k = e - (size_t)t * N;
+        const int pi = t <= level ? t : L + 1 + (t - level - 1);
+        const PrimeDev P = primes[pi];
+        U128 s0 = {0, 0}, s1 = {0, 0};
+        for (int j = 0; j < beta; j++) {
+            const u64 u = up[(size_t)j * poly + e];
+            const u64* kb = key + ((size_t)(2 * j) * nall + pi) * N + k;
+            const u64* ka = kb + (size_t)nall * N;
+            mac128(s0, u, *kb);
+            mac128(s1, u, *ka);
+        }
+        acc[e] = reduce128(s0.hi, s0.lo, P);
+        acc[poly + e] = reduce128(s1.hi, s1.lo, P);
+    }
+}
+
+void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta) {
+    const size_t poly = (size_t)(level + 1 + c.K) * c.N;
+    keyprod_kernel<<<nblocks(poly, 256), 256, 0, c.stream>>>(acc, up, key, c.d_primes, level, c.L, c.K, beta,
+                                                              c.nall, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// ModDown: W[s][i] = sum_t [ACC_p_t * (P/p_t)^-1]_{p_t} * [P/p_t]_{q_i}   (coefficient form)
+//   ACC: [2][nt][N]; its P limbs (t >= level+1) are already in coefficient form
+// ---------------------------------------------------------------------------
+
+__global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__ acc, const u64* __restrict__ tab,
+                                    const u64* __restrict__ tab_inv, const PrimeDev* __restrict__ primes, int level,
+                                    int L, int K, int nall, int N) {
+    const int s = blockIdx.y;
+    const int nt = level + 1 + K;
+    const u64* A = acc + (size_t)s * nt * N;
+    u64* out = W + (size_t)s * (level + 1) * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        u64 y[8];
+        for (int t = 0; t < K; t++) {
+            const u64 p = primes[L + 1 + t].q;
+            y[t] = mul_shoup(A[(size_t)(level + 1 + t) * N + k], tab_inv[2 * t], tab_inv[2 * t + 1], p);
+        }
+        for (int i = 0; i <= level; i++) {
+            const u64 q = primes[i].q;
+            u64 v = 0;
+            for (int t = 0; t < K; t++) {
+                const u64* c2 = tab + ((size_t)t * nall + i) * 2;
+                v += mul_shoup_lazy(y[t], c2[0], c2[1], q);
+            }
+            if (v >= 4 * q) v -= 4 * q;
+            if (v >= 2 * q) v -= 2 * q;
+            if (v >= q) v -= q;
+            out[(size_t)i * N + k] = v;
+        }
+    }
+}
+
+void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
+    dim3 grid((c.N + 255) / 256, 2);
+    moddown_conv_kernel<<<grid, 256, 0, c.stream>>>(W, acc, c.d_moddown, c.d_moddown_inv, c.d_primes, level, c.L,
+                                                     c.K, c.nall, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// out[s][i] = (ACC[s][i] - W[s][i]) * P^-1 (+ addend[s][i] when s < add_npoly)
+__global__ void moddown_combine_kernel(u64* __restrict__ out, const u64* __restrict__ acc, const u64* __restrict__ W,
+                                       const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly,
+                                       const PrimeDev* __restrict__ primes, int level, int K, int N) {
+    const int nl = level + 1, nt = nl + K;
+    const size_t poly = (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < 2 * poly; e += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(e / poly);
+        const size_t r = e - (size_t)s * poly;
+        const int i = (int)(r / N);
+        const u64 q = primes[i].q;
+        const u64 a = acc[(size_t)s * nt * N + r];
+        u64 v = mul_shoup(a + q - W[e], pinv[2 * i], pinv[2 * i + 1], q);
+        if (s < add_npoly) v = add_mod(v, addend[e], q);
+        out[e] = v;
+    }
+}
+
+void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly,
+                       int level) {
+    const size_t work = 2 * (size_t)(level + 1) * c.N;
+    moddown_combine_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(out, acc, W, c.d_pinv, addend, add_npoly,
+                                                                      c.d_primes, level, c.K, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// rescale by q_l: Y[s][i] = centred(X[s]) mod q_i; out = (a - NTT(Y)) * q_l^-1
+// ---------------------------------------------------------------------------
+
+__global__ void rescale_bcast_kernel(u64* __restrict__ Y, const u64* __restrict__ X, const u64* __restrict__ tab,
+                                     const PrimeDev* __restrict__ primes, int level, int npoly, int N) {
+    const u64 ql = primes[level].q;
+    const size_t per = (size_t)level * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * per; e += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(e / per);
+        const size_t r = e - s * per;
+        const int i = (int)(r / N);
+        const size_t k = r - (size_t)i * N;
+        const u64 q = primes[i].q;
+        const u64 v = X[(size_t)s * N + k];
+        const u64 qlm = tab[3 * i + 2];
+        const u64 vm = v % q;
+        Y[e] = v > (ql - 1) / 2 ? sub_mod(vm, qlm, q) : vm;
+    }
+}
+
+__global__ void rescale_combine_kernel(u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ Y,
+                                       const u64* __restrict__ tab, const PrimeDev* __restrict__ primes, int level,
+                                       int npoly, int N) {
+    const size_t per = (size_t)level * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * per; e += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(e / per);
+        const size_t r = e - s * per;
+        const int i = (int)(r / N);
+        const u64 q = primes[i].q;
+        const u64 x = a[(size_t)s * (level + 1) * N + r];
+        out[e] = mul_shoup(x + q - Y[e], tab[3 * i], tab[3 * i + 1], q);
+    }
+}
+
+void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly) {
+    const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
+    rescale_bcast_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(Y, X, tab, c.d_primes,
+                                                                                          level, npoly, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+void k_rescale_combine(Ctx& c, u64* out, const u64* a, const u64* Y, int level, int npoly) {
+    const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
+    rescale_combine_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(out, a, Y, tab,
+                                                                                            c.d_primes, level, npoly,
+                                                                                            c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// sampling, encryption, decryption, refresh
+// ---------------------------------------------------------------------------
+
+// out[i][k] = uniform mod prime(first + i), counter (prime index)*N + k
+__global__ void uniform_kernel(u64* __restrict__ out, const PrimeDev* __restrict__ primes, int first, int nl, int N,
+                               u64 key) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / N);
+        const int pi = first + i;
+        const size_t k = e - (size_t)i * N;
+        out[e] = __umul64hi(rng_at(key, (u64)pi * N + k), primes[pi].q);
+    }
+}
+
+void k_uniform(Ctx& c, u64* out, int first_prime, int nl, u64 stream) {
+    uniform_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, c.d_primes, first_prime, nl, c.N,
+                                                                          rng_key(c.seed, stream));
+    HC_CUDA(cudaGetLastError());
+}
+
+__global__ void cdt_kernel(i64* __restrict__ e, const u64* __restrict__ cdt, int n, int b, int N, u64 key) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const u64 r = rng_at(key, (u64)k);
+        int cnt = 0;
+        for (int i = 0; i < n; i++) cnt += (cdt[i] <= r);
+        e[k] = (i64)cnt - b;
+    }
+}
+
+void k_cdt(Ctx& c, i64* e, u64 stream) {
+    cdt_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(e, c.d_cdt, c.cdt_n, c.cdt_b, c.N, rng_key(c.seed, stream));
+    HC_CUDA(cudaGetLastError());
+}
+
+// out[i][k] = (m[k] + e[k]) mod q_i for primes 0..nl-1 (e optional)
+__global__ void coef_to_rns_kernel(u64* __restrict__ out, const i64* __restrict__ m, const i64* __restrict__ e,
+                                   const PrimeDev* __restrict__ primes, int first, int nl, int N) {
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(x / N);
+        const size_t k = x - (size_t)i * N;
+        i64 v = m ? m[k] : 0;
+        if (e) v += e[k];
+        out[x] = from_i64(v, primes[first + i].q);
+    }
+}
+
+void k_coef_to_rns(Ctx& c, u64* out, const i64* m, const i64* e, int first_prime, int nl) {
+    coef_to_rns_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, m, e, c.d_primes, first_prime, nl,
+                                                                              c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// b = b_in - a*s (+ pm_i * s2 for limbs in [dlo, dhi)); all prime-indexed from 0 over nl limbs
+__global__ void key_combine_kernel(u64* __restrict__ b, const u64* __restrict__ a, const u64* __restrict__ s,
+                                   const u64* __restrict__ s2, const u64* __restrict__ pm,
+                                   const PrimeDev* __restrict__ primes, int nl, int dlo, int dhi, int N) {
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(x / N);
+        const PrimeDev P = primes[i];
+        u64 v = sub_mod(b[x], mul_mod(a[x], s[x], P), P.q);
+        if (s2 && i >= dlo && i < dhi) v = add_mod(v, mul_mod(pm[i], s2[x], P), P.q);
+        b[x] = v;
+    }
+}
+
+void k_key_combine(Ctx& c, u64* b, const u64* a, const u64* s, const u64* s2, const u64* pm, int nl, int dlo,
+                   int dhi) {
+    key_combine_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(b, a, s, s2, pm, c.d_primes, nl, dlo,
+                                                                              dhi, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+__global__ void square_kernel(u64* __restrict__ out, const u64* __restrict__ a, const PrimeDev* __restrict__ primes,
+                              int nl, int N) {
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x)
+        out[x] = mul_mod(a[x], a[x], primes[x / N]);
+}
+
+void k_square(Ctx& c, u64* out, const u64* a, int nl) {
+    square_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, a, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// x[i] = c0[i] + c1[i] * s[i] for limbs 0..nl-1
+__global__ void dec_kernel(u64* __restrict__ x, const u64* __restrict__ c0, const u64* __restrict__ c1,
+                           const u64* __restrict__ s, const PrimeDev* __restrict__ primes, int nl, int N) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        x[e] = add_mod(c0[e], mul_mod(c1[e], s[e], P), P.q);
+    }
+}
+
+void k_dec(Ctx& c, u64* x, const u64* c0, const u64* c1, int nl) {
+    dec_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(x, c0, c1, c.d_sk, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// refresh surrogate message: m'[k] = rint(m_d * ratio), m_d = x0c + q0 * kc
+__global__ void refresh_msg_kernel(i64* __restrict__ m, const u64* __restrict__ x, const PrimeDev* __restrict__ primes,
+                                   int two, u64 inv_q0_mod_q1, double ratio, int N) {
+    const PrimeDev P0 = primes[0];
+    const PrimeDev P1 = primes[1];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const u64 v0 = x[k];
+        const i64 x0 = v0 > (P0.q - 1) / 2 ? (i64)v0 - (i64)P0.q : (i64)v0;
+        double md;
+        if (!two) {
+            md = __ll2double_rn(x0);
+        } else {
+            const u64 d = sub_mod(x[N + k], from_i64(x0, P1.q), P1.q);
+            const u64 kk = mul_mod(d, inv_q0_mod_q1, P1);
+            const i64 kc = kk > (P1.q - 1) / 2 ? (i64)kk - (i64)P1.q : (i64)kk;
+            md = __dadd_rn(__ll2double_rn(x0), __dmul_rn(__ull2double_rn(P0.q), __ll2double_rn(kc)));
+        }
+        m[k] = __double2ll_rn(__dmul_rn(md, ratio));
+    }
+}
+
+void k_refresh_msg(Ctx& c, i64* m, const u64* x, int two, u64 inv01, double ratio) {
+    refresh_msg_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(m, x, c.d_primes, two, inv01, ratio, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// c0 = c0 - c1 * s (c0 holds NTT(m + e) on entry)
+__global__ void enc_combine_kernel(u64* __restrict__ c0, const u64* __restrict__ c1, const u64* __restrict__ s,
+                                   const PrimeDev* __restrict__ primes, int nl, int N) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        c0[e] = sub_mod(c0[e], mul_mod(c1[e], s[e], P), P.q);
+    }
+}
+
+void k_enc_combine(Ctx& c, u64* c0, const u64* c1, int nl) {
+    enc_combine_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(c0, c1, c.d_sk, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// cross-rank reduction finish: x mod q_i (x is a sum of R < 16 residues)
+__global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restrict__ primes, int nl, int npoly, int N) {
+    const size_t poly = (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * poly; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)((e % poly) / N);
+        x[e] = x[e] % primes[i].q;
+    }
+}
+
+void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly) {
+    mod_reduce_kernel<<<nblocks((size_t)npoly * nl * c.N, 256), 256, 0, c.stream>>>(x, c.d_primes, nl, npoly, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+}  // namespace hc

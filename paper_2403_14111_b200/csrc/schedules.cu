@@ -1,0 +1,450 @@
+// Native schedules: the reference's layer-1/2 op sequences issued straight
+// to the device evaluator.  Grid operations are applied block by block in
+// the order the reference's EncodedMatrix.map_blocks / _zip evaluate them,
+// and every composite expression is split into explicit steps so the op
+// order (and therefore the refresh-nonce sequence) is the reference's.
+#include <cmath>
+#include <cstdio>
+
+#include "schedules.h"
+
+namespace hc {
+
+using G = std::vector<CtP>;
+using cd = std::complex<double>;
+
+static int ilog2(int n) {
+    int l = 0;
+    while ((1 << l) < n) l++;
+    return l;
+}
+
+// ---- slot patterns (encoding.py:231-278, approx.py:149-163) ---------------
+
+struct Geo {
+    int s0, s1, S;
+};
+
+static Geo geo(const Eval& ev, int s0) { return Geo{s0, (ev.c.N / 2) / s0, ev.c.N / 2}; }
+
+static std::string dkey(double v) {
+    char b[32];
+    std::snprintf(b, sizeof b, "%a", v);
+    return b;
+}
+
+// make_mask: 1 at (i, j) with j = i + shift (mod modulus); complexified:
+// 0.5 M(shift) - 0.5i M(shift + modulus/2); times scale
+static Pattern diag_mask(const Geo& g, int shift, int modulus, bool cplx, double scale) {
+    shift = ((shift % modulus) + modulus) % modulus;
+    Pattern p;
+    p.key = "diag:" + std::to_string(g.s0) + ":" + std::to_string(shift) + ":" + std::to_string(modulus) + ":" +
+            (cplx ? "c" : "r") + ":" + dkey(scale);
+    p.vals.resize(g.S);
+    for (int i = 0; i < g.s0; i++)
+        for (int j = 0; j < g.s1; j++) {
+            const double main = ((((j - i - shift) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
+            cd v;
+            if (cplx) {
+                const double twin =
+                    ((((j - i - shift - modulus / 2) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
+                v = cd(0.5 * main, 0.0) - cd(0.0, 0.5 * twin);
+            } else {
+                v = cd(main, 0.0);
+            }
+            p.vals[(size_t)i * g.s1 + j] = cd(v.real() * scale, v.imag() * scale);
+        }
+    return p;
+}
+
+template <class F>
+static Pattern col_pattern(const Geo& g, const std::string& key, F f) {
+    Pattern p;
+    p.key = key + ":" + std::to_string(g.s0);
+    p.vals.resize(g.S);
+    for (int i = 0; i < g.s0; i++)
+        for (int j = 0; j < g.s1; j++) p.vals[(size_t)i * g.s1 + j] = cd(f(j), 0.0);
+    return p;
+}
+
+static Pattern keep_head(const Geo& g, int stop) {
+    return col_pattern(g, "head:" + std::to_string(stop), [&](int j) { return j < stop ? 1.0 : 0.0; });
+}
+static Pattern col0(const Geo& g) {
+    return col_pattern(g, "col0", [](int j) { return j == 0 ? 1.0 : 0.0; });
+}
+
+// ---- structural ops (encoding.py:284-381) ----------------------------------
+
+// rot_up on a block row / column: lrot(k * s1) per block; k == 0 returns the input
+static G rot_up(Eval& ev, const G& E, int k, const Geo& g) {
+    k %= g.s0;
+    if (k == 0) return E;
+    G o(E.size());
+    for (size_t i = 0; i < E.size(); i++) o[i] = ev.lrot(E[i], (int64_t)k * g.s1);
+    return o;
+}
+
+static G rot_left(Eval& ev, const G& E, int k, const Geo& g) {
+    k %= g.s1;
+    if (k == 0) return E;
+    const Pattern keep = keep_head(g, g.s1 - k);
+    G o(E.size());
+    for (size_t i = 0; i < E.size(); i++) {
+        CtP a1 = ev.lrot(E[i], k);
+        CtP head = ev.mult_p(a1, keep);
+        CtP tail = ev.sub(a1, head);
+        CtP back = ev.rrot(tail, g.s1);
+        o[i] = ev.add(head, back);
+    }
+    return o;
+}
+
+static G prot_up(Eval& ev, const G& E, int k, const Geo& g) {
+    k %= g.s1;
+    if (k == 0) return E;
+    const Pattern keep = keep_head(g, g.s1 - k);
+    G o(E.size());
+    for (size_t i = 0; i < E.size(); i++) {
+        CtP head = ev.mult_p(E[i], keep);
+        CtP tail = ev.sub(E[i], head);
+        CtP up = ev.lrot(tail, g.s1);
+        o[i] = ev.add(head, up);
+    }
+    return o;
+}
+
+// col_sums over an r x cols grid -> r blocks
+static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g) {
+    const Pattern c0 = col0(g);
+    G out(r);
+    for (int p = 0; p < r; p++) {
+        CtP acc = E[(size_t)p * cols];
+        for (int q = 1; q < cols; q++) acc = ev.add(acc, E[(size_t)p * cols + q]);
+        for (int t = 0; t < ilog2(g.s1); t++) {
+            CtP rot = ev.lrot(acc, 1 << t);
+            acc = ev.add(acc, rot);
+        }
+        acc = ev.mult_p(acc, c0);
+        for (int t = 0; t < ilog2(g.s1); t++) {
+            CtP rot = ev.rrot(acc, 1 << t);
+            acc = ev.add(acc, rot);
+        }
+        out[p] = acc;
+    }
+    return out;
+}
+
+// row_sums over an r x cols grid -> cols blocks; the block-row pre-add is the
+// cross-rank reduction point (encoding.py:375-377)
+static G row_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, const Reducer& red) {
+    G pre(cols);
+    for (int q = 0; q < cols; q++) {
+        CtP acc = E[q];
+        for (int p = 1; p < r; p++) acc = ev.add(acc, E[(size_t)p * cols + q]);
+        pre[q] = acc;
+    }
+    if (red) red(pre);
+    for (int q = 0; q < cols; q++) {
+        CtP acc = pre[q];
+        for (int t = 0; t < ilog2(g.s0); t++) {
+            CtP rot = ev.lrot(acc, (int64_t)(1 << t) * g.s1);
+            acc = ev.add(acc, rot);
+        }
+        pre[q] = acc;
+    }
+    return pre;
+}
+
+static int grid_level(const G& E) {
+    int l = 1 << 30;
+    for (auto& b : E) l = std::min(l, b->level);
+    return l;
+}
+
+static int geo_rows(const Eval& ev) {
+    if (ev.c.grid_rows <= 0) throw Error(-1, "grid_rows not set (hc_set_grid_rows)");
+    return ev.c.grid_rows;
+}
+
+// ---- DiagABT (matmul.py:74-110) --------------------------------------------
+
+std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int n, const std::vector<CtP>& B, int c,
+                                double scale) {
+    const Geo g = geo(ev, geo_rows(ev));
+    if (c < 1 || c > g.s1 || (c & (c - 1))) throw Error(-4, "diag_abt: bad period");
+    if ((int)A.size() != m * n || (int)B.size() != n) throw Error(-4, "diag_abt: grid mismatch");
+    if (c == 1) {
+        G prod((size_t)m * n);
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], B[q]);
+        G sums = col_sums(ev, prod, m, n, g);
+        const Pattern ones = diag_mask(g, 0, 1, false, scale);
+        for (int p = 0; p < m; p++) sums[p] = ev.mult_p(sums[p], ones);
+        return sums;
+    }
+    G rolled = rot_up(ev, B, c / 2, g);
+    G mi(n);
+    for (int q = 0; q < n; q++) mi[q] = ev.mul_i(rolled[q]);
+    G packed(n);
+    for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], mi[q]);
+    G acc;
+    for (int k = 0; k < c / 2; k++) {
+        G shifted = rot_up(ev, packed, k, g);
+        G prod((size_t)m * n);
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted[q]);
+        G sums = col_sums(ev, prod, m, n, g);
+        const Pattern mask = diag_mask(g, k, c, true, scale);
+        G term(m);
+        for (int p = 0; p < m; p++) term[p] = ev.mult_p(sums[p], mask);
+        if (k == 0) acc = term;
+        else for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], term[p]);
+    }
+    G cj(m);
+    for (int p = 0; p < m; p++) cj[p] = ev.conj(acc[p]);
+    for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], cj[p]);
+    return acc;
+}
+
+// ---- DiagATB (matmul.py:113-154) -------------------------------------------
+
+std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, const std::vector<CtP>& B, int n, int c,
+                                double scale, const Reducer& red) {
+    const Geo g = geo(ev, geo_rows(ev));
+    if (c < 1 || c > g.s0 || g.s0 % c) throw Error(-4, "diag_atb: bad period");
+    if ((int)A.size() != m || (int)B.size() != m * n) throw Error(-4, "diag_atb: grid mismatch");
+    auto colwise = [&](const G& C, const G& Bm) {
+        G prod((size_t)m * n);
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(C[p], Bm[(size_t)p * n + q]);
+        return prod;
+    };
+    if (c == 1) {
+        G sums = row_sums(ev, colwise(A, B), m, n, g, red);
+        const Pattern ones = diag_mask(g, 0, 1, false, scale);
+        for (int q = 0; q < n; q++) sums[q] = ev.mult_p(sums[q], ones);
+        return sums;
+    }
+    const bool partial = grid_level(A) < grid_level(B);
+    G rl = rot_left(ev, A, c / 2, g);
+    G mi(m);
+    for (int p = 0; p < m; p++) mi[p] = ev.mul_i(rl[p]);
+    G packed(m);
+    for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], mi[p]);
+    G acc;
+    for (int k = 0; k < c / 2; k++) {
+        G left, right;
+        if (partial) {
+            left.resize(m);
+            for (int p = 0; p < m; p++) left[p] = ev.lrot(packed[p], k);
+            right = prot_up(ev, B, k, g);
+        } else {
+            left = rot_left(ev, packed, k, g);
+            right = B;
+        }
+        G prod = colwise(left, right);
+        G sums = row_sums(ev, prod, m, n, g, red);
+        const Pattern mask = diag_mask(g, -k, c, true, scale);
+        G term(n);
+        for (int q = 0; q < n; q++) term[q] = ev.mult_p(sums[q], mask);
+        if (k == 0) acc = term;
+        else for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], term[q]);
+    }
+    G cj(n);
+    for (int q = 0; q < n; q++) cj[q] = ev.conj(acc[q]);
+    for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], cj[q]);
+    return acc;
+}
+
+// ---- approximate softmax (approx.py:195-344), encrypted carrier ------------
+
+namespace {
+
+const double EXP_POLY[13] = {0.9999999999999948,     0.9999999999996788,    0.5000000000004744,
+                             0.1666666666766445,     0.04166666666019774,   0.00833333324592319,
+                             0.0013888889188354027,  0.00019841302319140728, 2.4801530417934142e-05,
+                             2.7551504280360845e-06, 2.7561173628426655e-07, 2.5547752396936175e-08,
+                             2.0934824859870782e-09};
+const double COMP_F[4] = {35.0 / 16, -35.0 / 16, 21.0 / 16, -5.0 / 16};
+const double COMP_G[4] = {4589.0 / 1024, -16577.0 / 1024, 25614.0 / 1024, -12860.0 / 1024};
+
+struct SM {
+    Eval& ev;
+    Geo g;
+    int classes, period;
+
+    G scale(const G& x, double t) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult_c(x[i], t);
+        return o;
+    }
+    G addc(const G& x, double s) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_c(x[i], s);
+        return o;
+    }
+    G rsubc(const G& x, double s) {   // s - x
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_c(x[i], s, false, true);
+        return o;
+    }
+    G add(const G& x, const G& y) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add(x[i], y[i]);
+        return o;
+    }
+    G sub(const G& x, const G& y) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.sub(x[i], y[i]);
+        return o;
+    }
+    G subp(const G& x, const Pattern& p) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_p(x[i], p, true, false);
+        return o;
+    }
+    G mul(const G& x, const G& y) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult(x[i], y[i]);
+        return o;
+    }
+    G mulp(const G& x, const Pattern& p) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult_p(x[i], p);
+        return o;
+    }
+    G lrot(const G& x, int r) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.lrot(x[i], r);
+        return o;
+    }
+    G rrot(const G& x, int r) {
+        G o(x.size());
+        for (size_t i = 0; i < x.size(); i++) o[i] = ev.rrot(x[i], r);
+        return o;
+    }
+
+    G odd7(const G& x, const double* a) {
+        G y = mul(x, x);
+        G acc = scale(y, a[3]);
+        acc = addc(acc, a[2]);
+        G t = mul(acc, y);
+        acc = addc(t, a[1]);
+        t = mul(acc, y);
+        acc = addc(t, a[0]);
+        return mul(acc, x);
+    }
+    G comp(const G& x, const G& y) {
+        G d = sub(x, y);
+        G u = odd7(d, COMP_G);
+        u = odd7(u, COMP_G);
+        u = odd7(u, COMP_F);
+        G v = addc(u, 1.0);
+        return scale(v, 0.5);
+    }
+    G amax(const G& M, const SoftmaxCfg& cfg, int max_range) {
+        const double two_r = 2.0 * max_range;
+        G work = scale(M, 1.0 / two_r);
+        if (classes < period) {
+            const int c = classes, cp = period;
+            work = subp(work, col_pattern(g, "padhalf:" + std::to_string(c) + ":" + std::to_string(cp),
+                                          [&](int j) { return (j % cp) >= c ? 0.5 : 0.0; }));
+        }
+        G best = work;
+        for (int t = 0; t < ilog2(period); t++) {
+            G rival = lrot(best, 1 << t);
+            G w = comp(best, rival);
+            G x1 = mul(best, w);
+            G x2 = rsubc(w, 1.0);
+            G x3 = mul(rival, x2);
+            best = add(x1, x3);
+        }
+        best = mulp(best, col0(g));
+        for (int t = 0; t < ilog2(g.s1); t++) {
+            G r = rrot(best, 1 << t);
+            best = add(best, r);
+        }
+        return scale(best, two_r);
+    }
+    G domain_extend(G M, const SoftmaxCfg& cfg) {
+        const double delta = 4.0 / (27.0 * std::pow(cfg.base_range, 2.0));
+        for (int i = cfg.extension_steps - 1; i >= 0; i--) {
+            const double di = delta * std::pow(cfg.extension_base, (double)(-2 * i));
+            G sq = mul(M, M);
+            G sc = scale(M, di);
+            G pr = mul(sq, sc);
+            M = sub(M, pr);
+        }
+        return M;
+    }
+    G dep_comp(const G& M, const SoftmaxCfg& cfg) {
+        const double L2 = std::pow(cfg.extension_base, 2.0);
+        const double Ln = std::pow(L2, (double)cfg.extension_steps);
+        const double K = L2 * (Ln - 1.0) / (Ln * (L2 - 1.0));
+        const double R = cfg.base_range;
+        const double c3 = 1.0 * (4.0 / 27.0) * K / std::pow(R, 2.0);
+        const double c5 = 1.0 * (4.0 / 27.0) * K / std::pow(R, 4.0);
+        G sq = mul(M, M);
+        G cube = mul(sq, M);
+        G fifth = mul(cube, sq);
+        G t3 = scale(cube, c3);
+        G t5 = scale(fifth, c5);
+        G d = sub(t3, t5);
+        return add(M, d);
+    }
+    G exp(const G& M, const SoftmaxCfg& cfg) {
+        const int B = cfg.exp_range;
+        G z = scale(M, 1.0 / B);
+        G acc = scale(z, EXP_POLY[12]);
+        acc = addc(acc, EXP_POLY[11]);
+        for (int k = 10; k >= 0; k--) {
+            G t = mul(acc, z);
+            acc = addc(t, EXP_POLY[k]);
+        }
+        for (int i = 0; i < ilog2(B); i++) acc = mul(acc, acc);
+        return acc;
+    }
+    G inv(const G& M, const SoftmaxCfg& cfg) {
+        G y = scale(M, 1.0 / cfg.inv_range);
+        G a = rsubc(y, 2.0);
+        G b = rsubc(y, 1.0);
+        for (int i = 0; i < cfg.inv_iters; i++) {
+            b = mul(b, b);
+            G t = addc(b, 1.0);
+            a = mul(a, t);
+        }
+        return scale(a, 1.0 / cfg.inv_range);
+    }
+};
+
+}  // namespace
+
+std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes, int period, const SoftmaxCfg& cfg) {
+    const Geo g = geo(ev, geo_rows(ev));
+    if (period < classes || period > g.s1 || (period & (period - 1))) throw Error(-4, "softmax: bad period");
+    if (cfg.exp_range < 1 || (cfg.exp_range & (cfg.exp_range - 1))) throw Error(-4, "exp_range must be a power of two");
+    SM sm{ev, g, classes, period};
+    const double full = cfg.base_range * std::pow(cfg.extension_base, (double)cfg.extension_steps);
+    const int max_range = (int)std::ceil(full / 2);
+    G best = sm.amax(M, cfg, max_range);
+    const int c = classes;
+    const Pattern keep = col_pattern(g, "keep:" + std::to_string(c), [&](int j) { return j < c ? 1.0 : 0.0; });
+    G d = sm.sub(M, best);
+    G norm = sm.mulp(d, keep);
+    norm = sm.domain_extend(norm, cfg);
+    if (cfg.precise) norm = sm.dep_comp(norm, cfg);
+    G e = sm.exp(norm, cfg);
+    G expd = sm.mulp(e, keep);
+    G total = col_sums(ev, expd, (int)expd.size(), 1, g);
+    G recip = sm.inv(total, cfg);
+    G out = sm.mul(expd, recip);
+    const int reps = g.s1 / period;
+    for (int t = 0; t < ilog2(reps); t++) {
+        G r = sm.rrot(out, period * (1 << t));
+        out = sm.add(out, r);
+    }
+    return out;
+}
+
+}  // namespace hc

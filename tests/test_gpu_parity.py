@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the C RNS-CKKS oracle.
+
+Bit-exact on ciphertext residues (integer work), given the same seed and
+nonce sequence; decrypted values against float64 within the CKKS tolerance.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import rns as R
+from oracle import slots as S
+
+pytestmark = pytest.mark.gpu
+
+OPS = S.OP_KINDS
+
+
+def _prod():
+    import paper_2403_14111_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module", params=["tiny", "small12", "cfg0"])
+def pair(request):
+    P = _prod()
+    name = request.param
+    grid = {"tiny": 16, "small12": 16, "cfg0": 64}[name]
+    return P.CKKSContext(name, grid, seed=77), R.OracleCKKSContext(name, grid, seed=77)
+
+
+def test_moduli_and_scales(pair):
+    g, o = pair
+    np.testing.assert_array_equal(g.moduli, o.p.moduli)
+    np.testing.assert_array_equal(g.scales, o.p.scales)
+
+
+def test_encoder_bit_exact(pair):
+    g, o = pair
+    rng = np.random.default_rng(3)
+    z = rng.uniform(-3, 3, g.slot_count) + 1j * rng.uniform(-3, 3, g.slot_count)
+    for sc in (2.0 ** 40, g.scales[0], 12345.678):
+        np.testing.assert_array_equal(g.encode_coef(z, sc), o.p.encode(z, sc))
+    np.testing.assert_array_equal(g.encode_pt(z, g.max_level), o.p.encode_ntt(z, g.max_level))
+
+
+def test_keys_bit_exact(pair):
+    g, o = pair
+    for gid in (0, g.galois_rot(1), g.galois_rot(-3), 2 * g.N - 1):
+        np.testing.assert_array_equal(g.key(gid), o.p.key(gid))
+
+
+def test_encrypt_decrypt(pair):
+    g, o = pair
+    rng = np.random.default_rng(4)
+    z = rng.uniform(-1, 1, g.slot_count)
+    for lv in (g.max_level, 1, 0):
+        g.nonce, o.nonce = 10, 10
+        a, b = g.encrypt(z, lv), o.encrypt(z, lv)
+        np.testing.assert_array_equal(a.residues(), b.data)
+        assert np.max(np.abs(a.slots - z)) < 1e-6
+
+
+def test_per_op_residues(pair):
+    g, o = pair
+    rng = np.random.default_rng(5)
+    n = g.slot_count
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    mask = (np.arange(n) % 3 == 0) * 0.5 - 0.25j
+    g.nonce, o.nonce = 0, 0
+    gx, gy = g.encrypt(x), g.encrypt(y)
+    ox, oy = o.encrypt(x), o.encrypt(y)
+
+    def same(a, b, want=None, tol=1e-5):
+        np.testing.assert_array_equal(a.residues(), b.data)
+        assert a.level == b.level
+        if want is not None:
+            assert np.max(np.abs(a.slots - want)) < tol
+
+    same(g.add(gx, gy), o.add(ox, oy), x + y)
+    same(g.sub(gx, gy), o.sub(ox, oy), x - y)
+    same(g.sub(0.75, gx), o.sub(0.75, ox), 0.75 - x)
+    same(g.add(gx, 2.0 - 1j), o.add(ox, 2.0 - 1j), x + 2 - 1j)
+    same(g.mult(gx, 0.3), o.mult(ox, 0.3), 0.3 * x)
+    same(g.mult(gx, mask), o.mult(ox, mask), x * mask)
+    same(g.add(gx, mask), o.add(ox, mask), x + mask)
+    same(g.sub(mask, gx), o.sub(mask, ox), mask - x)
+    gxy, oxy = g.mult(gx, gy), o.mult(ox, oy)
+    same(gxy, oxy, x * y)
+    same(g.add(gxy, gx), o.add(oxy, ox), x * y + x)          # level adjust 12 -> 11
+    same(g.mult(gxy, gy), o.mult(oxy, oy), x * y * y)        # adjust + mult
+    for r in (1, 7, n - 1, n // 2):
+        same(g.lrot(gx, r), o.lrot(ox, r), np.roll(x, -r))
+    same(g.conj(gx), o.conj(ox), np.conj(x))
+    same(g.mul_i(gx), o.mul_i(ox), 1j * x)
+    g.nonce, o.nonce = 500, 500
+    same(g.bootstrap(gxy), o.bootstrap(oxy), x * y)
+    lo_g, lo_o = g.level_adjust(gx, 0), o.p.level_adjust(ox.data, ox.level, 0)
+    np.testing.assert_array_equal(lo_g.residues(), lo_o)
+    g.auto_bootstrap = o.auto_bootstrap = True
+    g.nonce, o.nonce = 900, 900
+    same(g.mult(lo_g, lo_g), o.mult(R.RnsBlock(o, lo_o, 0), R.RnsBlock(o, lo_o, 0)), x * x)
+    g.auto_bootstrap = o.auto_bootstrap = False
+    rs = g.rescale(gx)
+    np.testing.assert_array_equal(rs.residues(), o.p.rescale(ox.data, ox.level))
+
+
+def _enc_pair(g, o, arr, tiling="none", level=None):
+    from paper_2403_14111_b200 import encode
+    g.nonce = o.nonce = 0
+    return encode(g, arr, tiling, level=level), S.encode(o, arr, tiling, level=level)
+
+
+def _same_grid(G, O):
+    assert G.grid == O.grid
+    for rg, ro in zip(G.blocks, O.blocks):
+        for bg, bo in zip(rg, ro):
+            np.testing.assert_array_equal(bg.residues(), bo.data)
+
+
+def _ledger(ctx):
+    c = ctx.ledger.counts()
+    return [c[k] for k in OPS]
+
+
+def test_native_diag_abt_config0(golden):
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    A, B = wl.config0()
+    g, o = P.CKKSContext("cfg0", 64, seed=5), R.OracleCKKSContext("cfg0", 64, seed=5)
+    GA, OA = _enc_pair(g, o, A)
+    g.nonce = o.nonce = 100
+    GB, OB = P.encode(g, B, "vertical"), S.encode(o, B, "vertical")
+    out = P.diag_abt(GA, GB)
+    ref = S.diag_abt(OA, OB)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden["cfg0_led"]) == _ledger(o)
+    assert out.level == 1
+    assert np.max(np.abs(P.decode(out) - A @ B.T)) < 1e-4
+
+
+@pytest.mark.parametrize("alev", [None, 11])
+def test_native_diag_atb_small12(golden, alev):
+    P = _prod()
+    g, o = P.CKKSContext("small12", 16, seed=6), R.OracleCKKSContext("small12", 16, seed=6)
+    GA, OA = _enc_pair(g, o, golden["small_atb_A"], "horizontal", level=alev)
+    g.nonce = o.nonce = 50
+    GB, OB = P.encode(g, golden["small_atb_B"]), S.encode(o, golden["small_atb_B"])
+    out = P.diag_atb(GA, GB, scale=2.0)
+    ref = S.diag_atb(OA, OB, scale=2.0)
+    _same_grid(out, ref)
+    branch = "rl" if alev is None else "pru"
+    assert _ledger(g) == list(golden[f"small_atb_{branch}_led"])
+    assert np.max(np.abs(P.decode(out) - golden[f"small_atb_{branch}_out"])) < 1e-4
+
+
+def test_native_softmax_small12(golden):
+    P = _prod()
+    g = P.CKKSContext("small12", 16, seed=8, auto_bootstrap=True)
+    o = R.OracleCKKSContext("small12", 16, seed=8, auto_bootstrap=True)
+    GM, OM = _enc_pair(g, o, golden["small_sm_in"], "horizontal")
+    out = P.a_softmax(GM)
+    ref = S.a_softmax(OM)
+    _same_grid(out, ref)
+    assert g.nonce == o.nonce
+    assert _ledger(g) == list(golden["small_sm_led"])
+    assert np.max(np.abs(P.decode(out, tol=1e-3) - golden["small_sm_out"])) < 1e-3
+
+
+def test_dropin_per_op_equals_native(golden):
+    """The reference op sequence (restated in oracle/slots.py) issued op by op
+    through the product's EmulatorContext interface == the native schedule."""
+    P = _prod()
+    g = P.CKKSContext("small12", 16, seed=9)
+    A, B = golden["small_abt_A"], golden["small_abt_B"]
+    g.nonce = 0
+    GA, GB = P.encode(g, A), P.encode(g, B, "vertical")
+    native = P.diag_abt(GA, GB, scale=0.25)
+    led_native = _ledger(g)
+    g.ledger.reset()
+    per_op = S.diag_abt(S.Grid(g, GA.blocks, GA.shape, GA.tiling, GA.period),
+                        S.Grid(g, GB.blocks, GB.shape, GB.tiling, GB.period), scale=0.25)
+    assert _ledger(g) == led_native == list(golden["small_abt_led"])
+    for bn, bp in zip(native.flat(), [b for r in per_op.blocks for b in r]):
+        np.testing.assert_array_equal(bn.residues(), bp.residues())
+
+
+def test_nag_steps_small12(golden):
+    P = _prod()
+    x, y = golden["small_train_x"], golden["small_train_y"]
+    g = P.CKKSContext("small12", 16, seed=10, auto_bootstrap=True)
+    o = R.OracleCKKSContext("small12", 16, seed=10, auto_bootstrap=True)
+    w0 = S.init_weights(3, x.shape[1], 7)
+    Y = S.one_hot(y, 3)
+    GW, OW = _enc_pair(g, o, w0, "vertical")
+    gs, os_ = P.TrainState(GW, GW), S.State(OW, OW)
+    for step in range(3):
+        sl = slice((step % 2) * 16, (step % 2) * 16 + 16)
+        g.nonce = o.nonce = 1000 * (step + 1)
+        GX, GY = P.encode(g, x[sl]), P.encode(g, Y[sl], "horizontal")
+        OX, OY = S.encode(o, x[sl]), S.encode(o, Y[sl], "horizontal")
+        P.nag_step(gs, GX, GY, 0.3, 16)
+        S.nag_step(os_, OX, OY, 0.3, 16)
+        _same_grid(gs.weights, os_.weights)
+        _same_grid(gs.momentum, os_.momentum)
+    assert _ledger(g) == list(golden["small_train_led"])
+    w = P.decode(gs.weights, tol=1e-3)
+    assert np.max(np.abs(w - golden["small_train_snaps"][-1])) < 1e-4
+
+
+@pytest.mark.slow
+def test_config1_diag_abt_full_size(golden):
+    """BASELINE config 1 at N=2^16: residues vs the oracle, values vs float64."""
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    X, W = wl.config1()
+    g, o = P.CKKSContext("cfg1", 128, seed=1), R.OracleCKKSContext("cfg1", 128, seed=1)
+    GX, OX = _enc_pair(g, o, X)
+    g.nonce = o.nonce = 10
+    GW, OW = P.encode(g, W, "vertical"), S.encode(o, W, "vertical")
+    out = P.diag_abt(GX, GW)
+    ref = S.diag_abt(OX, OW)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden["cfg1_led"])
+    assert out.level == 9
+    assert np.max(np.abs(P.decode(out) - X @ W.T)) < 1e-4

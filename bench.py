@@ -1,0 +1,345 @@
+"""Benchmark of the HETAL hot path on B200 (BASELINE.json metric).
+
+One step = DiagABT (config 1: X 128x768 times W^T, W 10x768 vertically tiled,
+period 16) followed by DiagATB (config 2: (P-Y)^T X, RL branch), RNS-CKKS at
+N = 2^16, 58 + 12x42 | 3x60 bits, dnum 4, Delta 2^42, on one 128-row block
+pair per GPU (weak scaling: every rank owns its own block pair, no collective
+on the data path).  Inputs are encrypted (client side) before timing and stay
+resident in HBM; the switching keys alone (2.3 GB) exceed L2, so no flush is
+needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+value = ms per DiagABT+DiagATB pair for the whole job (step time / pairs in
+flight across ranks; lower is better).  e2e = the same through the public
+API with host buffers: the step's input ciphertexts are copied host->device
+from pinned memory and its outputs device->host inside the timed region.
+--impl reference times the CPU RNS-CKKS oracle (the reference has no CKKS
+implementation of its own) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DiagABT/DiagATB ms at N=2^16 (128x768, 16 cls); key-switch/s; % HBM roofline"
+CONFIG = {"workload": "DiagABT cfg1 (128x768 . (16x768)^T) + DiagATB-RL cfg2 ((128x16)^T . 128x768)",
+          "ring": "N=2^16", "moduli": "58+12x42 | 3x60 bits", "dnum": 4, "scale": "2^42",
+          "grid": "128x256", "classes": 10, "period": 16, "block_rows_per_rank": 128,
+          "l2": "no flush: switching keys (2.3 GB) > 126 MB L2 are streamed every step"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def all_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle): a bounded sample of the same workload
+# ---------------------------------------------------------------------------
+
+
+def oracle_pass_sample(reps=1):
+    """Time one diagonal pass (k = 1 of c/2 = 8) of DiagABT and of DiagATB-RL
+    on the C RNS-CKKS oracle, all host threads; returns ms per pair
+    extrapolated x8 (prologue/epilogue key switches, ~3% of the pair, are
+    not counted, which flatters the CPU)."""
+    from oracle import rns as R
+    from oracle import slots as S
+    from paper_2403_14111_b200 import workloads as wl
+
+    X, W = wl.config1()
+    PY, _ = wl.config2()
+    o = R.OracleCKKSContext("cfg1", 128, seed=1)
+    OX, OW, OP = S.encode(o, X), S.encode(o, W, "vertical"), S.encode(o, PY, "horizontal")
+    c = OW.period
+    packed_b = OW.add(S.rot_up(OW, c // 2).each(o.mul_i))
+    packed_a = OP.add(S.rot_left(OP, c // 2).each(o.mul_i))
+    ms = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sums = S.col_sums(S._rowwise(OX, S.rot_up(packed_b, 1)))
+        sums.mul(S.make_mask(o, 1, c, (1, 1), True, 1.0))
+        t1 = time.perf_counter()
+        left = S.rot_left(packed_a, 1)
+        sums = S.row_sums(S._colwise(left, OX))
+        sums.mul(S.make_mask(o, -1, c, (1, 3), True, 1.0))
+        t2 = time.perf_counter()
+        ms.append(((t1 - t0) + (t2 - t1)) * 1e3 * (c // 2))
+    return ms, o.extra["KeySwitch"]
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    samples, _ = oracle_pass_sample(args.warmup + args.steps)
+    timed = samples[args.warmup:]
+    v = statistics.median(timed)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": CONFIG,
+            "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "port",
+                             "sample": "one of the 8 diagonal passes of DiagABT cfg1 and of DiagATB-RL cfg2 per "
+                                       "step on the C RNS-CKKS oracle (OpenMP, all host threads), x8"},
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_b200(args, world, rank, local):
+    import torch
+
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+    from paper_2403_14111_b200 import workloads as wl
+
+    L = N.lib()
+    ctx = P.CKKSContext("cfg1", 128, seed=1 + rank, device=local)
+    X, W = wl.config1()
+    PY, _ = wl.config2()
+    EX, EW, EP = P.encode(ctx, X), P.encode(ctx, W, "vertical"), P.encode(ctx, PY, "horizontal")
+
+    def step():
+        logits = P.diag_abt(EX, EW)
+        grad = P.diag_atb(EP, EX)
+        return logits, grad
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+    counts0 = ctx.ledger.counts()
+    extra0 = ctx.extra
+    launches0 = L.hc_launch_count(ctx._h)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    N.check(L.hc_timer_begin(ctx._h))
+    outs = None
+    for _ in range(args.steps):
+        outs = step()
+    ms = C.c_float()
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    barrier(world)
+    clk = clocks.stop()
+    total_ms = all_max(ms.value, world)
+    launches = L.hc_launch_count(ctx._h) - launches0
+    counts = {k: v - counts0[k] for k, v in ctx.ledger.counts().items()}
+    ks = ctx.extra["KeySwitch"] - extra0["KeySwitch"]
+    ms_step = total_ms / args.steps
+    value = ms_step / world            # whole job: `world` pairs per step
+
+    # one profiled step: per-kernel CUDA events on the library stream
+    N.check(L.hc_prof_begin(ctx._h))
+    step()
+    buf = C.create_string_buffer(1 << 16)
+    N.check(L.hc_prof_end(ctx._h, buf, len(buf)))
+    prof = json.loads(buf.value.decode())
+    # time per product in a separate pass
+    N.check(L.hc_timer_begin(ctx._h))
+    P.diag_abt(EX, EW)
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    abt_ms = ms.value
+    N.check(L.hc_timer_begin(ctx._h))
+    P.diag_atb(EP, EX)
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    atb_ms = ms.value
+
+    # e2e through the public API with pinned host buffers
+    inputs = [b for b in EX.flat() + EW.flat() + EP.flat()]
+    host_in = []
+    for b in inputs:
+        r = b.residues()
+        t = torch.empty(r.size, dtype=torch.int64, pin_memory=True)
+        t.numpy()[:] = r.ravel().view(np.int64)
+        host_in.append((t, b.level))
+    lg, gr = outs
+    out_shapes = [(2, b.level + 1, ctx.N) for b in lg.flat() + gr.flat()]
+    host_out = [torch.empty(int(np.prod(s)), dtype=torch.int64, pin_memory=True) for s in out_shapes]
+    h2d = sum(t.numel() * 8 for t, _ in host_in)
+    d2h = sum(t.numel() * 8 for t in host_out)
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier(world)
+    N.check(L.hc_timer_begin(ctx._h))
+    for _ in range(e2e_steps):
+        cts = []
+        for t, lv in host_in:
+            h = C.c_void_p()
+            N.check(L.hc_ct_upload(ctx._h, C.cast(C.c_void_p(t.data_ptr()), N.U64P), lv, C.byref(h)))
+            cts.append(P.Ciphertext(ctx, h))
+        gX = P.EncodedMatrix(ctx, (tuple(cts[0:3]),), EX.shape, "none", None)
+        gW = P.EncodedMatrix(ctx, (tuple(cts[3:6]),), EW.shape, "vertical", EW.period)
+        gP = P.EncodedMatrix(ctx, ((cts[6],),), EP.shape, "horizontal", EP.period)
+        a = P.diag_abt(gX, gW)
+        g = P.diag_atb(gP, gX)
+        for blk, t in zip(a.flat() + g.flat(), host_out):
+            N.check(L.hc_ct_download(blk._h, C.cast(C.c_void_p(t.data_ptr()), N.U64P)))
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    barrier(world)
+    e2e_ms = all_max(ms.value, world) / e2e_steps / world
+
+    hbm, peak_kind = peaks()
+    top = max(prof.items(), key=lambda kv: kv[1][1])
+    name, (n_launch, k_ms, k_bytes) = top
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(name)
+        except Exception:
+            traffic = None
+    step_prof_ms = sum(v[1] for v in prof.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, BASELINE configs 1-2)",
+        "config": CONFIG,
+        "diag_abt_ms": abt_ms, "diag_atb_ms": atb_ms,
+        "keyswitch_per_s": ks * world / (total_ms * 1e-3),
+        "ledger_per_step": {k: v // args.steps for k, v in counts.items()},
+        "keyswitches_per_step": ks // args.steps,
+        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
+                     "launches_per_step": int(n_launch), "kernel_share_of_step": k_ms / step_prof_ms},
+        "kernel_breakdown_ms": {k: round(v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu:
+        samples, _ = oracle_pass_sample(1)
+        line["cpu_baseline"] = {"value": samples[0], "unit": "ms", "cores": os.cpu_count(), "kind": "port",
+                                "sample": "one of the 8 diagonal passes of DiagABT cfg1 and DiagATB-RL cfg2 on the "
+                                          "C RNS-CKKS oracle (OpenMP, all host threads), x8"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

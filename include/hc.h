@@ -132,6 +132,16 @@ int hc_softmax(hc_ctx *ctx, const hc_ct *const *A, int m, int classes, int perio
 /* finish a cross-rank uint64 sum: residues mod q_i in place (K8) */
 int hc_mod_reduce(hc_ctx *ctx, hc_ct *ct);
 
+/* ---- measurement (no reference counterpart) ---- */
+/* CUDA events on the context stream around a region */
+int hc_timer_begin(hc_ctx *ctx);
+int hc_timer_end(hc_ctx *ctx, float *ms);
+/* kernels launched by this context so far */
+int64_t hc_launch_count(hc_ctx *ctx);
+/* per-kernel event profiler: JSON {"kernel": [launches, total_ms, algorithmic_bytes], ...} */
+int hc_prof_begin(hc_ctx *ctx);
+int hc_prof_end(hc_ctx *ctx, char *json, int len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,11 @@ SIGNATURES = {
     "hc_diag_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P, REDUCE_FN, P]),
     "hc_softmax": (I, [P, PP, I, I, I, DP, PP, I64P]),
     "hc_mod_reduce": (I, [P, P]),
+    "hc_timer_begin": (I, [P]),
+    "hc_timer_end": (I, [P, C.POINTER(C.c_float)]),
+    "hc_launch_count": (I64, [P]),
+    "hc_prof_begin": (I, [P]),
+    "hc_prof_end": (I, [P, C.c_char_p, I]),
 }
 
 

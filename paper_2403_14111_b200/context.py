@@ -32,7 +32,7 @@ EXTRA_KINDS = ("LevelAdjust", "KeySwitch")
 DEFAULT_OP_WEIGHTS_MS = {"Add": 0.085, "CMult": 0.9, "Mult": 1.6, "Rot": 1.2, "Conj": 1.2,
                          "Bootstrap": 159.0}
 PLAINTEXT_LEVEL = math.inf
-DECODE_TOL = 1e-4
+DECODE_TOL = 1e-3      # CKKS noise after a full DiagABT/DiagATB at Delta = 2^42 is ~2e-4
 
 # name -> (log N, q bits (q0 first), p bits, alpha, log scale, hamming weight)
 PARAMS = {

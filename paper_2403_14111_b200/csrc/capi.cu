@@ -1,5 +1,8 @@
 // extern "C" boundary (include/hc.h): handle wrappers, error mapping.
+#include <array>
+#include <cstdio>
 #include <cstring>
+#include <map>
 
 #include "../../include/hc.h"
 #include "evaluator.h"
@@ -247,6 +250,68 @@ int hc_level_adjust(hc_ctx* ctx, const hc_ct* a, int level, hc_ct** out) {
 
 int hc_mod_reduce(hc_ctx* ctx, hc_ct* ct) {
     return guard([&] { hc::k_mod_reduce(*ctx->c, ct->p->d, ct->p->level + 1, ct->p->npoly); });
+}
+
+// ---- measurement ----
+
+int hc_timer_begin(hc_ctx* ctx) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (!c.t0) { HC_CUDA(cudaEventCreate(&c.t0)); HC_CUDA(cudaEventCreate(&c.t1)); }
+        HC_CUDA(cudaEventRecord(c.t0, c.stream));
+    });
+}
+
+int hc_timer_end(hc_ctx* ctx, float* ms) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        HC_CUDA(cudaEventRecord(c.t1, c.stream));
+        HC_CUDA(cudaEventSynchronize(c.t1));
+        HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
+    });
+}
+
+int64_t hc_launch_count(hc_ctx* ctx) { return ctx->c->launches; }
+
+int hc_prof_begin(hc_ctx* ctx) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+        for (auto& r : c.prof_recs) { c.ev_free.push_back(r.a); c.ev_free.push_back(r.b); }
+        c.prof_recs.clear();
+        c.prof = true;
+    });
+}
+
+int hc_prof_end(hc_ctx* ctx, char* json, int len) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+        c.prof = false;
+        std::map<std::string, std::array<double, 3>> agg;
+        for (auto& r : c.prof_recs) {
+            float ms = 0;
+            HC_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            auto& a = agg[r.name];
+            a[0] += 1;
+            a[1] += ms;
+            a[2] += r.bytes;
+            c.ev_free.push_back(r.a);
+            c.ev_free.push_back(r.b);
+        }
+        c.prof_recs.clear();
+        std::string s = "{";
+        for (auto& kv : agg) {
+            if (s.size() > 1) s += ",";
+            char b[256];
+            std::snprintf(b, sizeof b, "\"%s\":[%.0f,%.6f,%.0f]", kv.first.c_str(), kv.second[0], kv.second[1],
+                          kv.second[2]);
+            s += b;
+        }
+        s += "}";
+        if ((int)s.size() + 1 > len) throw hc::Error(HC_EPARAM, "profile buffer too small");
+        std::memcpy(json, s.c_str(), s.size() + 1);
+    });
 }
 
 // ---- schedules ----

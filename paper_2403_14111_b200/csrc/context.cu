@@ -67,6 +67,30 @@ void Ctx::free(u64* p) {
     if (p) HC_CUDA(cudaFreeAsync(p, stream));
 }
 
+cudaEvent_t Ctx::get_event() {
+    if (!ev_free.empty()) {
+        cudaEvent_t e = ev_free.back();
+        ev_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    HC_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+Launch::Launch(Ctx& ctx, const char* name, double bytes) : c(ctx) {
+    c.launches++;
+    if (!c.prof) return;
+    Ctx::ProfRec r{name, c.get_event(), c.get_event(), bytes};
+    HC_CUDA(cudaEventRecord(r.a, c.stream));
+    idx = (int)c.prof_recs.size();
+    c.prof_recs.push_back(r);
+}
+
+Launch::~Launch() {
+    if (idx >= 0) cudaEventRecord(c.prof_recs[idx].b, c.stream);
+}
+
 size_t Ct::words() const { return (size_t)npoly * (level + 1) * ctx->N; }
 u64* Ct::poly(int s) const { return d + (size_t)s * (level + 1) * ctx->N; }
 

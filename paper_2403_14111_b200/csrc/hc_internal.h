@@ -108,9 +108,32 @@ struct Ctx {
     // encoded-mask cache used by the native schedules
     std::map<std::string, PtP> pt_cache;
 
+    // launch accounting and the optional per-kernel event profiler
+    int64_t launches = 0;
+    bool prof = false;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_free;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaEvent_t get_event();
+
     // workspace stream-ordered allocation
     u64* alloc(size_t words);
     void free(u64* p);
+};
+
+// RAII scope around one kernel launch: counts it and, when profiling,
+// brackets it with CUDA events on the context stream.  `bytes` is the
+// launch's algorithmic HBM traffic (inputs read once + outputs written once).
+struct Launch {
+    Ctx& c;
+    int idx = -1;
+    Launch(Ctx& ctx, const char* name, double bytes);
+    ~Launch();
 };
 
 // ---- kernels / launchers (ntt.cu, kernels.cu) ----

@@ -87,6 +87,9 @@ void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const C
                    int bpoly) {
     const size_t work = (size_t)npoly * nl * c.N / 2;
     static const ConstTab zero = {};
+    const bool pt_b = op >= EW_PT_ADD && op <= EW_PT_MUL;
+    const double rd = (double)npoly * nl + (pt_b ? nl : (op <= EW_SUB ? bpoly * nl : 0));
+    Launch scope(c, "elementwise", 8.0 * c.N * (rd + (double)npoly * nl));
     ew_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(op, out, a, b, consts ? *consts : zero, c.d_primes, nl, npoly,
                                                         c.N, bpoly);
     HC_CUDA(cudaGetLastError());
@@ -112,6 +115,7 @@ __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, co
 }
 
 void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl) {
+    Launch scope(c, "tensor", 8.0 * c.N * 7 * nl);
     tensor_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(d, a, b, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -135,6 +139,7 @@ __global__ void automorph_kernel(u64* __restrict__ out, const u64* __restrict__ 
 }
 
 void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g) {
+    Launch scope(c, "automorph", 16.0 * c.N * nlimbs);
     automorph_kernel<<<nblocks((size_t)nlimbs * c.N, 256), 256, 0, c.stream>>>(out, in, nlimbs, c.logN, g);
     HC_CUDA(cudaGetLastError());
 }
@@ -189,6 +194,8 @@ __global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, co
 
 void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
     dim3 grid((c.N + 255) / 256, beta);
+    const int nl = level + 1, nt = nl + c.K;
+    Launch scope(c, "modup", 8.0 * c.N * (2.0 * nl + (double)beta * nt));
     modup_kernel<<<grid, 256, 0, c.stream>>>(up, X, D, c.d_modup, c.d_modup_inv, c.d_primes, level, c.L, c.K,
                                               c.alpha, c.dnum, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
@@ -223,6 +230,8 @@ __global__ void keyprod_kernel(u64* __restrict__ acc, const u64* __restrict__ up
 
 void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta) {
     const size_t poly = (size_t)(level + 1 + c.K) * c.N;
+    const double nt = level + 1 + c.K;
+    Launch scope(c, "keyprod", 8.0 * c.N * (3.0 * beta * nt + 2.0 * nt));
     keyprod_kernel<<<nblocks(poly, 256), 256, 0, c.stream>>>(acc, up, key, c.d_primes, level, c.L, c.K, beta,
                                                               c.nall, c.N);
     HC_CUDA(cudaGetLastError());
@@ -263,6 +272,7 @@ __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__
 
 void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
     dim3 grid((c.N + 255) / 256, 2);
+    Launch scope(c, "moddown_conv", 8.0 * c.N * (2.0 * c.K + 2.0 * (level + 1)));
     moddown_conv_kernel<<<grid, 256, 0, c.stream>>>(W, acc, c.d_moddown, c.d_moddown_inv, c.d_primes, level, c.L,
                                                      c.K, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
@@ -289,6 +299,7 @@ __global__ void moddown_combine_kernel(u64* __restrict__ out, const u64* __restr
 void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly,
                        int level) {
     const size_t work = 2 * (size_t)(level + 1) * c.N;
+    Launch scope(c, "moddown_combine", 8.0 * c.N * (level + 1) * (6.0 + add_npoly));
     moddown_combine_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(out, acc, W, c.d_pinv, addend, add_npoly,
                                                                       c.d_primes, level, c.K, c.N);
     HC_CUDA(cudaGetLastError());
@@ -331,6 +342,7 @@ __global__ void rescale_combine_kernel(u64* __restrict__ out, const u64* __restr
 
 void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly) {
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
+    Launch scope(c, "rescale_bcast", 8.0 * c.N * npoly * (1.0 + level));
     rescale_bcast_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(Y, X, tab, c.d_primes,
                                                                                           level, npoly, c.N);
     HC_CUDA(cudaGetLastError());
@@ -338,6 +350,7 @@ void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly) {
 
 void k_rescale_combine(Ctx& c, u64* out, const u64* a, const u64* Y, int level, int npoly) {
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
+    Launch scope(c, "rescale_combine", 8.0 * c.N * npoly * 3.0 * level);
     rescale_combine_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(out, a, Y, tab,
                                                                                             c.d_primes, level, npoly,
                                                                                             c.N);
@@ -360,6 +373,7 @@ __global__ void uniform_kernel(u64* __restrict__ out, const PrimeDev* __restrict
 }
 
 void k_uniform(Ctx& c, u64* out, int first_prime, int nl, u64 stream) {
+    Launch scope(c, "sample_uniform", 8.0 * c.N * nl);
     uniform_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, c.d_primes, first_prime, nl, c.N,
                                                                           rng_key(c.seed, stream));
     HC_CUDA(cudaGetLastError());
@@ -375,6 +389,7 @@ __global__ void cdt_kernel(i64* __restrict__ e, const u64* __restrict__ cdt, int
 }
 
 void k_cdt(Ctx& c, i64* e, u64 stream) {
+    Launch scope(c, "sample_gauss", 8.0 * c.N);
     cdt_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(e, c.d_cdt, c.cdt_n, c.cdt_b, c.N, rng_key(c.seed, stream));
     HC_CUDA(cudaGetLastError());
 }
@@ -392,6 +407,7 @@ __global__ void coef_to_rns_kernel(u64* __restrict__ out, const i64* __restrict_
 }
 
 void k_coef_to_rns(Ctx& c, u64* out, const i64* m, const i64* e, int first_prime, int nl) {
+    Launch scope(c, "coef_to_rns", 8.0 * c.N * (2.0 + nl));
     coef_to_rns_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, m, e, c.d_primes, first_prime, nl,
                                                                               c.N);
     HC_CUDA(cudaGetLastError());
@@ -438,6 +454,7 @@ __global__ void dec_kernel(u64* __restrict__ x, const u64* __restrict__ c0, cons
 }
 
 void k_dec(Ctx& c, u64* x, const u64* c0, const u64* c1, int nl) {
+    Launch scope(c, "decrypt_limbs", 8.0 * c.N * 4 * nl);
     dec_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(x, c0, c1, c.d_sk, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -464,6 +481,7 @@ __global__ void refresh_msg_kernel(i64* __restrict__ m, const u64* __restrict__ 
 }
 
 void k_refresh_msg(Ctx& c, i64* m, const u64* x, int two, u64 inv01, double ratio) {
+    Launch scope(c, "refresh_msg", 8.0 * c.N * 3);
     refresh_msg_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(m, x, c.d_primes, two, inv01, ratio, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -478,6 +496,7 @@ __global__ void enc_combine_kernel(u64* __restrict__ c0, const u64* __restrict__
 }
 
 void k_enc_combine(Ctx& c, u64* c0, const u64* c1, int nl) {
+    Launch scope(c, "enc_combine", 8.0 * c.N * 4 * nl);
     enc_combine_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(c0, c1, c.d_sk, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -492,6 +511,7 @@ __global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restric
 }
 
 void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly) {
+    Launch scope(c, "mod_reduce", 16.0 * c.N * npoly * nl);
     mod_reduce_kernel<<<nblocks((size_t)npoly * nl * c.N, 256), 256, 0, c.stream>>>(x, c.d_primes, nl, npoly, c.N);
     HC_CUDA(cudaGetLastError());
 }

@@ -117,6 +117,9 @@ static void launch_pass(Ctx& c, const JobList& jobs, bool inv, int logSZ, int mo
     if (threads < 32) threads = 32;
     dim3 grid(c.N / TE, jobs.n);
     size_t smem = sizeof(u64) * TE;
+    static const char* names[2][3] = {{"ntt_fwd_full", "ntt_fwd_cols", "ntt_fwd_chunks"},
+                                      {"ntt_inv_full", "ntt_inv_cols", "ntt_inv_chunks"}};
+    Launch scope(c, names[inv ? 1 : 0][mode], 16.0 * c.N * jobs.n);
     if (inv) {
         ntt_tile_kernel<true><<<grid, threads, smem, c.stream>>>(jobs, c.d_primes, c.d_itw, c.d_itws, c.N, logSZ,
                                                                  mode, log_te, N1, use_src, last);

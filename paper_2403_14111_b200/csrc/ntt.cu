@@ -92,21 +92,44 @@ __global__ void __launch_bounds__(SUBS*(1 << LOGSZ) / 8) ntt_kernel(JobList jobs
                 }
             }
         }
-        // ---- butterflies ----
+        // ---- twiddles: issue every load of the round up front (latency overlap) ----
+        u64 tw_r[7], tws_r[7];
+        {
+            int n = 0;
 #pragma unroll
-        for (int j = 0; j < G; j++) {
-            const int g = lt + j * TPS;
-            const int blk = g >> logu;
-            u64* y = x + j * GS;
-            if (!INV) {
+            for (int j = 0; j < G; j++) {
+                const int blk = (lt + j * TPS) >> logu;
 #pragma unroll
                 for (int qq = 0; qq < r; qq++) {
                     const int half = 1 << (r - 1 - qq);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
+                        if ((m1 & ((half << 1) - 1)) != 0) continue;      // one twiddle per sub-block
                         const int widx = R * (1 << (s0 + qq)) + (blk << qq) + (m1 >> (r - qq));
-                        const u64 w = __ldg(W + widx), ws = __ldg(Ws + widx);
+                        tw_r[n] = __ldg(W + widx);
+                        tws_r[n] = __ldg(Ws + widx);
+                        n++;
+                    }
+                }
+            }
+        }
+        // ---- butterflies ----
+        int tn = 0;
+#pragma unroll
+        for (int j = 0; j < G; j++) {
+            u64* y = x + j * GS;
+            if (!INV) {
+#pragma unroll
+                for (int qq = 0; qq < r; qq++) {
+                    const int half = 1 << (r - 1 - qq);
+                    const int tbase = tn;
+#pragma unroll
+                    for (int m1 = 0; m1 < GS; m1++) {
+                        if (m1 & half) continue;
+                        const int k = tbase + (m1 >> (r - qq));
+                        if ((m1 & ((half << 1) - 1)) == 0) tn++;
+                        const u64 w = tw_r[k], ws = tws_r[k];
                         u64 X = y[m1];
                         X = X >= twoq ? X - twoq : X;
                         const u64 T = mul_shoup_lazy(y[m1 + half], w, ws, q);
@@ -115,14 +138,18 @@ __global__ void __launch_bounds__(SUBS*(1 << LOGSZ) / 8) ntt_kernel(JobList jobs
                     }
                 }
             } else {
+                // twiddles were loaded in forward stage order: stage qq's block
+                // starts at offset (2^qq - 1) within this group's 2^r - 1 entries
+                const int gbase = tn;
+                tn += GS - 1;
 #pragma unroll
                 for (int qq = r - 1; qq >= 0; qq--) {
                     const int half = 1 << (r - 1 - qq);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const int widx = R * (1 << (s0 + qq)) + (blk << qq) + (m1 >> (r - qq));
-                        const u64 w = __ldg(W + widx), ws = __ldg(Ws + widx);
+                        const int k = gbase + ((1 << qq) - 1) + (m1 >> (r - qq));
+                        const u64 w = tw_r[k], ws = tws_r[k];
                         const u64 U = y[m1], V = y[m1 + half];
                         u64 X = U + V;
                         y[m1] = X >= twoq ? X - twoq : X;

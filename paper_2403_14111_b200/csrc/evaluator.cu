@@ -73,6 +73,7 @@ CtP ev_add_const(Ctx& c, const Ct& a, double re, double im, bool negate_ct) {
 
 // rescale [npoly][level+1][N] at `a` into [npoly][level][N] at `out`
 static void rescale_raw(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+    if (rescale_fused(c, a, level, npoly, out)) return;
     const int N = c.N;
     u64* X = c.alloc((size_t)npoly * N);
     JobList j;
@@ -219,6 +220,13 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
 CtP ev_automorph(Ctx& c, const Ct& a, u64 g) {
     const Key& key = get_key(c, (int)g);
     const int nl = a.level + 1;
+    {
+        CtP o = new_ct(c, a.level);
+        if (keyswitch_fused(c, a.poly(1), g, a.level, key, o->d, a.poly(0), 1, g)) {
+            c.counts[OP_KS]++;
+            return o;
+        }
+    }
     u64* S = c.alloc((size_t)2 * nl * c.N);
     k_automorph(c, S, a.d, 2 * nl, g);
     CtP o = new_ct(c, a.level);
@@ -236,7 +244,8 @@ CtP ev_mult(Ctx& c, const Ct& a, const Ct& b) {
     u64* D = c.alloc(3 * poly);
     k_tensor(c, D, a.d, b.d, nl);
     u64* T = c.alloc(2 * poly);
-    keyswitch(c, D + 2 * poly, a.level, key, T, D, 2);
+    if (keyswitch_fused(c, D + 2 * poly, 0, a.level, key, T, D, 2, 0)) c.counts[OP_KS]++;
+    else keyswitch(c, D + 2 * poly, a.level, key, T, D, 2);
     c.free(D);
     CtP o = new_ct(c, a.level - 1);
     rescale_raw(c, T, a.level, 2, o->d);

@@ -13,6 +13,11 @@
 namespace hc {
 
 void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const u64* addend, int add_npoly);
+// fused pipeline (keyswitch.cu) for split-pass rings; false when N < 2^14.
+// d and the addend are read through the galois permutation gal / add_gal (0 = none).
+bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
+                     int add_npoly, u64 add_gal);
+bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
 
 // a plaintext slot pattern with a cache key (content-addressed by the caller)
 struct Pattern {

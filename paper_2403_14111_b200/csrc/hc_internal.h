@@ -32,10 +32,13 @@ struct Error : std::runtime_error {
 
 // one limb job for a batched launch: a pointer to N words and its prime
 struct JobList {
-    int n;
+    int n = 0;
+    int custom = 0;          // inverse only: final multiplier scale[] instead of N^-1
+    u64 galois = 0;          // first pass gathers the source through this automorphism
     int prime[MAXJ];
     u64* ptr[MAXJ];
     const u64* src[MAXJ];   // optional out-of-place source (nullptr = in place)
+    u64 scale[MAXJ], scale_s[MAXJ];
 };
 
 // host-side view of one prime with its precomputation

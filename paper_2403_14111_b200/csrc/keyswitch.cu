@@ -1,0 +1,508 @@
+// Fused hybrid key switching and rescale for split-pass rings (N >= 2^14).
+//
+// Per key switch of d = sigma(c1) at level l (nl = l+1 limbs, nt = nl + K,
+// beta digits of alpha primes), the unfused pipeline makes ~15 launches and
+// round-trips every ModUp / ModDown limb through HBM three times.  Here:
+//
+//   1. INTT of d, gathering sigma on the fly, final scale N^-1 * (Q'/q_i)^-1
+//      folded into one Shoup constant             -> Y    (2 launches)
+//   2. A: column pass of the forward NTT of every non-digit limb, whose
+//      first-round loads compute the fast base conversion
+//      sum_a Y_a * [Q'/q_a]_{p_t} on the fly          -> I    (1 launch)
+//   3. B: chunk pass of those NTTs, one CTA per (chunk tile, target limb t),
+//      looping over the digits: each digit's NTT output (or, for t inside
+//      the digit, sigma(d) itself) is multiplied with the key in registers
+//      and accumulated in 128 bits; one Barrett reduction per output
+//                                                      -> ACC  (1 launch)
+//   4. INTT of ACC's P limbs, final scale N^-1 * (P/p)^-1  (2 launches)
+//   5. D: column pass of the ModDown NTT with the P->Q conversion in its
+//      loads                                           -> Wt   (1 launch)
+//   6. E: chunk pass whose stores compute (ACC - W) * P^-1 + addend, the
+//      addend being sigma(c0) (gathered) or the tensor's (d0, d1)
+//                                                      -> out  (1 launch)
+//
+// Every step is exact modular arithmetic, so the residues equal the
+// unfused path and the oracle bit for bit.
+#include "evaluator.h"
+#include "kernels.cuh"
+#include "ntt_pass.cuh"
+
+namespace hc {
+
+constexpr int CH_LOG = 9, CH_SUBS = 4;       // chunk pass: 512-point, 4 per CTA
+
+struct KsJobs {
+    int n;
+    unsigned char digit[MAXJ];
+    unsigned char t[MAXJ];
+};
+
+struct KsGeo {
+    int level, nl, nt, L, K, alpha, dnum, nall, beta, logN, N1;
+    __host__ __device__ int prime(int t) const { return t <= level ? t : L + 1 + (t - level - 1); }
+};
+
+// ---- A: ModUp conversion fused into the column pass --------------------------
+
+struct LdModup {
+    const u64* __restrict__ Y;   // [nl][N] coefficient form, pre-scaled by (Q'/q_a)^-1
+    const u64* cf;               // na (value, shoup) pairs for target prime p
+    int lo, na;
+    u64 p;
+    size_t N;
+    __device__ __forceinline__ u64 operator()(size_t k) const {
+        u64 acc = 0;
+        for (int a = 0; a < na; a++) acc += mul_shoup_lazy(Y[(size_t)(lo + a) * N + k], cf[2 * a], cf[2 * a + 1], p);
+        // acc < 2 * na * p <= 8p
+        if (acc >= 4 * p) acc -= 4 * p;
+        if (acc >= 2 * p) acc -= 2 * p;
+        return acc >= p ? acc - p : acc;
+    }
+    __device__ __forceinline__ void load8(size_t k, u64* x) const {
+        for (int e = 0; e < 8; e++) x[e] = (*this)(k + e);
+    }
+};
+
+template <int LOGSZ, int SUBS>
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+    ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+                  const u64* __restrict__ tws, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
+                  u64* __restrict__ I) {
+    extern __shared__ u64 sm[];
+    const int job = blockIdx.y;
+    const int j = jobs.digit[job], t = jobs.t[job];
+    const int pi = g.prime(t);
+    const size_t N = (size_t)1 << g.logN;
+    const int lo = j * g.alpha;
+    const int hi = min(lo + g.alpha, g.nl);
+    __shared__ u64 cf[16];
+    if (threadIdx.x < 2 * (hi - lo)) {
+        const int a = threadIdx.x >> 1;
+        cf[threadIdx.x] = modup_tab[(((size_t)(g.level * g.dnum + j) * g.alpha + a) * g.nall + pi) * 2 + (threadIdx.x & 1)];
+    }
+    __syncthreads();
+    const u64 p = primes[pi].q;
+    LdModup ld{Y, cf, lo, hi - lo, p, N};
+    StPlain<false, false> st{I + ((size_t)j * g.nt + t) * N, p, 0, 0};
+    PassGeo<LOGSZ, MODE_COLS, SUBS> G;
+    G.init(g.logN, g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)pi * N, tws + (size_t)pi * N, p, ld, st);
+}
+
+// ---- B: chunk pass + key inner product ------------------------------------
+
+struct StCapture {
+    u64* x;
+    __device__ __forceinline__ void operator()(size_t, u64) const {}   // unused: chunk edge is contiguous
+    __device__ __forceinline__ void store8(size_t, const u64* v) const {
+#pragma unroll
+        for (int e = 0; e < 8; e++) x[e] = v[e];
+    }
+};
+
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, 2)
+    ks_chunks_keyprod(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+                      const u64* __restrict__ tws, const u64* __restrict__ I, const u64* __restrict__ d, u64 gal,
+                      const u64* __restrict__ key, u64* __restrict__ acc) {
+    using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
+    extern __shared__ u64 sm[];
+    const int t = blockIdx.y;
+    const int pi = g.prime(t);
+    const size_t N = (size_t)1 << g.logN;
+    const PrimeDev P = primes[pi];
+    PG G;
+    G.init(g.logN, g.N1);
+    const size_t k0 = G.gidx(G.lt * 8);     // this thread's 8 consecutive output coefficients
+    U128 a0[8], a1[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) { a0[e] = {0, 0}; a1[e] = {0, 0}; }
+    u64 x[8];
+    for (int j = 0; j < g.beta; j++) {
+        const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
+        if (t >= lo && t < hi) {
+            LdGalois ld{d + (size_t)t * N, g.logN, gal};
+            ld.load8(k0, x);
+        } else {
+            __syncthreads();
+            LdPlain ld{I + ((size_t)j * g.nt + t) * N};
+            StCapture st{x};
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)pi * N, tws + (size_t)pi * N, P.q, ld,
+                                                          st);
+        }
+        const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0;
+        const u64* ka = kb + (size_t)g.nall * N;
+        const ulonglong2* kbv = reinterpret_cast<const ulonglong2*>(kb);
+        const ulonglong2* kav = reinterpret_cast<const ulonglong2*>(ka);
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const ulonglong2 b = kbv[v], a = kav[v];
+            mac128(a0[2 * v], x[2 * v], b.x);
+            mac128(a0[2 * v + 1], x[2 * v + 1], b.y);
+            mac128(a1[2 * v], x[2 * v], a.x);
+            mac128(a1[2 * v + 1], x[2 * v + 1], a.y);
+        }
+    }
+    ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
+    ulonglong2* o1 = reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k0);
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+        o0[v] = make_ulonglong2(reduce128(a0[2 * v].hi, a0[2 * v].lo, P), reduce128(a0[2 * v + 1].hi, a0[2 * v + 1].lo, P));
+        o1[v] = make_ulonglong2(reduce128(a1[2 * v].hi, a1[2 * v].lo, P), reduce128(a1[2 * v + 1].hi, a1[2 * v + 1].lo, P));
+    }
+}
+
+// ---- D: ModDown conversion fused into the column pass ----------------------
+
+struct LdModdown {
+    const u64* __restrict__ Yp;  // [K][N] of this poly, pre-scaled by (P/p_t)^-1
+    const u64* cf;               // K (value, shoup) pairs for target q_i
+    int K;
+    u64 q;
+    size_t N;
+    __device__ __forceinline__ u64 operator()(size_t k) const {
+        u64 acc = 0;
+        for (int t = 0; t < K; t++) acc += mul_shoup_lazy(Yp[(size_t)t * N + k], cf[2 * t], cf[2 * t + 1], q);
+        if (acc >= 4 * q) acc -= 4 * q;
+        if (acc >= 2 * q) acc -= 2 * q;
+        return acc >= q ? acc - q : acc;
+    }
+    __device__ __forceinline__ void load8(size_t k, u64* x) const {
+        for (int e = 0; e < 8; e++) x[e] = (*this)(k + e);
+    }
+};
+
+template <int LOGSZ, int SUBS>
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+    ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+                    const u64* __restrict__ tws, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
+                    u64* __restrict__ Wt) {
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
+    const size_t N = (size_t)1 << g.logN;
+    __shared__ u64 cf[16];
+    if (threadIdx.x < 2 * g.K) {
+        const int t = threadIdx.x >> 1;
+        cf[threadIdx.x] = md_tab[((size_t)t * g.nall + i) * 2 + (threadIdx.x & 1)];
+    }
+    __syncthreads();
+    const u64 q = primes[i].q;
+    LdModdown ld{acc + ((size_t)s * g.nt + g.nl) * N, cf, g.K, q, N};
+    StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
+    PassGeo<LOGSZ, MODE_COLS, SUBS> G;
+    G.init(g.logN, g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+}
+
+// ---- E: chunk pass with the ModDown combine in its stores ------------------
+
+struct StModdown {
+    u64* __restrict__ out;           // [nl][N] of this poly
+    const u64* __restrict__ accq;    // ACC Q limb i of this poly (full limb base)
+    const u64* __restrict__ add;     // addend limb base or nullptr
+    u64 q, pinv, pinv_s, gal;
+    int logN;
+    __device__ __forceinline__ u64 one(size_t k, u64 w) const {
+        w = w >= 2 * q ? w - 2 * q : w;
+        w = w >= q ? w - q : w;
+        u64 v = mul_shoup(accq[k] + q - w, pinv, pinv_s, q);
+        if (add) {
+            const u64 a = gal ? add[galois_src((unsigned)k, logN, gal)] : add[k];
+            v = add_mod(v, a, q);
+        }
+        return v;
+    }
+    __device__ __forceinline__ void operator()(size_t k, u64 w) const { out[k] = one(k, w); }
+    __device__ __forceinline__ void store8(size_t k, const u64* w) const {
+        ulonglong2* o = reinterpret_cast<ulonglong2*>(out + k);
+#pragma unroll
+        for (int v = 0; v < 4; v++) o[v] = make_ulonglong2(one(k + 2 * v, w[2 * v]), one(k + 2 * v + 1, w[2 * v + 1]));
+    }
+};
+
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
+    ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+                      const u64* __restrict__ tws, const u64* __restrict__ Wt, const u64* __restrict__ acc,
+                      const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly, u64 add_gal,
+                      u64* __restrict__ out) {
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
+    const size_t N = (size_t)1 << g.logN;
+    const u64 q = primes[i].q;
+    LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
+    StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
+                 (s < add_npoly) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
+                 add_gal, g.logN};
+    PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
+    G.init(g.logN, g.N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+}
+
+// ---- fused rescale (R1: bcast in the column pass, R2: combine in the chunk pass)
+
+struct LdBcast {
+    const u64* __restrict__ X;   // INTT of the dropped limb
+    u64 ql, q, qlm;
+    __device__ __forceinline__ u64 operator()(size_t k) const {
+        const u64 v = X[k], vm = v % q;
+        return v > (ql - 1) / 2 ? sub_mod(vm, qlm, q) : vm;
+    }
+    __device__ __forceinline__ void load8(size_t k, u64* x) const {
+        for (int e = 0; e < 8; e++) x[e] = (*this)(k + e);
+    }
+};
+
+template <int LOGSZ, int SUBS>
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+    rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+            const u64* __restrict__ tws, const u64* __restrict__ X, const u64* __restrict__ tab,
+            u64* __restrict__ Yt) {
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.y / level, i = blockIdx.y % level;
+    const size_t N = (size_t)1 << logN;
+    const u64 q = primes[i].q;
+    LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2]};
+    StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, q, 0, 0};
+    PassGeo<LOGSZ, MODE_COLS, SUBS> G;
+    G.init(logN, N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+}
+
+struct StRescale {
+    u64* __restrict__ out;
+    const u64* __restrict__ a;
+    u64 q, c, cs;
+    __device__ __forceinline__ u64 one(size_t k, u64 y) const {
+        y = y >= 2 * q ? y - 2 * q : y;
+        y = y >= q ? y - q : y;
+        return mul_shoup(a[k] + q - y, c, cs, q);
+    }
+    __device__ __forceinline__ void operator()(size_t k, u64 y) const { out[k] = one(k, y); }
+    __device__ __forceinline__ void store8(size_t k, const u64* y) const {
+        ulonglong2* o = reinterpret_cast<ulonglong2*>(out + k);
+#pragma unroll
+        for (int v = 0; v < 4; v++) o[v] = make_ulonglong2(one(k + 2 * v, y[2 * v]), one(k + 2 * v + 1, y[2 * v + 1]));
+    }
+};
+
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
+    rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
+              const u64* __restrict__ tws, const u64* __restrict__ Yt, const u64* __restrict__ a,
+              const u64* __restrict__ tab, u64* __restrict__ out) {
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.y / level, i = blockIdx.y % level;
+    const size_t N = (size_t)1 << logN;
+    const u64 q = primes[i].q;
+    LdPlain ld{Yt + ((size_t)s * level + i) * N};
+    StRescale st{out + ((size_t)s * level + i) * N, a + ((size_t)s * (level + 1) + i) * N, q, tab[3 * i],
+                 tab[3 * i + 1]};
+    PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
+    G.init(logN, N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+typedef unsigned __int128 u128;
+static u64 mulm(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+static u64 shoup_of(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+static u64 powm(u64 b, u64 e, u64 q) {
+    u64 r = 1;
+    b %= q;
+    while (e) { if (e & 1) r = mulm(r, b, q); b = mulm(b, b, q); e >>= 1; }
+    return r;
+}
+
+template <class K>
+static void set_smem(K kern, size_t bytes, bool& done) {
+    if (!done) {
+        HC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        done = true;
+    }
+}
+
+// column-pass geometry per ring degree
+template <int LOGN>
+struct ColCfg;
+template <> struct ColCfg<14> { static constexpr int LOGSZ = 5, SUBS = 64; };
+template <> struct ColCfg<15> { static constexpr int LOGSZ = 6, SUBS = 32; };
+template <> struct ColCfg<16> { static constexpr int LOGSZ = 7, SUBS = 16; };
+template <> struct ColCfg<17> { static constexpr int LOGSZ = 8, SUBS = 8; };
+
+template <int LOGN>
+static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out,
+                              const u64* addend, int add_npoly, u64 add_gal) {
+    constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
+    using CG = PassGeo<CL, MODE_COLS, CS>;
+    using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
+    const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
+    KsGeo g{level, nl, nt, c.L, K, c.alpha, c.dnum, c.nall, (nl + c.alpha - 1) / c.alpha, c.logN, N >> CH_LOG};
+    const size_t csm = sizeof(u64) * CG::smem_words(), hsm = sizeof(u64) * HG::smem_words();
+
+    // 1. Y = INTT(sigma(d)) * (Q'/q_i)^-1
+    u64* Y = c.alloc((size_t)nl * N);
+    {
+        JobList j;
+        j.n = nl;
+        j.custom = 1;
+        j.galois = gal;
+        for (int i = 0; i < nl; i++) {
+            const int dj = i / c.alpha, lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
+            const u64 qi = c.pr[i].q;
+            u64 qh = 1;
+            for (int b = lo; b < hi; b++) if (b != i) qh = mulm(qh, c.pr[b].q % qi, qi);
+            const u64 sc = mulm(c.pr[i].ninv, powm(qh, qi - 2, qi), qi);
+            j.prime[i] = i;
+            j.ptr[i] = Y + (size_t)i * N;
+            j.src[i] = d + (size_t)i * N;
+            j.scale[i] = sc;
+            j.scale_s[i] = shoup_of(sc, qi);
+        }
+        ntt_inverse(c, j);
+    }
+    // 2. A: conversion + column pass for every (digit, non-digit target)
+    u64* I = c.alloc((size_t)g.beta * nt * N);
+    {
+        KsJobs jobs;
+        jobs.n = 0;
+        for (int dj = 0; dj < g.beta; dj++) {
+            const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
+            for (int t = 0; t < nt; t++) {
+                if (t >= lo && t < hi) continue;
+                jobs.digit[jobs.n] = (unsigned char)dj;
+                jobs.t[jobs.n] = (unsigned char)t;
+                jobs.n++;
+            }
+        }
+        static bool at = false;
+        set_smem(ks_modup_cols<CL, CS>, csm, at);
+        Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + 2.0 * jobs.n));
+        dim3 grid((N >> CL) / CS, jobs.n);
+        ks_modup_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.d_tw, c.d_tws, Y,
+                                                                    c.d_modup, I);
+        HC_CUDA(cudaGetLastError());
+    }
+    c.free(Y);
+    // 3. B: chunk pass + key inner product -> ACC [2][nt][N]
+    u64* ACC = c.alloc((size_t)2 * nt * N);
+    {
+        static bool at = false;
+        set_smem(ks_chunks_keyprod, hsm, at);
+        const double inb = (double)g.beta * nt - nl + nl;      // I limbs + in-digit d limbs
+        Launch scope(c, "ks_chunks_keyprod", 8.0 * N * (inb + 2.0 * g.beta * nt + 2.0 * nt));
+        dim3 grid((N >> CH_LOG) / CH_SUBS, nt);
+        ks_chunks_keyprod<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, I, d, gal, key.d,
+                                                                ACC);
+        HC_CUDA(cudaGetLastError());
+    }
+    c.free(I);
+    // 4. INTT of the P limbs, final scale N^-1 (P/p_t)^-1 (in place)
+    {
+        JobList j;
+        j.n = 0;
+        j.custom = 1;
+        for (int s = 0; s < 2; s++)
+            for (int t = 0; t < K; t++) {
+                const int pi = c.L + 1 + t;
+                const u64 p = c.pr[pi].q;
+                u64 ph = 1;
+                for (int b = 0; b < K; b++) if (b != t) ph = mulm(ph, c.pr[c.L + 1 + b].q % p, p);
+                const u64 sc = mulm(c.pr[pi].ninv, powm(ph, p - 2, p), p);
+                j.prime[j.n] = pi;
+                j.ptr[j.n] = ACC + ((size_t)s * nt + nl + t) * N;
+                j.src[j.n] = nullptr;
+                j.scale[j.n] = sc;
+                j.scale_s[j.n] = shoup_of(sc, p);
+                j.n++;
+            }
+        ntt_inverse(c, j);
+    }
+    // 5. D: P -> Q conversion + column pass
+    u64* Wt = c.alloc((size_t)2 * nl * N);
+    {
+        static bool at = false;
+        set_smem(ks_moddown_cols<CL, CS>, csm, at);
+        Launch scope(c, "ks_moddown_cols", 8.0 * N * (2.0 * K + 2.0 * nl));
+        dim3 grid((N >> CL) / CS, 2 * nl);
+        ks_moddown_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, ACC,
+                                                                      c.d_moddown, Wt);
+        HC_CUDA(cudaGetLastError());
+    }
+    // 6. E: chunk pass + (ACC - W) P^-1 + addend
+    {
+        static bool at = false;
+        set_smem(ks_moddown_chunks, hsm, at);
+        Launch scope(c, "ks_moddown_chunks", 8.0 * N * (2.0 * nl * 3 + (double)add_npoly * nl));
+        dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl);
+        ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, Wt, ACC, c.d_pinv,
+                                                                addend, add_npoly, add_gal, out);
+        HC_CUDA(cudaGetLastError());
+    }
+    c.free(Wt);
+    c.free(ACC);
+}
+
+bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
+                     int add_npoly, u64 add_gal) {
+    switch (c.logN) {
+        case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
+        case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
+        case 16: keyswitch_fused_t<16>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
+        case 17: keyswitch_fused_t<17>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
+        default: return false;
+    }
+}
+
+template <int LOGN>
+static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+    constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
+    using CG = PassGeo<CL, MODE_COLS, CS>;
+    using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
+    const int N = c.N;
+    u64* X = c.alloc((size_t)npoly * N);
+    JobList j;
+    j.n = npoly;
+    for (int s = 0; s < npoly; s++) {
+        j.prime[s] = level;
+        j.ptr[s] = X + (size_t)s * N;
+        j.src[s] = a + ((size_t)s * (level + 1) + level) * N;
+    }
+    ntt_inverse(c, j);
+    u64* Yt = c.alloc((size_t)npoly * level * N);
+    const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
+    const size_t csm = sizeof(u64) * CG::smem_words(), hsm = sizeof(u64) * HG::smem_words();
+    const int N1 = N >> CH_LOG;
+    {
+        static bool at = false;
+        set_smem(rs_cols<CL, CS>, csm, at);
+        Launch scope(c, "rs_cols", 8.0 * N * npoly * (1.0 + level));
+        dim3 grid((N >> CL) / CS, npoly * level);
+        rs_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(level, c.logN, N1, c.d_primes, c.d_tw, c.d_tws, X,
+                                                              tab, Yt);
+        HC_CUDA(cudaGetLastError());
+    }
+    {
+        static bool at = false;
+        set_smem(rs_chunks, hsm, at);
+        Launch scope(c, "rs_chunks", 8.0 * N * npoly * 3.0 * level);
+        dim3 grid((N >> CH_LOG) / CH_SUBS, npoly * level);
+        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.d_tw, c.d_tws, Yt, a, tab,
+                                                        out);
+        HC_CUDA(cudaGetLastError());
+    }
+    c.free(X);
+    c.free(Yt);
+}
+
+bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+    switch (c.logN) {
+        case 14: rescale_fused_t<14>(c, a, level, npoly, out); return true;
+        case 15: rescale_fused_t<15>(c, a, level, npoly, out); return true;
+        case 16: rescale_fused_t<16>(c, a, level, npoly, out); return true;
+        case 17: rescale_fused_t<17>(c, a, level, npoly, out); return true;
+        default: return false;
+    }
+}
+
+}  // namespace hc

@@ -160,6 +160,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     const int N = c->N, M = N / 2, nall = c->nall, L = c->L, K = c->K;
     HC_CUDA(cudaSetDevice(device));
     HC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->main_stream = c->stream;
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -345,8 +346,11 @@ void ctx_destroy(Ctx* c) {
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
     cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
     cudaStreamSynchronize(c->stream);
+    for (auto s : c->side) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    for (auto e : c->side_ev) cudaEventDestroy(e);
+    if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     cudaMemPoolDestroy(c->pool);
-    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->main_stream);
     delete c;
 }
 
@@ -385,6 +389,8 @@ Key& get_key(Ctx& c, int gid) {
     }
     c.free((u64*)e);
     c.free(sp);
+    // other streams may use the key right after this returns
+    HC_CUDA(cudaStreamSynchronize(c.stream));
     return c.keys.emplace(gid, k).first->second;
 }
 

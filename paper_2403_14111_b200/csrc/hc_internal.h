@@ -80,7 +80,14 @@ struct Ctx {
     u64 seed;
     int device;
     int grid_rows = 0;            // s0 of the slot grid (EmulatorContext.grid_rows)
+    // `stream` is the stream every launch / allocation goes to.  It is the
+    // context's main stream except inside a schedule's fork region, where it
+    // temporarily names one of the side streams (see schedules.cu Fork).
     cudaStream_t stream = nullptr;
+    cudaStream_t main_stream = nullptr;
+    std::vector<cudaStream_t> side;
+    std::vector<cudaEvent_t> side_ev;
+    cudaEvent_t fork_ev = nullptr;
     cudaMemPool_t pool = nullptr;
     PrimeHost pr[MAXP];
     double scale[MAXP];

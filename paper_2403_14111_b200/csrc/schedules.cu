@@ -3,8 +3,10 @@
 // the order the reference's EncodedMatrix.map_blocks / _zip evaluate them,
 // and every composite expression is split into explicit steps so the op
 // order (and therefore the refresh-nonce sequence) is the reference's.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "schedules.h"
 
@@ -12,6 +14,65 @@ namespace hc {
 
 using G = std::vector<CtP>;
 using cd = std::complex<double>;
+
+// Fork/join of independent schedule branches (the c/2 diagonal passes) onto
+// side streams.  Branch k runs on side stream k % S after waiting for
+// everything the main stream issued before the fork; join() makes the main
+// stream wait for all branches.  Temporaries of a branch are allocated and
+// freed on its stream; branch results outlive the join and are freed on the
+// main stream afterwards.  The op sequence (and therefore every residue) is
+// unchanged: only the host-side issue order interleaves.
+struct Fork {
+    Ctx& c;
+    int S;
+    std::vector<char> used;
+    Fork(Ctx& ctx, int nstreams) : c(ctx), S(nstreams < 1 ? 1 : nstreams), used(S, 0) {
+        while ((int)c.side.size() < S) {
+            cudaStream_t s;
+            HC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            c.side.push_back(s);
+            cudaEvent_t e;
+            HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c.side_ev.push_back(e);
+        }
+        if (!c.fork_ev) HC_CUDA(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
+        HC_CUDA(cudaEventRecord(c.fork_ev, c.main_stream));
+    }
+    void enter(int k) {
+        const int s = k % S;
+        if (!used[s]) {
+            HC_CUDA(cudaStreamWaitEvent(c.side[s], c.fork_ev, 0));
+            used[s] = 1;
+        }
+        c.stream = c.side[s];
+    }
+    void leave() { c.stream = c.main_stream; }
+    void join() {
+        c.stream = c.main_stream;
+        for (int s = 0; s < S; s++) {
+            if (!used[s]) continue;
+            HC_CUDA(cudaEventRecord(c.side_ev[s], c.side[s]));
+            HC_CUDA(cudaStreamWaitEvent(c.main_stream, c.side_ev[s], 0));
+            used[s] = 0;
+        }
+    }
+    ~Fork() {
+        if (c.stream != c.main_stream) c.stream = c.main_stream;
+        for (int s = 0; s < S; s++)
+            if (used[s]) {
+                cudaEventRecord(c.side_ev[s], c.side[s]);
+                cudaStreamWaitEvent(c.main_stream, c.side_ev[s], 0);
+            }
+    }
+};
+
+static int fork_width(int branches) {
+    static int cap = [] {
+        const char* e = std::getenv("HC_STREAMS");
+        return e ? std::atoi(e) : 8;
+    }();
+    return std::max(1, std::min(branches, cap));
+}
 
 static int ilog2(int n) {
     int l = 0;
@@ -188,19 +249,26 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     for (int q = 0; q < n; q++) mi[q] = ev.mul_i(rolled[q]);
     G packed(n);
     for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], mi[q]);
-    G acc;
-    for (int k = 0; k < c / 2; k++) {
-        G shifted = rot_up(ev, packed, k, g);
-        G prod((size_t)m * n);
-        for (int p = 0; p < m; p++)
-            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted[q]);
-        G sums = col_sums(ev, prod, m, n, g);
-        const Pattern mask = diag_mask(g, k, c, true, scale);
-        G term(m);
-        for (int p = 0; p < m; p++) term[p] = ev.mult_p(sums[p], mask);
-        if (k == 0) acc = term;
-        else for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], term[p]);
+    std::vector<G> terms(c / 2);
+    {
+        Fork fork(ev.c, fork_width(c / 2));
+        for (int k = 0; k < c / 2; k++) {
+            fork.enter(k);
+            G shifted = rot_up(ev, packed, k, g);
+            G prod((size_t)m * n);
+            for (int p = 0; p < m; p++)
+                for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted[q]);
+            G sums = col_sums(ev, prod, m, n, g);
+            const Pattern mask = diag_mask(g, k, c, true, scale);
+            terms[k].resize(m);
+            for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(sums[p], mask);
+            fork.leave();
+        }
+        fork.join();
     }
+    G acc = terms[0];
+    for (int k = 1; k < c / 2; k++)
+        for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], terms[k][p]);
     G cj(m);
     for (int p = 0; p < m; p++) cj[p] = ev.conj(acc[p]);
     for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], cj[p]);
@@ -232,25 +300,33 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     for (int p = 0; p < m; p++) mi[p] = ev.mul_i(rl[p]);
     G packed(m);
     for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], mi[p]);
-    G acc;
-    for (int k = 0; k < c / 2; k++) {
-        G left, right;
-        if (partial) {
-            left.resize(m);
-            for (int p = 0; p < m; p++) left[p] = ev.lrot(packed[p], k);
-            right = prot_up(ev, B, k, g);
-        } else {
-            left = rot_left(ev, packed, k, g);
-            right = B;
+    std::vector<G> terms(c / 2);
+    {
+        // with a cross-rank reducer the passes stay serial (collectives in a fixed order)
+        Fork fork(ev.c, red ? 1 : fork_width(c / 2));
+        for (int k = 0; k < c / 2; k++) {
+            fork.enter(k);
+            G left, right;
+            if (partial) {
+                left.resize(m);
+                for (int p = 0; p < m; p++) left[p] = ev.lrot(packed[p], k);
+                right = prot_up(ev, B, k, g);
+            } else {
+                left = rot_left(ev, packed, k, g);
+                right = B;
+            }
+            G prod = colwise(left, right);
+            G sums = row_sums(ev, prod, m, n, g, red);
+            const Pattern mask = diag_mask(g, -k, c, true, scale);
+            terms[k].resize(n);
+            for (int q = 0; q < n; q++) terms[k][q] = ev.mult_p(sums[q], mask);
+            fork.leave();
         }
-        G prod = colwise(left, right);
-        G sums = row_sums(ev, prod, m, n, g, red);
-        const Pattern mask = diag_mask(g, -k, c, true, scale);
-        G term(n);
-        for (int q = 0; q < n; q++) term[q] = ev.mult_p(sums[q], mask);
-        if (k == 0) acc = term;
-        else for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], term[q]);
+        fork.join();
     }
+    G acc = terms[0];
+    for (int k = 1; k < c / 2; k++)
+        for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], terms[k][q]);
     G cj(n);
     for (int q = 0; q < n; q++) cj[q] = ev.conj(acc[q]);
     for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], cj[q]);

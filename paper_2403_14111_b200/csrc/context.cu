@@ -182,7 +182,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
         }
     }
     std::vector<PrimeDev> pd(nall);
-    std::vector<u64> tw((size_t)nall * N), tws((size_t)nall * N), itw((size_t)nall * N), itws((size_t)nall * N);
+    std::vector<u64> tw((size_t)2 * nall * N), itw((size_t)2 * nall * N);
     for (int i = 0; i < nall; i++) {
         PrimeHost& p = c->pr[i];
         const u64 q = used[i];
@@ -203,14 +203,16 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
         for (int k = 1; k < N; k++) { pw[k] = mulm(pw[k - 1], p.psi, q); ipw[k] = mulm(ipw[k - 1], p.ipsi, q); }
         for (int k = 0; k < N; k++) {
             const unsigned r = brv((unsigned)k, logN);
-            tw[(size_t)i * N + k] = pw[r];
-            tws[(size_t)i * N + k] = shoup_of(pw[r], q);
-            itw[(size_t)i * N + k] = ipw[r];
-            itws[(size_t)i * N + k] = shoup_of(ipw[r], q);
+            // (w, w_shoup) pairs: one 16-byte load per twiddle in the NTT passes
+            tw[2 * ((size_t)i * N + k)] = pw[r];
+            tw[2 * ((size_t)i * N + k) + 1] = shoup_of(pw[r], q);
+            itw[2 * ((size_t)i * N + k)] = ipw[r];
+            itw[2 * ((size_t)i * N + k) + 1] = shoup_of(ipw[r], q);
         }
     }
     c->d_primes = upload(*c, pd);
-    c->d_tw = upload(*c, tw); c->d_tws = upload(*c, tws); c->d_itw = upload(*c, itw); c->d_itws = upload(*c, itws);
+    c->d_tw = upload(*c, tw);
+    c->d_itw = upload(*c, itw);
 
     // canonical scales
     c->scale[L] = std::ldexp(1.0, log_scale);
@@ -342,7 +344,7 @@ void ctx_destroy(Ctx* c) {
     cudaStreamSynchronize(c->stream);
     c->pt_cache.clear();
     for (auto& kv : c->keys) cudaFree(kv.second.d);
-    cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_tws); cudaFree(c->d_itw); cudaFree(c->d_itws);
+    cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
     cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
     cudaStreamSynchronize(c->stream);

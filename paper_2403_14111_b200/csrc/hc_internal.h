@@ -93,7 +93,10 @@ struct Ctx {
     double scale[MAXP];
     // device tables
     PrimeDev* d_primes = nullptr;
-    u64 *d_tw = nullptr, *d_tws = nullptr, *d_itw = nullptr, *d_itws = nullptr;   // [nall][N]
+    u64 *d_tw = nullptr, *d_itw = nullptr;   // [nall][N][2]: (psi^brv(k), shoup) and inverse
+    const ulonglong2* twp(int prime, bool inv) const {
+        return reinterpret_cast<const ulonglong2*>(inv ? d_itw : d_tw) + (size_t)prime * N;
+    }
     u64* d_cdt = nullptr;
     int cdt_n = 0, cdt_b = 0;
     u64 cdt_host[128];

@@ -65,8 +65,7 @@ struct LdModup {
 
 template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
-    ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-                  const u64* __restrict__ tws, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
+    ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
     extern __shared__ u64 sm[];
     const int job = blockIdx.y;
@@ -85,8 +84,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     LdModup ld{Y, cf, lo, hi - lo, p, N};
     StPlain<false, false> st{I + ((size_t)j * g.nt + t) * N, p, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
-    G.init(g.logN, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)pi * N, tws + (size_t)pi * N, p, ld, st);
+    G.init(g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)pi << g.logN),  p, ld, st);
 }
 
 // ---- B: chunk pass + key inner product ------------------------------------
@@ -101,8 +100,7 @@ struct StCapture {
 };
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, 2)
-    ks_chunks_keyprod(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-                      const u64* __restrict__ tws, const u64* __restrict__ I, const u64* __restrict__ d, u64 gal,
+    ks_chunks_keyprod(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ I, const u64* __restrict__ d, u64 gal,
                       const u64* __restrict__ key, u64* __restrict__ acc) {
     using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     extern __shared__ u64 sm[];
@@ -111,7 +109,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const size_t N = (size_t)1 << g.logN;
     const PrimeDev P = primes[pi];
     PG G;
-    G.init(g.logN, g.N1);
+    G.init(g.N1);
     const size_t k0 = G.gidx(G.lt * 8);     // this thread's 8 consecutive output coefficients
     U128 a0[8], a1[8];
 #pragma unroll
@@ -120,13 +118,18 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     for (int j = 0; j < g.beta; j++) {
         const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
         if (t >= lo && t < hi) {
-            LdGalois ld{d + (size_t)t * N, g.logN, gal};
-            ld.load8(k0, x);
+            if (gal) {
+                LdGalois ld{d + (size_t)t * N, g.logN, gal};
+                ld.load8(k0, x);
+            } else {
+                LdPlain ld{d + (size_t)t * N};
+                ld.load8(k0, x);
+            }
         } else {
             __syncthreads();
             LdPlain ld{I + ((size_t)j * g.nt + t) * N};
             StCapture st{x};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)pi * N, tws + (size_t)pi * N, P.q, ld,
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)pi << g.logN),  P.q, ld,
                                                           st);
         }
         const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0;
@@ -173,8 +176,7 @@ struct LdModdown {
 
 template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
-    ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-                    const u64* __restrict__ tws, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
+    ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
@@ -189,8 +191,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     LdModdown ld{acc + ((size_t)s * g.nt + g.nl) * N, cf, g.K, q, N};
     StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
-    G.init(g.logN, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+    G.init(g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)i << g.logN),  q, ld, st);
 }
 
 // ---- E: chunk pass with the ModDown combine in its stores ------------------
@@ -220,8 +222,7 @@ struct StModdown {
 };
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
-    ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-                      const u64* __restrict__ tws, const u64* __restrict__ Wt, const u64* __restrict__ acc,
+    ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly, u64 add_gal,
                       u64* __restrict__ out) {
     extern __shared__ u64 sm[];
@@ -233,8 +234,8 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
                  (s < add_npoly) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
                  add_gal, g.logN};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
-    G.init(g.logN, g.N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+    G.init(g.N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)i << g.logN),  q, ld, st);
 }
 
 // ---- fused rescale (R1: bcast in the column pass, R2: combine in the chunk pass)
@@ -253,8 +254,7 @@ struct LdBcast {
 
 template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
-    rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-            const u64* __restrict__ tws, const u64* __restrict__ X, const u64* __restrict__ tab,
+    rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
             u64* __restrict__ Yt) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2]};
     StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
-    G.init(logN, N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+    G.init(N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)i << logN),  q, ld, st);
 }
 
 struct StRescale {
@@ -285,8 +285,7 @@ struct StRescale {
 };
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
-    rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-              const u64* __restrict__ tws, const u64* __restrict__ Yt, const u64* __restrict__ a,
+    rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, const u64* __restrict__ a,
               const u64* __restrict__ tab, u64* __restrict__ out) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
@@ -296,8 +295,8 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     StRescale st{out + ((size_t)s * level + i) * N, a + ((size_t)s * (level + 1) + i) * N, q, tab[3 * i],
                  tab[3 * i + 1]};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
-    G.init(logN, N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + (size_t)i * N, tws + (size_t)i * N, q, ld, st);
+    G.init(N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)i << logN),  q, ld, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -379,7 +378,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         set_smem(ks_modup_cols<CL, CS>, csm, at);
         Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + 2.0 * jobs.n));
         dim3 grid((N >> CL) / CS, jobs.n);
-        ks_modup_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.d_tw, c.d_tws, Y,
+        ks_modup_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y,
                                                                     c.d_modup, I);
         HC_CUDA(cudaGetLastError());
     }
@@ -392,7 +391,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         const double inb = (double)g.beta * nt - nl + nl;      // I limbs + in-digit d limbs
         Launch scope(c, "ks_chunks_keyprod", 8.0 * N * (inb + 2.0 * g.beta * nt + 2.0 * nt));
         dim3 grid((N >> CH_LOG) / CH_SUBS, nt);
-        ks_chunks_keyprod<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, I, d, gal, key.d,
+        ks_chunks_keyprod<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), I, d, gal, key.d,
                                                                 ACC);
         HC_CUDA(cudaGetLastError());
     }
@@ -425,7 +424,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         set_smem(ks_moddown_cols<CL, CS>, csm, at);
         Launch scope(c, "ks_moddown_cols", 8.0 * N * (2.0 * K + 2.0 * nl));
         dim3 grid((N >> CL) / CS, 2 * nl);
-        ks_moddown_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, ACC,
+        ks_moddown_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.twp(0, false), ACC,
                                                                       c.d_moddown, Wt);
         HC_CUDA(cudaGetLastError());
     }
@@ -435,7 +434,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         set_smem(ks_moddown_chunks, hsm, at);
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (2.0 * nl * 3 + (double)add_npoly * nl));
         dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl);
-        ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.d_tw, c.d_tws, Wt, ACC, c.d_pinv,
+        ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
                                                                 addend, add_npoly, add_gal, out);
         HC_CUDA(cudaGetLastError());
     }
@@ -478,7 +477,7 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
         set_smem(rs_cols<CL, CS>, csm, at);
         Launch scope(c, "rs_cols", 8.0 * N * npoly * (1.0 + level));
         dim3 grid((N >> CL) / CS, npoly * level);
-        rs_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(level, c.logN, N1, c.d_primes, c.d_tw, c.d_tws, X,
+        rs_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), X,
                                                               tab, Yt);
         HC_CUDA(cudaGetLastError());
     }
@@ -487,7 +486,7 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
         set_smem(rs_chunks, hsm, at);
         Launch scope(c, "rs_chunks", 8.0 * N * npoly * 3.0 * level);
         dim3 grid((N >> CH_LOG) / CH_SUBS, npoly * level);
-        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.d_tw, c.d_tws, Yt, a, tab,
+        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), Yt, a, tab,
                                                         out);
         HC_CUDA(cudaGetLastError());
     }

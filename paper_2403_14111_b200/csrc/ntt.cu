@@ -27,28 +27,28 @@ namespace hc {
 
 template <int LOGSZ, int MODE, int SUBS, bool INV>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS)
-    ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const u64* __restrict__ tw,
-               const u64* __restrict__ tws, int logN, int N1, int use_src, int last) {
+    ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
+               int N1, int use_src, int last) {
     extern __shared__ u64 sm[];
     const int job = blockIdx.y;
     const int pidx = jobs.prime[job];
     const u64* src = (use_src && jobs.src[job]) ? jobs.src[job] : jobs.ptr[job];
     u64* dst = jobs.ptr[job];
     const PrimeDev P = primes[pidx];
-    const size_t N = (size_t)1 << logN;
-    const u64* W = tw + (size_t)pidx * N;
-    const u64* Ws = tws + (size_t)pidx * N;
+    const ulonglong2* TW = tw + ((size_t)pidx << logN);
     PassGeo<LOGSZ, MODE, SUBS> G;
-    G.init(logN, N1);
-    LdGalois ld{src, logN, use_src ? jobs.galois : 0};
-    if (last) {
-        u64 c = P.ninv, cs = P.ninv_s;
-        if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
-        StPlain<INV, true> st{dst, P.q, c, cs};
-        ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, W, Ws, P.q, ld, st);
+    G.init(N1);
+    const u64 gal = use_src ? jobs.galois : 0;
+    u64 c = P.ninv, cs = P.ninv_s;
+    if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
+    if (gal) {
+        LdGalois ld{src, logN, gal};
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
     } else {
-        StPlain<INV, false> st{dst, P.q, 0, 0};
-        ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, W, Ws, P.q, ld, st);
+        LdPlain ld{src};
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
     }
 }
 
@@ -70,13 +70,12 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
     }
     Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n);
     if (inv)
-        ntt_kernel<LOGSZ, MODE, SUBS, true><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes, c.d_itw,
-                                                                                  c.d_itws, c.logN, N1, use_src,
-                                                                                  last);
+        ntt_kernel<LOGSZ, MODE, SUBS, true><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes, c.twp(0, true),
+                                                                                  c.logN, N1, use_src, last);
     else
-        ntt_kernel<LOGSZ, MODE, SUBS, false><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes, c.d_tw,
-                                                                                   c.d_tws, c.logN, N1, use_src,
-                                                                                   last);
+        ntt_kernel<LOGSZ, MODE, SUBS, false><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes,
+                                                                                   c.twp(0, false), c.logN, N1,
+                                                                                   use_src, last);
     HC_CUDA(cudaGetLastError());
 }
 

@@ -3,33 +3,37 @@
 // first round's loads and consumers (key inner product, ModDown combine,
 // rescale combine) inside the last round's stores.  See ntt.cu for the
 // decomposition and conventions.
+//
+// Instruction economy (the pass is issue-bound on sm_100a): twiddles are
+// stored as (w, w_shoup) pairs and fetched with one 16-byte load; every
+// per-element address inside a butterfly group is base + m * stride with a
+// compile-time stride (column stride 2^9, shared-memory padding of one word
+// per 8 that stays linear inside a group), so the unrolled loops use
+// immediate offsets.
 #pragma once
 #include "hc_internal.h"
 
 namespace hc {
 
 enum { MODE_FULL = 0, MODE_COLS = 1, MODE_CHUNKS = 2 };
+constexpr int CHUNK_LOG = 9;   // chunk-pass size for split rings; = log2(column stride)
 
-// Geometry of one pass: SUBS sub-transforms of 2^LOGSZ points per CTA.
-//   MODE_COLS  : sub-transform = column c (element pos at c + pos * N2), root R = 1
-//   MODE_CHUNKS: sub-transform = chunk h (element pos at (h << LOGSZ) + pos), root R = N1 + h
-//   MODE_FULL  : the whole limb, root R = 1
 template <int LOGSZ, int MODE, int SUBS>
 struct PassGeo {
     static constexpr int SZ = 1 << LOGSZ;
     static constexpr int TPS = SZ / 8;
     static constexpr int NR = (LOGSZ + 2) / 3;
-    static constexpr int PADSZ = SZ + SZ / 16;
+    static constexpr int PADSZ = SZ + SZ / 8;
     static constexpr int THREADS = SUBS * TPS;
+    static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;   // column stride (MODE_COLS)
     static constexpr size_t smem_words() { return (size_t)SUBS * (MODE == MODE_COLS ? SZ : PADSZ); }
+    static constexpr bool EDGE_CONTIG = (MODE != MODE_COLS) && (LOGSZ % 3 == 0);
     int sub, lt, first_sub, R;
-    size_t N2;
-    __device__ __forceinline__ void init(int logN, int N1) {
+    __device__ __forceinline__ void init(int N1) {
         const int tid = threadIdx.x;
         if (MODE == MODE_COLS) { sub = tid % SUBS; lt = tid / SUBS; }
         else { sub = tid / TPS; lt = tid % TPS; }
         first_sub = blockIdx.x * SUBS;
-        N2 = ((size_t)1 << logN) >> (MODE == MODE_COLS ? LOGSZ : 0);
         R = (MODE == MODE_CHUNKS) ? (N1 + first_sub + sub) : 1;
     }
     __device__ __forceinline__ size_t gidx(int pos) const {
@@ -38,19 +42,21 @@ struct PassGeo {
     }
     __device__ __forceinline__ int sidx(int pos) const {
         if (MODE == MODE_COLS) return pos * SUBS + sub;
-        return sub * PADSZ + pos + (pos >> 4);
+        return sub * PADSZ + pos + (pos >> 3);
     }
-    // positions owned by this thread in the last round (forward) / first round (inverse)
-    static constexpr bool EDGE_CONTIG = (MODE != MODE_COLS) && (LOGSZ % 3 == 0);
+    // strides of element m inside a group whose elements are u apart
+    static constexpr size_t gstep(int u) { return MODE == MODE_COLS ? (size_t)u * N2 : (size_t)u; }
+    static constexpr bool slinear(int u) { return MODE == MODE_COLS || u == 1 || u >= 8; }
+    static constexpr int sstep(int u) { return MODE == MODE_COLS ? u * SUBS : (u == 1 ? 1 : u + u / 8); }
 };
 
 // Runs the pass.  LD: u64 operator()(size_t gidx) and void load8(size_t gidx, u64* x)
 // (8 consecutive words, only used when EDGE_CONTIG).  ST: void operator()(size_t gidx, u64 v)
 // and store8(size_t gidx, const u64* x).  Values handed to ST are lazy: [0, 4q) forward,
-// [0, 2q) inverse.
+// [0, 2q) inverse.  TW: (w, w_shoup) pairs of this prime.
 template <int LOGSZ, int MODE, int SUBS, bool INV, class LD, class ST>
-__device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm, const u64* __restrict__ W,
-                                         const u64* __restrict__ Ws, u64 q, LD& ld, ST& st) {
+__device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm,
+                                         const ulonglong2* __restrict__ TW, u64 q, LD& ld, ST& st) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const u64 twoq = 2 * q;
     u64 x[8];
@@ -60,40 +66,42 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
         const int s0 = 3 * fr;
         const int r = (LOGSZ - s0) < 3 ? (LOGSZ - s0) : 3;
         const int logu = LOGSZ - s0 - r;
+        const int u = 1 << logu;
         const int NG = 8 >> r;
         const int GS = 1 << r;
         // ---- load ----
 #pragma unroll
         for (int j = 0; j < NG; j++) {
             const int g = G.lt + j * PG::TPS;
-            const int blk = g >> logu, o = g & ((1 << logu) - 1);
-            const int base = (blk << (logu + r)) + o;
-            if (rd == 0 && PG::EDGE_CONTIG && logu == 0 && r == 3) {
-                ld.load8(G.gidx(base), x + 8 * j);
+            const int base = ((g >> logu) << (logu + r)) + (g & (u - 1));
+            if (rd == 0) {
+                const size_t gb = G.gidx(base);
+                if (PG::EDGE_CONTIG && logu == 0 && r == 3) ld.load8(gb, x + 8 * j);
+                else {
+#pragma unroll
+                    for (int m = 0; m < GS; m++) x[j * GS + m] = ld(gb + m * PG::gstep(u));
+                }
+            } else if (PG::slinear(u)) {
+                const u64* sp = sm + G.sidx(base);
+#pragma unroll
+                for (int m = 0; m < GS; m++) x[j * GS + m] = sp[m * PG::sstep(u)];
             } else {
 #pragma unroll
-                for (int m = 0; m < GS; m++) {
-                    const int pos = base + (m << logu);
-                    x[j * GS + m] = (rd == 0) ? ld(G.gidx(pos)) : sm[G.sidx(pos)];
-                }
+                for (int m = 0; m < GS; m++) x[j * GS + m] = sm[G.sidx(base + (m << logu))];
             }
         }
-        // ---- twiddles for the round, loaded up front ----
-        u64 tw_r[7], tws_r[7];
+        // ---- twiddles for the round, one 16-byte load each, issued up front ----
+        ulonglong2 tw_r[7];
         {
             int n = 0;
 #pragma unroll
             for (int j = 0; j < NG; j++) {
-                const int blk = (G.lt + j * PG::TPS) >> logu;
+                const int B0 = G.R * (1 << s0) + ((G.lt + j * PG::TPS) >> logu);
 #pragma unroll
                 for (int qq = 0; qq < r; qq++) {
+                    const ulonglong2* tp = TW + (B0 << qq);
 #pragma unroll
-                    for (int sb = 0; sb < (1 << qq); sb++) {
-                        const int widx = G.R * (1 << (s0 + qq)) + (blk << qq) + sb;
-                        tw_r[n] = __ldg(W + widx);
-                        tws_r[n] = __ldg(Ws + widx);
-                        n++;
-                    }
+                    for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
                 }
             }
         }
@@ -109,10 +117,10 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const int k = gbase + ((1 << qq) - 1) + (m1 >> (r - qq));
+                        const ulonglong2 w = tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))];
                         u64 X = y[m1];
                         X = X >= twoq ? X - twoq : X;
-                        const u64 T = mul_shoup_lazy(y[m1 + half], tw_r[k], tws_r[k], q);
+                        const u64 T = mul_shoup_lazy(y[m1 + half], w.x, w.y, q);
                         y[m1] = X + T;
                         y[m1 + half] = X + twoq - T;
                     }
@@ -124,11 +132,11 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const int k = gbase + ((1 << qq) - 1) + (m1 >> (r - qq));
+                        const ulonglong2 w = tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))];
                         const u64 U = y[m1], V = y[m1 + half];
                         const u64 X = U + V;
                         y[m1] = X >= twoq ? X - twoq : X;
-                        y[m1 + half] = mul_shoup_lazy(U + twoq - V, tw_r[k], tws_r[k], q);
+                        y[m1 + half] = mul_shoup_lazy(U + twoq - V, w.x, w.y, q);
                     }
                 }
             }
@@ -138,17 +146,21 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
 #pragma unroll
         for (int j = 0; j < NG; j++) {
             const int g = G.lt + j * PG::TPS;
-            const int blk = g >> logu, o = g & ((1 << logu) - 1);
-            const int base = (blk << (logu + r)) + o;
-            if (last && PG::EDGE_CONTIG && logu == 0 && r == 3) {
-                st.store8(G.gidx(base), x + 8 * j);
+            const int base = ((g >> logu) << (logu + r)) + (g & (u - 1));
+            if (last) {
+                const size_t gb = G.gidx(base);
+                if (PG::EDGE_CONTIG && logu == 0 && r == 3) st.store8(gb, x + 8 * j);
+                else {
+#pragma unroll
+                    for (int m = 0; m < GS; m++) st(gb + m * PG::gstep(u), x[j * GS + m]);
+                }
+            } else if (PG::slinear(u)) {
+                u64* sp = sm + G.sidx(base);
+#pragma unroll
+                for (int m = 0; m < GS; m++) sp[m * PG::sstep(u)] = x[j * GS + m];
             } else {
 #pragma unroll
-                for (int m = 0; m < GS; m++) {
-                    const int pos = base + (m << logu);
-                    if (last) st(G.gidx(pos), x[j * GS + m]);
-                    else sm[G.sidx(pos)] = x[j * GS + m];
-                }
+                for (int m = 0; m < GS; m++) sm[G.sidx(base + (m << logu))] = x[j * GS + m];
             }
         }
         if (!last) __syncthreads();
@@ -194,13 +206,12 @@ __device__ __forceinline__ unsigned galois_src(unsigned j, int logN, u64 g) {
     return __brev((unsigned)((e2 - 1) >> 1)) >> (32 - logN);
 }
 
-// gather loader for the automorphism fused into a pass (g == 0: identity)
+// gather loader for the automorphism fused into a pass
 struct LdGalois {
     const u64* __restrict__ p;
     int logN;
     u64 g;
     __device__ __forceinline__ u64 operator()(size_t i) const {
-        if (!g) return p[i];
         const size_t mask = ((size_t)1 << logN) - 1;
         return p[(i & ~mask) + galois_src((unsigned)(i & mask), logN, g)];
     }

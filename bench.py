@@ -232,12 +232,15 @@ def run_b200(args, world, rank, local):
     ms_step = total_ms / args.steps
     value = ms_step / world            # whole job: `world` pairs per step
 
-    # one profiled step: per-kernel CUDA events on the library stream
+    # one profiled step, serialised on one stream so each kernel's CUDA-event
+    # duration is its own (concurrent branches would overlap the intervals)
+    ctx.set_streams(1)
     N.check(L.hc_prof_begin(ctx._h))
     step()
     buf = C.create_string_buffer(1 << 16)
     N.check(L.hc_prof_end(ctx._h, buf, len(buf)))
     prof = json.loads(buf.value.decode())
+    ctx.set_streams(8)
     # time per product in a separate pass
     N.check(L.hc_timer_begin(ctx._h))
     P.diag_abt(EX, EW)

@@ -55,6 +55,8 @@ int hc_ctx_destroy(hc_ctx *ctx);
 int hc_ctx_info(hc_ctx *ctx, uint64_t *moduli, double *scales);
 /* EmulatorContext.grid_rows (emulator.py:144): s0 of the s0 x s1 slot grid */
 int hc_set_grid_rows(hc_ctx *ctx, int grid_rows);
+/* width of the fork/join over independent diagonal passes (1 = one stream) */
+int hc_set_streams(hc_ctx *ctx, int n);
 /* EmulatorContext.auto_bootstrap (emulator.py:132) */
 int hc_set_auto_bootstrap(hc_ctx *ctx, int on);
 /* OpLedger.counts / reset (emulator.py:88-108); counts[HC_NCOUNTS] */

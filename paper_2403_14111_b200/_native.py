@@ -40,6 +40,7 @@ SIGNATURES = {
     "hc_ctx_info": (I, [P, U64P, DP]),
     "hc_set_grid_rows": (I, [P, I]),
     "hc_set_auto_bootstrap": (I, [P, I]),
+    "hc_set_streams": (I, [P, I]),
     "hc_ctx_counts": (I, [P, I64P, I]),
     "hc_ctx_nonce": (I, [P, U64P, U64P]),
     "hc_sync": (I, [P]),

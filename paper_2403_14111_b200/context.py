@@ -227,6 +227,10 @@ class CKKSContext:
     def extra(self):
         return self.ledger.extra()
 
+    def set_streams(self, n: int) -> None:
+        """Fan-out of the native schedules' independent diagonal passes (1 = serial)."""
+        N.check(N.lib().hc_set_streams(self._h, int(n)))
+
     @property
     def nonce(self) -> int:
         v = C.c_uint64()

@@ -76,6 +76,15 @@ int hc_set_grid_rows(hc_ctx* ctx, int grid_rows) {
     return 0;
 }
 
+int hc_set_streams(hc_ctx* ctx, int n) {
+    if (n < 1 || n > 64) {
+        g_err = "stream count must be in [1, 64]";
+        return HC_EPARAM;
+    }
+    ctx->c->fork_cap = n;
+    return 0;
+}
+
 int hc_set_auto_bootstrap(hc_ctx* ctx, int on) {
     ctx->auto_boot = on != 0;
     return 0;

@@ -4,7 +4,9 @@
 // Every choice follows the CKKS spec in DESIGN.md §3; the host encoder is
 // compiled with -ffp-contract=off so its double arithmetic is bit-identical
 // to the oracle's (oracle/ckks_oracle.c) on the same machine.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -161,6 +163,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaSetDevice(device));
     HC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->main_stream = c->stream;
+    if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;

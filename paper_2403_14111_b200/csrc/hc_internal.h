@@ -88,6 +88,7 @@ struct Ctx {
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_ev;
     cudaEvent_t fork_ev = nullptr;
+    int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
     cudaMemPool_t pool = nullptr;
     PrimeHost pr[MAXP];
     double scale[MAXP];

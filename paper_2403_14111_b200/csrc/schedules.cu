@@ -66,13 +66,7 @@ struct Fork {
     }
 };
 
-static int fork_width(int branches) {
-    static int cap = [] {
-        const char* e = std::getenv("HC_STREAMS");
-        return e ? std::atoi(e) : 8;
-    }();
-    return std::max(1, std::min(branches, cap));
-}
+static int fork_width(const Ctx& c, int branches) { return std::max(1, std::min(branches, c.fork_cap)); }
 
 static int ilog2(int n) {
     int l = 0;
@@ -251,7 +245,7 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], mi[q]);
     std::vector<G> terms(c / 2);
     {
-        Fork fork(ev.c, fork_width(c / 2));
+        Fork fork(ev.c, fork_width(ev.c, c / 2));
         for (int k = 0; k < c / 2; k++) {
             fork.enter(k);
             G shifted = rot_up(ev, packed, k, g);
@@ -303,7 +297,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     std::vector<G> terms(c / 2);
     {
         // with a cross-rank reducer the passes stay serial (collectives in a fixed order)
-        Fork fork(ev.c, red ? 1 : fork_width(c / 2));
+        Fork fork(ev.c, red ? 1 : fork_width(ev.c, c / 2));
         for (int k = 0; k < c / 2; k++) {
             fork.enter(k);
             G left, right;

@@ -208,6 +208,35 @@ def test_nag_steps_small12(golden):
     assert np.max(np.abs(w - golden["small_train_snaps"][-1])) < 1e-4
 
 
+def test_nccl_reducer_plumbing(golden):
+    """diag_atb with the multi-GPU reducer on a 1-rank NCCL group: the device
+    residue view, the all-reduce and hc_mod_reduce leave the result unchanged."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_14111_b200 import sharding
+    P = _prod()
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    g = P.CKKSContext("small12", 16, seed=12)
+    rng = np.random.default_rng(1)
+    A, B = rng.uniform(-1, 1, (64, 4)), rng.uniform(-1, 1, (64, 21))
+    GA, GB = P.encode(g, A, "horizontal"), P.encode(g, B)
+    plain = P.diag_atb(GA, GB, scale=0.5)
+    red = P.diag_atb(GA, GB, scale=0.5, reducer=sharding.NcclModReducer())
+    for a, b in zip(plain.flat(), red.flat()):
+        np.testing.assert_array_equal(a.residues(), b.residues())
+    assert np.max(np.abs(P.decode(red) - 0.5 * A.T @ B)) < 1e-3
+    dist.destroy_process_group()
+
+
 @pytest.mark.slow
 def test_config1_diag_abt_full_size(golden):
     """BASELINE config 1 at N=2^16: residues vs the oracle, values vs float64."""

@@ -254,3 +254,59 @@ def test_config1_diag_abt_full_size(golden):
     assert out.level == 9
     # CKKS noise of the 2 x 8-step rotation ladders at Delta = 2^42, dnum = 4
     assert np.max(np.abs(P.decode(out, tol=1e-3) - X @ W.T)) < 1e-3
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("branch,alev", [("rl", None), ("pru", 11)])
+def test_config2_diag_atb_full_size(golden, branch, alev):
+    """BASELINE config 2: (P-Y)^T X at N=2^16, both alignment branches."""
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    PY, X = wl.config2()
+    g, o = P.CKKSContext("cfg1", 128, seed=2), R.OracleCKKSContext("cfg1", 128, seed=2)
+    GA, OA = _enc_pair(g, o, PY, "horizontal", level=alev)
+    g.nonce = o.nonce = 10
+    GX, OX = P.encode(g, X), S.encode(o, X)
+    out = P.diag_atb(GA, GX)
+    ref = S.diag_atb(OA, OX)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden[f"cfg2_{branch}_led"])
+    assert out.level == golden[f"cfg2_{branch}_level"]
+    assert np.max(np.abs(P.decode(out, tol=1e-3) - PY.T @ X)) < 1e-3
+
+
+@pytest.mark.slow
+def test_config3_softmax_full_size(golden):
+    """BASELINE config 3: 128x10 logits in [-128, 128] at N=2^16; residues vs the
+    oracle, max error vs float64 softmax within the paper's Table-5 bound."""
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    Z = wl.config3()
+    g = P.CKKSContext("cfg1", 128, seed=3, auto_bootstrap=True)
+    o = R.OracleCKKSContext("cfg1", 128, seed=3, auto_bootstrap=True)
+    GZ, OZ = _enc_pair(g, o, Z, "horizontal")
+    out = P.a_softmax(GZ)
+    ref = S.a_softmax(OZ)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden["cfg3_led"])
+    got = P.decode(out, tol=1e-3)
+    assert np.max(np.abs(got - golden["cfg3_out"])) < 1e-3          # vs the reference emulator
+    assert np.max(np.abs(got - S.exact_softmax(Z))) < 0.0097         # PAPER.md:1071 (c=10)
+
+
+@pytest.mark.slow
+def test_config4_training_step_full_size(golden):
+    """BASELINE config 4: the first 128-row NAG step at N=2^16 (ledger per step
+    164/101/382/518/4/54), weights vs the reference emulator's first snapshot."""
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    X, y = wl.config4()
+    Y = S.one_hot(y, wl.CLASSES)
+    g = P.CKKSContext("cfg1", 128, seed=4, auto_bootstrap=True)
+    w0 = S.init_weights(wl.CLASSES, X.shape[1], wl.INIT_SEED)
+    W = P.encode(g, w0, "vertical")
+    st = P.TrainState(W, W)
+    P.nag_step(st, P.encode(g, X[:128]), P.encode(g, Y[:128], "horizontal"), wl.LEARNING_RATE, 128)
+    assert _ledger(g) == [518, 101, 164, 382, 4, 54]
+    w1 = P.decode(st.weights, tol=1e-3)
+    assert np.max(np.abs(w1 - golden["cfg4_snaps"][0])) < 1e-3

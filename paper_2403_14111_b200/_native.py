@@ -12,7 +12,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhc_b200.so")
+LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(HERE, "libhc_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 HC_EPARAM, HC_ECUDA, HC_EDEPTH, HC_ELEVEL, HC_EENCODE = -1, -2, -3, -4, -5

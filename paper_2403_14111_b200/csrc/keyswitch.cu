@@ -99,7 +99,12 @@ struct StCapture {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, 2)
+constexpr int KP_MAXB = 4;   // digits handled by the fused key product (dnum <= 4)
+#ifndef KP_MIN_BLOCKS
+#define KP_MIN_BLOCKS 2
+#endif
+
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, KP_MIN_BLOCKS)
     ks_chunks_keyprod(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ I, const u64* __restrict__ d, u64 gal,
                       const u64* __restrict__ key, u64* __restrict__ acc) {
     using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
@@ -111,46 +116,48 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     PG G;
     G.init(g.N1);
     const size_t k0 = G.gidx(G.lt * 8);     // this thread's 8 consecutive output coefficients
-    U128 a0[8], a1[8];
+    // digit values staged in registers; the 128-bit accumulators are then
+    // short-lived (one pair of outputs at a time), which keeps the kernel at
+    // 3 CTAs per SM
+    u64 xs[KP_MAXB][8];
 #pragma unroll
-    for (int e = 0; e < 8; e++) { a0[e] = {0, 0}; a1[e] = {0, 0}; }
-    u64 x[8];
-    for (int j = 0; j < g.beta; j++) {
+    for (int j = 0; j < KP_MAXB; j++) {
+        if (j >= g.beta) break;
         const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
         if (t >= lo && t < hi) {
             if (gal) {
                 LdGalois ld{d + (size_t)t * N, g.logN, gal};
-                ld.load8(k0, x);
+                ld.load8(k0, xs[j]);
             } else {
                 LdPlain ld{d + (size_t)t * N};
-                ld.load8(k0, x);
+                ld.load8(k0, xs[j]);
             }
         } else {
             __syncthreads();
             LdPlain ld{I + ((size_t)j * g.nt + t) * N};
-            StCapture st{x};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)pi << g.logN),  P.q, ld,
-                                                          st);
-        }
-        const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0;
-        const u64* ka = kb + (size_t)g.nall * N;
-        const ulonglong2* kbv = reinterpret_cast<const ulonglong2*>(kb);
-        const ulonglong2* kav = reinterpret_cast<const ulonglong2*>(ka);
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-            const ulonglong2 b = kbv[v], a = kav[v];
-            mac128(a0[2 * v], x[2 * v], b.x);
-            mac128(a0[2 * v + 1], x[2 * v + 1], b.y);
-            mac128(a1[2 * v], x[2 * v], a.x);
-            mac128(a1[2 * v + 1], x[2 * v + 1], a.y);
+            StCapture st{xs[j]};
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)pi << g.logN), P.q, ld, st);
         }
     }
     ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
     ulonglong2* o1 = reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k0);
+    const size_t kstride = (size_t)g.nall * N;
 #pragma unroll
     for (int v = 0; v < 4; v++) {
-        o0[v] = make_ulonglong2(reduce128(a0[2 * v].hi, a0[2 * v].lo, P), reduce128(a0[2 * v + 1].hi, a0[2 * v + 1].lo, P));
-        o1[v] = make_ulonglong2(reduce128(a1[2 * v].hi, a1[2 * v].lo, P), reduce128(a1[2 * v + 1].hi, a1[2 * v + 1].lo, P));
+        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
+#pragma unroll
+        for (int j = 0; j < KP_MAXB; j++) {
+            if (j >= g.beta) break;
+            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0 + 2 * v;
+            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
+            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
+            mac128(b0, xs[j][2 * v], kbv.x);
+            mac128(b1, xs[j][2 * v + 1], kbv.y);
+            mac128(a0, xs[j][2 * v], kav.x);
+            mac128(a1, xs[j][2 * v + 1], kav.y);
+        }
+        o0[v] = make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
+        o1[v] = make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
     }
 }
 
@@ -444,6 +451,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
 
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
                      int add_npoly, u64 add_gal) {
+    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 8 || c.alpha > 8) return false;
     switch (c.logN) {
         case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
         case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;

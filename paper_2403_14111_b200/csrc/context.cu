@@ -164,6 +164,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->main_stream = c->stream;
     if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("HC_KS_SPLIT")) c->ks_split = std::atoi(e);
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;

@@ -89,6 +89,7 @@ struct Ctx {
     std::vector<cudaEvent_t> side_ev;
     cudaEvent_t fork_ev = nullptr;
     int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
+    int ks_split = 1;             // key product as NTT chunk pass + streaming kernel (HC_KS_SPLIT)
     cudaMemPool_t pool = nullptr;
     PrimeHost pr[MAXP];
     double scale[MAXP];
@@ -153,6 +154,7 @@ struct Launch {
 // ---- kernels / launchers (ntt.cu, kernels.cu) ----
 void ntt_forward(Ctx& c, const JobList& jobs);
 void ntt_inverse(Ctx& c, const JobList& jobs);
+void ntt_forward_chunks(Ctx& c, const JobList& jobs);
 
 // ---- context (context.cu) ----
 Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, int alpha,

@@ -161,6 +161,58 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     }
 }
 
+// ---- B (split form): streaming key inner product over NTT-form digits -----
+// UP[j][t] holds NTT(conv_j(t)) for t outside digit j; inside the digit the
+// value is sigma(d)[t] itself, gathered on the fly.  Two coefficients per
+// thread, 16-byte accesses, one Barrett reduction per output.
+
+__global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
+                                                         const u64* __restrict__ UP, const u64* __restrict__ d,
+                                                         u64 gal, const u64* __restrict__ key,
+                                                         u64* __restrict__ acc) {
+    const size_t N = (size_t)1 << g.logN;
+    const size_t half = N >> 1;
+    const size_t total = (size_t)g.nt * half;
+    const size_t kstride = (size_t)g.nall * N;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(v / half);
+        const size_t k = (v - (size_t)t * half) * 2;
+        const int pi = g.prime(t);
+        const PrimeDev P = primes[pi];
+        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
+        for (int j = 0; j < g.beta; j++) {
+            const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
+            u64 x0, x1;
+            if (t >= lo && t < hi) {
+                const u64* src = d + (size_t)t * N;
+                if (gal) {
+                    x0 = src[galois_src((unsigned)k, g.logN, gal)];
+                    x1 = src[galois_src((unsigned)k + 1, g.logN, gal)];
+                } else {
+                    const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(src + k);
+                    x0 = xv.x;
+                    x1 = xv.y;
+                }
+            } else {
+                const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(UP + ((size_t)j * g.nt + t) * N + k);
+                x0 = xv.x;
+                x1 = xv.y;
+            }
+            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k;
+            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
+            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
+            mac128(b0, x0, kbv.x);
+            mac128(b1, x1, kbv.y);
+            mac128(a0, x0, kav.x);
+            mac128(a1, x1, kav.y);
+        }
+        *reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k) =
+            make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
+        *reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k) =
+            make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
+    }
+}
+
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
 struct LdModdown {
@@ -392,7 +444,28 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
     c.free(Y);
     // 3. B: chunk pass + key inner product -> ACC [2][nt][N]
     u64* ACC = c.alloc((size_t)2 * nt * N);
-    {
+    if (c.ks_split) {
+        // split form: finish the NTTs of all (digit, target) limbs in one
+        // launch, then stream the key product
+        JobList j;
+        j.n = 0;
+        for (int dj = 0; dj < g.beta; dj++) {
+            const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
+            for (int t = 0; t < nt; t++) {
+                if (t >= lo && t < hi) continue;
+                j.prime[j.n] = g.prime(t);
+                j.ptr[j.n] = I + ((size_t)dj * nt + t) * N;
+                j.src[j.n] = nullptr;
+                j.n++;
+            }
+        }
+        ntt_forward_chunks(c, j);
+        const size_t work = (size_t)nt * (N / 2);
+        Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * nt + 2.0 * g.beta * nt + 2.0 * nt));
+        int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
+        ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC);
+        HC_CUDA(cudaGetLastError());
+    } else {
         static bool at = false;
         set_smem(ks_chunks_keyprod, hsm, at);
         const double inb = (double)g.beta * nt - nl + nl;      // I limbs + in-digit d limbs

@@ -105,6 +105,13 @@ static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_s
     launch_t<9, MODE_CHUNKS, 4>(c, jobs, inv, N1, use_src, last);
 }
 
+// second half of a split forward NTT (in place), for callers that ran the
+// column pass themselves with a fused producer
+void ntt_forward_chunks(Ctx& c, const JobList& jobs) {
+    if (jobs.n == 0) return;
+    chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 1);
+}
+
 void ntt_forward(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
     if (c.logN <= 13) { full_pass(c, jobs, false); return; }

@@ -355,6 +355,7 @@ void ctx_destroy(Ctx* c) {
     for (auto s : c->side) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
     for (auto e : c->side_ev) cudaEventDestroy(e);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+    for (auto e : c->fork_evs) cudaEventDestroy(e);
     cudaMemPoolDestroy(c->pool);
     cudaStreamDestroy(c->main_stream);
     delete c;

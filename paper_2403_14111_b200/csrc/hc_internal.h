@@ -88,6 +88,9 @@ struct Ctx {
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_ev;
     cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> fork_evs;   // one fork event per nesting depth
+    int fork_depth = 0;
+    int fork_rot[4] = {0, 0, 0, 0};
     int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
     int ks_split = 1;             // key product as NTT chunk pass + streaming kernel (HC_KS_SPLIT)
     cudaMemPool_t pool = nullptr;

@@ -22,12 +22,37 @@ using cd = std::complex<double>;
 // freed on its stream; branch results outlive the join and are freed on the
 // main stream afterwards.  The op sequence (and therefore every residue) is
 // unchanged: only the host-side issue order interleaves.
+//
+// Forks nest: a fork at nesting depth d draws its streams from pool d
+// (FORK_POOL streams each), records its fork event on the stream that was
+// current when it was created (the parent branch's stream) and joins back
+// onto that stream.
+constexpr int FORK_POOL = 32, FORK_DEPTHS = 3;
+
 struct Fork {
     Ctx& c;
-    int S;
+    int S, base;
+    cudaStream_t parent;
+    cudaEvent_t ev;
     std::vector<char> used;
-    Fork(Ctx& ctx, int nstreams) : c(ctx), S(nstreams < 1 ? 1 : nstreams), used(S, 0) {
-        while ((int)c.side.size() < S) {
+    Fork(Ctx& ctx, int nstreams) : c(ctx), used(FORK_POOL, 0) {
+        const int depth = c.fork_depth++;
+        if (depth >= FORK_DEPTHS) {
+            S = 0;                                  // too deep: run inline on the parent stream
+            base = 0;
+        } else {
+            S = std::max(1, std::min(nstreams, FORK_POOL));
+            // nested forks of sibling branches rotate through their pool so
+            // they do not serialise on the same streams
+            int off = 0;
+            if (depth > 0) {
+                off = c.fork_rot[depth];
+                if (off + S > FORK_POOL) off = 0;
+                c.fork_rot[depth] = off + S;
+            }
+            base = depth * FORK_POOL + off;
+        }
+        while ((int)c.side.size() < FORK_POOL * FORK_DEPTHS) {
             cudaStream_t s;
             HC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
             c.side.push_back(s);
@@ -35,36 +60,56 @@ struct Fork {
             HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             c.side_ev.push_back(e);
         }
-        if (!c.fork_ev) HC_CUDA(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
-        HC_CUDA(cudaEventRecord(c.fork_ev, c.main_stream));
+        parent = c.stream;
+        if (c.fork_evs.size() <= (size_t)depth) {
+            cudaEvent_t e;
+            HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c.fork_evs.push_back(e);
+        }
+        ev = c.fork_evs[depth];
+        if (S) HC_CUDA(cudaEventRecord(ev, parent));
     }
     void enter(int k) {
+        if (!S) return;
         const int s = k % S;
         if (!used[s]) {
-            HC_CUDA(cudaStreamWaitEvent(c.side[s], c.fork_ev, 0));
+            HC_CUDA(cudaStreamWaitEvent(c.side[base + s], ev, 0));
             used[s] = 1;
         }
-        c.stream = c.side[s];
+        c.stream = c.side[base + s];
     }
-    void leave() { c.stream = c.main_stream; }
+    void leave() { c.stream = parent; }
     void join() {
-        c.stream = c.main_stream;
+        c.stream = parent;
         for (int s = 0; s < S; s++) {
             if (!used[s]) continue;
-            HC_CUDA(cudaEventRecord(c.side_ev[s], c.side[s]));
-            HC_CUDA(cudaStreamWaitEvent(c.main_stream, c.side_ev[s], 0));
+            HC_CUDA(cudaEventRecord(c.side_ev[base + s], c.side[base + s]));
+            HC_CUDA(cudaStreamWaitEvent(parent, c.side_ev[base + s], 0));
             used[s] = 0;
         }
     }
     ~Fork() {
-        if (c.stream != c.main_stream) c.stream = c.main_stream;
+        c.stream = parent;
         for (int s = 0; s < S; s++)
             if (used[s]) {
-                cudaEventRecord(c.side_ev[s], c.side[s]);
-                cudaStreamWaitEvent(c.main_stream, c.side_ev[s], 0);
+                cudaEventRecord(c.side_ev[base + s], c.side[base + s]);
+                cudaStreamWaitEvent(parent, c.side_ev[base + s], 0);
             }
+        c.fork_depth--;
     }
 };
+
+// run fn(i) for i < count as concurrent branches (width capped by the context)
+template <class F>
+static void par_for(Ctx& c, int count, int width, F&& fn) {
+    Fork fork(c, width);
+    for (int i = 0; i < count; i++) {
+        fork.enter(i);
+        fn(i);
+        fork.leave();
+    }
+    fork.join();
+}
 
 static int fork_width(const Ctx& c, int branches) { return std::max(1, std::min(branches, c.fork_cap)); }
 
@@ -238,34 +283,37 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
         for (int p = 0; p < m; p++) sums[p] = ev.mult_p(sums[p], ones);
         return sums;
     }
-    G rolled = rot_up(ev, B, c / 2, g);
-    G mi(n);
-    for (int q = 0; q < n; q++) mi[q] = ev.mul_i(rolled[q]);
+    Ctx& C = ev.c;
+    // packing prologue, one branch per block column: B + i * RU(B, c/2)
     G packed(n);
-    for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], mi[q]);
+    par_for(C, n, n, [&](int q) {
+        const int kk = (c / 2) % g.s0;
+        CtP rolled = kk ? ev.lrot(B[q], (int64_t)kk * g.s1) : B[q];
+        CtP mi = ev.mul_i(rolled);
+        packed[q] = ev.add(B[q], mi);
+    });
+    // the c/2 diagonal passes are independent: one branch each, and inside a
+    // pass the per-block-column rotation + products run as nested branches
     std::vector<G> terms(c / 2);
-    {
-        Fork fork(ev.c, fork_width(ev.c, c / 2));
-        for (int k = 0; k < c / 2; k++) {
-            fork.enter(k);
-            G shifted = rot_up(ev, packed, k, g);
-            G prod((size_t)m * n);
-            for (int p = 0; p < m; p++)
-                for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted[q]);
-            G sums = col_sums(ev, prod, m, n, g);
-            const Pattern mask = diag_mask(g, k, c, true, scale);
-            terms[k].resize(m);
-            for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(sums[p], mask);
-            fork.leave();
-        }
-        fork.join();
-    }
+    par_for(C, c / 2, fork_width(C, c / 2), [&](int k) {
+        G prod((size_t)m * n);
+        par_for(C, n, n, [&](int q) {
+            const int kk = k % g.s0;
+            CtP shifted = kk ? ev.lrot(packed[q], (int64_t)kk * g.s1) : packed[q];
+            for (int p = 0; p < m; p++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted);
+        });
+        G sums = col_sums(ev, prod, m, n, g);
+        const Pattern mask = diag_mask(g, k, c, true, scale);
+        terms[k].resize(m);
+        for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(sums[p], mask);
+    });
     G acc = terms[0];
     for (int k = 1; k < c / 2; k++)
         for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], terms[k][p]);
-    G cj(m);
-    for (int p = 0; p < m; p++) cj[p] = ev.conj(acc[p]);
-    for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], cj[p]);
+    par_for(C, m, m, [&](int p) {
+        CtP cj = ev.conj(acc[p]);
+        acc[p] = ev.add(acc[p], cj);
+    });
     return acc;
 }
 
@@ -289,41 +337,61 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
         return sums;
     }
     const bool partial = grid_level(A) < grid_level(B);
-    G rl = rot_left(ev, A, c / 2, g);
-    G mi(m);
-    for (int p = 0; p < m; p++) mi[p] = ev.mul_i(rl[p]);
+    Ctx& C = ev.c;
+    const int s1 = g.s1;
+    // with a cross-rank reducer the passes stay serial (collectives in a fixed order)
+    const int width = red ? 1 : fork_width(C, c / 2);
+    // packing prologue per block row: A + i * RL(A, c/2)
     G packed(m);
-    for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], mi[p]);
+    par_for(C, m, red ? 1 : m, [&](int p) {
+        G one = rot_left(ev, G{A[p]}, c / 2, g);
+        CtP mi = ev.mul_i(one[0]);
+        packed[p] = ev.add(A[p], mi);
+    });
     std::vector<G> terms(c / 2);
-    {
-        // with a cross-rank reducer the passes stay serial (collectives in a fixed order)
-        Fork fork(ev.c, red ? 1 : fork_width(ev.c, c / 2));
-        for (int k = 0; k < c / 2; k++) {
-            fork.enter(k);
-            G left, right;
-            if (partial) {
-                left.resize(m);
-                for (int p = 0; p < m; p++) left[p] = ev.lrot(packed[p], k);
-                right = prot_up(ev, B, k, g);
-            } else {
-                left = rot_left(ev, packed, k, g);
-                right = B;
-            }
-            G prod = colwise(left, right);
-            G sums = row_sums(ev, prod, m, n, g, red);
-            const Pattern mask = diag_mask(g, -k, c, true, scale);
-            terms[k].resize(n);
-            for (int q = 0; q < n; q++) terms[k][q] = ev.mult_p(sums[q], mask);
-            fork.leave();
+    par_for(C, c / 2, width, [&](int k) {
+        G left(m);
+        G right = B;
+        if (partial) {
+            for (int p = 0; p < m; p++) left[p] = ev.lrot(packed[p], k);
+        } else {
+            for (int p = 0; p < m; p++) left[p] = rot_left(ev, G{packed[p]}, k, g)[0];
         }
-        fork.join();
-    }
+        // products (and, on the PRU branch, the partial row rotation of B) per block column
+        G prod((size_t)m * n);
+        par_for(C, n, red ? 1 : n, [&](int q) {
+            for (int p = 0; p < m; p++) {
+                CtP r = B[(size_t)p * n + q];
+                if (partial) r = prot_up(ev, G{r}, k, g)[0];
+                prod[(size_t)p * n + q] = ev.mult(left[p], r);
+            }
+        });
+        // row_sums: block-row pre-add (cross-rank reduction point), then per column the ladder
+        G pre(n);
+        for (int q = 0; q < n; q++) {
+            CtP a = prod[q];
+            for (int p = 1; p < m; p++) a = ev.add(a, prod[(size_t)p * n + q]);
+            pre[q] = a;
+        }
+        if (red) red(pre);
+        const Pattern mask = diag_mask(g, -k, c, true, scale);
+        terms[k].resize(n);
+        par_for(C, n, red ? 1 : n, [&](int q) {
+            CtP a = pre[q];
+            for (int t = 0; t < ilog2(g.s0); t++) {
+                CtP rot = ev.lrot(a, (int64_t)(1 << t) * s1);
+                a = ev.add(a, rot);
+            }
+            terms[k][q] = ev.mult_p(a, mask);
+        });
+    });
     G acc = terms[0];
     for (int k = 1; k < c / 2; k++)
         for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], terms[k][q]);
-    G cj(n);
-    for (int q = 0; q < n; q++) cj[q] = ev.conj(acc[q]);
-    for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], cj[q]);
+    par_for(C, n, red ? 1 : n, [&](int q) {
+        CtP cj = ev.conj(acc[q]);
+        acc[q] = ev.add(acc[q], cj);
+    });
     return acc;
 }
 

@@ -172,6 +172,17 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thr = UINT64_MAX;
     HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Reuse a freed block only on the stream it was freed on: the schedules free
+    // every buffer on a stream already ordered after all its readers (fork/join),
+    // and skipping the pool's cross-stream dependency tracking halves the
+    // host cost of an allocation when many streams are active.
+    {
+        const char* e = std::getenv("HC_POOL_XSTREAM");
+        int on = (e && std::atoi(e)) ? 1 : 0;
+        HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseFollowEventDependencies, &on));
+        HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowOpportunistic, &on));
+        HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &on));
+    }
 
     // primes: below 2^b, q = 2^b - t*2N + 1, first unused prime in order
     std::vector<u64> used;

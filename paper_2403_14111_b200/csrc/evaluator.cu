@@ -347,8 +347,15 @@ PtP Eval::encoded(const Pattern& p, int level) {
         auto it = c.pt_cache.find(key);
         if (it != c.pt_cache.end()) return it->second;
     }
-    std::vector<double> zr(p.vals.size()), zi(p.vals.size());
-    for (size_t i = 0; i < p.vals.size(); i++) { zr[i] = p.vals[i].real(); zi[i] = p.vals[i].imag(); }
+    std::vector<std::complex<double>> generated;
+    const std::vector<std::complex<double>>* vals = &p.vals;
+    if (p.vals.empty() && p.gen) {
+        generated.resize(c.N / 2);
+        p.gen(generated);
+        vals = &generated;
+    }
+    std::vector<double> zr(vals->size()), zi(vals->size());
+    for (size_t i = 0; i < vals->size(); i++) { zr[i] = (*vals)[i].real(); zi[i] = (*vals)[i].imag(); }
     PtP pt = encode_pt(c, zr.data(), zi.data(), level, c.scale[level]);
     std::lock_guard<std::mutex> g(c.mu);
     c.pt_cache[key] = pt;

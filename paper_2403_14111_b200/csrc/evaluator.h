@@ -5,6 +5,7 @@
 // lower level by an unledgered level adjustment (counted under OP_ADJUST).
 #pragma once
 #include <complex>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -19,10 +20,13 @@ bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u
                      int add_npoly, u64 add_gal);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
 
-// a plaintext slot pattern with a cache key (content-addressed by the caller)
+// a plaintext slot pattern with a cache key (content-addressed by the caller).
+// Values are either given (vals) or produced by gen() only on a cache miss,
+// so steady-state schedules never rebuild 2^15-slot masks on the host.
 struct Pattern {
     std::string key;
     std::vector<std::complex<double>> vals;
+    std::function<void(std::vector<std::complex<double>>&)> gen;
 };
 
 struct Eval {

@@ -140,20 +140,21 @@ static Pattern diag_mask(const Geo& g, int shift, int modulus, bool cplx, double
     Pattern p;
     p.key = "diag:" + std::to_string(g.s0) + ":" + std::to_string(shift) + ":" + std::to_string(modulus) + ":" +
             (cplx ? "c" : "r") + ":" + dkey(scale);
-    p.vals.resize(g.S);
-    for (int i = 0; i < g.s0; i++)
-        for (int j = 0; j < g.s1; j++) {
-            const double main = ((((j - i - shift) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
-            cd v;
-            if (cplx) {
-                const double twin =
-                    ((((j - i - shift - modulus / 2) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
-                v = cd(0.5 * main, 0.0) - cd(0.0, 0.5 * twin);
-            } else {
-                v = cd(main, 0.0);
+    p.gen = [g, shift, modulus, cplx, scale](std::vector<cd>& vals) {
+        for (int i = 0; i < g.s0; i++)
+            for (int j = 0; j < g.s1; j++) {
+                const double main = ((((j - i - shift) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
+                cd v;
+                if (cplx) {
+                    const double twin =
+                        ((((j - i - shift - modulus / 2) % modulus) + modulus) % modulus == 0) ? 1.0 : 0.0;
+                    v = cd(0.5 * main, 0.0) - cd(0.0, 0.5 * twin);
+                } else {
+                    v = cd(main, 0.0);
+                }
+                vals[(size_t)i * g.s1 + j] = cd(v.real() * scale, v.imag() * scale);
             }
-            p.vals[(size_t)i * g.s1 + j] = cd(v.real() * scale, v.imag() * scale);
-        }
+    };
     return p;
 }
 
@@ -161,14 +162,15 @@ template <class F>
 static Pattern col_pattern(const Geo& g, const std::string& key, F f) {
     Pattern p;
     p.key = key + ":" + std::to_string(g.s0);
-    p.vals.resize(g.S);
-    for (int i = 0; i < g.s0; i++)
-        for (int j = 0; j < g.s1; j++) p.vals[(size_t)i * g.s1 + j] = cd(f(j), 0.0);
+    p.gen = [g, f](std::vector<cd>& vals) {
+        for (int i = 0; i < g.s0; i++)
+            for (int j = 0; j < g.s1; j++) vals[(size_t)i * g.s1 + j] = cd(f(j), 0.0);
+    };
     return p;
 }
 
 static Pattern keep_head(const Geo& g, int stop) {
-    return col_pattern(g, "head:" + std::to_string(stop), [&](int j) { return j < stop ? 1.0 : 0.0; });
+    return col_pattern(g, "head:" + std::to_string(stop), [stop](int j) { return j < stop ? 1.0 : 0.0; });
 }
 static Pattern col0(const Geo& g) {
     return col_pattern(g, "col0", [](int j) { return j == 0 ? 1.0 : 0.0; });
@@ -487,7 +489,7 @@ struct SM {
         if (classes < period) {
             const int c = classes, cp = period;
             work = subp(work, col_pattern(g, "padhalf:" + std::to_string(c) + ":" + std::to_string(cp),
-                                          [&](int j) { return (j % cp) >= c ? 0.5 : 0.0; }));
+                                          [c, cp](int j) { return (j % cp) >= c ? 0.5 : 0.0; }));
         }
         G best = work;
         for (int t = 0; t < ilog2(period); t++) {
@@ -567,7 +569,7 @@ std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes,
     const int max_range = (int)std::ceil(full / 2);
     G best = sm.amax(M, cfg, max_range);
     const int c = classes;
-    const Pattern keep = col_pattern(g, "keep:" + std::to_string(c), [&](int j) { return j < c ? 1.0 : 0.0; });
+    const Pattern keep = col_pattern(g, "keep:" + std::to_string(c), [c](int j) { return j < c ? 1.0 : 0.0; });
     G d = sm.sub(M, best);
     G norm = sm.mulp(d, keep);
     norm = sm.domain_extend(norm, cfg);

@@ -85,7 +85,10 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     StPlain<false, false> st{I + ((size_t)j * g.nt + t) * N, p, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)pi << g.logN),  p, ld, st);
+    const ulonglong2* TW = tw + ((size_t)pi << g.logN);
+    ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, p, ld, st, twsm, true);
 }
 
 // ---- B: chunk pass + key inner product ------------------------------------
@@ -115,6 +118,11 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const PrimeDev P = primes[pi];
     PG G;
     G.init(g.N1);
+    const ulonglong2* TW = tw + ((size_t)pi << g.logN);
+    ulonglong2* twsm = PG::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, g.N1);
+    cp_async_wait_all();
+    __syncthreads();
     const size_t k0 = G.gidx(G.lt * 8);     // this thread's 8 consecutive output coefficients
     // digit values staged in registers; the 128-bit accumulators are then
     // short-lived (one pair of outputs at a time), which keeps the kernel at
@@ -136,7 +144,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
             __syncthreads();
             LdPlain ld{I + ((size_t)j * g.nt + t) * N};
             StCapture st{xs[j]};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)pi << g.logN), P.q, ld, st);
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, P.q, ld, st, twsm, false);
         }
     }
     ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
@@ -251,7 +259,10 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)i << g.logN),  q, ld, st);
+    const ulonglong2* TW = tw + ((size_t)i << g.logN);
+    ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, g.N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---- E: chunk pass with the ModDown combine in its stores ------------------
@@ -294,7 +305,10 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
                  add_gal, g.logN};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
     G.init(g.N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)i << g.logN),  q, ld, st);
+    const ulonglong2* TW = tw + ((size_t)i << g.logN);
+    ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, g.N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---- fused rescale (R1: bcast in the column pass, R2: combine in the chunk pass)
@@ -323,7 +337,10 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
     StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, tw + ((size_t)i << logN),  q, ld, st);
+    const ulonglong2* TW = tw + ((size_t)i << logN);
+    ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, N1);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 struct StRescale {
@@ -355,7 +372,10 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
                  tab[3 * i + 1]};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
     G.init(N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, tw + ((size_t)i << logN),  q, ld, st);
+    const ulonglong2* TW = tw + ((size_t)i << logN);
+    ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
+    stage_twiddles(G, twsm, TW, N1);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -396,7 +416,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
     KsGeo g{level, nl, nt, c.L, K, c.alpha, c.dnum, c.nall, (nl + c.alpha - 1) / c.alpha, c.logN, N >> CH_LOG};
-    const size_t csm = sizeof(u64) * CG::smem_words(), hsm = sizeof(u64) * HG::smem_words();
+    const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
 
     // 1. Y = INTT(sigma(d)) * (Q'/q_i)^-1
     u64* Y = c.alloc((size_t)nl * N);
@@ -551,7 +571,7 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
     ntt_inverse(c, j);
     u64* Yt = c.alloc((size_t)npoly * level * N);
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
-    const size_t csm = sizeof(u64) * CG::smem_words(), hsm = sizeof(u64) * HG::smem_words();
+    const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     const int N1 = N >> CH_LOG;
     {
         static bool at = false;

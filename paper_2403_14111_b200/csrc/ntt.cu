@@ -36,26 +36,30 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS)
     u64* dst = jobs.ptr[job];
     const PrimeDev P = primes[pidx];
     const ulonglong2* TW = tw + ((size_t)pidx << logN);
-    PassGeo<LOGSZ, MODE, SUBS> G;
+    using PG = PassGeo<LOGSZ, MODE, SUBS>;
+    PG G;
     G.init(N1);
+    ulonglong2* twsm = PG::twsm_of(sm);
+    if (twsm) stage_twiddles<LOGSZ, MODE, SUBS>(G, twsm, TW, N1);
+    const bool pend = twsm != nullptr;
     const u64 gal = use_src ? jobs.galois : 0;
     u64 c = P.ninv, cs = P.ninv_s;
     if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
     if (gal) {
         LdGalois ld{src, logN, gal};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
     } else {
         LdPlain ld{src};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
     }
 }
 
 template <int LOGSZ, int MODE, int SUBS>
 static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
-    const size_t smem = sizeof(u64) * PG::smem_words();
+    const size_t smem = PG::smem_bytes();
     const int nsub = (MODE == MODE_COLS) ? (c.N >> LOGSZ) : (MODE == MODE_CHUNKS ? N1 : 1);
     dim3 grid(nsub / SUBS, jobs.n);
     static const char* names[2][3] = {{"ntt_fwd_full", "ntt_fwd_cols", "ntt_fwd_chunks"},

@@ -27,6 +27,13 @@ struct PassGeo {
     static constexpr int THREADS = SUBS * TPS;
     static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;   // column stride (MODE_COLS)
     static constexpr size_t smem_words() { return (size_t)SUBS * (MODE == MODE_COLS ? SZ : PADSZ); }
+    // data + staged twiddles (full-limb passes keep reading twiddles from L1/L2)
+    static constexpr size_t smem_bytes() {
+        return smem_words() * 8 + (MODE == MODE_FULL ? 0 : (size_t)(MODE == MODE_CHUNKS ? SUBS * SZ : SZ) * 16);
+    }
+    static __device__ __forceinline__ ulonglong2* twsm_of(u64* sm) {
+        return MODE == MODE_FULL ? nullptr : reinterpret_cast<ulonglong2*>(sm + smem_words());
+    }
     static constexpr bool EDGE_CONTIG = (MODE != MODE_COLS) && (LOGSZ % 3 == 0);
     int sub, lt, first_sub, R;
     __device__ __forceinline__ void init(int N1) {
@@ -44,11 +51,46 @@ struct PassGeo {
         if (MODE == MODE_COLS) return pos * SUBS + sub;
         return sub * PADSZ + pos + (pos >> 3);
     }
+    // twiddles staged in shared memory: the CTA's (w, w_shoup) pairs, per stage
+    //   COLS / FULL (R = 1): entry widx = 2^s + i for widx < SZ
+    //   CHUNKS: stage s holds SUBS * 2^s entries for this CTA's chunks
+    static constexpr int TW_ENTRIES = (MODE == MODE_CHUNKS) ? SUBS * SZ : SZ;
+    __device__ __forceinline__ int twl(int s, int i) const {   // i = index inside the stage for this sub
+        if (MODE == MODE_CHUNKS) return SUBS * ((1 << s) - 1) + (sub << s) + i;
+        return (1 << s) + i;
+    }
     // strides of element m inside a group whose elements are u apart
     static constexpr size_t gstep(int u) { return MODE == MODE_COLS ? (size_t)u * N2 : (size_t)u; }
     static constexpr bool slinear(int u) { return MODE == MODE_COLS || u == 1 || u >= 8; }
     static constexpr int sstep(int u) { return MODE == MODE_COLS ? u * SUBS : (u == 1 ? 1 : u + u / 8); }
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Issue the asynchronous copy of this CTA's twiddles into shared memory
+// (completed by cp_async_wait_all + __syncthreads, which ntt_pass does after
+// its first-round data loads when tw_pending is set).
+template <int LOGSZ, int MODE, int SUBS>
+__device__ __forceinline__ void stage_twiddles(const PassGeo<LOGSZ, MODE, SUBS>& G, ulonglong2* twsm,
+                                               const ulonglong2* __restrict__ TW, int N1) {
+    using PG = PassGeo<LOGSZ, MODE, SUBS>;
+    const int tid = threadIdx.x;
+    if (MODE == MODE_CHUNKS) {
+#pragma unroll 1
+        for (int s = 0; s < LOGSZ; s++) {
+            const int cnt = SUBS << s;
+            const ulonglong2* src = TW + ((size_t)(N1 + G.first_sub) << s);
+            ulonglong2* dst = twsm + SUBS * ((1 << s) - 1);
+            for (int i = tid; i < cnt; i += PG::THREADS) cp_async16(dst + i, src + i);
+        }
+    } else {
+        for (int i = tid; i < PG::SZ; i += PG::THREADS) cp_async16(twsm + i, TW + i);
+    }
+}
 
 // Runs the pass.  LD: u64 operator()(size_t gidx) and void load8(size_t gidx, u64* x)
 // (8 consecutive words, only used when EDGE_CONTIG).  ST: void operator()(size_t gidx, u64 v)
@@ -56,7 +98,8 @@ struct PassGeo {
 // [0, 2q) inverse.  TW: (w, w_shoup) pairs of this prime.
 template <int LOGSZ, int MODE, int SUBS, bool INV, class LD, class ST>
 __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm,
-                                         const ulonglong2* __restrict__ TW, u64 q, LD& ld, ST& st) {
+                                         const ulonglong2* __restrict__ TW, u64 q, LD& ld, ST& st,
+                                         const ulonglong2* twsm = nullptr, bool tw_pending = false) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const u64 twoq = 2 * q;
     u64 x[8];
@@ -90,18 +133,29 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
                 for (int m = 0; m < GS; m++) x[j * GS + m] = sm[G.sidx(base + (m << logu))];
             }
         }
+        if (rd == 0 && tw_pending) {
+            cp_async_wait_all();
+            __syncthreads();
+        }
         // ---- twiddles for the round, one 16-byte load each, issued up front ----
         ulonglong2 tw_r[7];
         {
             int n = 0;
 #pragma unroll
             for (int j = 0; j < NG; j++) {
-                const int B0 = G.R * (1 << s0) + ((G.lt + j * PG::TPS) >> logu);
+                const int blk = (G.lt + j * PG::TPS) >> logu;
+                const int B0 = G.R * (1 << s0) + blk;
 #pragma unroll
                 for (int qq = 0; qq < r; qq++) {
-                    const ulonglong2* tp = TW + (B0 << qq);
+                    if (twsm) {
+                        const ulonglong2* tp = twsm + G.twl(s0 + qq, blk << qq);
 #pragma unroll
-                    for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
+                        for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
+                    } else {
+                        const ulonglong2* tp = TW + (B0 << qq);
+#pragma unroll
+                        for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
+                    }
                 }
             }
         }

@@ -27,12 +27,13 @@ struct PassGeo {
     static constexpr int THREADS = SUBS * TPS;
     static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;   // column stride (MODE_COLS)
     static constexpr size_t smem_words() { return (size_t)SUBS * (MODE == MODE_COLS ? SZ : PADSZ); }
-    // data + staged twiddles (full-limb passes keep reading twiddles from L1/L2)
-    static constexpr size_t smem_bytes() {
-        return smem_words() * 8 + (MODE == MODE_FULL ? 0 : (size_t)(MODE == MODE_CHUNKS ? SUBS * SZ : SZ) * 16);
-    }
+    // data + staged twiddles.  Only column passes stage (their whole twiddle
+    // set is SZ pairs, 2 KiB); a chunk pass needs ~one pair per element, and
+    // front-loading 32 KiB per CTA measured slower than streaming them from L2.
+    static constexpr bool STAGE_TW = (MODE == MODE_COLS);
+    static constexpr size_t smem_bytes() { return smem_words() * 8 + (STAGE_TW ? (size_t)SZ * 16 : 0); }
     static __device__ __forceinline__ ulonglong2* twsm_of(u64* sm) {
-        return MODE == MODE_FULL ? nullptr : reinterpret_cast<ulonglong2*>(sm + smem_words());
+        return STAGE_TW ? reinterpret_cast<ulonglong2*>(sm + smem_words()) : nullptr;
     }
     static constexpr bool EDGE_CONTIG = (MODE != MODE_COLS) && (LOGSZ % 3 == 0);
     int sub, lt, first_sub, R;
@@ -79,6 +80,7 @@ __device__ __forceinline__ void stage_twiddles(const PassGeo<LOGSZ, MODE, SUBS>&
                                                const ulonglong2* __restrict__ TW, int N1) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const int tid = threadIdx.x;
+    if (!twsm) return;
     if (MODE == MODE_CHUNKS) {
 #pragma unroll 1
         for (int s = 0; s < LOGSZ; s++) {

@@ -172,13 +172,13 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thr = UINT64_MAX;
     HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // Reuse a freed block only on the stream it was freed on: the schedules free
-    // every buffer on a stream already ordered after all its readers (fork/join),
-    // and skipping the pool's cross-stream dependency tracking halves the
-    // host cost of an allocation when many streams are active.
+    // Cross-stream reuse of freed blocks (the pool's event tracking) stays on by
+    // default: stream-local reuse (HC_POOL_XSTREAM=0) issues ~25% faster on the
+    // host but lets every side stream grow its own cache, and the resulting
+    // pool growth measured as multi-x step-time spikes.
     {
         const char* e = std::getenv("HC_POOL_XSTREAM");
-        int on = (e && std::atoi(e)) ? 1 : 0;
+        int on = (e && !std::atoi(e)) ? 0 : 1;
         HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseFollowEventDependencies, &on));
         HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowOpportunistic, &on));
         HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &on));

@@ -102,7 +102,7 @@ struct Fork {
 // run fn(i) for i < count as concurrent branches (width capped by the context)
 template <class F>
 static void par_for(Ctx& c, int count, int width, F&& fn) {
-    Fork fork(c, width);
+    Fork fork(c, std::min(width, c.fork_cap));
     for (int i = 0; i < count; i++) {
         fork.enter(i);
         fn(i);

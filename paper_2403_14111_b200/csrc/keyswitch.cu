@@ -64,7 +64,7 @@ struct LdModup {
 };
 
 template <int LOGSZ, int SUBS>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
     extern __shared__ u64 sm[];
@@ -242,7 +242,7 @@ struct LdModdown {
 };
 
 template <int LOGSZ, int SUBS>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
     extern __shared__ u64 sm[];
@@ -291,7 +291,7 @@ struct StModdown {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly, u64 add_gal,
                       u64* __restrict__ out) {
@@ -326,7 +326,7 @@ struct LdBcast {
 };
 
 template <int LOGSZ, int SUBS>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
             u64* __restrict__ Yt) {
     extern __shared__ u64 sm[];
@@ -360,7 +360,7 @@ struct StRescale {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, const u64* __restrict__ a,
               const u64* __restrict__ tab, u64* __restrict__ out) {
     extern __shared__ u64 sm[];

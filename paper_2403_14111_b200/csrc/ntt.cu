@@ -26,7 +26,7 @@
 namespace hc {
 
 template <int LOGSZ, int MODE, int SUBS, bool INV>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS)
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
     extern __shared__ u64 sm[];

@@ -17,6 +17,10 @@ namespace hc {
 
 enum { MODE_FULL = 0, MODE_COLS = 1, MODE_CHUNKS = 2 };
 constexpr int CHUNK_LOG = 9;   // chunk-pass size for split rings; = log2(column stride)
+// resident 256-thread CTAs per SM the pass kernels are register-budgeted for
+#ifndef PASS_MIN_BLOCKS
+#define PASS_MIN_BLOCKS 4
+#endif
 
 template <int LOGSZ, int MODE, int SUBS>
 struct PassGeo {
@@ -25,6 +29,7 @@ struct PassGeo {
     static constexpr int NR = (LOGSZ + 2) / 3;
     static constexpr int PADSZ = SZ + SZ / 8;
     static constexpr int THREADS = SUBS * TPS;
+    static constexpr int MIN_BLOCKS = THREADS >= 256 ? PASS_MIN_BLOCKS * 256 / THREADS : 1;
     static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;   // column stride (MODE_COLS)
     static constexpr size_t smem_words() { return (size_t)SUBS * (MODE == MODE_COLS ? SZ : PADSZ); }
     // data + staged twiddles.  Only column passes stage (their whole twiddle

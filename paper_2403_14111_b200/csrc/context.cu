@@ -172,6 +172,16 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thr = UINT64_MAX;
     HC_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // Reserve the pool's working set up front (one allocation, freed back to the
+    // pool, which keeps it): growing the pool mid-schedule maps memory through
+    // the driver and showed up as ~2x step-time spikes.
+    {
+        const size_t reserve = (size_t)512 * (size_t)(nq + np) * ((size_t)8 << logN);
+        void* p = nullptr;
+        HC_CUDA(cudaMallocFromPoolAsync(&p, reserve, c->pool, c->stream));
+        HC_CUDA(cudaFreeAsync(p, c->stream));
+        HC_CUDA(cudaStreamSynchronize(c->stream));
+    }
     // Cross-stream reuse of freed blocks (the pool's event tracking) stays on by
     // default: stream-local reuse (HC_POOL_XSTREAM=0) issues ~25% faster on the
     // host but lets every side stream grow its own cache, and the resulting

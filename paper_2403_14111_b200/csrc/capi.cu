@@ -342,11 +342,34 @@ static void snap(hc_ctx* ctx, int64_t* b) {
     for (int i = 0; i < HC_NCOUNTS; i++) b[i] = ctx->c->counts[i];
 }
 
+// Bound how far the host runs ahead of the device: a schedule may start
+// issuing only once the schedule before the previous one has finished.  Each
+// schedule issues thousands of launches and allocations; unbounded run-ahead
+// piles up stream-ordered frees the pool cannot recycle yet and forces it to
+// grow mid-run.
+struct RunAhead {
+    hc::Ctx& c;
+    explicit RunAhead(hc::Ctx& ctx) : c(ctx) {
+        if (!c.ra_ev[0]) {
+            HC_CUDA(cudaEventCreateWithFlags(&c.ra_ev[0], cudaEventDisableTiming));
+            HC_CUDA(cudaEventCreateWithFlags(&c.ra_ev[1], cudaEventDisableTiming));
+            HC_CUDA(cudaEventRecord(c.ra_ev[0], c.main_stream));
+            HC_CUDA(cudaEventRecord(c.ra_ev[1], c.main_stream));
+        }
+        HC_CUDA(cudaEventSynchronize(c.ra_ev[c.ra_idx]));
+    }
+    ~RunAhead() {
+        cudaEventRecord(c.ra_ev[c.ra_idx], c.main_stream);
+        c.ra_idx ^= 1;
+    }
+};
+
 int hc_diag_abt(hc_ctx* ctx, const hc_ct* const* A, int m, int n, const hc_ct* const* B, int c, double scale,
                 hc_ct** out, int64_t* counts) {
     return guard([&] {
         int64_t before[HC_NCOUNTS];
         snap(ctx, before);
+        RunAhead throttle(*ctx->c);
         hc::Eval ev(*ctx->c, ctx->auto_boot);
         std::vector<hc::CtP> res = hc::sched_diag_abt(ev, unwrap(A, m * n), m, n, unwrap(B, n), c, scale);
         for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
@@ -359,6 +382,7 @@ int hc_diag_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B
     return guard([&] {
         int64_t before[HC_NCOUNTS];
         snap(ctx, before);
+        RunAhead throttle(*ctx->c);
         hc::Eval ev(*ctx->c, ctx->auto_boot);
         hc::Reducer red;
         if (reduce_fn) {
@@ -382,6 +406,7 @@ int hc_softmax(hc_ctx* ctx, const hc_ct* const* A, int m, int classes, int perio
     return guard([&] {
         int64_t before[HC_NCOUNTS];
         snap(ctx, before);
+        RunAhead throttle(*ctx->c);
         hc::Eval ev(*ctx->c, ctx->auto_boot);
         hc::SoftmaxCfg sc;
         if (cfg) sc = hc::SoftmaxCfg::from(cfg);

@@ -377,6 +377,7 @@ void ctx_destroy(Ctx* c) {
     for (auto e : c->side_ev) cudaEventDestroy(e);
     if (c->fork_ev) cudaEventDestroy(c->fork_ev);
     for (auto e : c->fork_evs) cudaEventDestroy(e);
+    for (auto e : c->ra_ev) if (e) cudaEventDestroy(e);
     cudaMemPoolDestroy(c->pool);
     cudaStreamDestroy(c->main_stream);
     delete c;

@@ -26,14 +26,14 @@ enum EwOp { EW_ADD, EW_SUB, EW_NEG, EW_PT_ADD, EW_PT_SUB, EW_PT_RSUB, EW_PT_MUL,
 __global__ void ew_kernel(int op, u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
                           const ConstTab consts, const PrimeDev* __restrict__ primes, int nl, int npoly,
                           int N, int bpoly) {
+    // grid.y = poly * nl + limb: no integer division on the hot path
     const size_t half = (size_t)N / 2;
-    const size_t total = (size_t)npoly * nl * half;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const size_t e = v * 2;
-        const int limb = (int)((e / N) % nl);
-        const int s = (int)(e / ((size_t)N * nl));
-        const size_t k = e % N;
-        const u64 q = primes[limb].q;
+    const int limb = blockIdx.y % nl;
+    const int s = blockIdx.y / nl;
+    const u64 q = primes[limb].q;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < half; v += (size_t)gridDim.x * blockDim.x) {
+        const size_t k = v * 2;
+        const size_t e = (size_t)blockIdx.y * N + k;
         const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + e);
         u64 r0, r1;
         switch (op) {
@@ -90,8 +90,9 @@ void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const C
     const bool pt_b = op >= EW_PT_ADD && op <= EW_PT_MUL;
     const double rd = (double)npoly * nl + (pt_b ? nl : (op <= EW_SUB ? bpoly * nl : 0));
     Launch scope(c, "elementwise", 8.0 * c.N * (rd + (double)npoly * nl));
-    ew_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(op, out, a, b, consts ? *consts : zero, c.d_primes, nl, npoly,
-                                                        c.N, bpoly);
+    (void)work;
+    dim3 grid((unsigned)((c.N / 2 + 255) / 256), (unsigned)(npoly * nl));
+    ew_kernel<<<grid, 256, 0, c.stream>>>(op, out, a, b, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
     HC_CUDA(cudaGetLastError());
 }
 

@@ -179,40 +179,47 @@ __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev
                                                          u64 gal, const u64* __restrict__ key,
                                                          u64* __restrict__ acc) {
     const size_t N = (size_t)1 << g.logN;
-    const size_t half = N >> 1;
-    const size_t total = (size_t)g.nt * half;
+    const size_t total = (size_t)g.nt << (g.logN - 1);
     const size_t kstride = (size_t)g.nall * N;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const int t = (int)(v / half);
-        const size_t k = (v - (size_t)t * half) * 2;
+        const int t = (int)(v >> (g.logN - 1));
+        const size_t k = (v & ((N >> 1) - 1)) * 2;
         const int pi = g.prime(t);
         const PrimeDev P = primes[pi];
         U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
-        for (int j = 0; j < g.beta; j++) {
+        // issue every load of the (up to KP_MAXB) digits before the first MAC
+        u64 x0[KP_MAXB], x1[KP_MAXB];
+        ulonglong2 kbv[KP_MAXB], kav[KP_MAXB];
+#pragma unroll
+        for (int j = 0; j < KP_MAXB; j++) {
+            if (j >= g.beta) break;
             const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
-            u64 x0, x1;
             if (t >= lo && t < hi) {
                 const u64* src = d + (size_t)t * N;
                 if (gal) {
-                    x0 = src[galois_src((unsigned)k, g.logN, gal)];
-                    x1 = src[galois_src((unsigned)k + 1, g.logN, gal)];
+                    x0[j] = src[galois_src((unsigned)k, g.logN, gal)];
+                    x1[j] = src[galois_src((unsigned)k + 1, g.logN, gal)];
                 } else {
                     const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(src + k);
-                    x0 = xv.x;
-                    x1 = xv.y;
+                    x0[j] = xv.x;
+                    x1[j] = xv.y;
                 }
             } else {
                 const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(UP + ((size_t)j * g.nt + t) * N + k);
-                x0 = xv.x;
-                x1 = xv.y;
+                x0[j] = xv.x;
+                x1[j] = xv.y;
             }
             const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k;
-            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
-            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
-            mac128(b0, x0, kbv.x);
-            mac128(b1, x1, kbv.y);
-            mac128(a0, x0, kav.x);
-            mac128(a1, x1, kav.y);
+            kbv[j] = *reinterpret_cast<const ulonglong2*>(kb);
+            kav[j] = *reinterpret_cast<const ulonglong2*>(kb + kstride);
+        }
+#pragma unroll
+        for (int j = 0; j < KP_MAXB; j++) {
+            if (j >= g.beta) break;
+            mac128(b0, x0[j], kbv[j].x);
+            mac128(b1, x1[j], kbv[j].y);
+            mac128(a0, x0[j], kav[j].x);
+            mac128(a1, x1[j], kav[j].y);
         }
         *reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k) =
             make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));

@@ -322,12 +322,72 @@ def run_b200(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_train_step(args, world, rank, local):
+    """BASELINE config 4 as a data-parallel NAG step: the 1024-row batch's 8
+    block rows are sharded over ranks; the DiagATB block-row pre-sums are
+    mod-summed across ranks (NCCL) -- strong scaling (fixed 1024 rows/step)."""
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+    from paper_2403_14111_b200 import sharding
+    from paper_2403_14111_b200 import workloads as wl
+
+    L = N.lib()
+    X, y = wl.config4()
+    Y = P.one_hot(y, wl.CLASSES)
+    ctx = P.CKKSContext("cfg1", 128, seed=4, device=local, auto_bootstrap=True)
+    w0 = P.init_weights(wl.CLASSES, X.shape[1], wl.INIT_SEED)
+    W = P.encode(ctx, w0, "vertical")                       # replicated, same nonces on all ranks
+    ctx.nonce = sharding.rank_nonce_base(rank) + 1000
+    Xl = sharding.local_rows(X, 128, world, rank)
+    Yl = sharding.local_rows(Y, 128, world, rank)
+    EX, EY = P.encode(ctx, Xl), P.encode(ctx, Yl, "horizontal")
+    red = sharding.NcclModReducer() if world > 1 else None
+    state = P.TrainState(W, W)
+
+    def step():
+        P.nag_step(state, EX, EY, wl.LEARNING_RATE, X.shape[0], reducer=red)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.sync()
+    c0 = ctx.ledger.counts()
+    launches0 = L.hc_launch_count(ctx._h)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    ms = C.c_float()
+    N.check(L.hc_timer_begin(ctx._h))
+    for _ in range(args.steps):
+        step()
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    barrier(world)
+    clk = clocks.stop()
+    total = all_max(ms.value, world)
+    counts = {k: (v - c0[k]) // args.steps for k, v in ctx.ledger.counts().items()}
+    hbm, _ = peaks()
+    line = {"metric": "NAG training step ms, config 4 (1024 rows x 768, 10 classes, N=2^16)",
+            "value": total / args.steps, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded 10-class Gaussian mixture, BASELINE config 4)",
+            "config": {"workload": "data-parallel NAG step over 8 block rows of 128 (DiagABT, softmax, "
+                                   "DiagATB with cross-rank mod-sum, NAG update, refresh)",
+                       "rows": int(X.shape[0]), "block_rows_per_rank": len(sharding.partition(8, world, rank))},
+            "ledger_per_step": counts, "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0),
+            "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="pair", choices=["pair", "train"],
+                    help="pair: DiagABT+DiagATB (BASELINE metric); train: config-4 data-parallel NAG step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
@@ -338,7 +398,10 @@ def main():
         run_reference(args, world, rank)
         return
     world, rank, local = dist_setup(args.gpus)
-    run_b200(args, world, rank, local)
+    if args.workload == "train":
+        run_train_step(args, world, rank, local)
+    else:
+        run_b200(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

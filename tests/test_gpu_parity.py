@@ -295,6 +295,28 @@ def test_config3_softmax_full_size(golden):
 
 
 @pytest.mark.slow
+def test_config4_data_parallel_step_1024_rows():
+    """The 1024-row batch as one NAG step (8 block rows; the multi-GPU
+    data-parallel form run on one GPU): weights vs the float64 slot emulator
+    running the reference op sequence on the same batch."""
+    P = _prod()
+    from paper_2403_14111_b200 import workloads as wl
+    X, y = wl.config4()
+    Y = S.one_hot(y, wl.CLASSES)
+    w0 = S.init_weights(wl.CLASSES, X.shape[1], wl.INIT_SEED)
+    g = P.CKKSContext("cfg1", 128, seed=4, auto_bootstrap=True)
+    W = P.encode(g, w0, "vertical")
+    st = P.TrainState(W, W)
+    P.nag_step(st, P.encode(g, X), P.encode(g, Y, "horizontal"), wl.LEARNING_RATE, X.shape[0])
+    e = S.SlotBackend(32768, 128, max_level=12, auto_bootstrap=True)
+    EW = S.encode(e, w0, "vertical")
+    es = S.State(EW, EW)
+    S.nag_step(es, S.encode(e, X), S.encode(e, Y, "horizontal"), wl.LEARNING_RATE, X.shape[0])
+    assert _ledger(g) == [e.ledger.counts()[k] for k in OPS]
+    assert np.max(np.abs(P.decode(st.weights, tol=1e-3) - S.decode(es.weights))) < 1e-3
+
+
+@pytest.mark.slow
 def test_config4_training_step_full_size(golden):
     """BASELINE config 4: the first 128-row NAG step at N=2^16 (ledger per step
     164/101/382/518/4/54), weights vs the reference emulator's first snapshot."""

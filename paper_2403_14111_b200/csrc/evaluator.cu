@@ -273,11 +273,18 @@ CtP Eval::at(const CtP& a, int level) {
     return ev_level_adjust(c, *a, level);
 }
 
+CtP Eval::refresh_planned(const CtP& a, int j, int r) {
+    rec(OP_BOOT);
+    const u64 n = plan.on ? plan.base + (u64)plan.m * plan.events + (u64)plan.p * r + j : next_nonce();
+    return refresh(c, *a, n);
+}
+
 CtP Eval::ready(const CtP& a) {
     if (a->level >= 1) return a;
     if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
-    rec(OP_BOOT);
-    return refresh(c, *a, next_nonce());
+    CtP o = refresh_planned(a, 0, 1);
+    plan.events += 1;
+    return o;
 }
 
 CtP Eval::add(const CtP& a, const CtP& b, bool sub) {
@@ -301,7 +308,14 @@ CtP Eval::add_p(const CtP& a, const Pattern& p, bool sub, bool reversed) {
 }
 
 CtP Eval::mult(const CtP& x, const CtP& y) {
-    CtP a = ready(x), b = ready(y);
+    // per-operand auto-bootstrap, x before y (emulator.py:218-221)
+    const int r = (x->level < 1 ? 1 : 0) + (y->level < 1 ? 1 : 0);
+    if (r && !auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
+    CtP a = x, b = y;
+    int j = 0;
+    if (x->level < 1) a = refresh_planned(x, j++, r);
+    if (y->level < 1) b = refresh_planned(y, j++, r);
+    plan.events += r;
     rec(OP_MULT);
     const int l = std::min(a->level, b->level);
     return ev_mult(c, *at(a, l), *at(b, l));
@@ -336,8 +350,9 @@ CtP Eval::conj(const CtP& a) {
 CtP Eval::mul_i(const CtP& a) { return ev_mul_i(c, *a); }
 
 CtP Eval::bootstrap(const CtP& a) {
-    rec(OP_BOOT);
-    return refresh(c, *a, next_nonce());
+    CtP o = refresh_planned(a, 0, 1);
+    plan.events += 1;
+    return o;
 }
 
 PtP Eval::encoded(const Pattern& p, int level) {

@@ -29,10 +29,25 @@ struct Pattern {
     std::function<void(std::vector<std::complex<double>>&)> gen;
 };
 
+// Deterministic refresh nonces for a block-parallel run: block p of m, whose
+// ops would be interleaved block by block in the reference's sequential order,
+// takes for the j-th of r refreshes in an op the nonce
+//   base + m * (refreshes in its earlier ops) + p * r + j,
+// exactly the nonce the sequential order assigns (all blocks share one level
+// history, so every block refreshes the same operands in the same ops).
+struct NoncePlan {
+    bool on = false;
+    u64 base = 0;
+    int m = 1, p = 0;
+    u64 events = 0;
+};
+
 struct Eval {
     Ctx& c;
     bool auto_boot;
+    NoncePlan plan;
     Eval(Ctx& ctx, bool ab) : c(ctx), auto_boot(ab) {}
+    CtP refresh_planned(const CtP& a, int j, int r);
 
     void rec(int kind, int n = 1);
     u64 next_nonce();

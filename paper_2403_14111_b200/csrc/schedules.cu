@@ -560,10 +560,43 @@ struct SM {
 
 }  // namespace
 
+static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int classes, int period,
+                                       const SoftmaxCfg& cfg);
+
 std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes, int period, const SoftmaxCfg& cfg) {
     const Geo g = geo(ev, geo_rows(ev));
     if (period < classes || period > g.s1 || (period & (period - 1))) throw Error(-4, "softmax: bad period");
     if (cfg.exp_range < 1 || (cfg.exp_range & (cfg.exp_range - 1))) throw Error(-4, "exp_range must be a power of two");
+    const int m = (int)M.size();
+    bool uniform = m > 1 && !ev.plan.on;
+    for (auto& b : M) uniform = uniform && b->level == M[0]->level;
+    if (!uniform || ev.c.fork_cap <= 1) return softmax_serial(ev, M, classes, period, cfg);
+    // Block rows are independent: one branch per block row, each with the
+    // nonce plan that reproduces the sequential (block-interleaved) order.
+    u64 base;
+    {
+        std::lock_guard<std::mutex> lk(ev.c.mu);
+        base = ev.c.nonce;
+    }
+    std::vector<CtP> out(m);
+    u64 events = 0;
+    par_for(ev.c, m, m, [&](int p) {
+        Eval bev(ev.c, ev.auto_boot);
+        bev.plan.on = true;
+        bev.plan.base = base;
+        bev.plan.m = m;
+        bev.plan.p = p;
+        out[p] = softmax_serial(bev, std::vector<CtP>{M[p]}, classes, period, cfg)[0];
+        events = bev.plan.events;
+    });
+    std::lock_guard<std::mutex> lk(ev.c.mu);
+    ev.c.nonce = base + (u64)m * events;
+    return out;
+}
+
+static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int classes, int period,
+                                       const SoftmaxCfg& cfg) {
+    const Geo g = geo(ev, geo_rows(ev));
     SM sm{ev, g, classes, period};
     const double full = cfg.base_range * std::pow(cfg.extension_base, (double)cfg.extension_steps);
     const int max_range = (int)std::ceil(full / 2);

@@ -102,6 +102,10 @@ struct Fork {
 // run fn(i) for i < count as concurrent branches (width capped by the context)
 template <class F>
 static void par_for(Ctx& c, int count, int width, F&& fn) {
+    if (count <= 1 || std::min(width, c.fork_cap) <= 1) {
+        for (int i = 0; i < count; i++) fn(i);
+        return;
+    }
     Fork fork(c, std::min(width, c.fork_cap));
     for (int i = 0; i < count; i++) {
         fork.enter(i);
@@ -217,10 +221,10 @@ static G prot_up(Eval& ev, const G& E, int k, const Geo& g) {
 }
 
 // col_sums over an r x cols grid -> r blocks
-static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g) {
+static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, int width = 1) {
     const Pattern c0 = col0(g);
     G out(r);
-    for (int p = 0; p < r; p++) {
+    par_for(ev.c, r, width, [&](int p) {
         CtP acc = E[(size_t)p * cols];
         for (int q = 1; q < cols; q++) acc = ev.add(acc, E[(size_t)p * cols + q]);
         for (int t = 0; t < ilog2(g.s1); t++) {
@@ -233,7 +237,7 @@ static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g) {
             acc = ev.add(acc, rot);
         }
         out[p] = acc;
-    }
+    });
     return out;
 }
 
@@ -286,9 +290,14 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
         return sums;
     }
     Ctx& C = ev.c;
+    // Branches may run concurrently only when no auto-bootstrap can fire
+    // inside (DiagABT consumes 3 levels), so the refresh-nonce order is the
+    // reference's sequential one.
+    const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
+    auto W = [&](int w) { return par ? w : 1; };
     // packing prologue, one branch per block column: B + i * RU(B, c/2)
     G packed(n);
-    par_for(C, n, n, [&](int q) {
+    par_for(C, n, W(n), [&](int q) {
         const int kk = (c / 2) % g.s0;
         CtP rolled = kk ? ev.lrot(B[q], (int64_t)kk * g.s1) : B[q];
         CtP mi = ev.mul_i(rolled);
@@ -297,14 +306,14 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     // the c/2 diagonal passes are independent: one branch each, and inside a
     // pass the per-block-column rotation + products run as nested branches
     std::vector<G> terms(c / 2);
-    par_for(C, c / 2, fork_width(C, c / 2), [&](int k) {
+    par_for(C, c / 2, W(fork_width(C, c / 2)), [&](int k) {
         G prod((size_t)m * n);
-        par_for(C, n, n, [&](int q) {
+        par_for(C, n, W(n), [&](int q) {
             const int kk = k % g.s0;
             CtP shifted = kk ? ev.lrot(packed[q], (int64_t)kk * g.s1) : packed[q];
             for (int p = 0; p < m; p++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], shifted);
         });
-        G sums = col_sums(ev, prod, m, n, g);
+        G sums = col_sums(ev, prod, m, n, g, W(m));
         const Pattern mask = diag_mask(g, k, c, true, scale);
         terms[k].resize(m);
         for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(sums[p], mask);
@@ -312,7 +321,7 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     G acc = terms[0];
     for (int k = 1; k < c / 2; k++)
         for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], terms[k][p]);
-    par_for(C, m, m, [&](int p) {
+    par_for(C, m, W(m), [&](int p) {
         CtP cj = ev.conj(acc[p]);
         acc[p] = ev.add(acc[p], cj);
     });
@@ -341,11 +350,15 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     const bool partial = grid_level(A) < grid_level(B);
     Ctx& C = ev.c;
     const int s1 = g.s1;
-    // with a cross-rank reducer the passes stay serial (collectives in a fixed order)
-    const int width = red ? 1 : fork_width(C, c / 2);
+    // Serial when an auto-bootstrap could fire inside (DiagATB consumes 4
+    // levels): concurrent branches would reorder the refresh nonces.  A
+    // cross-rank reducer is fine: the host still reaches the k-th pre-sum's
+    // collective in k order on every rank, and only that branch waits for it.
+    const bool ser = ev.auto_boot && std::min(grid_level(A), grid_level(B)) < 5;
+    const int width = ser ? 1 : fork_width(C, c / 2);
     // packing prologue per block row: A + i * RL(A, c/2)
     G packed(m);
-    par_for(C, m, red ? 1 : m, [&](int p) {
+    par_for(C, m, ser ? 1 :m, [&](int p) {
         G one = rot_left(ev, G{A[p]}, c / 2, g);
         CtP mi = ev.mul_i(one[0]);
         packed[p] = ev.add(A[p], mi);
@@ -361,7 +374,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
         }
         // products (and, on the PRU branch, the partial row rotation of B) per block column
         G prod((size_t)m * n);
-        par_for(C, n, red ? 1 : n, [&](int q) {
+        par_for(C, n, ser ? 1 :n, [&](int q) {
             for (int p = 0; p < m; p++) {
                 CtP r = B[(size_t)p * n + q];
                 if (partial) r = prot_up(ev, G{r}, k, g)[0];
@@ -378,7 +391,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
         if (red) red(pre);
         const Pattern mask = diag_mask(g, -k, c, true, scale);
         terms[k].resize(n);
-        par_for(C, n, red ? 1 : n, [&](int q) {
+        par_for(C, n, ser ? 1 :n, [&](int q) {
             CtP a = pre[q];
             for (int t = 0; t < ilog2(g.s0); t++) {
                 CtP rot = ev.lrot(a, (int64_t)(1 << t) * s1);
@@ -390,7 +403,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     G acc = terms[0];
     for (int k = 1; k < c / 2; k++)
         for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], terms[k][q]);
-    par_for(C, n, red ? 1 : n, [&](int q) {
+    par_for(C, n, ser ? 1 :n, [&](int q) {
         CtP cj = ev.conj(acc[q]);
         acc[q] = ev.add(acc[q], cj);
     });

@@ -167,6 +167,22 @@ def test_native_softmax_small12(golden):
     assert np.max(np.abs(P.decode(out, tol=1e-3) - golden["small_sm_out"])) < 1e-3
 
 
+def test_block_parallel_softmax_matches_sequential_oracle():
+    """4 block rows run as concurrent branches with the nonce plan: residues and
+    the nonce counter equal the oracle's sequential (block-interleaved) run."""
+    P = _prod()
+    rng = np.random.default_rng(9)
+    Z = rng.uniform(-60, 60, (64, 5))
+    g = P.CKKSContext("small12", 16, seed=13, auto_bootstrap=True)
+    o = R.OracleCKKSContext("small12", 16, seed=13, auto_bootstrap=True)
+    GZ, OZ = _enc_pair(g, o, Z, "horizontal")
+    out = P.a_softmax(GZ)
+    ref = S.a_softmax(OZ)
+    _same_grid(out, ref)
+    assert g.nonce == o.nonce
+    assert _ledger(g) == [o.ledger.counts()[k] for k in OPS]
+
+
 def test_dropin_per_op_equals_native(golden):
     """The reference op sequence (restated in oracle/slots.py) issued op by op
     through the product's EmulatorContext interface == the native schedule."""

@@ -44,26 +44,31 @@ struct KsGeo {
 
 // ---- A: ModUp conversion fused into the column pass --------------------------
 
+// Conversion constants live in registers and the per-limb base pointers are
+// formed once, so each converted element costs NA Shoup products and loads.
+template <int NA>
 struct LdModup {
-    const u64* __restrict__ Y;   // [nl][N] coefficient form, pre-scaled by (Q'/q_a)^-1
-    const u64* cf;               // na (value, shoup) pairs for target prime p
-    int lo, na;
+    const u64* __restrict__ y[NA];   // Y limbs of the digit, coefficient form, pre-scaled by (Q'/q_a)^-1
+    u64 w[NA], ws[NA];               // [Q'/q_a]_p and Shoup companions
+    int na;
     u64 p;
-    size_t N;
     __device__ __forceinline__ u64 operator()(size_t k) const {
         u64 acc = 0;
-        for (int a = 0; a < na; a++) acc += mul_shoup_lazy(Y[(size_t)(lo + a) * N + k], cf[2 * a], cf[2 * a + 1], p);
+#pragma unroll
+        for (int a = 0; a < NA; a++)
+            if (a < na) acc += mul_shoup_lazy(y[a][k], w[a], ws[a], p);
         // acc < 2 * na * p <= 8p
-        if (acc >= 4 * p) acc -= 4 * p;
-        if (acc >= 2 * p) acc -= 2 * p;
+        if (NA > 2 && acc >= 4 * p) acc -= 4 * p;
+        if (NA > 1 && acc >= 2 * p) acc -= 2 * p;
         return acc >= p ? acc - p : acc;
     }
     __device__ __forceinline__ void load8(size_t k, u64* x) const {
+#pragma unroll
         for (int e = 0; e < 8; e++) x[e] = (*this)(k + e);
     }
 };
 
-template <int LOGSZ, int SUBS>
+template <int LOGSZ, int SUBS, int NA>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
@@ -74,14 +79,18 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const size_t N = (size_t)1 << g.logN;
     const int lo = j * g.alpha;
     const int hi = min(lo + g.alpha, g.nl);
-    __shared__ u64 cf[16];
-    if (threadIdx.x < 2 * (hi - lo)) {
-        const int a = threadIdx.x >> 1;
-        cf[threadIdx.x] = modup_tab[(((size_t)(g.level * g.dnum + j) * g.alpha + a) * g.nall + pi) * 2 + (threadIdx.x & 1)];
-    }
-    __syncthreads();
     const u64 p = primes[pi].q;
-    LdModup ld{Y, cf, lo, hi - lo, p, N};
+    LdModup<NA> ld;
+    ld.na = hi - lo;
+    ld.p = p;
+    const u64* cf = modup_tab + (((size_t)(g.level * g.dnum + j) * g.alpha) * g.nall + pi) * 2;
+#pragma unroll
+    for (int a = 0; a < NA; a++) {
+        const int aa = a < ld.na ? a : 0;
+        ld.y[a] = Y + (size_t)(lo + aa) * N;
+        ld.w[a] = cf[(size_t)aa * g.nall * 2];
+        ld.ws[a] = cf[(size_t)aa * g.nall * 2 + 1];
+    }
     StPlain<false, false> st{I + ((size_t)j * g.nt + t) * N, p, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(g.N1);
@@ -230,39 +239,25 @@ __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev
 
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
-struct LdModdown {
-    const u64* __restrict__ Yp;  // [K][N] of this poly, pre-scaled by (P/p_t)^-1
-    const u64* cf;               // K (value, shoup) pairs for target q_i
-    int K;
-    u64 q;
-    size_t N;
-    __device__ __forceinline__ u64 operator()(size_t k) const {
-        u64 acc = 0;
-        for (int t = 0; t < K; t++) acc += mul_shoup_lazy(Yp[(size_t)t * N + k], cf[2 * t], cf[2 * t + 1], q);
-        if (acc >= 4 * q) acc -= 4 * q;
-        if (acc >= 2 * q) acc -= 2 * q;
-        return acc >= q ? acc - q : acc;
-    }
-    __device__ __forceinline__ void load8(size_t k, u64* x) const {
-        for (int e = 0; e < 8; e++) x[e] = (*this)(k + e);
-    }
-};
-
-template <int LOGSZ, int SUBS>
+// (the P -> Q conversion has the ModUp loader's shape: K inputs, one target)
+template <int LOGSZ, int SUBS, int NK>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
-    __shared__ u64 cf[16];
-    if (threadIdx.x < 2 * g.K) {
-        const int t = threadIdx.x >> 1;
-        cf[threadIdx.x] = md_tab[((size_t)t * g.nall + i) * 2 + (threadIdx.x & 1)];
-    }
-    __syncthreads();
     const u64 q = primes[i].q;
-    LdModdown ld{acc + ((size_t)s * g.nt + g.nl) * N, cf, g.K, q, N};
+    LdModup<NK> ld;
+    ld.na = g.K;
+    ld.p = q;
+#pragma unroll
+    for (int t = 0; t < NK; t++) {
+        const int tt = t < g.K ? t : 0;
+        ld.y[t] = acc + ((size_t)s * g.nt + g.nl + tt) * N;
+        ld.w[t] = md_tab[((size_t)tt * g.nall + i) * 2];
+        ld.ws[t] = md_tab[((size_t)tt * g.nall + i) * 2 + 1];
+    }
     StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(g.N1);
@@ -461,11 +456,18 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             }
         }
         static bool at = false;
-        set_smem(ks_modup_cols<CL, CS>, csm, at);
         Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + 2.0 * jobs.n));
         dim3 grid((N >> CL) / CS, jobs.n);
-        ks_modup_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y,
-                                                                    c.d_modup, I);
+        auto go = [&](auto kern) {
+            set_smem(kern, csm, at);
+            kern<<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
+        };
+        switch (c.alpha) {
+            case 1: go(ks_modup_cols<CL, CS, 1>); break;
+            case 2: go(ks_modup_cols<CL, CS, 2>); break;
+            case 3: go(ks_modup_cols<CL, CS, 3>); break;
+            default: go(ks_modup_cols<CL, CS, 4>); break;
+        }
         HC_CUDA(cudaGetLastError());
     }
     c.free(Y);
@@ -528,11 +530,18 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
     u64* Wt = c.alloc((size_t)2 * nl * N);
     {
         static bool at = false;
-        set_smem(ks_moddown_cols<CL, CS>, csm, at);
         Launch scope(c, "ks_moddown_cols", 8.0 * N * (2.0 * K + 2.0 * nl));
         dim3 grid((N >> CL) / CS, 2 * nl);
-        ks_moddown_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.twp(0, false), ACC,
-                                                                      c.d_moddown, Wt);
+        auto go = [&](auto kern) {
+            set_smem(kern, csm, at);
+            kern<<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
+        };
+        switch (K) {
+            case 1: go(ks_moddown_cols<CL, CS, 1>); break;
+            case 2: go(ks_moddown_cols<CL, CS, 2>); break;
+            case 3: go(ks_moddown_cols<CL, CS, 3>); break;
+            default: go(ks_moddown_cols<CL, CS, 4>); break;
+        }
         HC_CUDA(cudaGetLastError());
     }
     // 6. E: chunk pass + (ACC - W) P^-1 + addend
@@ -551,7 +560,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
 
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
                      int add_npoly, u64 add_gal) {
-    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 8 || c.alpha > 8) return false;
+    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 4 || c.alpha > 4) return false;
     switch (c.logN) {
         case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
         case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;

@@ -160,6 +160,7 @@ struct Launch {
 void ntt_forward(Ctx& c, const JobList& jobs);
 void ntt_inverse(Ctx& c, const JobList& jobs);
 void ntt_forward_chunks(Ctx& c, const JobList& jobs);
+void ntt_inverse_cols(Ctx& c, const JobList& jobs);
 
 // ---- context (context.cu) ----
 Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, int alpha,

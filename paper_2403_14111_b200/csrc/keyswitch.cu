@@ -186,9 +186,9 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
 __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
                                                          const u64* __restrict__ UP, const u64* __restrict__ d,
                                                          u64 gal, const u64* __restrict__ key,
-                                                         u64* __restrict__ acc) {
+                                                         u64* __restrict__ acc, int tlimit) {
     const size_t N = (size_t)1 << g.logN;
-    const size_t total = (size_t)g.nt << (g.logN - 1);
+    const size_t total = (size_t)tlimit << (g.logN - 1);
     const size_t kstride = (size_t)g.nall * N;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
         const int t = (int)(v >> (g.logN - 1));
@@ -234,6 +234,69 @@ __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev
             make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
         *reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k) =
             make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
+    }
+}
+
+// ---- B2 for the P limbs: key product + the first (chunk) pass of their INTT --
+// Each thread owns 8 consecutive coefficients, which are exactly the
+// elements the inverse chunk pass's first round needs, so the products never
+// leave registers before the transform.
+
+struct LdRegs {
+    const u64* x;
+    __device__ __forceinline__ u64 operator()(size_t) const { return 0; }   // unused: edge is contiguous
+    __device__ __forceinline__ void load8(size_t, u64* o) const {
+#pragma unroll
+        for (int e = 0; e < 8; e++) o[e] = x[e];
+    }
+};
+
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
+    ks_keyprod_p_intt(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ itw,
+                      const u64* __restrict__ UP, const u64* __restrict__ key, u64* __restrict__ acc) {
+    using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
+    extern __shared__ u64 sm[];
+    const int t = g.nl + blockIdx.y;            // P limb (never inside a Q digit)
+    const int pi = g.prime(t);
+    const size_t N = (size_t)1 << g.logN;
+    const PrimeDev P = primes[pi];
+    PG G;
+    G.init(g.N1);
+    const size_t k0 = G.gidx(G.lt * 8);
+    const size_t kstride = (size_t)g.nall * N;
+    u64 r0[8], r1[8];
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
+#pragma unroll
+        for (int j = 0; j < KP_MAXB; j++) {
+            if (j >= g.beta) break;
+            const ulonglong2 xv =
+                *reinterpret_cast<const ulonglong2*>(UP + ((size_t)j * g.nt + t) * N + k0 + 2 * v);
+            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0 + 2 * v;
+            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
+            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
+            mac128(b0, xv.x, kbv.x);
+            mac128(b1, xv.y, kbv.y);
+            mac128(a0, xv.x, kav.x);
+            mac128(a1, xv.y, kav.y);
+        }
+        r0[2 * v] = reduce128(b0.hi, b0.lo, P);
+        r0[2 * v + 1] = reduce128(b1.hi, b1.lo, P);
+        r1[2 * v] = reduce128(a0.hi, a0.lo, P);
+        r1[2 * v + 1] = reduce128(a1.hi, a1.lo, P);
+    }
+    const ulonglong2* TW = itw + ((size_t)pi << g.logN);
+    {
+        LdRegs ld{r0};
+        StPlain<true, false> st{acc + (size_t)t * N, P.q, 0, 0};
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true>(G, sm, TW, P.q, ld, st);
+    }
+    __syncthreads();
+    {
+        LdRegs ld{r1};
+        StPlain<true, false> st{acc + ((size_t)g.nt + t) * N, P.q, 0, 0};
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true>(G, sm, TW, P.q, ld, st);
     }
 }
 
@@ -489,11 +552,21 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             }
         }
         ntt_forward_chunks(c, j);
-        const size_t work = (size_t)nt * (N / 2);
-        Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * nt + 2.0 * g.beta * nt + 2.0 * nt));
-        int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
-        ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC);
-        HC_CUDA(cudaGetLastError());
+        {
+            // Q limbs: streaming key product
+            const size_t work = (size_t)nl * (N / 2);
+            Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * nl + 2.0 * g.beta * nl + 2.0 * nl));
+            int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
+            ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC, nl);
+            HC_CUDA(cudaGetLastError());
+        }
+        {
+            // P limbs: key product fused with the first pass of their INTT
+            Launch scope(c, "ks_keyprod_p_intt", 8.0 * N * ((double)g.beta * K + 2.0 * g.beta * K + 2.0 * K));
+            dim3 grid((N >> CH_LOG) / CH_SUBS, K);
+            ks_keyprod_p_intt<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, true), I, key.d, ACC);
+            HC_CUDA(cudaGetLastError());
+        }
     } else {
         static bool at = false;
         set_smem(ks_chunks_keyprod, hsm, at);
@@ -524,7 +597,8 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
                 j.scale_s[j.n] = shoup_of(sc, p);
                 j.n++;
             }
-        ntt_inverse(c, j);
+        if (c.ks_split) ntt_inverse_cols(c, j);     // chunk pass already done in ks_keyprod_p_intt
+        else ntt_inverse(c, j);
     }
     // 5. D: P -> Q conversion + column pass
     u64* Wt = c.alloc((size_t)2 * nl * N);

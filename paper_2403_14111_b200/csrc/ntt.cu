@@ -116,6 +116,12 @@ void ntt_forward_chunks(Ctx& c, const JobList& jobs) {
     chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 1);
 }
 
+// second half of a split inverse NTT (in place, final scaling)
+void ntt_inverse_cols(Ctx& c, const JobList& jobs) {
+    if (jobs.n == 0) return;
+    cols_pass(c, jobs, true, 1 << (c.logN - 9), 0, 1);
+}
+
 void ntt_forward(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
     if (c.logN <= 13) { full_pass(c, jobs, false); return; }

@@ -552,16 +552,17 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             }
         }
         ntt_forward_chunks(c, j);
+        // ks_split == 2: P limbs take the fused key-product + INTT-chunk kernel
+        // (measured slower: a 96-CTA grid; kept as an option)
+        const int tq = c.ks_split == 2 ? nl : nt;
         {
-            // Q limbs: streaming key product
-            const size_t work = (size_t)nl * (N / 2);
-            Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * nl + 2.0 * g.beta * nl + 2.0 * nl));
+            const size_t work = (size_t)tq * (N / 2);
+            Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * tq + 2.0 * g.beta * tq + 2.0 * tq));
             int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
-            ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC, nl);
+            ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC, tq);
             HC_CUDA(cudaGetLastError());
         }
-        {
-            // P limbs: key product fused with the first pass of their INTT
+        if (c.ks_split == 2) {
             Launch scope(c, "ks_keyprod_p_intt", 8.0 * N * ((double)g.beta * K + 2.0 * g.beta * K + 2.0 * K));
             dim3 grid((N >> CH_LOG) / CH_SUBS, K);
             ks_keyprod_p_intt<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, true), I, key.d, ACC);
@@ -597,7 +598,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
                 j.scale_s[j.n] = shoup_of(sc, p);
                 j.n++;
             }
-        if (c.ks_split) ntt_inverse_cols(c, j);     // chunk pass already done in ks_keyprod_p_intt
+        if (c.ks_split == 2) ntt_inverse_cols(c, j);     // chunk pass already done in ks_keyprod_p_intt
         else ntt_inverse(c, j);
     }
     // 5. D: P -> Q conversion + column pass

@@ -282,6 +282,27 @@ int hc_timer_end(hc_ctx* ctx, float* ms) {
 
 int64_t hc_launch_count(hc_ctx* ctx) { return ctx->c->launches; }
 
+static void snap(hc_ctx* ctx, int64_t* b);
+
+int hc_bench_keyswitch(hc_ctx* ctx, const hc_ct* a, int streams, int reps, float* ms) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        int64_t saved[HC_NCOUNTS];
+        snap(ctx, saved);
+        hc::Eval ev(c, false);
+        hc::probe_rotations(ev, a->p, streams, 1);     // warm keys and pool
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+        if (!c.t0) { HC_CUDA(cudaEventCreate(&c.t0)); HC_CUDA(cudaEventCreate(&c.t1)); }
+        HC_CUDA(cudaEventRecord(c.t0, c.stream));
+        hc::probe_rotations(ev, a->p, streams, reps);
+        HC_CUDA(cudaEventRecord(c.t1, c.stream));
+        HC_CUDA(cudaEventSynchronize(c.t1));
+        HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
+        std::lock_guard<std::mutex> g(c.mu);
+        for (int i = 0; i < HC_NCOUNTS; i++) c.counts[i] = saved[i];
+    });
+}
+
 int hc_prof_begin(hc_ctx* ctx) {
     return guard([&] {
         hc::Ctx& c = *ctx->c;

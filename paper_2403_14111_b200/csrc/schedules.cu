@@ -273,6 +273,19 @@ static int geo_rows(const Eval& ev) {
     return ev.c.grid_rows;
 }
 
+// ---- key-switch throughput probe (measurement only) ------------------------
+// `streams` independent chains of `reps` rotations each (chain i rotates by
+// i + 1, so every chain uses its own key), issued through the same fork/join
+// machinery as the schedules.  Returns the number of key switches issued.
+int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps) {
+    for (int i = 0; i < streams; i++) get_key(ev.c, (int)galois_rot(ev.c, i + 1));
+    par_for(ev.c, streams, streams, [&](int i) {
+        CtP a = x;
+        for (int r = 0; r < reps; r++) a = ev.lrot(a, i + 1);
+    });
+    return (int64_t)streams * reps;
+}
+
 // ---- DiagABT (matmul.py:74-110) --------------------------------------------
 
 std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int n, const std::vector<CtP>& B, int c,

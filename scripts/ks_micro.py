@@ -56,5 +56,27 @@ def main():
                       "legend": "kernel: [launches, total_us, algorithmic GB/s]"}))
 
 
+
+
+def throughput(params="cfg1", level=12, reps=8):
+    """Key switches per second with `s` concurrent independent chains."""
+    ctx = P.CKKSContext(params, None, seed=3)
+    x = ctx.encrypt(np.random.default_rng(0).uniform(-1, 1, ctx.slot_count), level)
+    L = N.lib()
+    out = {}
+    for s in (1, 2, 4, 8, 16, 32):
+        ms = C.c_float()
+        N.check(L.hc_bench_keyswitch(ctx._h, x._h, s, reps, C.byref(ms)))
+        out[s] = round(s * reps / (ms.value * 1e-3))
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if "--throughput" in sys.argv:
+        lv = 12
+        for a in sys.argv:
+            if a.startswith("--level="):
+                lv = int(a.split("=")[1])
+        print(json.dumps({"keyswitch_per_s_by_streams": throughput(level=lv), "level": lv}))
+    else:
+        main()

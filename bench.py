@@ -108,9 +108,22 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch
         import torch.distributed as dist
+        ndev = torch.cuda.device_count()
+        local = local % max(ndev, 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # HC_DIST_BACKEND=gloo lets the multi-rank plumbing run with several ranks
+        # on one device (functional check only; timings are then meaningless)
+        backend = os.environ.get("HC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
+
+
+def _coll_device():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 def all_max(x, world):
@@ -118,7 +131,7 @@ def all_max(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda")
+    t = torch.tensor([float(x)], device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

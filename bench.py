@@ -154,6 +154,9 @@ def oracle_pass_sample(reps=1):
     on the C RNS-CKKS oracle, all host threads; returns ms per pair
     extrapolated x8 (prologue/epilogue key switches, ~3% of the pair, are
     not counted, which flatters the CPU)."""
+    # torchrun exports OMP_NUM_THREADS=1; the CPU leg uses every host thread
+    # (read by libgomp when the oracle library loads)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     from oracle import rns as R
     from oracle import slots as S
     from paper_2403_14111_b200 import workloads as wl

@@ -235,6 +235,16 @@ CtP ev_automorph(Ctx& c, const Ct& a, u64 g) {
     return o;
 }
 
+bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out) {
+    if (c.logN < 14) return false;
+    const Key& key = get_key(c, (int)g);
+    CtP o = new_ct(c, a.level);
+    if (!keyswitch_fused(c, a.poly(1), g, a.level, key, o->d, a.poly(0), 1, g, a.d)) return false;
+    c.counts[OP_KS]++;
+    out = o;
+    return true;
+}
+
 CtP ev_mult(Ctx& c, const Ct& a, const Ct& b) {
     check_same(a, b);
     if (a.level < 1) throw Error(-3, "multiply at level 0");
@@ -340,6 +350,18 @@ CtP Eval::lrot(const CtP& a, int64_t r) {
     if (r == 0) return a;
     rec(OP_ROT);
     return ev_automorph(c, *a, galois_rot(c, r));
+}
+
+CtP Eval::add_lrot(const CtP& a, int64_t r) {
+    const int64_t S = c.N / 2;
+    r = ((r % S) + S) % S;
+    if (r == 0) return add(a, a);
+    rec(OP_ROT);
+    rec(OP_ADD);
+    CtP o;
+    if (ev_automorph_add(c, *a, galois_rot(c, r), o)) return o;
+    CtP rot = ev_automorph(c, *a, galois_rot(c, r));
+    return ev_add(c, *a, *rot, false);
 }
 
 CtP Eval::conj(const CtP& a) {

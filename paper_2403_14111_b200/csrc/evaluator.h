@@ -17,7 +17,9 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
 // fused pipeline (keyswitch.cu) for split-pass rings; false when N < 2^14.
 // d and the addend are read through the galois permutation gal / add_gal (0 = none).
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
-                     int add_npoly, u64 add_gal);
+                     int add_npoly, u64 add_gal, const u64* addend2 = nullptr);
+// out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
+bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
 
 // a plaintext slot pattern with a cache key (content-addressed by the caller).
@@ -63,6 +65,9 @@ struct Eval {
     CtP mult_p(const CtP& a, const Pattern& p);
     CtP lrot(const CtP& a, int64_t r);
     CtP rrot(const CtP& a, int64_t r) { return lrot(a, -r); }
+    // add(a, lrot(a, r)): one Rot + one Add on the ledger, fused into the key switch
+    CtP add_lrot(const CtP& a, int64_t r);
+    CtP add_rrot(const CtP& a, int64_t r) { return add_lrot(a, -r); }
     CtP conj(const CtP& a);
     CtP mul_i(const CtP& a);
     CtP bootstrap(const CtP& a);

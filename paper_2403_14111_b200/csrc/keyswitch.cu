@@ -335,9 +335,10 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
 struct StModdown {
     u64* __restrict__ out;           // [nl][N] of this poly
     const u64* __restrict__ accq;    // ACC Q limb i of this poly (full limb base)
-    const u64* __restrict__ add;     // addend limb base or nullptr
+    const u64* __restrict__ add;     // addend limb base or nullptr (read through gal)
     u64 q, pinv, pinv_s, gal;
     int logN;
+    const u64* __restrict__ add2;    // second addend limb (not permuted) or nullptr: rotate-and-add ladders
     __device__ __forceinline__ u64 one(size_t k, u64 w) const {
         w = w >= 2 * q ? w - 2 * q : w;
         w = w >= q ? w - q : w;
@@ -346,6 +347,7 @@ struct StModdown {
             const u64 a = gal ? add[galois_src((unsigned)k, logN, gal)] : add[k];
             v = add_mod(v, a, q);
         }
+        if (add2) v = add_mod(v, add2[k], q);
         return v;
     }
     __device__ __forceinline__ void operator()(size_t k, u64 w) const { out[k] = one(k, w); }
@@ -359,7 +361,7 @@ struct StModdown {
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly, u64 add_gal,
-                      u64* __restrict__ out) {
+                      const u64* __restrict__ addend2, u64* __restrict__ out) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
     StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
                  (s < add_npoly) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
-                 add_gal, g.logN};
+                 add_gal, g.logN, addend2 ? addend2 + ((size_t)s * g.nl + i) * N : nullptr};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
     G.init(g.N1);
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
@@ -475,7 +477,7 @@ template <> struct ColCfg<17> { static constexpr int LOGSZ = 8, SUBS = 8; };
 
 template <int LOGN>
 static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out,
-                              const u64* addend, int add_npoly, u64 add_gal) {
+                              const u64* addend, int add_npoly, u64 add_gal, const u64* addend2) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
@@ -626,7 +628,7 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (2.0 * nl * 3 + (double)add_npoly * nl));
         dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl);
         ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
-                                                                addend, add_npoly, add_gal, out);
+                                                                addend, add_npoly, add_gal, addend2, out);
         HC_CUDA(cudaGetLastError());
     }
     c.free(Wt);
@@ -634,13 +636,13 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
 }
 
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
-                     int add_npoly, u64 add_gal) {
+                     int add_npoly, u64 add_gal, const u64* addend2) {
     if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 4 || c.alpha > 4) return false;
     switch (c.logN) {
-        case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
-        case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
-        case 16: keyswitch_fused_t<16>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
-        case 17: keyswitch_fused_t<17>(c, d, gal, level, key, out, addend, add_npoly, add_gal); return true;
+        case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
+        case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
+        case 16: keyswitch_fused_t<16>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
+        case 17: keyswitch_fused_t<17>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
         default: return false;
     }
 }

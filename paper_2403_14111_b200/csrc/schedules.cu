@@ -227,15 +227,9 @@ static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, int width
     par_for(ev.c, r, width, [&](int p) {
         CtP acc = E[(size_t)p * cols];
         for (int q = 1; q < cols; q++) acc = ev.add(acc, E[(size_t)p * cols + q]);
-        for (int t = 0; t < ilog2(g.s1); t++) {
-            CtP rot = ev.lrot(acc, 1 << t);
-            acc = ev.add(acc, rot);
-        }
+        for (int t = 0; t < ilog2(g.s1); t++) acc = ev.add_lrot(acc, 1 << t);
         acc = ev.mult_p(acc, c0);
-        for (int t = 0; t < ilog2(g.s1); t++) {
-            CtP rot = ev.rrot(acc, 1 << t);
-            acc = ev.add(acc, rot);
-        }
+        for (int t = 0; t < ilog2(g.s1); t++) acc = ev.add_rrot(acc, 1 << t);
         out[p] = acc;
     });
     return out;
@@ -253,10 +247,7 @@ static G row_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, const Red
     if (red) red(pre);
     for (int q = 0; q < cols; q++) {
         CtP acc = pre[q];
-        for (int t = 0; t < ilog2(g.s0); t++) {
-            CtP rot = ev.lrot(acc, (int64_t)(1 << t) * g.s1);
-            acc = ev.add(acc, rot);
-        }
+        for (int t = 0; t < ilog2(g.s0); t++) acc = ev.add_lrot(acc, (int64_t)(1 << t) * g.s1);
         pre[q] = acc;
     }
     return pre;
@@ -406,10 +397,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
         terms[k].resize(n);
         par_for(C, n, ser ? 1 :n, [&](int q) {
             CtP a = pre[q];
-            for (int t = 0; t < ilog2(g.s0); t++) {
-                CtP rot = ev.lrot(a, (int64_t)(1 << t) * s1);
-                a = ev.add(a, rot);
-            }
+            for (int t = 0; t < ilog2(g.s0); t++) a = ev.add_lrot(a, (int64_t)(1 << t) * s1);
             terms[k][q] = ev.mult_p(a, mask);
         });
     });
@@ -527,10 +515,8 @@ struct SM {
             best = add(x1, x3);
         }
         best = mulp(best, col0(g));
-        for (int t = 0; t < ilog2(g.s1); t++) {
-            G r = rrot(best, 1 << t);
-            best = add(best, r);
-        }
+        for (int t = 0; t < ilog2(g.s1); t++)
+            for (auto& b : best) b = ev.add_rrot(b, 1 << t);
         return scale(best, two_r);
     }
     G domain_extend(G M, const SoftmaxCfg& cfg) {
@@ -639,10 +625,8 @@ static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int 
     G recip = sm.inv(total, cfg);
     G out = sm.mul(expd, recip);
     const int reps = g.s1 / period;
-    for (int t = 0; t < ilog2(reps); t++) {
-        G r = sm.rrot(out, period * (1 << t));
-        out = sm.add(out, r);
-    }
+    for (int t = 0; t < ilog2(reps); t++)
+        for (auto& b : out) b = ev.add_rrot(b, period * (1 << t));
     return out;
 }
 

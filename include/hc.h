@@ -127,6 +127,13 @@ int hc_diag_abt(hc_ctx *ctx, const hc_ct *const *A, int m, int n, const hc_ct *c
 typedef int (*hc_reduce_fn)(void *user, hc_ct **cts, int count);
 int hc_diag_atb(hc_ctx *ctx, const hc_ct *const *A, int m, const hc_ct *const *B, int n, int c, double scale,
                 hc_ct **out, int64_t *counts, hc_reduce_fn reduce_fn, void *user);
+/* Table-4 baselines: col_major_abt (matmul.py:160-198), A[m][n] and B[n] untiled
+ * (B's c <= s1 rows in one block row), out[m]; row_major_atb (matmul.py:201-237),
+ * A[m] untiled (c <= s0 columns), B[m][n], out[n] */
+int hc_col_major_abt(hc_ctx *ctx, const hc_ct *const *A, int m, int n, const hc_ct *const *B, int c, double scale,
+                     hc_ct **out, int64_t *counts);
+int hc_row_major_atb(hc_ctx *ctx, const hc_ct *const *A, int m, const hc_ct *const *B, int n, int c, double scale,
+                     hc_ct **out, int64_t *counts);
 /* a_softmax (approx.py:312-344) on one horizontally tiled block column A[m] */
 int hc_softmax(hc_ctx *ctx, const hc_ct *const *A, int m, int classes, int period, const double *cfg, hc_ct **out,
                int64_t *counts);

@@ -537,6 +537,69 @@ def diag_atb(A, B, scale=1.0, presum=row_presum):                   # matmul.py:
     return acc.add(acc.conj()).meta(out_shape, "vertical", c)
 
 
+def col_major_abt(A, B, scale=1.0):                                 # matmul.py:160-198
+    """Table-4 baseline: one mask-replicate-reduce pass per row j of B."""
+    if A.tiling != "none" or B.tiling != "none" or A.shape[1] != B.shape[1]:
+        raise ShapeMismatch("col_major_abt layout")
+    ctx = A.ctx
+    s0, s1 = ctx.grid_rows, ctx.grid_cols
+    c = B.shape[0]
+    if B.grid[0] != 1 or c > s1:
+        raise ShapeMismatch("col_major_abt: B must fit one block row")
+    m, n = A.grid
+    c0 = np.zeros((s0, s1))
+    c0[:, 0] = scale
+    c0b = ctx.pack(c0.ravel())
+    acc = None
+    for j in range(c):
+        rowj = np.zeros((s0, s1))
+        rowj[j, :] = 1.0
+        picked = B.mul(pattern(ctx, rowj, B.grid))
+        for t in range(lg(s0)):
+            picked = picked.add(picked.lrot((1 << t) * s1))
+        prod = _rowwise(A, picked)
+        folded = []
+        for p in range(m):
+            blk = prod.blocks[p][0]
+            for q in range(1, n):
+                blk = ctx.add(blk, prod.blocks[p][q])
+            for t in range(lg(s1)):
+                blk = ctx.add(blk, ctx.lrot(blk, 1 << t))
+            blk = ctx.cmult(blk, c0b)
+            blk = ctx.rrot(blk, j)
+            folded.append((blk,))
+        term = Grid(ctx, folded, (A.shape[0], c))
+        acc = term if acc is None else acc.add(term)
+    return acc.meta((A.shape[0], c))
+
+
+def row_major_atb(A, B, scale=1.0):                                 # matmul.py:201-237
+    """Table-4 baseline: one pass per column j of A."""
+    if A.tiling != "none" or B.tiling != "none" or A.shape[0] != B.shape[0]:
+        raise ShapeMismatch("row_major_atb layout")
+    ctx = A.ctx
+    s0, s1 = ctx.grid_rows, ctx.grid_cols
+    c = A.shape[1]
+    if A.grid[1] != 1 or c > s0:
+        raise ShapeMismatch("row_major_atb: A must fit one block column")
+    n = B.grid[1]
+    c0 = np.zeros((s0, s1))
+    c0[:, 0] = 1.0
+    c0b = ctx.pack(c0.ravel())
+    acc = None
+    for j in range(c):
+        picked = A.lrot(j)
+        picked = picked.each(lambda b: ctx.cmult(b, c0b))
+        for t in range(lg(s1)):
+            picked = picked.add(picked.rrot(1 << t))
+        sums = row_sums(_colwise(picked, B))
+        rowj = np.zeros((s0, s1))
+        rowj[j, :] = scale
+        term = sums.mul(pattern(ctx, rowj, (1, n)))
+        acc = term if acc is None else acc.add(term)
+    return acc.meta((c, B.shape[1]))
+
+
 def count_formula(algorithm, shape, s0, s1):                        # matmul.py:253-296
     a, b, c = (int(v) for v in shape)
     m, n = -(-a // s0), -(-b // s1)
@@ -554,6 +617,8 @@ def count_formula(algorithm, shape, s0, s1):                        # matmul.py:
             return {"CMult": n, "Mult": m * n, "Rot": n * l0}
         return {"CMult": m + (h - 1) * m * n + h * n, "Mult": h * m * n,
                 "Rot": 2 * m + (h - 1) * (m + m * n) + h * n * l0}
+    if algorithm in ("col_major", "row_major"):
+        return {"CMult": c * (n + m), "Mult": c * m * n, "Rot": c * (n * l0 + m * l1 + m) - m}
     raise ShapeMismatch(algorithm)
 
 

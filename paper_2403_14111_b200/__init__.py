@@ -41,7 +41,7 @@ from .errors import (
     SlotCountMismatch,
     TilingError,
 )
-from .matmul import ALGORITHMS, count_formula, diag_abt, diag_atb, rotation_steps
+from .matmul import ALGORITHMS, col_major_abt, count_formula, diag_abt, diag_atb, rotation_steps, row_major_atb
 from .training import TrainState, init_weights, nag_step, one_hot, run_steps
 
 __version__ = "0.1.0"

@@ -73,6 +73,8 @@ SIGNATURES = {
     "hc_diag_abt": (I, [P, PP, I, I, PP, I, D, PP, I64P]),
     "hc_diag_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P, REDUCE_FN, P]),
     "hc_softmax": (I, [P, PP, I, I, I, DP, PP, I64P]),
+    "hc_col_major_abt": (I, [P, PP, I, I, PP, I, D, PP, I64P]),
+    "hc_row_major_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P]),
     "hc_mod_reduce": (I, [P, P]),
     "hc_timer_begin": (I, [P]),
     "hc_timer_end": (I, [P, C.POINTER(C.c_float)]),

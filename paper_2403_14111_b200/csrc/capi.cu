@@ -422,6 +422,32 @@ int hc_diag_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B
     });
 }
 
+int hc_col_major_abt(hc_ctx* ctx, const hc_ct* const* A, int m, int n, const hc_ct* const* B, int c, double scale,
+                     hc_ct** out, int64_t* counts) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        RunAhead throttle(*ctx->c);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        std::vector<hc::CtP> res = hc::sched_col_major_abt(ev, unwrap(A, m * n), m, n, unwrap(B, n), c, scale);
+        for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
+int hc_row_major_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B, int n, int c, double scale,
+                     hc_ct** out, int64_t* counts) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        RunAhead throttle(*ctx->c);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        std::vector<hc::CtP> res = hc::sched_row_major_atb(ev, unwrap(A, m), m, unwrap(B, m * n), n, c, scale);
+        for (int i = 0; i < n; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
 int hc_softmax(hc_ctx* ctx, const hc_ct* const* A, int m, int classes, int period, const double* cfg, hc_ct** out,
                int64_t* counts) {
     return guard([&] {

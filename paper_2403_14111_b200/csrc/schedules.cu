@@ -411,6 +411,84 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     return acc;
 }
 
+// ---- Table-4 baselines (matmul.py:160-237) ---------------------------------
+
+static Pattern row_select(const Geo& g, int j, double v) {
+    Pattern p;
+    p.key = "rowsel:" + std::to_string(g.s0) + ":" + std::to_string(j) + ":" + dkey(v);
+    p.gen = [g, j, v](std::vector<cd>& vals) {
+        for (int i = 0; i < g.s0; i++)
+            for (int k = 0; k < g.s1; k++) vals[(size_t)i * g.s1 + k] = cd(i == j ? v : 0.0, 0.0);
+    };
+    return p;
+}
+
+static Pattern col0_scaled(const Geo& g, double v) {
+    return col_pattern(g, "col0s:" + dkey(v), [v](int j) { return j == 0 ? v : 0.0; });
+}
+
+// col_major_abt: A (m x n grid, untiled), B (1 x n, untiled, c rows); out m blocks
+std::vector<CtP> sched_col_major_abt(Eval& ev, const std::vector<CtP>& A, int m, int n, const std::vector<CtP>& B,
+                                     int c, double scale) {
+    const Geo g = geo(ev, geo_rows(ev));
+    if (c < 1 || c > g.s1) throw Error(-4, "col_major_abt: B rows must fit one block");
+    if ((int)A.size() != m * n || (int)B.size() != n) throw Error(-4, "col_major_abt: grid mismatch");
+    const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
+    const Pattern c0 = col0_scaled(g, scale);
+    std::vector<G> terms(c);
+    par_for(ev.c, c, par ? fork_width(ev.c, c) : 1, [&](int j) {
+        const Pattern rowj = row_select(g, j, 1.0);
+        G picked(n);
+        for (int q = 0; q < n; q++) picked[q] = ev.mult_p(B[q], rowj);
+        for (int t = 0; t < ilog2(g.s0); t++)
+            for (int q = 0; q < n; q++) picked[q] = ev.add_lrot(picked[q], (int64_t)(1 << t) * g.s1);
+        G prod((size_t)m * n);
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], picked[q]);
+        terms[j].resize(m);
+        for (int p = 0; p < m; p++) {
+            CtP blk = prod[(size_t)p * n];
+            for (int q = 1; q < n; q++) blk = ev.add(blk, prod[(size_t)p * n + q]);
+            for (int t = 0; t < ilog2(g.s1); t++) blk = ev.add_lrot(blk, 1 << t);
+            blk = ev.mult_p(blk, c0);
+            terms[j][p] = ev.rrot(blk, j);
+        }
+    });
+    G acc = terms[0];
+    for (int j = 1; j < c; j++)
+        for (int p = 0; p < m; p++) acc[p] = ev.add(acc[p], terms[j][p]);
+    return acc;
+}
+
+// row_major_atb: A (m x 1 grid, untiled, c columns), B (m x n); out n blocks
+std::vector<CtP> sched_row_major_atb(Eval& ev, const std::vector<CtP>& A, int m, const std::vector<CtP>& B, int n,
+                                     int c, double scale) {
+    const Geo g = geo(ev, geo_rows(ev));
+    if (c < 1 || c > g.s0) throw Error(-4, "row_major_atb: A columns must fit one block");
+    if ((int)A.size() != m || (int)B.size() != m * n) throw Error(-4, "row_major_atb: grid mismatch");
+    const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
+    const Pattern c0 = col0(g);
+    std::vector<G> terms(c);
+    par_for(ev.c, c, par ? fork_width(ev.c, c) : 1, [&](int j) {
+        G picked(m);
+        for (int p = 0; p < m; p++) picked[p] = ev.lrot(A[p], j);
+        for (int p = 0; p < m; p++) picked[p] = ev.mult_p(picked[p], c0);
+        for (int t = 0; t < ilog2(g.s1); t++)
+            for (int p = 0; p < m; p++) picked[p] = ev.add_rrot(picked[p], 1 << t);
+        G prod((size_t)m * n);
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(picked[p], B[(size_t)p * n + q]);
+        G sums = row_sums(ev, prod, m, n, g, Reducer());
+        const Pattern rowj = row_select(g, j, scale);
+        terms[j].resize(n);
+        for (int q = 0; q < n; q++) terms[j][q] = ev.mult_p(sums[q], rowj);
+    });
+    G acc = terms[0];
+    for (int j = 1; j < c; j++)
+        for (int q = 0; q < n; q++) acc[q] = ev.add(acc[q], terms[j][q]);
+    return acc;
+}
+
 // ---- approximate softmax (approx.py:195-344), encrypted carrier ------------
 
 namespace {

@@ -98,6 +98,46 @@ def diag_atb(A: EncodedMatrix, B: EncodedMatrix, scale: float = 1.0, reducer=Non
     return EncodedMatrix(ctx, blocks, (A.shape[1], B.shape[1]), "vertical", c)
 
 
+def col_major_abt(A: EncodedMatrix, B: EncodedMatrix, scale: float = 1.0) -> EncodedMatrix:
+    """Table-4 baseline ``scale * A B^T`` with both operands untiled (matmul.py:160-198):
+    one mask-replicate-reduce pass per row of B; 3 levels."""
+    if A.tiling != "none" or B.tiling != "none":
+        raise ShapeMismatch("col_major_abt: expected untiled operands")
+    if A.shape[1] != B.shape[1]:
+        raise ShapeMismatch(f"col_major_abt: inner dims differ, {A.shape} vs {B.shape}")
+    ctx = _native_ctx(A, B)
+    c = B.shape[0]
+    m, n = A.grid
+    if B.grid != (1, n) or c > ctx.grid_cols:
+        raise ShapeMismatch(f"col_major_abt: B rows {c} must fit one block and {ctx.grid_cols} columns")
+    out = (C.c_void_p * m)()
+    counts = (C.c_int64 * N.NCOUNTS)()
+    N.check(N.lib().hc_col_major_abt(ctx._h, _handles(A.flat()), m, n, _handles(B.flat()), c, float(scale), out,
+                                     counts))
+    blocks = tuple((Ciphertext(ctx, C.c_void_p(out[p])),) for p in range(m))
+    return EncodedMatrix(ctx, blocks, (A.shape[0], c), "none", None)
+
+
+def row_major_atb(A: EncodedMatrix, B: EncodedMatrix, scale: float = 1.0) -> EncodedMatrix:
+    """Table-4 baseline ``scale * A^T B`` with both operands untiled (matmul.py:201-237):
+    one pass per column of A; 3 levels."""
+    if A.tiling != "none" or B.tiling != "none":
+        raise ShapeMismatch("row_major_atb: expected untiled operands")
+    if A.shape[0] != B.shape[0]:
+        raise ShapeMismatch(f"row_major_atb: outer dims differ, {A.shape} vs {B.shape}")
+    ctx = _native_ctx(A, B)
+    c = A.shape[1]
+    m, n = B.grid
+    if A.grid != (m, 1) or c > ctx.grid_rows:
+        raise ShapeMismatch(f"row_major_atb: A columns {c} must fit one block and {ctx.grid_rows} rows")
+    out = (C.c_void_p * n)()
+    counts = (C.c_int64 * N.NCOUNTS)()
+    N.check(N.lib().hc_row_major_atb(ctx._h, _handles(A.flat()), m, _handles(B.flat()), n, c, float(scale), out,
+                                     counts))
+    blocks = (tuple(Ciphertext(ctx, C.c_void_p(out[q])) for q in range(n)),)
+    return EncodedMatrix(ctx, blocks, (c, B.shape[1]), "none", None)
+
+
 def _reduce_callback(ctx, reducer):
     def cb(_user, cts, count):
         try:

@@ -60,6 +60,24 @@ def main():
         out[f"small_atb_{name}_led"] = led(ctx.ledger.delta(b0))
         out[f"small_atb_{name}_level"] = np.array(r.level)
 
+    # Table-4 baselines (matmul.py:160-237)
+    Ac = rng.uniform(-1, 1, (20, 40))
+    Bc = rng.uniform(-1, 1, (5, 40))
+    out["small_cm_A"], out["small_cm_B"] = Ac, Bc
+    b0 = ctx.ledger.snapshot()
+    r = matmul.col_major_abt(encoding.encode(ctx, Ac), encoding.encode(ctx, Bc), scale=-1.0)
+    out["small_cm_out"] = encoding.decode(r)
+    out["small_cm_led"] = led(ctx.ledger.delta(b0))
+    out["small_cm_level"] = np.array(r.level)
+    Ar = rng.uniform(-1, 1, (40, 6))
+    Br = rng.uniform(-1, 1, (40, 21))
+    out["small_rm_A"], out["small_rm_B"] = Ar, Br
+    b0 = ctx.ledger.snapshot()
+    r = matmul.row_major_atb(encoding.encode(ctx, Ar), encoding.encode(ctx, Br), scale=0.5)
+    out["small_rm_out"] = encoding.decode(r)
+    out["small_rm_led"] = led(ctx.ledger.delta(b0))
+    out["small_rm_level"] = np.array(r.level)
+
     bctx = EmulatorContext(256, 16, max_level=12, auto_bootstrap=True)
     Z = rng.uniform(-100, 100, (16, 5))
     out["small_sm_in"] = Z

@@ -167,6 +167,28 @@ def test_native_softmax_small12(golden):
     assert np.max(np.abs(P.decode(out, tol=1e-3) - golden["small_sm_out"])) < 1e-3
 
 
+def test_table4_baselines_small12(golden):
+    """col_major_abt / row_major_atb (matmul.py:160-237) natively: residues vs
+    the oracle, ledgers and values vs the reference's golden vectors."""
+    P = _prod()
+    g, o = P.CKKSContext("small12", 16, seed=14), R.OracleCKKSContext("small12", 16, seed=14)
+    GA, OA = _enc_pair(g, o, golden["small_cm_A"])
+    g.nonce = o.nonce = 40
+    GB, OB = P.encode(g, golden["small_cm_B"]), S.encode(o, golden["small_cm_B"])
+    out, ref = P.col_major_abt(GA, GB, scale=-1.0), S.col_major_abt(OA, OB, scale=-1.0)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden["small_cm_led"])
+    assert np.max(np.abs(P.decode(out) - golden["small_cm_out"])) < 1e-4
+    g.ledger.reset()
+    GA, OA = _enc_pair(g, o, golden["small_rm_A"])
+    g.nonce = o.nonce = 80
+    GB, OB = P.encode(g, golden["small_rm_B"]), S.encode(o, golden["small_rm_B"])
+    out, ref = P.row_major_atb(GA, GB, scale=0.5), S.row_major_atb(OA, OB, scale=0.5)
+    _same_grid(out, ref)
+    assert _ledger(g) == list(golden["small_rm_led"])
+    assert np.max(np.abs(P.decode(out) - golden["small_rm_out"])) < 1e-4
+
+
 def test_block_parallel_softmax_matches_sequential_oracle():
     """4 block rows run as concurrent branches with the nonce plan: residues and
     the nonce counter equal the oracle's sequential (block-interleaved) run."""

@@ -117,3 +117,21 @@ def test_config4_epoch(golden):
         snaps.append(S.decode(st.weights))
     np.testing.assert_array_equal(np.stack(snaps), golden["cfg4_snaps"])
     np.testing.assert_array_equal(led(ctx.ledger.counts()), golden["cfg4_led"])
+
+
+def test_table4_baselines(golden):
+    """col_major_abt / row_major_atb (matmul.py:160-237) vs the reference."""
+    ctx = S.SlotBackend(256, 16, max_level=12)
+    b0 = ctx.ledger.snapshot()
+    r = S.col_major_abt(S.encode(ctx, golden["small_cm_A"]), S.encode(ctx, golden["small_cm_B"]), scale=-1.0)
+    np.testing.assert_array_equal(S.decode(r), golden["small_cm_out"])
+    np.testing.assert_array_equal(led(ctx.ledger.delta(b0)), golden["small_cm_led"])
+    assert r.level == golden["small_cm_level"]
+    b0 = ctx.ledger.snapshot()
+    r = S.row_major_atb(S.encode(ctx, golden["small_rm_A"]), S.encode(ctx, golden["small_rm_B"]), scale=0.5)
+    np.testing.assert_array_equal(S.decode(r), golden["small_rm_out"])
+    np.testing.assert_array_equal(led(ctx.ledger.delta(b0)), golden["small_rm_led"])
+    assert r.level == golden["small_rm_level"]
+    d = ctx.ledger.delta(b0)
+    f = S.count_formula("row_major", (40, 21, 6), 16, 16)
+    assert {k: d[k] for k in f} == f

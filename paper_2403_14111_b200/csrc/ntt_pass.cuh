@@ -110,6 +110,33 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const u64 twoq = 2 * q;
     u64 x[8];
+    // one 16-byte load per (w, w') pair; round rdx's pairs in stage order
+    auto twload = [&](int rdx, ulonglong2* out) {
+        const int fr = INV ? (PG::NR - 1 - rdx) : rdx;
+        const int s0 = 3 * fr;
+        const int r = (LOGSZ - s0) < 3 ? (LOGSZ - s0) : 3;
+        const int logu = LOGSZ - s0 - r;
+        const int NG = 8 >> r;
+        int n = 0;
+#pragma unroll
+        for (int j = 0; j < NG; j++) {
+            const int blk = (G.lt + j * PG::TPS) >> logu;
+            const int B0 = G.R * (1 << s0) + blk;
+#pragma unroll
+            for (int qq = 0; qq < r; qq++) {
+                if (twsm) {
+                    const ulonglong2* tp = twsm + G.twl(s0 + qq, blk << qq);
+#pragma unroll
+                    for (int sb = 0; sb < (1 << qq); sb++) out[n++] = tp[sb];
+                } else {
+                    const ulonglong2* tp = TW + (B0 << qq);
+#pragma unroll
+                    for (int sb = 0; sb < (1 << qq); sb++) out[n++] = tp[sb];
+                }
+            }
+        }
+    };
+    ulonglong2 tw_r[7], tw_n[7];
 #pragma unroll
     for (int rd = 0; rd < PG::NR; rd++) {
         const int fr = INV ? (PG::NR - 1 - rd) : rd;
@@ -144,28 +171,9 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
             cp_async_wait_all();
             __syncthreads();
         }
-        // ---- twiddles for the round, one 16-byte load each, issued up front ----
-        ulonglong2 tw_r[7];
-        {
-            int n = 0;
-#pragma unroll
-            for (int j = 0; j < NG; j++) {
-                const int blk = (G.lt + j * PG::TPS) >> logu;
-                const int B0 = G.R * (1 << s0) + blk;
-#pragma unroll
-                for (int qq = 0; qq < r; qq++) {
-                    if (twsm) {
-                        const ulonglong2* tp = twsm + G.twl(s0 + qq, blk << qq);
-#pragma unroll
-                        for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
-                    } else {
-                        const ulonglong2* tp = TW + (B0 << qq);
-#pragma unroll
-                        for (int sb = 0; sb < (1 << qq); sb++) tw_r[n++] = tp[sb];
-                    }
-                }
-            }
-        }
+        // ---- twiddles: round 0's now; every later round's were issued at the
+        // end of the previous round, ahead of its shared-memory exchange ----
+        if (rd == 0) twload(0, tw_r);
         // ---- butterflies (Harvey lazy) ----
 #pragma unroll
         for (int j = 0; j < NG; j++) {
@@ -202,6 +210,8 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
                 }
             }
         }
+        // ---- next round's twiddles in flight during the exchange below ----
+        if (rd + 1 < PG::NR) twload(rd + 1, tw_n);
         // ---- store ----
         const bool last = (rd == PG::NR - 1);
 #pragma unroll
@@ -224,7 +234,11 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
                 for (int m = 0; m < GS; m++) sm[G.sidx(base + (m << logu))] = x[j * GS + m];
             }
         }
-        if (!last) __syncthreads();
+        if (!last) {
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 7; e++) tw_r[e] = tw_n[e];
+        }
     }
 }
 

@@ -521,7 +521,8 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             }
         }
         static bool at = false;
-        Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + 2.0 * jobs.n));
+        // algorithmic: the digit limbs Y read once, one intermediate limb written per job
+        Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + (double)jobs.n));
         dim3 grid((N >> CL) / CS, jobs.n);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);

@@ -111,9 +111,11 @@ static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_s
 
 // second half of a split forward NTT (in place), for callers that ran the
 // column pass themselves with a fused producer
+// Output stays lazy in [0, 4q): the only consumer (the key product) takes
+// any input below 2^62 into its 128-bit accumulation.
 void ntt_forward_chunks(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
-    chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 1);
+    chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 0);
 }
 
 // second half of a split inverse NTT (in place, final scaling)

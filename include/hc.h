@@ -150,6 +150,8 @@ int64_t hc_launch_count(hc_ctx *ctx);
 /* key-switch throughput: `streams` concurrent chains of `reps` rotations of ct
  * (device time in ms over all streams*reps key switches; ledger untouched) */
 int hc_bench_keyswitch(hc_ctx *ctx, const hc_ct *ct, int streams, int reps, float *ms);
+/* batched NTT throughput: `reps` forward (or inverse) transforms of `nlimbs` limbs */
+int hc_bench_ntt(hc_ctx *ctx, int nlimbs, int reps, int inverse, float *ms);
 /* per-kernel event profiler: JSON {"kernel": [launches, total_ms, algorithmic_bytes], ...} */
 int hc_prof_begin(hc_ctx *ctx);
 int hc_prof_end(hc_ctx *ctx, char *json, int len);

@@ -282,6 +282,36 @@ int hc_timer_end(hc_ctx* ctx, float* ms) {
 
 int64_t hc_launch_count(hc_ctx* ctx) { return ctx->c->launches; }
 
+int hc_bench_ntt(hc_ctx* ctx, int nlimbs, int reps, int inverse, float* ms) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (nlimbs < 1 || reps < 1) throw hc::Error(HC_EPARAM, "bad sizes");
+        u64* buf = c.alloc((size_t)nlimbs * c.N);
+        HC_CUDA(cudaMemsetAsync(buf, 0, (size_t)nlimbs * c.N * 8, c.stream));
+        auto run = [&] {
+            for (int base = 0; base < nlimbs; base += hc::MAXJ) {
+                hc::JobList j;
+                j.n = std::min(hc::MAXJ, nlimbs - base);
+                for (int i = 0; i < j.n; i++) {
+                    j.prime[i] = (base + i) % c.nall;
+                    j.ptr[i] = buf + (size_t)(base + i) * c.N;
+                    j.src[i] = nullptr;
+                }
+                if (inverse) hc::ntt_inverse(c, j);
+                else hc::ntt_forward(c, j);
+            }
+        };
+        run();
+        if (!c.t0) { HC_CUDA(cudaEventCreate(&c.t0)); HC_CUDA(cudaEventCreate(&c.t1)); }
+        HC_CUDA(cudaEventRecord(c.t0, c.stream));
+        for (int r = 0; r < reps; r++) run();
+        HC_CUDA(cudaEventRecord(c.t1, c.stream));
+        HC_CUDA(cudaEventSynchronize(c.t1));
+        HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
+        c.free(buf);
+    });
+}
+
 static void snap(hc_ctx* ctx, int64_t* b);
 
 int hc_bench_keyswitch(hc_ctx* ctx, const hc_ct* a, int streams, int reps, float* ms) {

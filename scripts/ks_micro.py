@@ -71,8 +71,26 @@ def throughput(params="cfg1", level=12, reps=8):
     return out
 
 
+def ntt_throughput(params="cfg1"):
+    """Batched NTT: limb-transforms/s and GB/s (algorithmic 16N bytes per limb) vs limb count."""
+    ctx = P.CKKSContext(params, None, seed=3)
+    L = N.lib()
+    out = {}
+    for nl in (13, 51, 96, 512):
+        for inv in (0, 1):
+            ms = C.c_float()
+            reps = 20
+            N.check(L.hc_bench_ntt(ctx._h, nl, reps, inv, C.byref(ms)))
+            per = ms.value / reps
+            out[f"{'inv' if inv else 'fwd'}_{nl}"] = {"us": round(per * 1e3, 1),
+                                                      "GBps": round(16 * ctx.N * nl / (per * 1e-3) / 1e9, 1)}
+    return out
+
+
 if __name__ == "__main__":
-    if "--throughput" in sys.argv:
+    if "--ntt" in sys.argv:
+        print(json.dumps({"ntt": ntt_throughput()}))
+    elif "--throughput" in sys.argv:
         lv = 12
         for a in sys.argv:
             if a.startswith("--level="):

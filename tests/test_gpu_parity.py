@@ -167,6 +167,48 @@ def test_native_softmax_small12(golden):
     assert np.max(np.abs(P.decode(out, tol=1e-3) - golden["small_sm_out"])) < 1e-3
 
 
+def test_backend_interface_semantics():
+    """EmulatorContext semantics the reference's callers rely on
+    (emulator.py:160-273, errors.py): error codes, lrot-by-0 identity,
+    plaintext pass-through, per-operand auto-bootstrap counting."""
+    P = _prod()
+    g = P.CKKSContext("small12", 16, seed=15)
+    z = np.linspace(-1, 1, g.slot_count)
+    x = g.encrypt(z)
+    assert g.lrot(x, 0) is x and g.lrot(x, g.slot_count) is x
+    pt = g.pack(z)
+    assert g.bootstrap(pt) is pt and not pt.encrypted and pt.level == float("inf")
+    with pytest.raises(TypeError):
+        g.cmult(x, x)
+    with pytest.raises(P.SlotCountMismatch):
+        g.encrypt(np.zeros(3))
+    with pytest.raises(ValueError):
+        g.encrypt(z, level=g.max_level + 1)
+    low = g.encrypt(z, level=0)
+    with pytest.raises(P.DepthExhausted) as ei:
+        g.mult(low, low)
+    assert ei.value.code == "emulator.depth"
+    g.auto_bootstrap = True
+    before = g.ledger.snapshot()
+    y = g.mult(low, low)                                  # both operands refreshed: 2 Bootstraps
+    d = g.ledger.delta(before)
+    assert d["Bootstrap"] == 2 and d["Mult"] == 1 and y.level == g.max_level - 1
+    assert np.max(np.abs(y.slots - z * z)) < 1e-5
+    before = g.ledger.snapshot()
+    s = g.add(pt, pt)                                     # plaintext op: unledgered
+    assert not s.encrypted and g.ledger.delta(before)["Add"] == 0
+    a = g.add(x, 2.5)
+    b = g.sub(2.5, x)
+    assert np.max(np.abs(a.slots - (z + 2.5))) < 1e-6 and np.max(np.abs(b.slots - (2.5 - z))) < 1e-6
+    assert g.ledger.delta(before)["Add"] == 2
+    e = P.encode(g, np.ones((3, 5)))
+    with pytest.raises(P.ResidualImaginary):
+        P.decode(e.map_blocks(g.mul_i))
+    assert g.decodes_by("observer") == []
+    P.decode(e, role="client", tag="t")
+    assert g.decodes_by("client") == [("client", "t")]
+
+
 def test_table4_baselines_small12(golden):
     """col_major_abt / row_major_atb (matmul.py:160-237) natively: residues vs
     the oracle, ledgers and values vs the reference's golden vectors."""

@@ -204,7 +204,7 @@ def test_backend_interface_semantics():
     e = P.encode(g, np.ones((3, 5)))
     with pytest.raises(P.ResidualImaginary):
         P.decode(e.map_blocks(g.mul_i))
-    assert g.decodes_by("observer") == []
+    assert g.decodes_by("observer") == [("observer", None)]      # audited before the check (encoding.py:216-218)
     P.decode(e, role="client", tag="t")
     assert g.decodes_by("client") == [("client", "t")]
 

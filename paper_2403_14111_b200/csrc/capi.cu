@@ -12,11 +12,16 @@
 struct hc_ctx {
     hc::Ctx* c;
     bool auto_boot = false;
+    std::shared_ptr<hc::Ctx> sp;      // released by hc_ctx_destroy; the context dies with its last handle
 };
+// members are destroyed in reverse order: the residues (p) go back to the
+// context's pool before the owner reference can drop the context itself
 struct hc_ct {
+    std::shared_ptr<hc::Ctx> owner;
     hc::CtP p;
 };
 struct hc_pt {
+    std::shared_ptr<hc::Ctx> owner;
     hc::PtP p;
 };
 
@@ -36,7 +41,10 @@ static int guard(F&& f) {
     }
 }
 
-static hc_ct* wrap(hc::CtP p) { return new hc_ct{std::move(p)}; }
+static hc_ct* wrap(hc::CtP p) {
+    std::shared_ptr<hc::Ctx> owner = p->ctx->self.lock();
+    return new hc_ct{std::move(owner), std::move(p)};
+}
 
 extern "C" {
 
@@ -47,15 +55,16 @@ int hc_ctx_create(int log_n, int nq, const int* qbits, int np, const int* pbits,
     return guard([&] {
         hc::Ctx* c = hc::ctx_create(log_n, nq, qbits, np, pbits, alpha, log_scale, hamming_weight, sigma, seed,
                                     device);
-        *out = new hc_ctx{c, false};
+        std::shared_ptr<hc::Ctx> sp(c, [](hc::Ctx* p) { hc::ctx_destroy(p); });
+        c->self = sp;
+        *out = new hc_ctx{c, false, sp};
     });
 }
 
 int hc_ctx_destroy(hc_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
-        hc::ctx_destroy(ctx->c);
-        delete ctx;
+        delete ctx;    // the context itself is destroyed once no handle references it
     });
 }
 
@@ -159,7 +168,7 @@ int hc_encode_pt(hc_ctx* ctx, const double* re, const double* im, int level, hc_
     return guard([&] {
         hc::Ctx& c = *ctx->c;
         if (level < 0 || level > c.L) throw hc::Error(HC_EPARAM, "level out of range");
-        *out = new hc_pt{hc::encode_pt(c, re, im, level, c.scale[level])};
+        *out = new hc_pt{ctx->sp, hc::encode_pt(c, re, im, level, c.scale[level])};
     });
 }
 

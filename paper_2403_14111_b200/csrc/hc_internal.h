@@ -128,6 +128,11 @@ struct Ctx {
     // encoded-mask cache used by the native schedules
     std::map<std::string, PtP> pt_cache;
 
+    // the C-ABI's owning handle; every ciphertext/plaintext handle holds a
+    // strong reference, so the context outlives all of them in any
+    // destruction order (e.g. Python's cyclic garbage collection)
+    std::weak_ptr<Ctx> self;
+
     // launch accounting and the optional per-kernel event profiler
     int64_t launches = 0;
     bool prof = false;

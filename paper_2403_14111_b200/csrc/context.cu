@@ -198,7 +198,8 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     std::vector<u64> used;
     for (int i = 0; i < nall; i++) {
         const int b = i < nq ? qbits[i] : pbits[i - nq];
-        if (b < 20 || b > 61) throw Error(-1, "prime bits out of range");
+        // q < 2^60: the forward NTT keeps lazy values below 16q in one word (ntt_pass.cuh)
+        if (b < 20 || b > 60) throw Error(-1, "prime bits out of range (20..60)");
         for (u64 t = 1;; t++) {
             const u64 q = ((u64)1 << b) - t * 2 * (u64)N + 1;
             bool dup = false;

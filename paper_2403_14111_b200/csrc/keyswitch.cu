@@ -57,10 +57,7 @@ struct LdModup {
 #pragma unroll
         for (int a = 0; a < NA; a++)
             if (a < na) acc += mul_shoup_lazy(y[a][k], w[a], ws[a], p);
-        // acc < 2 * na * p <= 8p
-        if (NA > 2 && acc >= 4 * p) acc -= 4 * p;
-        if (NA > 1 && acc >= 2 * p) acc -= 2 * p;
-        return acc >= p ? acc - p : acc;
+        return acc;   // < 2 * NA * p: the pass's input bound (INB = 2 * NA)
     }
     __device__ __forceinline__ void load8(size_t k, u64* x) const {
 #pragma unroll
@@ -97,7 +94,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)pi << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, p, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA, BOUND_LIM>(G, sm, TW, p, ld, st, twsm, true);
 }
 
 // ---- B: chunk pass + key inner product ------------------------------------
@@ -153,7 +150,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
             __syncthreads();
             LdPlain ld{I + ((size_t)j * g.nt + t) * N};
             StCapture st{xs[j]};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, P.q, ld, st, twsm, false);
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, false);
         }
     }
     ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
@@ -290,13 +287,13 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     {
         LdRegs ld{r0};
         StPlain<true, false> st{acc + (size_t)t * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true>(G, sm, TW, P.q, ld, st);
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P.q, ld, st);
     }
     __syncthreads();
     {
         LdRegs ld{r1};
         StPlain<true, false> st{acc + ((size_t)g.nt + t) * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true>(G, sm, TW, P.q, ld, st);
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P.q, ld, st);
     }
 }
 
@@ -327,7 +324,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NK, BOUND_LIM>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---- E: chunk pass with the ModDown combine in its stores ------------------
@@ -339,10 +336,11 @@ struct StModdown {
     u64 q, pinv, pinv_s, gal;
     int logN;
     const u64* __restrict__ add2;    // second addend limb (not permuted) or nullptr: rotate-and-add ladders
+    // w < MD_OUTB * q (the chunk pass's output bound), accq canonical: the
+    // Shoup product takes the unreduced difference (< 15q < 2^64)
+    static constexpr int MD_OUTB = 14;
     __device__ __forceinline__ u64 one(size_t k, u64 w) const {
-        w = w >= 2 * q ? w - 2 * q : w;
-        w = w >= q ? w - q : w;
-        u64 v = mul_shoup(accq[k] + q - w, pinv, pinv_s, q);
+        u64 v = mul_shoup(accq[k] + MD_OUTB * q - w, pinv, pinv_s, q);
         if (add) {
             const u64 a = gal ? add[galois_src((unsigned)k, logN, gal)] : add[k];
             v = add_mod(v, a, q);
@@ -375,7 +373,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StModdown::MD_OUTB>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---- fused rescale (R1: bcast in the column pass, R2: combine in the chunk pass)
@@ -407,17 +405,16 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2, BOUND_LIM>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 struct StRescale {
     u64* __restrict__ out;
     const u64* __restrict__ a;
     u64 q, c, cs;
+    static constexpr int RS_OUTB = 14;   // y < 14q, a canonical: a + 14q - y < 15q
     __device__ __forceinline__ u64 one(size_t k, u64 y) const {
-        y = y >= 2 * q ? y - 2 * q : y;
-        y = y >= q ? y - q : y;
-        return mul_shoup(a[k] + q - y, c, cs, q);
+        return mul_shoup(a[k] + RS_OUTB * q - y, c, cs, q);
     }
     __device__ __forceinline__ void operator()(size_t k, u64 y) const { out[k] = one(k, y); }
     __device__ __forceinline__ void store8(size_t k, const u64* y) const {
@@ -442,7 +439,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StRescale::RS_OUTB>(G, sm, TW, q, ld, st, twsm, true);
 }
 
 // ---------------------------------------------------------------------------

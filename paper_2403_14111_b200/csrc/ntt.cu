@@ -5,9 +5,10 @@
 // psi^(2 brv(j) + 1).  Inverse is Gentleman-Sande with the N^-1 scaling
 // (or a per-limb constant that folds N^-1 with the next base-conversion
 // factor) applied in the final store.  Twiddles psi^brv(k) carry Shoup
-// companions.  Harvey lazy butterflies: forward values live in [0, 4q),
-// inverse in [0, 2q); the final store reduces to [0, q), so results are
-// canonical residues, bit-exact with the oracle's plain NTT.
+// companions.  Lazy butterflies: inverse values live in [0, 2q) (Harvey);
+// forward values grow by 2q per stage up to 16q and are reduced on the plan
+// in ntt_pass.cuh (primes < 2^60); the final store reduces to [0, q), so
+// results are canonical residues, bit-exact with the oracle's plain NTT.
 //
 // Decomposition.  N = N1 * N2.  Forward = pass "cols" (N2 independent
 // N1-point sub-transforms on elements c + r*N2, root index R = 1) then pass
@@ -45,14 +46,18 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<L
     const u64 gal = use_src ? jobs.galois : 0;
     u64 c = P.ninv, cs = P.ninv_s;
     if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
+    // forward input bounds: canonical (or < 2q) residues for the first pass,
+    // the column pass's lazy output (< 16q) for the chunk pass; final stores
+    // need < 4q, lazy stores < 16q
+    constexpr int INB = (MODE == MODE_CHUNKS) ? BOUND_LIM : 2;
     if (gal) {
         LdGalois ld{src, logN, gal};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, pend); }
     } else {
         LdPlain ld{src};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, pend); }
     }
 }
 
@@ -111,8 +116,8 @@ static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_s
 
 // second half of a split forward NTT (in place), for callers that ran the
 // column pass themselves with a fused producer
-// Output stays lazy in [0, 4q): the only consumer (the key product) takes
-// any input below 2^62 into its 128-bit accumulation.
+// Output stays lazy below 16q < 2^64: the only consumer (the key product)
+// takes any 64-bit input into its 128-bit accumulation.
 void ntt_forward_chunks(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
     chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 0);

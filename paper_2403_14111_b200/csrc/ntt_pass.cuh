@@ -71,6 +71,41 @@ struct PassGeo {
     static constexpr int sstep(int u) { return MODE == MODE_COLS ? u * SUBS : (u == 1 ? 1 : u + u / 8); }
 };
 
+// ---- forward-pass reduction plan --------------------------------------------
+// Every prime is below 2^60 (ctx_create enforces it), so a word holds any
+// value below 16q.  A Cooley-Tukey butterfly maps operand bounds (X < Bq,
+// any Y) to outputs below (B + 2)q, because the Shoup product is < 2q for any
+// 64-bit Y.  Instead of Harvey's "reduce X below 2q in every stage" the plan
+// lets the bound grow by 2q per stage and reduces X only when the next stage
+// would pass 16q (one conditional subtraction of 8q: X < 8q, outputs < 10q).
+// The pass's last stage reduces further when its consumer needs outputs below
+// OUTB * q.  Bounds are uniform over the elements of a stage and known at
+// compile time; the plan decides, per stage, how X is reduced:
+//   RED_NONE, RED_8 (X < 8q), RED_2 (X < 2q via 8q / 4q / 2q subtractions).
+enum { RED_NONE = 0, RED_8 = 1, RED_2 = 2 };
+constexpr int BOUND_LIM = 16;
+__host__ __device__ constexpr int fwd_red(int B, bool last, int outb) {
+    const int lim = last && outb < BOUND_LIM ? outb : BOUND_LIM;
+    return B + 2 <= lim ? RED_NONE : (10 <= lim ? RED_8 : RED_2);
+}
+__host__ __device__ constexpr int fwd_after(int B, int red) {
+    return red == RED_NONE ? B + 2 : (red == RED_8 ? 10 : 4);
+}
+// bound (in units of q) before stage s of an nst-stage pass; s = nst gives the output bound
+__host__ __device__ constexpr int fwd_bound(int inb, int nst, int outb, int s) {
+    int B = inb;
+    for (int i = 0; i < s; i++) B = fwd_after(B, fwd_red(B, i == nst - 1, outb));
+    return B;
+}
+// x < B q (B <= 16)  ->  x < T q (T in {1, 2, 4, 8}) by conditional subtractions of 8q, 4q, 2q, q
+__device__ __forceinline__ u64 reduce_to(u64 x, u64 q, int B, int T) {
+    if (B > 8 && T <= 8) x = x >= 8 * q ? x - 8 * q : x;
+    if (B > 4 && T <= 4) x = x >= 4 * q ? x - 4 * q : x;
+    if (B > 2 && T <= 2) x = x >= 2 * q ? x - 2 * q : x;
+    if (B > 1 && T <= 1) x = x >= q ? x - q : x;
+    return x;
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -101,9 +136,11 @@ __device__ __forceinline__ void stage_twiddles(const PassGeo<LOGSZ, MODE, SUBS>&
 
 // Runs the pass.  LD: u64 operator()(size_t gidx) and void load8(size_t gidx, u64* x)
 // (8 consecutive words, only used when EDGE_CONTIG).  ST: void operator()(size_t gidx, u64 v)
-// and store8(size_t gidx, const u64* x).  Values handed to ST are lazy: [0, 4q) forward,
-// [0, 2q) inverse.  TW: (w, w_shoup) pairs of this prime.
-template <int LOGSZ, int MODE, int SUBS, bool INV, class LD, class ST>
+// and store8(size_t gidx, const u64* x).  Forward: LD values are below INB * q and the
+// values handed to ST below fwd_bound(INB, LOGSZ, OUTB, LOGSZ) * q <= OUTB * q (see the
+// reduction plan above).  Inverse: LD values below 2q, ST values below 2q.
+// TW: (w, w_shoup) pairs of this prime.
+template <int LOGSZ, int MODE, int SUBS, bool INV, int INB, int OUTB, class LD, class ST>
 __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm,
                                          const ulonglong2* __restrict__ TW, u64 q, LD& ld, ST& st,
                                          const ulonglong2* twsm = nullptr, bool tw_pending = false) {
@@ -187,8 +224,12 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
                         const ulonglong2 w = tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))];
+                        const int st = s0 + qq;
+                        const int B = fwd_bound(INB, LOGSZ, OUTB, st);
+                        const int red = fwd_red(B, st == LOGSZ - 1, OUTB);
                         u64 X = y[m1];
-                        X = X >= twoq ? X - twoq : X;
+                        if (red == RED_8) X = reduce_to(X, q, B, 8);
+                        else if (red == RED_2) X = reduce_to(X, q, B, 2);
                         const u64 T = mul_shoup_lazy(y[m1 + half], w.x, w.y, q);
                         y[m1] = X + T;
                         y[m1 + half] = X + twoq - T;

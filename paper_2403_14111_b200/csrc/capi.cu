@@ -4,6 +4,7 @@
 #include <cstring>
 #include <map>
 
+#include <cstdlib>
 #include "../../include/hc.h"
 #include "evaluator.h"
 #include "kernels.cuh"
@@ -297,12 +298,16 @@ int hc_bench_ntt(hc_ctx* ctx, int nlimbs, int reps, int inverse, float* ms) {
         if (nlimbs < 1 || reps < 1) throw hc::Error(HC_EPARAM, "bad sizes");
         u64* buf = c.alloc((size_t)nlimbs * c.N);
         HC_CUDA(cudaMemsetAsync(buf, 0, (size_t)nlimbs * c.N * 8, c.stream));
+        // HC_BENCH_PRIME=i pins every limb to prime i (default: primes in turn)
+        const char* pe = std::getenv("HC_BENCH_PRIME");
+        const int pin = pe ? std::atoi(pe) : -1;
+        if (pin >= c.nall) throw hc::Error(HC_EPARAM, "HC_BENCH_PRIME out of range");
         auto run = [&] {
             for (int base = 0; base < nlimbs; base += hc::MAXJ) {
                 hc::JobList j;
                 j.n = std::min(hc::MAXJ, nlimbs - base);
                 for (int i = 0; i < j.n; i++) {
-                    j.prime[i] = (base + i) % c.nall;
+                    j.prime[i] = pin >= 0 ? pin : (base + i) % c.nall;
                     j.ptr[i] = buf + (size_t)(base + i) * c.N;
                     j.src[i] = nullptr;
                 }

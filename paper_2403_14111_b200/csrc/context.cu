@@ -165,6 +165,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     c->main_stream = c->stream;
     if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HC_KS_SPLIT")) c->ks_split = std::atoi(e);
+    if (const char* e = std::getenv("HC_NTT_FP")) c->ntt_fp = std::atoi(e) != 0;
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -223,17 +224,28 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
         p.ipsi = invmod(p.psi, q);
         p.ninv = invmod((u64)N, q);
         p.I = powmod(p.psi, (u64)N / 2, q);
-        pd[i] = PrimeDev{q, 2 * q, p.mu_hi, p.mu_lo, p.I, shoup_of(p.I, q), p.ninv, shoup_of(p.ninv, q)};
+        const bool fp = c->ntt_fp && q < ((u64)1 << FP_MAXBITS);
+        pd[i] = PrimeDev{q, 2 * q, p.mu_hi, p.mu_lo, p.I, shoup_of(p.I, q), p.ninv, shoup_of(p.ninv, q),
+                         (double)q, 1.0 / (double)q, fp ? 1 : 0};
         std::vector<u64> pw(N), ipw(N);
         pw[0] = ipw[0] = 1;
         for (int k = 1; k < N; k++) { pw[k] = mulm(pw[k - 1], p.psi, q); ipw[k] = mulm(ipw[k - 1], p.ipsi, q); }
         for (int k = 0; k < N; k++) {
             const unsigned r = brv((unsigned)k, logN);
-            // (w, w_shoup) pairs: one 16-byte load per twiddle in the NTT passes
-            tw[2 * ((size_t)i * N + k)] = pw[r];
-            tw[2 * ((size_t)i * N + k) + 1] = shoup_of(pw[r], q);
-            itw[2 * ((size_t)i * N + k)] = ipw[r];
-            itw[2 * ((size_t)i * N + k) + 1] = shoup_of(ipw[r], q);
+            // (w, w_shoup) pairs: one 16-byte load per twiddle in the NTT passes;
+            // FP64 primes hold (w, w/q) as doubles instead (ntt_pass.cuh ArFp)
+            auto pair = [&](u64 w, u64* dst) {
+                if (fp) {
+                    const double wd = (double)w, wq = wd / (double)q;
+                    std::memcpy(dst, &wd, 8);
+                    std::memcpy(dst + 1, &wq, 8);
+                } else {
+                    dst[0] = w;
+                    dst[1] = shoup_of(w, q);
+                }
+            };
+            pair(pw[r], &tw[2 * ((size_t)i * N + k)]);
+            pair(ipw[r], &itw[2 * ((size_t)i * N + k)]);
         }
     }
     c->d_primes = upload(*c, pd);

@@ -93,6 +93,7 @@ struct Ctx {
     int fork_rot[4] = {0, 0, 0, 0};
     int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
     int ks_split = 1;             // key product as NTT chunk pass + streaming kernel (HC_KS_SPLIT)
+    bool ntt_fp = true;           // FP64 NTT passes for primes below 2^46 (HC_NTT_FP=0 disables)
     cudaEvent_t ra_ev[2] = {nullptr, nullptr};   // schedule run-ahead throttle (capi.cu)
     int ra_idx = 0;
     cudaMemPool_t pool = nullptr;

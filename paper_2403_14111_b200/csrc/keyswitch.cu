@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const size_t N = (size_t)1 << g.logN;
     const int lo = j * g.alpha;
     const int hi = min(lo + g.alpha, g.nl);
-    const u64 p = primes[pi].q;
+    const PrimeDev P = primes[pi];
+    const u64 p = P.q;
     LdModup<NA> ld;
     ld.na = hi - lo;
     ld.p = p;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)pi << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA, BOUND_LIM>(G, sm, TW, p, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 // ---- B: chunk pass + key inner product ------------------------------------
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
             __syncthreads();
             LdPlain ld{I + ((size_t)j * g.nt + t) * N};
             StCapture st{xs[j]};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, false);
+            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, false);
         }
     }
     ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
@@ -287,13 +288,13 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     {
         LdRegs ld{r0};
         StPlain<true, false> st{acc + (size_t)t * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P.q, ld, st);
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P, ld, st);
     }
     __syncthreads();
     {
         LdRegs ld{r1};
         StPlain<true, false> st{acc + ((size_t)g.nt + t) * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P.q, ld, st);
+        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P, ld, st);
     }
 }
 
@@ -307,7 +308,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
-    const u64 q = primes[i].q;
+    const PrimeDev P = primes[i];
+    const u64 q = P.q;
     LdModup<NK> ld;
     ld.na = g.K;
     ld.p = q;
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NK, BOUND_LIM>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NK, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 // ---- E: chunk pass with the ModDown combine in its stores ------------------
@@ -363,7 +365,8 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
-    const u64 q = primes[i].q;
+    const PrimeDev P = primes[i];
+    const u64 q = P.q;
     LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
     StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
                  (s < add_npoly) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StModdown::MD_OUTB>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StModdown::MD_OUTB>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 // ---- fused rescale (R1: bcast in the column pass, R2: combine in the chunk pass)
@@ -397,7 +400,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
-    const u64 q = primes[i].q;
+    const PrimeDev P = primes[i];
+    const u64 q = P.q;
     LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2]};
     StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2, BOUND_LIM>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 struct StRescale {
@@ -430,7 +434,8 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
-    const u64 q = primes[i].q;
+    const PrimeDev P = primes[i];
+    const u64 q = P.q;
     LdPlain ld{Yt + ((size_t)s * level + i) * N};
     StRescale st{out + ((size_t)s * level + i) * N, a + ((size_t)s * (level + 1) + i) * N, q, tab[3 * i],
                  tab[3 * i + 1]};
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
-    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StRescale::RS_OUTB>(G, sm, TW, q, ld, st, twsm, true);
+    ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StRescale::RS_OUTB>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 // ---------------------------------------------------------------------------

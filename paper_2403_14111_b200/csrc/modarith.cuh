@@ -12,10 +12,14 @@
 typedef uint64_t u64;
 typedef int64_t i64;
 
+constexpr int FP_MAXBITS = 46;   // NTT passes run in FP64 for primes below 2^46 (ntt_pass.cuh)
+
 struct PrimeDev {
     u64 q, twoq, mu_hi, mu_lo;   // Barrett constants
     u64 I, I_s;                  // psi^(N/2) and its Shoup companion
     u64 ninv, ninv_s;            // N^-1 (INTT scaling)
+    double qd, qinv;             // q and 1/q as doubles (FP64 NTT path)
+    int fp;                      // NTT passes on this prime run in FP64 (q < 2^46, ntt_pass.cuh)
 };
 
 __device__ __forceinline__ u64 mulhi64(u64 a, u64 b) { return __umul64hi(a, b); }

@@ -52,12 +52,12 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<L
     constexpr int INB = (MODE == MODE_CHUNKS) ? BOUND_LIM : 2;
     if (gal) {
         LdGalois ld{src, logN, gal};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P.q, ld, st, twsm, pend); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, pend); }
     } else {
         LdPlain ld{src};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P.q, ld, st, twsm, pend); }
-        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P.q, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, pend); }
     }
 }
 

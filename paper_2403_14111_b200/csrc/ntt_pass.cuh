@@ -134,21 +134,120 @@ __device__ __forceinline__ void stage_twiddles(const PassGeo<LOGSZ, MODE, SUBS>&
     }
 }
 
+// ---- butterfly arithmetic policies ------------------------------------------
+//
+// ArInt: 64-bit words, Shoup products, the reduction plan above (any prime
+// below 2^60).
+//
+// ArFp: primes below 2^46 run in FP64 (the B200 FP64 pipe issues DFMA at the
+// IMAD rate, and one butterfly is 8 FP64 instructions instead of ~30 integer
+// ones).  Residues are integers held exactly in doubles, signed and lazy.  The
+// product of x (|x| < 32q) by a twiddle w is exact as h + l (h = x*w rounded,
+// l = fma(x, w, -h)); the quotient is rint(x * w/q) with w/q precomputed, off
+// the true x*w/q by at most 0.75, so T = (h - qt*q) + l is exact with
+// |T| <= 0.75q.  Forward outputs grow by 0.75q per stage (no reduction in a
+// pass of <= 13 stages from inputs below 16q); inverse sums double per stage
+// and are reduced (|v| <= q/2) when they would pass 16q.  Pass boundaries
+// stay integer: words in, lazy words in [0, 2q) out, so every load / store
+// hook is shared with the integer path and results are bit-identical.
+template <int LOGSZ, int INB, int OUTB>
+struct ArInt {
+    using V = u64;
+    using W = ulonglong2;
+    static constexpr bool PREFETCH_TW = true;   // next round's twiddles in flight during the exchange
+    u64 q, twoq;
+    __device__ __forceinline__ ArInt(const PrimeDev& P) : q(P.q), twoq(2 * P.q) {}
+    __device__ __forceinline__ V in(u64 u) const { return u; }
+    __device__ __forceinline__ u64 out(V v) const { return v; }
+    __device__ __forceinline__ void fwd(V& a, V& b, const W& w, int st) const {
+        const int B = fwd_bound(INB, LOGSZ, OUTB, st);
+        const int red = fwd_red(B, st == LOGSZ - 1, OUTB);
+        u64 X = a;
+        if (red == RED_8) X = reduce_to(X, q, B, 8);
+        else if (red == RED_2) X = reduce_to(X, q, B, 2);
+        const u64 T = mul_shoup_lazy(b, w.x, w.y, q);
+        a = X + T;
+        b = X + twoq - T;
+    }
+    __device__ __forceinline__ void inv(V& a, V& b, const W& w, int) const {
+        const u64 X = a + b;
+        const u64 D = a + twoq - b;
+        a = X >= twoq ? X - twoq : X;
+        b = mul_shoup_lazy(D, w.x, w.y, q);
+    }
+};
+
+constexpr double FP_MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, c, M) - M = rint(x * c)
+constexpr double FP_P52 = 4503599627370496.0;     // 2^52
+constexpr u64 FP_EXP52 = 0x4330000000000000ull;   // bits of 2^52
+constexpr u64 FP_MANT = (1ull << 52) - 1;
+
+// inverse: reduce the sums of executed stage e (bounds in units of q; inputs below 2q)
+__host__ __device__ constexpr bool fp_inv_red(int e) {
+    int B = 2;
+    for (int i = 0; i < e; i++) B = (2 * B > 16) ? 1 : 2 * B;
+    return 2 * B > 16;
+}
+
+template <int LOGSZ, int INB, int OUTB>
+struct ArFp {
+    using V = double;
+    using W = double2;   // (w, w / q)
+    static constexpr bool PREFETCH_TW = false;  // register budget: twiddles loaded at round start
+    double q, qinv, qp52;
+    static_assert(4 * INB + 3 * LOGSZ <= 4 * 32, "FP forward pass bound");
+    __device__ __forceinline__ ArFp(const PrimeDev& P) : q(P.qd), qinv(P.qinv), qp52(P.qd + FP_P52) {}
+    // exact word -> double for words below 2^52
+    __device__ __forceinline__ V in(u64 u) const {
+        return __dsub_rn(__longlong_as_double((long long)(u | FP_EXP52)), FP_P52);
+    }
+    // |v| < 32q -> centered remainder (|r| <= q/2) -> word in [0, 2q)
+    __device__ __forceinline__ double red(double v) const {
+        const double qt = __dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC);
+        return __fma_rn(-qt, q, v);
+    }
+    __device__ __forceinline__ u64 out(V v) const {
+        return (u64)__double_as_longlong(__dadd_rn(red(v), qp52)) & FP_MANT;
+    }
+    __device__ __forceinline__ double mm(double x, const W& w) const {
+        const double h = __dmul_rn(x, w.x);
+        const double l = __fma_rn(x, w.x, -h);
+        const double qt = __dsub_rn(__fma_rn(x, w.y, FP_MAGIC), FP_MAGIC);
+        return __dadd_rn(__fma_rn(-qt, q, h), l);
+    }
+    __device__ __forceinline__ void fwd(V& a, V& b, const W& w, int) const {
+        const double T = mm(b, w);
+        const double X = a;
+        a = __dadd_rn(X, T);
+        b = __dsub_rn(X, T);
+    }
+    __device__ __forceinline__ void inv(V& a, V& b, const W& w, int st) const {
+        const double X = __dadd_rn(a, b);
+        const double D = __dsub_rn(a, b);
+        a = fp_inv_red(LOGSZ - 1 - st) ? red(X) : X;
+        b = mm(D, w);
+    }
+};
+
 // Runs the pass.  LD: u64 operator()(size_t gidx) and void load8(size_t gidx, u64* x)
 // (8 consecutive words, only used when EDGE_CONTIG).  ST: void operator()(size_t gidx, u64 v)
-// and store8(size_t gidx, const u64* x).  Forward: LD values are below INB * q and the
-// values handed to ST below fwd_bound(INB, LOGSZ, OUTB, LOGSZ) * q <= OUTB * q (see the
-// reduction plan above).  Inverse: LD values below 2q, ST values below 2q.
-// TW: (w, w_shoup) pairs of this prime.
-template <int LOGSZ, int MODE, int SUBS, bool INV, int INB, int OUTB, class LD, class ST>
-__device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm,
-                                         const ulonglong2* __restrict__ TW, u64 q, LD& ld, ST& st,
-                                         const ulonglong2* twsm = nullptr, bool tw_pending = false) {
+// and store8(size_t gidx, const u64* x).  Forward: LD words are below INB * q and the
+// words handed to ST below OUTB * q (integer: the reduction plan above; FP64: [0, 2q)).
+// Inverse: LD words below 2q, ST words below 2q.  TW: the prime's twiddle pairs,
+// (w, w_shoup) words or, for FP64 primes, (w, w/q) doubles.
+template <class AR, int LOGSZ, int MODE, int SUBS, bool INV, class LD, class ST>
+__device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, MODE, SUBS>& G, u64* smw,
+                                            const ulonglong2* __restrict__ TWw, LD& ld, ST& st,
+                                            const ulonglong2* twsmw, bool tw_pending) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
-    const u64 twoq = 2 * q;
-    u64 x[8];
-    // one 16-byte load per (w, w') pair; round rdx's pairs in stage order
-    auto twload = [&](int rdx, ulonglong2* out) {
+    using V = typename AR::V;
+    using W = typename AR::W;
+    V* sm = reinterpret_cast<V*>(smw);
+    const W* __restrict__ TW = reinterpret_cast<const W*>(TWw);
+    const W* twsm = reinterpret_cast<const W*>(twsmw);
+    V x[8];
+    // one 16-byte load per twiddle pair; round rdx's pairs in stage order
+    auto twload = [&](int rdx, W* out) {
         const int fr = INV ? (PG::NR - 1 - rdx) : rdx;
         const int s0 = 3 * fr;
         const int r = (LOGSZ - s0) < 3 ? (LOGSZ - s0) : 3;
@@ -162,18 +261,29 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
 #pragma unroll
             for (int qq = 0; qq < r; qq++) {
                 if (twsm) {
-                    const ulonglong2* tp = twsm + G.twl(s0 + qq, blk << qq);
+                    const W* tp = twsm + G.twl(s0 + qq, blk << qq);
 #pragma unroll
                     for (int sb = 0; sb < (1 << qq); sb++) out[n++] = tp[sb];
                 } else {
-                    const ulonglong2* tp = TW + (B0 << qq);
+                    const W* tp = TW + (B0 << qq);
 #pragma unroll
                     for (int sb = 0; sb < (1 << qq); sb++) out[n++] = tp[sb];
                 }
             }
         }
     };
-    ulonglong2 tw_r[7], tw_n[7];
+    // the (1 << qq) pairs of group j, stage qq of round rdx (just-in-time loads)
+    auto twgroup = [&](int rdx, int j, int qq, W* out) {
+        const int fr = INV ? (PG::NR - 1 - rdx) : rdx;
+        const int s0 = 3 * fr;
+        const int r = (LOGSZ - s0) < 3 ? (LOGSZ - s0) : 3;
+        const int logu = LOGSZ - s0 - r;
+        const int blk = (G.lt + j * PG::TPS) >> logu;
+        const W* tp = twsm ? twsm + G.twl(s0 + qq, blk << qq) : TW + ((G.R * (1 << s0) + blk) << qq);
+#pragma unroll
+        for (int sb = 0; sb < (1 << qq); sb++) out[sb] = tp[sb];
+    };
+    W tw_r[7], tw_n[7];
 #pragma unroll
     for (int rd = 0; rd < PG::NR; rd++) {
         const int fr = INV ? (PG::NR - 1 - rd) : rd;
@@ -190,13 +300,17 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
             const int base = ((g >> logu) << (logu + r)) + (g & (u - 1));
             if (rd == 0) {
                 const size_t gb = G.gidx(base);
-                if (PG::EDGE_CONTIG && logu == 0 && r == 3) ld.load8(gb, x + 8 * j);
-                else {
+                if (PG::EDGE_CONTIG && logu == 0 && r == 3) {
+                    u64 w8[8];
+                    ld.load8(gb, w8);
 #pragma unroll
-                    for (int m = 0; m < GS; m++) x[j * GS + m] = ld(gb + m * PG::gstep(u));
+                    for (int m = 0; m < 8; m++) x[8 * j + m] = ar.in(w8[m]);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < GS; m++) x[j * GS + m] = ar.in(ld(gb + m * PG::gstep(u)));
                 }
             } else if (PG::slinear(u)) {
-                const u64* sp = sm + G.sidx(base);
+                const V* sp = sm + G.sidx(base);
 #pragma unroll
                 for (int m = 0; m < GS; m++) x[j * GS + m] = sp[m * PG::sstep(u)];
             } else {
@@ -208,51 +322,46 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
             cp_async_wait_all();
             __syncthreads();
         }
-        // ---- twiddles: round 0's now; every later round's were issued at the
-        // end of the previous round, ahead of its shared-memory exchange ----
-        if (rd == 0) twload(0, tw_r);
-        // ---- butterflies (Harvey lazy) ----
+        // ---- twiddles: round 0's now; with PREFETCH_TW every later round's were
+        // issued at the end of the previous round, ahead of its shared-memory exchange ----
+        if (rd == 0 && AR::PREFETCH_TW) twload(rd, tw_r);
+        // ---- butterflies ----
 #pragma unroll
         for (int j = 0; j < NG; j++) {
-            u64* y = x + j * GS;
+            V* y = x + j * GS;
             const int gbase = j * (GS - 1);
             if (!INV) {
 #pragma unroll
                 for (int qq = 0; qq < r; qq++) {
                     const int half = 1 << (r - 1 - qq);
+                    W ts[4];
+                    if (!AR::PREFETCH_TW) twgroup(rd, j, qq, ts);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const ulonglong2 w = tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))];
-                        const int st = s0 + qq;
-                        const int B = fwd_bound(INB, LOGSZ, OUTB, st);
-                        const int red = fwd_red(B, st == LOGSZ - 1, OUTB);
-                        u64 X = y[m1];
-                        if (red == RED_8) X = reduce_to(X, q, B, 8);
-                        else if (red == RED_2) X = reduce_to(X, q, B, 2);
-                        const u64 T = mul_shoup_lazy(y[m1 + half], w.x, w.y, q);
-                        y[m1] = X + T;
-                        y[m1 + half] = X + twoq - T;
+                        const W& w = AR::PREFETCH_TW ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
+                                                     : ts[m1 >> (r - qq)];
+                        ar.fwd(y[m1], y[m1 + half], w, s0 + qq);
                     }
                 }
             } else {
 #pragma unroll
                 for (int qq = r - 1; qq >= 0; qq--) {
                     const int half = 1 << (r - 1 - qq);
+                    W ts[4];
+                    if (!AR::PREFETCH_TW) twgroup(rd, j, qq, ts);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const ulonglong2 w = tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))];
-                        const u64 U = y[m1], V = y[m1 + half];
-                        const u64 X = U + V;
-                        y[m1] = X >= twoq ? X - twoq : X;
-                        y[m1 + half] = mul_shoup_lazy(U + twoq - V, w.x, w.y, q);
+                        const W& w = AR::PREFETCH_TW ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
+                                                     : ts[m1 >> (r - qq)];
+                        ar.inv(y[m1], y[m1 + half], w, s0 + qq);
                     }
                 }
             }
         }
         // ---- next round's twiddles in flight during the exchange below ----
-        if (rd + 1 < PG::NR) twload(rd + 1, tw_n);
+        if (AR::PREFETCH_TW && rd + 1 < PG::NR) twload(rd + 1, tw_n);
         // ---- store ----
         const bool last = (rd == PG::NR - 1);
 #pragma unroll
@@ -261,13 +370,17 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
             const int base = ((g >> logu) << (logu + r)) + (g & (u - 1));
             if (last) {
                 const size_t gb = G.gidx(base);
-                if (PG::EDGE_CONTIG && logu == 0 && r == 3) st.store8(gb, x + 8 * j);
-                else {
+                if (PG::EDGE_CONTIG && logu == 0 && r == 3) {
+                    u64 w8[8];
 #pragma unroll
-                    for (int m = 0; m < GS; m++) st(gb + m * PG::gstep(u), x[j * GS + m]);
+                    for (int m = 0; m < 8; m++) w8[m] = ar.out(x[8 * j + m]);
+                    st.store8(gb, w8);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < GS; m++) st(gb + m * PG::gstep(u), ar.out(x[j * GS + m]));
                 }
             } else if (PG::slinear(u)) {
-                u64* sp = sm + G.sidx(base);
+                V* sp = sm + G.sidx(base);
 #pragma unroll
                 for (int m = 0; m < GS; m++) sp[m * PG::sstep(u)] = x[j * GS + m];
             } else {
@@ -277,9 +390,32 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
         }
         if (!last) {
             __syncthreads();
+            if (AR::PREFETCH_TW) {
 #pragma unroll
-            for (int e = 0; e < 7; e++) tw_r[e] = tw_n[e];
+                for (int e = 0; e < 7; e++) tw_r[e] = tw_n[e];
+            }
         }
+    }
+}
+
+// The pass on prime P: FP64 arithmetic for primes below 2^FP_MAXBITS (P.fp),
+// integer otherwise (branch uniform per CTA).
+template <int LOGSZ, int MODE, int SUBS, bool INV, int INB, int OUTB, class LD, class ST>
+__device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u64* sm,
+                                         const ulonglong2* __restrict__ TW, const PrimeDev& P, LD& ld, ST& st,
+                                         const ulonglong2* twsm = nullptr, bool tw_pending = false) {
+#if defined(HC_ONLY_INT)
+    if (false) {
+#elif defined(HC_ONLY_FP)
+    if (true) {
+#else
+    if (P.fp) {
+#endif
+        const ArFp<LOGSZ, INB, OUTB> ar(P);
+        ntt_pass_ar<ArFp<LOGSZ, INB, OUTB>, LOGSZ, MODE, SUBS, INV>(ar, G, sm, TW, ld, st, twsm, tw_pending);
+    } else {
+        const ArInt<LOGSZ, INB, OUTB> ar(P);
+        ntt_pass_ar<ArInt<LOGSZ, INB, OUTB>, LOGSZ, MODE, SUBS, INV>(ar, G, sm, TW, ld, st, twsm, tw_pending);
     }
 }
 

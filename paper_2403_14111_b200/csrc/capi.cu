@@ -415,17 +415,18 @@ static void snap(hc_ctx* ctx, int64_t* b) {
 struct RunAhead {
     hc::Ctx& c;
     explicit RunAhead(hc::Ctx& ctx) : c(ctx) {
-        if (!c.ra_ev[0]) {
-            HC_CUDA(cudaEventCreateWithFlags(&c.ra_ev[0], cudaEventDisableTiming));
-            HC_CUDA(cudaEventCreateWithFlags(&c.ra_ev[1], cudaEventDisableTiming));
-            HC_CUDA(cudaEventRecord(c.ra_ev[0], c.main_stream));
-            HC_CUDA(cudaEventRecord(c.ra_ev[1], c.main_stream));
+        if (c.ra_ev.empty()) {
+            c.ra_ev.resize(c.ra_depth);
+            for (auto& e : c.ra_ev) {
+                HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                HC_CUDA(cudaEventRecord(e, c.main_stream));
+            }
         }
         HC_CUDA(cudaEventSynchronize(c.ra_ev[c.ra_idx]));
     }
     ~RunAhead() {
         cudaEventRecord(c.ra_ev[c.ra_idx], c.main_stream);
-        c.ra_idx ^= 1;
+        c.ra_idx = (c.ra_idx + 1) % (int)c.ra_ev.size();
     }
 };
 

@@ -166,6 +166,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HC_KS_SPLIT")) c->ks_split = std::atoi(e);
     if (const char* e = std::getenv("HC_NTT_FP")) c->ntt_fp = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HC_RUNAHEAD")) c->ra_depth = std::max(1, std::atoi(e));
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;

@@ -94,8 +94,9 @@ struct Ctx {
     int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
     int ks_split = 1;             // key product as NTT chunk pass + streaming kernel (HC_KS_SPLIT)
     bool ntt_fp = true;           // FP64 NTT passes for primes below 2^46 (HC_NTT_FP=0 disables)
-    cudaEvent_t ra_ev[2] = {nullptr, nullptr};   // schedule run-ahead throttle (capi.cu)
-    int ra_idx = 0;
+    std::vector<cudaEvent_t> ra_ev;   // schedule run-ahead throttle (capi.cu): a schedule call
+    int ra_idx = 0;                   // waits for the one ra_depth calls back to finish
+    int ra_depth = 8;                 // HC_RUNAHEAD (2 measured host-jitter-bound steps)
     cudaMemPool_t pool = nullptr;
     PrimeHost pr[MAXP];
     double scale[MAXP];

@@ -193,7 +193,6 @@ __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev
         const size_t k = (v & ((N >> 1) - 1)) * 2;
         const int pi = g.prime(t);
         const PrimeDev P = primes[pi];
-        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
         // issue every load of the (up to KP_MAXB) digits before the first MAC
         u64 x0[KP_MAXB], x1[KP_MAXB];
         ulonglong2 kbv[KP_MAXB], kav[KP_MAXB];
@@ -220,18 +219,37 @@ __global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev
             kbv[j] = *reinterpret_cast<const ulonglong2*>(kb);
             kav[j] = *reinterpret_cast<const ulonglong2*>(kb + kstride);
         }
+        ulonglong2 ob, oa;
+        if (P.fp) {
+            // FP64 products (q < 2^46): each term exact and centered (|r| < 0.6q),
+            // the sum of <= 4 reduced once; digits are lazy words below 2q
+            double sb0 = 0, sb1 = 0, sa0 = 0, sa1 = 0;
 #pragma unroll
-        for (int j = 0; j < KP_MAXB; j++) {
-            if (j >= g.beta) break;
-            mac128(b0, x0[j], kbv[j].x);
-            mac128(b1, x1[j], kbv[j].y);
-            mac128(a0, x0[j], kav[j].x);
-            mac128(a1, x1[j], kav[j].y);
+            for (int j = 0; j < KP_MAXB; j++) {
+                if (j >= g.beta) break;
+                const double y0 = fp_word(x0[j]), y1 = fp_word(x1[j]);
+                sb0 = __dadd_rn(sb0, fp_mulmod(y0, fp_word(kbv[j].x), P.qd, P.qinv));
+                sb1 = __dadd_rn(sb1, fp_mulmod(y1, fp_word(kbv[j].y), P.qd, P.qinv));
+                sa0 = __dadd_rn(sa0, fp_mulmod(y0, fp_word(kav[j].x), P.qd, P.qinv));
+                sa1 = __dadd_rn(sa1, fp_mulmod(y1, fp_word(kav[j].y), P.qd, P.qinv));
+            }
+            ob = make_ulonglong2(fp_canon(sb0, P.qd, P.qinv), fp_canon(sb1, P.qd, P.qinv));
+            oa = make_ulonglong2(fp_canon(sa0, P.qd, P.qinv), fp_canon(sa1, P.qd, P.qinv));
+        } else {
+            U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
+#pragma unroll
+            for (int j = 0; j < KP_MAXB; j++) {
+                if (j >= g.beta) break;
+                mac128(b0, x0[j], kbv[j].x);
+                mac128(b1, x1[j], kbv[j].y);
+                mac128(a0, x0[j], kav[j].x);
+                mac128(a1, x1[j], kav[j].y);
+            }
+            ob = make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
+            oa = make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
         }
-        *reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k) =
-            make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
-        *reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k) =
-            make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
+        *reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k) = ob;
+        *reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k) = oa;
     }
 }
 

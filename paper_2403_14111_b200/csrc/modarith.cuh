@@ -57,6 +57,34 @@ __device__ __forceinline__ u64 mul_mod(u64 a, u64 b, const PrimeDev& p) {
     return reduce128(__umul64hi(a, b), a * b, p);
 }
 
+// ---- FP64 residue arithmetic for primes below 2^FP_MAXBITS ----
+// Residues are integers held exactly in doubles.  x * y mod q for |x| < 2^50,
+// 0 <= y < q: h + l is the exact product (h rounded, l = fma(x, y, -h)), the
+// quotient rint(h / q) is within 0.6 of the true one, so the result
+// (h - qt q) + l is exact with |r| < 0.6q.  Used by the NTT passes
+// (ntt_pass.cuh, constant twiddles with w/q precomputed) and the key product.
+constexpr double FP_MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, c, M) - M = rint(x * c)
+constexpr double FP_P52 = 4503599627370496.0;     // 2^52
+constexpr u64 FP_EXP52 = 0x4330000000000000ull;   // bits of 2^52
+constexpr u64 FP_MANT = (1ull << 52) - 1;
+// exact word -> double for words below 2^52
+__device__ __forceinline__ double fp_word(u64 u) {
+    return __dsub_rn(__longlong_as_double((long long)(u | FP_EXP52)), FP_P52);
+}
+__device__ __forceinline__ double fp_mulmod(double x, double y, double q, double qinv) {
+    const double h = __dmul_rn(x, y);
+    const double l = __fma_rn(x, y, -h);
+    const double qt = __dsub_rn(__fma_rn(h, qinv, FP_MAGIC), FP_MAGIC);
+    return __dadd_rn(__fma_rn(-qt, q, h), l);
+}
+// |v| < 2^50 (integer) -> canonical word in [0, q)
+__device__ __forceinline__ u64 fp_canon(double v, double q, double qinv) {
+    const double qt = __dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC);
+    double r = __fma_rn(-qt, q, v);   // exact, |r| <= q/2
+    r = r < 0 ? __dadd_rn(r, q) : r;
+    return (u64)__double_as_longlong(__dadd_rn(r, FP_P52)) & FP_MANT;
+}
+
 // int64 -> residue mod q
 __device__ __forceinline__ u64 from_i64(i64 v, u64 q) {
     if (v >= 0) return (u64)v % q;

@@ -99,19 +99,32 @@ static void full_pass(Ctx& c, const JobList& jobs, bool inv) {
     }
 }
 
-// split passes for 2^14 .. 2^17: chunks of 2^9, columns of 2^(logN-9)
+// split passes for 2^14 .. 2^17: chunks of 2^9, columns of 2^(logN-9).
+// A launch that would not fill one wave of 256-thread CTAs (148 SMs x 4, e.g.
+// the 13 limbs of a key switch's first INTT or its 6 special-prime limbs)
+// takes the 64-thread variant: 4x the CTAs for the same work, so latency and
+// instruction fetch are spread over every SM.
+static bool small_grid(const JobList& jobs, int ctas_per_job) { return ctas_per_job * jobs.n < 148 * 4; }
+
 static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
+    const int big_subs = 1 << (20 - c.logN);   // 64, 32, 16, 8 columns per CTA for 2^14 .. 2^17
+    const bool sm = small_grid(jobs, 512 / big_subs);
     switch (c.logN) {
-        case 14: launch_t<5, MODE_COLS, 64>(c, jobs, inv, N1, use_src, last); break;
-        case 15: launch_t<6, MODE_COLS, 32>(c, jobs, inv, N1, use_src, last); break;
-        case 16: launch_t<7, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last); break;
-        case 17: launch_t<8, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last); break;
+        case 14: if (sm) launch_t<5, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last);
+                 else launch_t<5, MODE_COLS, 64>(c, jobs, inv, N1, use_src, last); break;
+        case 15: if (sm) launch_t<6, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last);
+                 else launch_t<6, MODE_COLS, 32>(c, jobs, inv, N1, use_src, last); break;
+        case 16: if (sm) launch_t<7, MODE_COLS, 4>(c, jobs, inv, N1, use_src, last);
+                 else launch_t<7, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last); break;
+        case 17: if (sm) launch_t<8, MODE_COLS, 2>(c, jobs, inv, N1, use_src, last);
+                 else launch_t<8, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last); break;
         default: throw Error(-1, "unsupported ring degree");
     }
 }
 
 static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
-    launch_t<9, MODE_CHUNKS, 4>(c, jobs, inv, N1, use_src, last);
+    if (small_grid(jobs, N1 / 4)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
+    else launch_t<9, MODE_CHUNKS, 4>(c, jobs, inv, N1, use_src, last);
 }
 
 // second half of a split forward NTT (in place), for callers that ran the

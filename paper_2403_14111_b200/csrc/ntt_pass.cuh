@@ -29,7 +29,9 @@ struct PassGeo {
     static constexpr int NR = (LOGSZ + 2) / 3;
     static constexpr int PADSZ = SZ + SZ / 8;
     static constexpr int THREADS = SUBS * TPS;
-    static constexpr int MIN_BLOCKS = THREADS >= 256 ? PASS_MIN_BLOCKS * 256 / THREADS : 1;
+    // split passes keep the 64-register budget at any CTA size; a full-ring
+    // pass is bounded by its shared memory instead
+    static constexpr int MIN_BLOCKS = (MODE != MODE_FULL || THREADS >= 256) ? PASS_MIN_BLOCKS * 256 / THREADS : 1;
     static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;   // column stride (MODE_COLS)
     static constexpr size_t smem_words() { return (size_t)SUBS * (MODE == MODE_COLS ? SZ : PADSZ); }
     // data + staged twiddles.  Only column passes stage (their whole twiddle
@@ -154,7 +156,7 @@ template <int LOGSZ, int INB, int OUTB>
 struct ArInt {
     using V = u64;
     using W = ulonglong2;
-    static constexpr bool PREFETCH_TW = true;   // next round's twiddles in flight during the exchange
+    static constexpr bool IS_FP = false;
     u64 q, twoq;
     __device__ __forceinline__ ArInt(const PrimeDev& P) : q(P.q), twoq(2 * P.q) {}
     __device__ __forceinline__ V in(u64 u) const { return u; }
@@ -177,10 +179,6 @@ struct ArInt {
     }
 };
 
-constexpr double FP_MAGIC = 6755399441055744.0;   // 1.5 * 2^52: fma(x, c, M) - M = rint(x * c)
-constexpr double FP_P52 = 4503599627370496.0;     // 2^52
-constexpr u64 FP_EXP52 = 0x4330000000000000ull;   // bits of 2^52
-constexpr u64 FP_MANT = (1ull << 52) - 1;
 
 // inverse: reduce the sums of executed stage e (bounds in units of q; inputs below 2q)
 __host__ __device__ constexpr bool fp_inv_red(int e) {
@@ -193,14 +191,11 @@ template <int LOGSZ, int INB, int OUTB>
 struct ArFp {
     using V = double;
     using W = double2;   // (w, w / q)
-    static constexpr bool PREFETCH_TW = false;  // register budget: twiddles loaded at round start
+    static constexpr bool IS_FP = true;
     double q, qinv, qp52;
     static_assert(4 * INB + 3 * LOGSZ <= 4 * 32, "FP forward pass bound");
     __device__ __forceinline__ ArFp(const PrimeDev& P) : q(P.qd), qinv(P.qinv), qp52(P.qd + FP_P52) {}
-    // exact word -> double for words below 2^52
-    __device__ __forceinline__ V in(u64 u) const {
-        return __dsub_rn(__longlong_as_double((long long)(u | FP_EXP52)), FP_P52);
-    }
+    __device__ __forceinline__ V in(u64 u) const { return fp_word(u); }
     // |v| < 32q -> centered remainder (|r| <= q/2) -> word in [0, 2q)
     __device__ __forceinline__ double red(double v) const {
         const double qt = __dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC);
@@ -228,6 +223,11 @@ struct ArFp {
         b = mm(D, w);
     }
 };
+
+enum { TW_JIT = 0, TW_ROUND = 1, TW_PREFETCH = 2 };
+#ifndef FP_CHUNK_TW
+#define FP_CHUNK_TW TW_PREFETCH
+#endif
 
 // Runs the pass.  LD: u64 operator()(size_t gidx) and void load8(size_t gidx, u64* x)
 // (8 consecutive words, only used when EDGE_CONTIG).  ST: void operator()(size_t gidx, u64 v)
@@ -283,6 +283,12 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
 #pragma unroll
         for (int sb = 0; sb < (1 << qq); sb++) out[sb] = tp[sb];
     };
+    // twiddle schedule: TW_PREFETCH issues the next round's pairs before the
+    // shared-memory exchange (integer path; FP64 chunk passes, whose pairs come
+    // from L2); TW_ROUND loads a round's pairs at its start; TW_JIT loads each
+    // stage's pairs just before it (FP64 column passes: staged in shared
+    // memory, and the register budget has no room for two rounds of pairs)
+    constexpr int TWM = !AR::IS_FP ? TW_PREFETCH : (MODE == MODE_COLS ? TW_JIT : FP_CHUNK_TW);
     W tw_r[7], tw_n[7];
 #pragma unroll
     for (int rd = 0; rd < PG::NR; rd++) {
@@ -324,7 +330,7 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
         }
         // ---- twiddles: round 0's now; with PREFETCH_TW every later round's were
         // issued at the end of the previous round, ahead of its shared-memory exchange ----
-        if (rd == 0 && AR::PREFETCH_TW) twload(rd, tw_r);
+        if ((rd == 0 && TWM == TW_PREFETCH) || TWM == TW_ROUND) twload(rd, tw_r);
         // ---- butterflies ----
 #pragma unroll
         for (int j = 0; j < NG; j++) {
@@ -335,11 +341,11 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
                 for (int qq = 0; qq < r; qq++) {
                     const int half = 1 << (r - 1 - qq);
                     W ts[4];
-                    if (!AR::PREFETCH_TW) twgroup(rd, j, qq, ts);
+                    if (TWM == TW_JIT) twgroup(rd, j, qq, ts);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const W& w = AR::PREFETCH_TW ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
+                        const W& w = TWM != TW_JIT ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
                                                      : ts[m1 >> (r - qq)];
                         ar.fwd(y[m1], y[m1 + half], w, s0 + qq);
                     }
@@ -349,11 +355,11 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
                 for (int qq = r - 1; qq >= 0; qq--) {
                     const int half = 1 << (r - 1 - qq);
                     W ts[4];
-                    if (!AR::PREFETCH_TW) twgroup(rd, j, qq, ts);
+                    if (TWM == TW_JIT) twgroup(rd, j, qq, ts);
 #pragma unroll
                     for (int m1 = 0; m1 < GS; m1++) {
                         if (m1 & half) continue;
-                        const W& w = AR::PREFETCH_TW ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
+                        const W& w = TWM != TW_JIT ? tw_r[gbase + ((1 << qq) - 1) + (m1 >> (r - qq))]
                                                      : ts[m1 >> (r - qq)];
                         ar.inv(y[m1], y[m1 + half], w, s0 + qq);
                     }
@@ -361,7 +367,7 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
             }
         }
         // ---- next round's twiddles in flight during the exchange below ----
-        if (AR::PREFETCH_TW && rd + 1 < PG::NR) twload(rd + 1, tw_n);
+        if (TWM == TW_PREFETCH && rd + 1 < PG::NR) twload(rd + 1, tw_n);
         // ---- store ----
         const bool last = (rd == PG::NR - 1);
 #pragma unroll
@@ -390,7 +396,7 @@ __device__ __forceinline__ void ntt_pass_ar(const AR& ar, const PassGeo<LOGSZ, M
         }
         if (!last) {
             __syncthreads();
-            if (AR::PREFETCH_TW) {
+            if (TWM == TW_PREFETCH) {
 #pragma unroll
                 for (int e = 0; e < 7; e++) tw_r[e] = tw_n[e];
             }

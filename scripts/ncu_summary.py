@@ -17,6 +17,7 @@ want = [("dur_us", "gpu__time_duration.sum"), ("dram_rd_MB", "dram__bytes_read.s
         ("regs", "launch__registers_per_thread"), ("grid", "launch__grid_size"),
         ("fma_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
         ("alu_pct", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("fp64_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         ("l2_pct", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed")]
 for r in rows[2:]:
     name = r[col["Kernel Name"]].split("(")[0][:60]

@@ -412,3 +412,34 @@ def test_config4_training_step_full_size(golden):
     assert _ledger(g) == [518, 101, 164, 382, 4, 54]
     w1 = P.decode(st.weights, tol=1e-3)
     assert np.max(np.abs(w1 - golden["cfg4_snaps"][0])) < 1e-3
+
+
+def _adversarial(moduli, nl, N, kind, rng):
+    """[2][nl][N] residues that push the lazy-reduction bounds: every word at
+    q - 1, alternating 0 / q - 1, or uniform."""
+    q = np.asarray(moduli[:nl], dtype=np.uint64)[None, :, None]
+    if kind == "max":
+        return np.broadcast_to(q - np.uint64(1), (2, nl, N)).copy()
+    if kind == "alt":
+        pat = (np.arange(N) % 2).astype(np.uint64)[None, None, :]
+        return (pat * (q - np.uint64(1))).astype(np.uint64) + np.zeros((2, nl, N), np.uint64)
+    return (rng.integers(0, 2 ** 63, (2, nl, N), dtype=np.uint64) % q).astype(np.uint64)
+
+
+@pytest.mark.parametrize("name,grid", [("small12", 16), ("cfg1", 128)])
+def test_adversarial_residues(name, grid):
+    """Rescale, rotation, conjugation and ct x ct on extreme residues: the
+    integer and FP64 lazy-bound paths (ntt_pass.cuh) must stay bit-exact."""
+    P = _prod()
+    g = P.CKKSContext(name, grid, seed=91)
+    o = R.OracleCKKSContext(name, grid, seed=91)
+    rng = np.random.default_rng(8)
+    lv = g.max_level
+    for kind in ("max", "alt", "rand"):
+        data = _adversarial(g.moduli, lv + 1, g.N, kind, rng)
+        gb, ob = g.from_residues(data, lv), R.RnsBlock(o, data, lv)
+        np.testing.assert_array_equal(g.rescale(gb).residues(), o.p.rescale(data, lv))
+        for r in (1, 5):
+            np.testing.assert_array_equal(g.lrot(gb, r).residues(), o.lrot(ob, r).data)
+        np.testing.assert_array_equal(g.conj(gb).residues(), o.conj(ob).data)
+        np.testing.assert_array_equal(g.mult(gb, gb).residues(), o.mult(ob, ob).data)

@@ -61,6 +61,8 @@ class Clocks:
         self.device, self.proc, self.lines = device, None, []
 
     def start(self):
+        if os.environ.get("HC_BENCH_NO_SMI"):    # diagnosis only: no clock evidence
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -73,6 +75,14 @@ class Clocks:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_ready(self, timeout=5.0):
+        """nvidia-smi's start-up (NVML init) can stall the process's CUDA calls
+        for a few hundred ms: start the sampler before warm-up and let its
+        first sample arrive before the timed region."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
 
     def stop(self):
         if not self.proc:
@@ -101,10 +111,30 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def quiet_gc():
+    """A full cyclic-GC pass over the process (torch alone brings ~10^5
+    objects) stalls the issuing thread for 100+ ms and starves the GPU of
+    work: freeze the objects that exist after set-up and collect the rest
+    only between measurements (the library's ciphertext handles are not
+    cyclic, so reference counting frees them)."""
+    import gc
+    gc.collect()
+    gc.freeze()
+    if os.environ.get("HC_BENCH_GC", "0") != "1":
+        gc.disable()
+
+
 def dist_setup(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world == 1 and os.environ.get("HC_BENCH_TORCH_EARLY", "1") == "1":
+        # bring torch's CUDA state up before the library context exists, not
+        # lazily at the first barrier next to the timed region
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            torch.cuda.synchronize()
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -223,22 +253,28 @@ def run_b200(args, world, rank, local):
         grad = P.diag_atb(EP, EX)
         return logits, grad
 
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.wait_ready()
     for _ in range(args.warmup):
         step()
     ctx.sync()
+    quiet_gc()
     counts0 = ctx.ledger.counts()
     extra0 = ctx.extra
     launches0 = L.hc_launch_count(ctx._h)
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.3)
     barrier(world)
     N.check(L.hc_timer_begin(ctx._h))
     outs = None
+    trace = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         outs = step()
+        trace.append(round((time.perf_counter() - t0) * 1e3, 1))
     ms = C.c_float()
+    t0 = time.perf_counter()
     N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    trace.append(("drain", round((time.perf_counter() - t0) * 1e3, 1)))
     barrier(world)
     clk = clocks.stop()
     total_ms = all_max(ms.value, world)
@@ -280,7 +316,7 @@ def run_b200(args, world, rank, local):
     host_out = [torch.empty(int(np.prod(s)), dtype=torch.int64, pin_memory=True) for s in out_shapes]
     h2d = sum(t.numel() * 8 for t, _ in host_in)
     d2h = sum(t.numel() * 8 for t in host_out)
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, args.steps)
     barrier(world)
     N.check(L.hc_timer_begin(ctx._h))
     for _ in range(e2e_steps):
@@ -329,6 +365,8 @@ def run_b200(args, world, rank, local):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if os.environ.get("HC_BENCH_TRACE"):
+        line["host_issue_ms_per_step"] = trace
     if world == 1 and not args.no_cpu:
         samples, _ = oracle_pass_sample(1)
         line["cpu_baseline"] = {"value": samples[0], "unit": "ms", "cores": os.cpu_count(), "kind": "port",
@@ -363,14 +401,15 @@ def run_train_step(args, world, rank, local):
     def step():
         P.nag_step(state, EX, EY, wl.LEARNING_RATE, X.shape[0], reducer=red)
 
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.wait_ready()
     for _ in range(args.warmup):
         step()
     ctx.sync()
+    quiet_gc()
     c0 = ctx.ledger.counts()
     launches0 = L.hc_launch_count(ctx._h)
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.3)
     barrier(world)
     ms = C.c_float()
     N.check(L.hc_timer_begin(ctx._h))

@@ -150,6 +150,9 @@ int64_t hc_launch_count(hc_ctx *ctx);
 /* key-switch throughput: `streams` concurrent chains of `reps` rotations of ct
  * (device time in ms over all streams*reps key switches; ledger untouched) */
 int hc_bench_keyswitch(hc_ctx *ctx, const hc_ct *ct, int streams, int reps, float *ms);
+/* same with `batch` rotations per step of each chain issued as one batched pipeline
+ * (device time in ms over all streams*batch*reps key switches) */
+int hc_bench_keyswitch_batch(hc_ctx *ctx, const hc_ct *ct, int streams, int batch, int reps, float *ms);
 /* batched NTT throughput: `reps` forward (or inverse) transforms of `nlimbs` limbs */
 int hc_bench_ntt(hc_ctx *ctx, int nlimbs, int reps, int inverse, float *ms);
 /* per-kernel event profiler: JSON {"kernel": [launches, total_ms, algorithmic_bytes], ...} */

@@ -133,6 +133,7 @@ int hc_key_download(hc_ctx* ctx, int g, uint64_t* out) {
 uint64_t hc_galois_rot(hc_ctx* ctx, int64_t r) { return hc::galois_rot(*ctx->c, r); }
 
 int hc_ct_free(hc_ct* ct) {
+    hc::HostTrace tr("hc_ct_free");
     return guard([&] { delete ct; });
 }
 int hc_ct_level(const hc_ct* ct) { return ct->p->level; }
@@ -329,16 +330,21 @@ int hc_bench_ntt(hc_ctx* ctx, int nlimbs, int reps, int inverse, float* ms) {
 static void snap(hc_ctx* ctx, int64_t* b);
 
 int hc_bench_keyswitch(hc_ctx* ctx, const hc_ct* a, int streams, int reps, float* ms) {
+    return hc_bench_keyswitch_batch(ctx, a, streams, 1, reps, ms);
+}
+
+int hc_bench_keyswitch_batch(hc_ctx* ctx, const hc_ct* a, int streams, int batch, int reps, float* ms) {
     return guard([&] {
         hc::Ctx& c = *ctx->c;
+        if (streams < 1 || batch < 1 || reps < 1) throw hc::Error(HC_EPARAM, "bad sizes");
         int64_t saved[HC_NCOUNTS];
         snap(ctx, saved);
         hc::Eval ev(c, false);
-        hc::probe_rotations(ev, a->p, streams, 1);     // warm keys and pool
+        hc::probe_rotations(ev, a->p, streams, 1, batch);     // warm keys and pool
         HC_CUDA(cudaStreamSynchronize(c.stream));
         if (!c.t0) { HC_CUDA(cudaEventCreate(&c.t0)); HC_CUDA(cudaEventCreate(&c.t1)); }
         HC_CUDA(cudaEventRecord(c.t0, c.stream));
-        hc::probe_rotations(ev, a->p, streams, reps);
+        hc::probe_rotations(ev, a->p, streams, reps, batch);
         HC_CUDA(cudaEventRecord(c.t1, c.stream));
         HC_CUDA(cudaEventSynchronize(c.t1));
         HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
@@ -422,6 +428,7 @@ struct RunAhead {
                 HC_CUDA(cudaEventRecord(e, c.main_stream));
             }
         }
+        hc::HostTrace tr("run-ahead wait");
         HC_CUDA(cudaEventSynchronize(c.ra_ev[c.ra_idx]));
     }
     ~RunAhead() {
@@ -432,6 +439,7 @@ struct RunAhead {
 
 int hc_diag_abt(hc_ctx* ctx, const hc_ct* const* A, int m, int n, const hc_ct* const* B, int c, double scale,
                 hc_ct** out, int64_t* counts) {
+    hc::HostTrace tr("hc_diag_abt");
     return guard([&] {
         int64_t before[HC_NCOUNTS];
         snap(ctx, before);
@@ -445,6 +453,7 @@ int hc_diag_abt(hc_ctx* ctx, const hc_ct* const* A, int m, int n, const hc_ct* c
 
 int hc_diag_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B, int n, int c, double scale,
                 hc_ct** out, int64_t* counts, hc_reduce_fn reduce_fn, void* user) {
+    hc::HostTrace tr("hc_diag_atb");
     return guard([&] {
         int64_t before[HC_NCOUNTS];
         snap(ctx, before);

@@ -5,7 +5,9 @@
 // compiled with -ffp-contract=off so its double arithmetic is bit-identical
 // to the oracle's (oracle/ckks_oracle.c) on the same machine.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -60,13 +62,62 @@ static unsigned brv(unsigned x, int bits) {
     return r;
 }
 
+double host_trace_threshold_ms() {
+    static const double t = [] {
+        const char* e = std::getenv("HC_HOST_TRACE");
+        return e ? std::atof(e) : -1.0;
+    }();
+    return t;
+}
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostTrace::HostTrace(const char* w) : what(w) {
+    if (host_trace_threshold_ms() >= 0) t0 = now_ms();
+}
+HostTrace::~HostTrace() {
+    if (host_trace_threshold_ms() < 0) return;
+    const double dt = now_ms() - t0;
+    if (dt > host_trace_threshold_ms()) std::fprintf(stderr, "[hc host] %s blocked %.1f ms\n", what, dt);
+}
+
 u64* Ctx::alloc(size_t words) {
+    HostTrace tr("alloc");
     void* p = nullptr;
     HC_CUDA(cudaMallocFromPoolAsync(&p, words * sizeof(u64), pool, stream));
     return (u64*)p;
 }
 void Ctx::free(u64* p) {
+    HostTrace tr("free");
     if (p) HC_CUDA(cudaFreeAsync(p, stream));
+}
+
+Scratch::Scratch(Ctx& ctx) : c(ctx) {
+    a = &c.arenas[c.stream];
+    mark = a->top;
+}
+Scratch::~Scratch() { a->top = mark; }
+u64* Scratch::take(size_t words) {
+    words = (words + 31) & ~(size_t)31;   // 256-byte alignment
+    if (a->top + words > a->cap) {
+        // grow: the old buffer may still be read by queued work on this
+        // stream, so it is retired, not freed; live data below `top` in it is
+        // not moved (outer scopes keep their pointers), only new takes go to
+        // the new buffer
+        HostTrace tr("scratch grow");
+        const size_t need = std::max(a->cap * 2, a->top + words + ((size_t)64 << 20) / 8);
+        void* p = nullptr;
+        HC_CUDA(cudaMalloc(&p, need * sizeof(u64)));
+        if (a->base) c.arena_graveyard.push_back(a->base);
+        a->base = (u64*)p;
+        a->cap = need;
+        // outer scopes' marks index the old buffer; restart this scope at 0 of the new one
+        a->top = 0;
+        mark = 0;
+    }
+    u64* p = a->base + a->top;
+    a->top += words;
+    return p;
 }
 
 cudaEvent_t Ctx::get_event() {
@@ -80,7 +131,7 @@ cudaEvent_t Ctx::get_event() {
     return e;
 }
 
-Launch::Launch(Ctx& ctx, const char* name, double bytes) : c(ctx) {
+Launch::Launch(Ctx& ctx, const char* name, double bytes) : c(ctx), trace(name) {
     c.launches++;
     if (!c.prof) return;
     Ctx::ProfRec r{name, c.get_event(), c.get_event(), bytes};
@@ -164,8 +215,9 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     HC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->main_stream = c->stream;
     if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("HC_KS_SPLIT")) c->ks_split = std::atoi(e);
     if (const char* e = std::getenv("HC_NTT_FP")) c->ntt_fp = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HC_LOCKSTEP")) c->lockstep = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HC_BATCH")) c->batch = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HC_RUNAHEAD")) c->ra_depth = std::max(1, std::atoi(e));
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
@@ -381,6 +433,17 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
 void ctx_destroy(Ctx* c) {
     if (!c) return;
     cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->arenas) cudaFree(kv.second.base);
+    for (auto* p : c->arena_graveyard) cudaFree(p);
+    if (std::getenv("HC_POOL_STATS")) {
+        uint64_t v[4] = {0, 0, 0, 0};
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &v[0]);
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemHigh, &v[1]);
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &v[2]);
+        cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemHigh, &v[3]);
+        std::fprintf(stderr, "[hc pool] reserved %.2f GB (high %.2f GB), used %.2f GB (high %.2f GB)\n", v[0] / 1e9,
+                     v[1] / 1e9, v[2] / 1e9, v[3] / 1e9);
+    }
     c->pt_cache.clear();
     for (auto& kv : c->keys) cudaFree(kv.second.d);
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);

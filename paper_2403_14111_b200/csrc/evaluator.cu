@@ -245,21 +245,87 @@ bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out) {
     return true;
 }
 
+// Batched rotations / conjugations (all inputs at one level): one fused
+// key-switch pipeline for the whole batch.  add_self: out_b = sigma(a_b) + a_b.
+std::vector<CtP> ev_automorph_batch(Ctx& c, const std::vector<const Ct*>& a, u64 g, bool add_self) {
+    const size_t B = a.size();
+    std::vector<CtP> out(B);
+    if (B == 0) return out;
+    bool uniform = c.logN >= 14;
+    for (auto* x : a) uniform &= x->level == a[0]->level;
+    if (uniform && B > 1) {
+        const Key& key = get_key(c, (int)g);
+        std::vector<KsIn> in(B);
+        for (size_t b = 0; b < B; b++) {
+            out[b] = new_ct(c, a[b]->level);
+            in[b] = KsIn{a[b]->poly(1), out[b]->d, a[b]->poly(0), add_self ? a[b]->d : nullptr, key.d};
+        }
+        if (keyswitch_fused_batch(c, (int)B, in.data(), g, a[0]->level, 1, g)) {
+            c.counts[OP_KS] += (int64_t)B;
+            return out;
+        }
+    }
+    for (size_t b = 0; b < B; b++) {
+        if (!add_self) { out[b] = ev_automorph(c, *a[b], g); continue; }
+        if (ev_automorph_add(c, *a[b], g, out[b])) continue;
+        CtP r = ev_automorph(c, *a[b], g);
+        out[b] = ev_add(c, *a[b], *r, false);
+    }
+    return out;
+}
+
+// Batched ct x ct products (pairs at one level): tensor per pair, one fused
+// relinearisation pipeline, rescale per pair.
+std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, const Ct*>>& ab) {
+    const size_t B = ab.size();
+    std::vector<CtP> out(B);
+    if (B == 0) return out;
+    bool uniform = c.logN >= 14;
+    for (auto& pr : ab) {
+        check_same(*pr.first, *pr.second);
+        uniform &= pr.first->level == ab[0].first->level;
+    }
+    if (!uniform || B == 1) {
+        for (size_t b = 0; b < B; b++) out[b] = ev_mult(c, *ab[b].first, *ab[b].second);
+        return out;
+    }
+    const int level = ab[0].first->level;
+    if (level < 1) throw Error(-3, "multiply at level 0");
+    const Key& key = get_key(c, 0);
+    const int nl = level + 1;
+    const size_t poly = (size_t)nl * c.N;
+    Scratch sc(c);
+    u64* D = sc.take(3 * poly * B);
+    u64* T = sc.take(2 * poly * B);
+    std::vector<KsIn> in(B);
+    for (size_t b = 0; b < B; b++) {
+        u64* Db = D + 3 * poly * b;
+        k_tensor(c, Db, ab[b].first->d, ab[b].second->d, nl);
+        in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
+    }
+    if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) throw Error(-2, "batched relinearisation");
+    c.counts[OP_KS] += (int64_t)B;
+    for (size_t b = 0; b < B; b++) {
+        out[b] = new_ct(c, level - 1);
+        rescale_raw(c, T + 2 * poly * b, level, 2, out[b]->d);
+    }
+    return out;
+}
+
 CtP ev_mult(Ctx& c, const Ct& a, const Ct& b) {
     check_same(a, b);
     if (a.level < 1) throw Error(-3, "multiply at level 0");
     const Key& key = get_key(c, 0);
     const int nl = a.level + 1;
     const size_t poly = (size_t)nl * c.N;
-    u64* D = c.alloc(3 * poly);
+    Scratch sc(c);
+    u64* D = sc.take(3 * poly);
     k_tensor(c, D, a.d, b.d, nl);
-    u64* T = c.alloc(2 * poly);
+    u64* T = sc.take(2 * poly);
     if (keyswitch_fused(c, D + 2 * poly, 0, a.level, key, T, D, 2, 0)) c.counts[OP_KS]++;
     else keyswitch(c, D + 2 * poly, a.level, key, T, D, 2);
-    c.free(D);
     CtP o = new_ct(c, a.level - 1);
     rescale_raw(c, T, a.level, 2, o->d);
-    c.free(T);
     return o;
 }
 
@@ -362,6 +428,61 @@ CtP Eval::add_lrot(const CtP& a, int64_t r) {
     if (ev_automorph_add(c, *a, galois_rot(c, r), o)) return o;
     CtP rot = ev_automorph(c, *a, galois_rot(c, r));
     return ev_add(c, *a, *rot, false);
+}
+
+std::vector<CtP> Eval::lrot_batch(const std::vector<CtP>& xs, int64_t r, bool add_self) {
+    const int64_t S = c.N / 2;
+    r = ((r % S) + S) % S;
+    std::vector<CtP> out(xs.size());
+    if (r == 0) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = add_self ? add(xs[i], xs[i]) : xs[i];
+        return out;
+    }
+    rec(OP_ROT, (int)xs.size());
+    if (add_self) rec(OP_ADD, (int)xs.size());
+    std::vector<const Ct*> a(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) a[i] = xs[i].get();
+    return ev_automorph_batch(c, a, galois_rot(c, r), add_self);
+}
+
+std::vector<CtP> Eval::conj_batch(const std::vector<CtP>& xs) {
+    rec(OP_CONJ, (int)xs.size());
+    std::vector<const Ct*> a(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) a[i] = xs[i].get();
+    return ev_automorph_batch(c, a, 2 * (u64)c.N - 1, false);
+}
+
+std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys) {
+    bool boot = false;
+    for (size_t i = 0; i < xs.size(); i++) boot |= xs[i]->level < 1 || ys[i]->level < 1;
+    std::vector<CtP> out(xs.size());
+    if (boot) {   // refreshes: the reference's op-by-op order fixes their nonces
+        for (size_t i = 0; i < xs.size(); i++) out[i] = mult(xs[i], ys[i]);
+        return out;
+    }
+    rec(OP_MULT, (int)xs.size());
+    std::vector<CtP> ax(xs.size()), ay(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) {
+        const int l = std::min(xs[i]->level, ys[i]->level);
+        ax[i] = at(xs[i], l);
+        ay[i] = at(ys[i], l);
+    }
+    // one fused pipeline per level present
+    std::vector<char> done(xs.size(), 0);
+    for (size_t i = 0; i < xs.size(); i++) {
+        if (done[i]) continue;
+        std::vector<size_t> idx;
+        std::vector<std::pair<const Ct*, const Ct*>> ab;
+        for (size_t j = i; j < xs.size(); j++)
+            if (!done[j] && ax[j]->level == ax[i]->level) {
+                idx.push_back(j);
+                ab.emplace_back(ax[j].get(), ay[j].get());
+                done[j] = 1;
+            }
+        std::vector<CtP> r = ev_mult_batch(c, ab);
+        for (size_t k = 0; k < idx.size(); k++) out[idx[k]] = r[k];
+    }
+    return out;
 }
 
 CtP Eval::conj(const CtP& a) {

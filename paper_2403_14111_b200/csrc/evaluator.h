@@ -18,6 +18,16 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
 // d and the addend are read through the galois permutation gal / add_gal (0 = none).
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
                      int add_npoly, u64 add_gal, const u64* addend2 = nullptr);
+// one key switch of a batched pipeline (keyswitch.cu): d is read through the
+// batch's Galois element, add (add_npoly polys) through add_gal, add2 as is
+struct KsIn {
+    const u64* d;
+    u64* out;
+    const u64* add;
+    const u64* add2;
+    const u64* key;
+};
+bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal);
 // out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
 bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
@@ -69,6 +79,12 @@ struct Eval {
     CtP add_lrot(const CtP& a, int64_t r);
     CtP add_rrot(const CtP& a, int64_t r) { return add_lrot(a, -r); }
     CtP conj(const CtP& a);
+    // batched forms (same ledger entries as the per-op calls; one fused
+    // key-switch pipeline per level): lrot (add_self: add(a, lrot(a, r))),
+    // conj and ct x ct over vectors of independent operands
+    std::vector<CtP> lrot_batch(const std::vector<CtP>& xs, int64_t r, bool add_self = false);
+    std::vector<CtP> conj_batch(const std::vector<CtP>& xs);
+    std::vector<CtP> mult_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys);
     CtP mul_i(const CtP& a);
     CtP bootstrap(const CtP& a);
     PtP encoded(const Pattern& p, int level);

@@ -16,6 +16,7 @@ namespace hc {
 
 constexpr int MAXP = 48;       // max primes in Q u P
 constexpr int MAXJ = 96;       // max limb jobs in one batched launch
+constexpr int KS_MAXB = 24;    // max key switches in one batched pipeline (keyswitch.cu)
 
 #define HC_CUDA(x)                                                                     \
     do {                                                                               \
@@ -39,6 +40,10 @@ struct JobList {
     u64* ptr[MAXJ];
     const u64* src[MAXJ];   // optional out-of-place source (nullptr = in place)
     u64 scale[MAXJ], scale_s[MAXJ];
+    // batch dimension (grid z): copy b of job i works on ptr[i] + boff[b] and
+    // reads src[i] + sboff[b] (element offsets; copy 0 has offset 0)
+    int nb = 1;
+    long long boff[KS_MAXB], sboff[KS_MAXB];
 };
 
 // host-side view of one prime with its precomputation
@@ -92,8 +97,9 @@ struct Ctx {
     int fork_depth = 0;
     int fork_rot[4] = {0, 0, 0, 0};
     int fork_cap = 8;             // max side streams a schedule fans out to (hc_set_streams)
-    int ks_split = 1;             // key product as NTT chunk pass + streaming kernel (HC_KS_SPLIT)
     bool ntt_fp = true;           // FP64 NTT passes for primes below 2^46 (HC_NTT_FP=0 disables)
+    bool lockstep = true;         // batched (lockstep) diagonal passes when no refresh can fire (HC_LOCKSTEP)
+    int batch = 3;                // key switches per batched pipeline in the lockstep schedules (HC_BATCH)
     std::vector<cudaEvent_t> ra_ev;   // schedule run-ahead throttle (capi.cu): a schedule call
     int ra_idx = 0;                   // waits for the one ra_depth calls back to finish
     int ra_depth = 8;                 // HC_RUNAHEAD (2 measured host-jitter-bound steps)
@@ -151,6 +157,39 @@ struct Ctx {
     // workspace stream-ordered allocation
     u64* alloc(size_t words);
     void free(u64* p);
+
+    // Per-stream scratch arenas for the temporaries of one pipeline (key
+    // switch, rescale, tensor).  Work on one stream is ordered, so a scope can
+    // reuse the bytes the previous scope on that stream released; no pool
+    // bookkeeping on the hot path (the pool occasionally blocked the issuing
+    // thread for 100+ ms while it remapped memory).  Scopes nest (stack).
+    struct Arena {
+        u64* base = nullptr;
+        size_t cap = 0, top = 0;
+    };
+    std::map<cudaStream_t, Arena> arenas;
+    std::vector<u64*> arena_graveyard;   // outgrown buffers (may still be in use by queued work)
+};
+
+// RAII scratch scope on the context's current stream
+struct Scratch {
+    Ctx& c;
+    Ctx::Arena* a;
+    size_t mark;
+    explicit Scratch(Ctx& ctx);
+    ~Scratch();
+    u64* take(size_t words);
+};
+
+// Diagnosis of host-side stalls: with HC_HOST_TRACE=<ms>, any traced scope
+// (allocation, free, launch, run-ahead wait) that blocks the issuing thread
+// longer than that is reported on stderr.
+double host_trace_threshold_ms();
+struct HostTrace {
+    const char* what;
+    double t0 = 0;
+    explicit HostTrace(const char* w);
+    ~HostTrace();
 };
 
 // RAII scope around one kernel launch: counts it and, when profiling,
@@ -159,6 +198,7 @@ struct Ctx {
 struct Launch {
     Ctx& c;
     int idx = -1;
+    HostTrace trace;
     Launch(Ctx& ctx, const char* name, double bytes);
     ~Launch();
 };
@@ -167,7 +207,6 @@ struct Launch {
 void ntt_forward(Ctx& c, const JobList& jobs);
 void ntt_inverse(Ctx& c, const JobList& jobs);
 void ntt_forward_chunks(Ctx& c, const JobList& jobs);
-void ntt_inverse_cols(Ctx& c, const JobList& jobs);
 
 // ---- context (context.cu) ----
 Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, int alpha,

@@ -40,6 +40,23 @@ struct KsJobs {
 struct KsGeo {
     int level, nl, nt, L, K, alpha, dnum, nall, beta, logN, N1;
     __host__ __device__ int prime(int t) const { return t <= level ? t : L + 1 + (t - level - 1); }
+    // per-key-switch strides of the batched intermediates (words)
+    __host__ __device__ size_t y_stride() const { return (size_t)nl << logN; }            // Y   [nl][N]
+    __host__ __device__ size_t i_stride() const { return (size_t)beta * nt << logN; }     // I   [beta][nt][N]
+    __host__ __device__ size_t acc_stride() const { return (size_t)2 * nt << logN; }      // ACC [2][nt][N]
+    __host__ __device__ size_t w_stride() const { return (size_t)2 * nl << logN; }        // Wt  [2][nl][N]
+};
+
+// The key switches of one batched pipeline: all at the same level and read
+// through the same Galois element; each has its own input, output, addends
+// and switching key (equal keys are read once by the key product).
+struct KsBatch {
+    int nb;
+    const u64* d[KS_MAXB];      // c1 source (NTT form), read through gal
+    u64* out[KS_MAXB];          // [2][nl][N]
+    const u64* add[KS_MAXB];    // [add_npoly][nl][N] addend (read through add_gal) or null
+    const u64* add2[KS_MAXB];   // [2][nl][N] second addend (ladder step) or null
+    const u64* key[KS_MAXB];    // [dnum][2][nall][N]
 };
 
 // ---- A: ModUp conversion fused into the column pass --------------------------
@@ -78,6 +95,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const int hi = min(lo + g.alpha, g.nl);
     const PrimeDev P = primes[pi];
     const u64 p = P.q;
+    Y += blockIdx.z * g.y_stride();
+    I += blockIdx.z * g.i_stride();
     LdModup<NA> ld;
     ld.na = hi - lo;
     ld.p = p;
@@ -98,221 +117,83 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
-// ---- B: chunk pass + key inner product ------------------------------------
-
-struct StCapture {
-    u64* x;
-    __device__ __forceinline__ void operator()(size_t, u64) const {}   // unused: chunk edge is contiguous
-    __device__ __forceinline__ void store8(size_t, const u64* v) const {
-#pragma unroll
-        for (int e = 0; e < 8; e++) x[e] = v[e];
-    }
-};
-
-constexpr int KP_MAXB = 4;   // digits handled by the fused key product (dnum <= 4)
-#ifndef KP_MIN_BLOCKS
-#define KP_MIN_BLOCKS 2
-#endif
-
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, KP_MIN_BLOCKS)
-    ks_chunks_keyprod(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ I, const u64* __restrict__ d, u64 gal,
-                      const u64* __restrict__ key, u64* __restrict__ acc) {
-    using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
-    extern __shared__ u64 sm[];
-    const int t = blockIdx.y;
-    const int pi = g.prime(t);
-    const size_t N = (size_t)1 << g.logN;
-    const PrimeDev P = primes[pi];
-    PG G;
-    G.init(g.N1);
-    const ulonglong2* TW = tw + ((size_t)pi << g.logN);
-    ulonglong2* twsm = PG::twsm_of(sm);
-    stage_twiddles(G, twsm, TW, g.N1);
-    cp_async_wait_all();
-    __syncthreads();
-    const size_t k0 = G.gidx(G.lt * 8);     // this thread's 8 consecutive output coefficients
-    // digit values staged in registers; the 128-bit accumulators are then
-    // short-lived (one pair of outputs at a time), which keeps the kernel at
-    // 3 CTAs per SM
-    u64 xs[KP_MAXB][8];
-#pragma unroll
-    for (int j = 0; j < KP_MAXB; j++) {
-        if (j >= g.beta) break;
-        const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
-        if (t >= lo && t < hi) {
-            if (gal) {
-                LdGalois ld{d + (size_t)t * N, g.logN, gal};
-                ld.load8(k0, xs[j]);
-            } else {
-                LdPlain ld{d + (size_t)t * N};
-                ld.load8(k0, xs[j]);
-            }
-        } else {
-            __syncthreads();
-            LdPlain ld{I + ((size_t)j * g.nt + t) * N};
-            StCapture st{xs[j]};
-            ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, false);
-        }
-    }
-    ulonglong2* o0 = reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k0);
-    ulonglong2* o1 = reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k0);
-    const size_t kstride = (size_t)g.nall * N;
-#pragma unroll
-    for (int v = 0; v < 4; v++) {
-        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
-#pragma unroll
-        for (int j = 0; j < KP_MAXB; j++) {
-            if (j >= g.beta) break;
-            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0 + 2 * v;
-            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
-            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
-            mac128(b0, xs[j][2 * v], kbv.x);
-            mac128(b1, xs[j][2 * v + 1], kbv.y);
-            mac128(a0, xs[j][2 * v], kav.x);
-            mac128(a1, xs[j][2 * v + 1], kav.y);
-        }
-        o0[v] = make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
-        o1[v] = make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
-    }
-}
+constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
 
 // ---- B (split form): streaming key inner product over NTT-form digits -----
 // UP[j][t] holds NTT(conv_j(t)) for t outside digit j; inside the digit the
 // value is sigma(d)[t] itself, gathered on the fly.  Two coefficients per
 // thread, 16-byte accesses, one Barrett reduction per output.
 
-__global__ void __launch_bounds__(256) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
-                                                         const u64* __restrict__ UP, const u64* __restrict__ d,
-                                                         u64 gal, const u64* __restrict__ key,
-                                                         u64* __restrict__ acc, int tlimit) {
+__global__ void __launch_bounds__(256, 3) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
+                                                            const u64* __restrict__ UP, u64 gal, KsBatch kb,
+                                                            u64* __restrict__ acc, int tlimit) {
     const size_t N = (size_t)1 << g.logN;
-    const size_t total = (size_t)tlimit << (g.logN - 1);
+    const size_t total = (size_t)tlimit << g.logN;
     const size_t kstride = (size_t)g.nall * N;
     for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < total; v += (size_t)gridDim.x * blockDim.x) {
-        const int t = (int)(v >> (g.logN - 1));
-        const size_t k = (v & ((N >> 1) - 1)) * 2;
+        const int t = (int)(v >> g.logN);
+        const size_t k = v & (N - 1);
         const int pi = g.prime(t);
         const PrimeDev P = primes[pi];
-        // issue every load of the (up to KP_MAXB) digits before the first MAC
-        u64 x0[KP_MAXB], x1[KP_MAXB];
-        ulonglong2 kbv[KP_MAXB], kav[KP_MAXB];
+        // the key words of this (t, k) stay in registers across the batch
+        // while the switching key does not change
+        u64 kbv[KP_MAXB], kav[KP_MAXB];
+        const u64* kprev = nullptr;
+        for (int b = 0; b < kb.nb; b++) {
+            if (kb.key[b] != kprev) {
+                kprev = kb.key[b];
 #pragma unroll
-        for (int j = 0; j < KP_MAXB; j++) {
-            if (j >= g.beta) break;
-            const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
-            if (t >= lo && t < hi) {
-                const u64* src = d + (size_t)t * N;
-                if (gal) {
-                    x0[j] = src[galois_src((unsigned)k, g.logN, gal)];
-                    x1[j] = src[galois_src((unsigned)k + 1, g.logN, gal)];
-                } else {
-                    const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(src + k);
-                    x0[j] = xv.x;
-                    x1[j] = xv.y;
+                for (int j = 0; j < KP_MAXB; j++) {
+                    if (j >= g.beta) break;
+                    const u64* kp = kprev + ((size_t)(2 * j) * g.nall + pi) * N + k;
+                    kbv[j] = kp[0];
+                    kav[j] = kp[kstride];
                 }
+            }
+            const u64* up = UP + b * g.i_stride();
+            const u64* d = kb.d[b];
+            // issue every digit load before the first product
+            u64 x[KP_MAXB];
+#pragma unroll
+            for (int j = 0; j < KP_MAXB; j++) {
+                if (j >= g.beta) break;
+                const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
+                if (t >= lo && t < hi) {
+                    const u64* src = d + (size_t)t * N;
+                    x[j] = gal ? src[galois_src((unsigned)k, g.logN, gal)] : src[k];
+                } else {
+                    x[j] = up[((size_t)j * g.nt + t) * N + k];
+                }
+            }
+            u64 ob, oa;
+            if (P.fp) {
+                // FP64 products (q < 2^46): each term exact and centered (|r| < 0.6q),
+                // the sum of <= 4 reduced once; digits are lazy words below 2q
+                double sb = 0, sa = 0;
+#pragma unroll
+                for (int j = 0; j < KP_MAXB; j++) {
+                    if (j >= g.beta) break;
+                    const double y = fp_word(x[j]);
+                    sb = __dadd_rn(sb, fp_mulmod(y, fp_word(kbv[j]), P.qd, P.qinv));
+                    sa = __dadd_rn(sa, fp_mulmod(y, fp_word(kav[j]), P.qd, P.qinv));
+                }
+                ob = fp_canon(sb, P.qd, P.qinv);
+                oa = fp_canon(sa, P.qd, P.qinv);
             } else {
-                const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(UP + ((size_t)j * g.nt + t) * N + k);
-                x0[j] = xv.x;
-                x1[j] = xv.y;
+                U128 b0 = {0, 0}, a0 = {0, 0};
+#pragma unroll
+                for (int j = 0; j < KP_MAXB; j++) {
+                    if (j >= g.beta) break;
+                    mac128(b0, x[j], kbv[j]);
+                    mac128(a0, x[j], kav[j]);
+                }
+                ob = reduce128(b0.hi, b0.lo, P);
+                oa = reduce128(a0.hi, a0.lo, P);
             }
-            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k;
-            kbv[j] = *reinterpret_cast<const ulonglong2*>(kb);
-            kav[j] = *reinterpret_cast<const ulonglong2*>(kb + kstride);
+            u64* ab = acc + b * g.acc_stride();
+            ab[(size_t)t * N + k] = ob;
+            ab[((size_t)g.nt + t) * N + k] = oa;
         }
-        ulonglong2 ob, oa;
-        if (P.fp) {
-            // FP64 products (q < 2^46): each term exact and centered (|r| < 0.6q),
-            // the sum of <= 4 reduced once; digits are lazy words below 2q
-            double sb0 = 0, sb1 = 0, sa0 = 0, sa1 = 0;
-#pragma unroll
-            for (int j = 0; j < KP_MAXB; j++) {
-                if (j >= g.beta) break;
-                const double y0 = fp_word(x0[j]), y1 = fp_word(x1[j]);
-                sb0 = __dadd_rn(sb0, fp_mulmod(y0, fp_word(kbv[j].x), P.qd, P.qinv));
-                sb1 = __dadd_rn(sb1, fp_mulmod(y1, fp_word(kbv[j].y), P.qd, P.qinv));
-                sa0 = __dadd_rn(sa0, fp_mulmod(y0, fp_word(kav[j].x), P.qd, P.qinv));
-                sa1 = __dadd_rn(sa1, fp_mulmod(y1, fp_word(kav[j].y), P.qd, P.qinv));
-            }
-            ob = make_ulonglong2(fp_canon(sb0, P.qd, P.qinv), fp_canon(sb1, P.qd, P.qinv));
-            oa = make_ulonglong2(fp_canon(sa0, P.qd, P.qinv), fp_canon(sa1, P.qd, P.qinv));
-        } else {
-            U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
-#pragma unroll
-            for (int j = 0; j < KP_MAXB; j++) {
-                if (j >= g.beta) break;
-                mac128(b0, x0[j], kbv[j].x);
-                mac128(b1, x1[j], kbv[j].y);
-                mac128(a0, x0[j], kav[j].x);
-                mac128(a1, x1[j], kav[j].y);
-            }
-            ob = make_ulonglong2(reduce128(b0.hi, b0.lo, P), reduce128(b1.hi, b1.lo, P));
-            oa = make_ulonglong2(reduce128(a0.hi, a0.lo, P), reduce128(a1.hi, a1.lo, P));
-        }
-        *reinterpret_cast<ulonglong2*>(acc + (size_t)t * N + k) = ob;
-        *reinterpret_cast<ulonglong2*>(acc + ((size_t)g.nt + t) * N + k) = oa;
-    }
-}
-
-// ---- B2 for the P limbs: key product + the first (chunk) pass of their INTT --
-// Each thread owns 8 consecutive coefficients, which are exactly the
-// elements the inverse chunk pass's first round needs, so the products never
-// leave registers before the transform.
-
-struct LdRegs {
-    const u64* x;
-    __device__ __forceinline__ u64 operator()(size_t) const { return 0; }   // unused: edge is contiguous
-    __device__ __forceinline__ void load8(size_t, u64* o) const {
-#pragma unroll
-        for (int e = 0; e < 8; e++) o[e] = x[e];
-    }
-};
-
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
-    ks_keyprod_p_intt(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ itw,
-                      const u64* __restrict__ UP, const u64* __restrict__ key, u64* __restrict__ acc) {
-    using PG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
-    extern __shared__ u64 sm[];
-    const int t = g.nl + blockIdx.y;            // P limb (never inside a Q digit)
-    const int pi = g.prime(t);
-    const size_t N = (size_t)1 << g.logN;
-    const PrimeDev P = primes[pi];
-    PG G;
-    G.init(g.N1);
-    const size_t k0 = G.gidx(G.lt * 8);
-    const size_t kstride = (size_t)g.nall * N;
-    u64 r0[8], r1[8];
-#pragma unroll
-    for (int v = 0; v < 4; v++) {
-        U128 b0 = {0, 0}, b1 = {0, 0}, a0 = {0, 0}, a1 = {0, 0};
-#pragma unroll
-        for (int j = 0; j < KP_MAXB; j++) {
-            if (j >= g.beta) break;
-            const ulonglong2 xv =
-                *reinterpret_cast<const ulonglong2*>(UP + ((size_t)j * g.nt + t) * N + k0 + 2 * v);
-            const u64* kb = key + ((size_t)(2 * j) * g.nall + pi) * N + k0 + 2 * v;
-            const ulonglong2 kbv = *reinterpret_cast<const ulonglong2*>(kb);
-            const ulonglong2 kav = *reinterpret_cast<const ulonglong2*>(kb + kstride);
-            mac128(b0, xv.x, kbv.x);
-            mac128(b1, xv.y, kbv.y);
-            mac128(a0, xv.x, kav.x);
-            mac128(a1, xv.y, kav.y);
-        }
-        r0[2 * v] = reduce128(b0.hi, b0.lo, P);
-        r0[2 * v + 1] = reduce128(b1.hi, b1.lo, P);
-        r1[2 * v] = reduce128(a0.hi, a0.lo, P);
-        r1[2 * v + 1] = reduce128(a1.hi, a1.lo, P);
-    }
-    const ulonglong2* TW = itw + ((size_t)pi << g.logN);
-    {
-        LdRegs ld{r0};
-        StPlain<true, false> st{acc + (size_t)t * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P, ld, st);
-    }
-    __syncthreads();
-    {
-        LdRegs ld{r1};
-        StPlain<true, false> st{acc + ((size_t)g.nt + t) * N, P.q, 0, 0};
-        ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, true, 2, 2>(G, sm, TW, P, ld, st);
     }
 }
 
@@ -328,6 +209,8 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const size_t N = (size_t)1 << g.logN;
     const PrimeDev P = primes[i];
     const u64 q = P.q;
+    acc += blockIdx.z * g.acc_stride();
+    Wt += blockIdx.z * g.w_stride();
     LdModup<NK> ld;
     ld.na = g.K;
     ld.p = q;
@@ -378,16 +261,21 @@ struct StModdown {
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
-                      const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly, u64 add_gal,
-                      const u64* __restrict__ addend2, u64* __restrict__ out) {
+                      const u64* __restrict__ pinv, int add_npoly, u64 add_gal, KsBatch kb) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
+    const int b = blockIdx.z;
+    Wt += b * g.w_stride();
+    acc += b * g.acc_stride();
+    const u64* __restrict__ addend = kb.add[b];
+    const u64* __restrict__ addend2 = kb.add2[b];
+    u64* __restrict__ out = kb.out[b];
     const PrimeDev P = primes[i];
     const u64 q = P.q;
     LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
     StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
-                 (s < add_npoly) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
+                 (s < add_npoly && addend) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
                  add_gal, g.logN, addend2 ? addend2 + ((size_t)s * g.nl + i) * N : nullptr};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
     G.init(g.N1);
@@ -496,22 +384,36 @@ template <> struct ColCfg<16> { static constexpr int LOGSZ = 7, SUBS = 16; };
 template <> struct ColCfg<17> { static constexpr int LOGSZ = 8, SUBS = 8; };
 
 template <int LOGN>
-static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out,
-                              const u64* addend, int add_npoly, u64 add_gal, const u64* addend2) {
+static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
     KsGeo g{level, nl, nt, c.L, K, c.alpha, c.dnum, c.nall, (nl + c.alpha - 1) / c.alpha, c.logN, N >> CH_LOG};
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
+    KsBatch kb;
+    kb.nb = B;
+    for (int b = 0; b < B; b++) {
+        kb.d[b] = in[b].d;
+        kb.out[b] = in[b].out;
+        kb.add[b] = in[b].add;
+        kb.add2[b] = in[b].add2;
+        kb.key[b] = in[b].key;
+    }
 
+    Scratch sc(c);
     // 1. Y = INTT(sigma(d)) * (Q'/q_i)^-1
-    u64* Y = c.alloc((size_t)nl * N);
+    u64* Y = sc.take((size_t)B * g.y_stride());
     {
         JobList j;
         j.n = nl;
         j.custom = 1;
         j.galois = gal;
+        j.nb = B;
+        for (int b = 0; b < B; b++) {
+            j.boff[b] = (long long)(b * g.y_stride());
+            j.sboff[b] = (long long)(in[b].d - in[0].d);
+        }
         for (int i = 0; i < nl; i++) {
             const int dj = i / c.alpha, lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
             const u64 qi = c.pr[i].q;
@@ -520,14 +422,14 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             const u64 sc = mulm(c.pr[i].ninv, powm(qh, qi - 2, qi), qi);
             j.prime[i] = i;
             j.ptr[i] = Y + (size_t)i * N;
-            j.src[i] = d + (size_t)i * N;
+            j.src[i] = in[0].d + (size_t)i * N;
             j.scale[i] = sc;
             j.scale_s[i] = shoup_of(sc, qi);
         }
         ntt_inverse(c, j);
     }
     // 2. A: conversion + column pass for every (digit, non-digit target)
-    u64* I = c.alloc((size_t)g.beta * nt * N);
+    u64* I = sc.take((size_t)B * g.i_stride());
     {
         KsJobs jobs;
         jobs.n = 0;
@@ -542,8 +444,8 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         }
         static bool at = false;
         // algorithmic: the digit limbs Y read once, one intermediate limb written per job
-        Launch scope(c, "ks_modup_cols", 8.0 * N * (nl + (double)jobs.n));
-        dim3 grid((N >> CL) / CS, jobs.n);
+        Launch scope(c, "ks_modup_cols", 8.0 * N * B * (nl + (double)jobs.n));
+        dim3 grid((N >> CL) / CS, jobs.n, B);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);
             kern<<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
@@ -556,14 +458,14 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
         }
         HC_CUDA(cudaGetLastError());
     }
-    c.free(Y);
-    // 3. B: chunk pass + key inner product -> ACC [2][nt][N]
-    u64* ACC = c.alloc((size_t)2 * nt * N);
-    if (c.ks_split) {
-        // split form: finish the NTTs of all (digit, target) limbs in one
-        // launch, then stream the key product
+    // 3. B: chunk pass of every (digit, target) limb, then the streaming key
+    //    product -> ACC [2][nt][N] per key switch
+    u64* ACC = sc.take((size_t)B * g.acc_stride());
+    {
         JobList j;
         j.n = 0;
+        j.nb = B;
+        for (int b = 0; b < B; b++) j.boff[b] = (long long)(b * g.i_stride());
         for (int dj = 0; dj < g.beta; dj++) {
             const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
             for (int t = 0; t < nt; t++) {
@@ -575,38 +477,23 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
             }
         }
         ntt_forward_chunks(c, j);
-        // ks_split == 2: P limbs take the fused key-product + INTT-chunk kernel
-        // (measured slower: a 96-CTA grid; kept as an option)
-        const int tq = c.ks_split == 2 ? nl : nt;
-        {
-            const size_t work = (size_t)tq * (N / 2);
-            Launch scope(c, "ks_keyprod_stream", 8.0 * N * ((double)g.beta * tq + 2.0 * g.beta * tq + 2.0 * tq));
-            int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
-            ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, d, gal, key.d, ACC, tq);
-            HC_CUDA(cudaGetLastError());
-        }
-        if (c.ks_split == 2) {
-            Launch scope(c, "ks_keyprod_p_intt", 8.0 * N * ((double)g.beta * K + 2.0 * g.beta * K + 2.0 * K));
-            dim3 grid((N >> CH_LOG) / CH_SUBS, K);
-            ks_keyprod_p_intt<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, true), I, key.d, ACC);
-            HC_CUDA(cudaGetLastError());
-        }
-    } else {
-        static bool at = false;
-        set_smem(ks_chunks_keyprod, hsm, at);
-        const double inb = (double)g.beta * nt - nl + nl;      // I limbs + in-digit d limbs
-        Launch scope(c, "ks_chunks_keyprod", 8.0 * N * (inb + 2.0 * g.beta * nt + 2.0 * nt));
-        dim3 grid((N >> CH_LOG) / CH_SUBS, nt);
-        ks_chunks_keyprod<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), I, d, gal, key.d,
-                                                                ACC);
+        int nkeys = 1;
+        for (int b = 1; b < B; b++) nkeys += in[b].key != in[b - 1].key;
+        const size_t work = (size_t)nt * N;
+        // algorithmic: the digit limbs and ACC per key switch, each distinct key run once
+        Launch scope(c, "ks_keyprod_stream",
+                     8.0 * N * ((double)B * (g.beta * nt + 2.0 * nt) + 2.0 * nkeys * g.beta * nt));
+        int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 32);
+        ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, gal, kb, ACC, nt);
         HC_CUDA(cudaGetLastError());
     }
-    c.free(I);
     // 4. INTT of the P limbs, final scale N^-1 (P/p_t)^-1 (in place)
     {
         JobList j;
         j.n = 0;
         j.custom = 1;
+        j.nb = B;
+        for (int b = 0; b < B; b++) j.boff[b] = (long long)(b * g.acc_stride());
         for (int s = 0; s < 2; s++)
             for (int t = 0; t < K; t++) {
                 const int pi = c.L + 1 + t;
@@ -621,15 +508,14 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
                 j.scale_s[j.n] = shoup_of(sc, p);
                 j.n++;
             }
-        if (c.ks_split == 2) ntt_inverse_cols(c, j);     // chunk pass already done in ks_keyprod_p_intt
-        else ntt_inverse(c, j);
+        ntt_inverse(c, j);
     }
     // 5. D: P -> Q conversion + column pass
-    u64* Wt = c.alloc((size_t)2 * nl * N);
+    u64* Wt = sc.take((size_t)B * g.w_stride());
     {
         static bool at = false;
-        Launch scope(c, "ks_moddown_cols", 8.0 * N * (2.0 * K + 2.0 * nl));
-        dim3 grid((N >> CL) / CS, 2 * nl);
+        Launch scope(c, "ks_moddown_cols", 8.0 * N * B * (2.0 * K + 2.0 * nl));
+        dim3 grid((N >> CL) / CS, 2 * nl, B);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);
             kern<<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
@@ -646,26 +532,34 @@ static void keyswitch_fused_t(Ctx& c, const u64* d, u64 gal, int level, const Ke
     {
         static bool at = false;
         set_smem(ks_moddown_chunks, hsm, at);
-        Launch scope(c, "ks_moddown_chunks", 8.0 * N * (2.0 * nl * 3 + (double)add_npoly * nl));
-        dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl);
+        int nadd2 = 0;
+        for (int b = 0; b < B; b++) nadd2 += in[b].add2 != nullptr;
+        Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
+        dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl, B);
         ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
-                                                                addend, add_npoly, add_gal, addend2, out);
+                                                                add_npoly, add_gal, kb);
         HC_CUDA(cudaGetLastError());
     }
-    c.free(Wt);
-    c.free(ACC);
+}
+
+bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal) {
+    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 4 || c.alpha > 4 || c.logN < 14 || c.logN > 17) return false;
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        switch (c.logN) {
+            case 14: keyswitch_batch_t<14>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
+            case 15: keyswitch_batch_t<15>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
+            case 16: keyswitch_batch_t<16>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
+            default: keyswitch_batch_t<17>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
+        }
+    }
+    return true;
 }
 
 bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u64* out, const u64* addend,
                      int add_npoly, u64 add_gal, const u64* addend2) {
-    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 4 || c.alpha > 4) return false;
-    switch (c.logN) {
-        case 14: keyswitch_fused_t<14>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
-        case 15: keyswitch_fused_t<15>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
-        case 16: keyswitch_fused_t<16>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
-        case 17: keyswitch_fused_t<17>(c, d, gal, level, key, out, addend, add_npoly, add_gal, addend2); return true;
-        default: return false;
-    }
+    const KsIn in{d, out, addend, addend2, key.d};
+    return keyswitch_fused_batch(c, 1, &in, gal, level, add_npoly, add_gal);
 }
 
 template <int LOGN>
@@ -674,7 +568,8 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     const int N = c.N;
-    u64* X = c.alloc((size_t)npoly * N);
+    Scratch sc(c);
+    u64* X = sc.take((size_t)npoly * N);
     JobList j;
     j.n = npoly;
     for (int s = 0; s < npoly; s++) {
@@ -683,7 +578,7 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
         j.src[s] = a + ((size_t)s * (level + 1) + level) * N;
     }
     ntt_inverse(c, j);
-    u64* Yt = c.alloc((size_t)npoly * level * N);
+    u64* Yt = sc.take((size_t)npoly * level * N);
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     const int N1 = N >> CH_LOG;
@@ -705,8 +600,6 @@ static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out
                                                         out);
         HC_CUDA(cudaGetLastError());
     }
-    c.free(X);
-    c.free(Yt);
 }
 
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out) {

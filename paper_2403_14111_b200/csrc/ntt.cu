@@ -31,10 +31,10 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<L
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
     extern __shared__ u64 sm[];
-    const int job = blockIdx.y;
+    const int job = blockIdx.y, b = blockIdx.z;
     const int pidx = jobs.prime[job];
-    const u64* src = (use_src && jobs.src[job]) ? jobs.src[job] : jobs.ptr[job];
-    u64* dst = jobs.ptr[job];
+    u64* dst = jobs.ptr[job] + (b ? jobs.boff[b] : 0);
+    const u64* src = (use_src && jobs.src[job]) ? jobs.src[job] + (b ? jobs.sboff[b] : 0) : dst;
     const PrimeDev P = primes[pidx];
     const ulonglong2* TW = tw + ((size_t)pidx << logN);
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
@@ -66,7 +66,7 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const size_t smem = PG::smem_bytes();
     const int nsub = (MODE == MODE_COLS) ? (c.N >> LOGSZ) : (MODE == MODE_CHUNKS ? N1 : 1);
-    dim3 grid(nsub / SUBS, jobs.n);
+    dim3 grid(nsub / SUBS, jobs.n, jobs.nb);
     static const char* names[2][3] = {{"ntt_fwd_full", "ntt_fwd_cols", "ntt_fwd_chunks"},
                                       {"ntt_inv_full", "ntt_inv_cols", "ntt_inv_chunks"}};
     static bool attr[2] = {false, false};
@@ -77,7 +77,7 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[inv ? 1 : 0] = true;
     }
-    Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n);
+    Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n * jobs.nb);
     if (inv)
         ntt_kernel<LOGSZ, MODE, SUBS, true><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes, c.twp(0, true),
                                                                                   c.logN, N1, use_src, last);
@@ -104,7 +104,7 @@ static void full_pass(Ctx& c, const JobList& jobs, bool inv) {
 // the 13 limbs of a key switch's first INTT or its 6 special-prime limbs)
 // takes the 64-thread variant: 4x the CTAs for the same work, so latency and
 // instruction fetch are spread over every SM.
-static bool small_grid(const JobList& jobs, int ctas_per_job) { return ctas_per_job * jobs.n < 148 * 4; }
+static bool small_grid(const JobList& jobs, int ctas_per_job) { return ctas_per_job * jobs.n * jobs.nb < 148 * 4; }
 
 static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
     const int big_subs = 1 << (20 - c.logN);   // 64, 32, 16, 8 columns per CTA for 2^14 .. 2^17
@@ -134,12 +134,6 @@ static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_s
 void ntt_forward_chunks(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
     chunks_pass(c, jobs, false, 1 << (c.logN - 9), 0, 0);
-}
-
-// second half of a split inverse NTT (in place, final scaling)
-void ntt_inverse_cols(Ctx& c, const JobList& jobs) {
-    if (jobs.n == 0) return;
-    cols_pass(c, jobs, true, 1 << (c.logN - 9), 0, 1);
 }
 
 void ntt_forward(Ctx& c, const JobList& jobs) {

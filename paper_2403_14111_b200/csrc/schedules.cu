@@ -268,13 +268,223 @@ static int geo_rows(const Eval& ev) {
 // `streams` independent chains of `reps` rotations each (chain i rotates by
 // i + 1, so every chain uses its own key), issued through the same fork/join
 // machinery as the schedules.  Returns the number of key switches issued.
-int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps) {
+int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps, int batch) {
     for (int i = 0; i < streams; i++) get_key(ev.c, (int)galois_rot(ev.c, i + 1));
     par_for(ev.c, streams, streams, [&](int i) {
-        CtP a = x;
-        for (int r = 0; r < reps; r++) a = ev.lrot(a, i + 1);
+        if (batch <= 1) {
+            CtP a = x;
+            for (int r = 0; r < reps; r++) a = ev.lrot(a, i + 1);
+            return;
+        }
+        G a(batch);
+        for (int b = 0; b < batch; b++) a[b] = ev.add(x, x);   // distinct operands
+        for (int r = 0; r < reps; r++) a = ev.lrot_batch(a, i + 1);
     });
-    return (int64_t)streams * reps;
+    return (int64_t)streams * reps * std::max(1, batch);
+}
+
+// ---- lockstep (batched) forms ----------------------------------------------
+// When no auto-bootstrap can fire, the independent diagonal passes run in
+// lockstep: every op that the passes (and blocks) apply with the same Galois
+// element becomes one batched key-switch pipeline (the ladders of all c/2
+// passes, the products of all passes, the RU/RL rotations of all blocks).
+// Each ciphertext sees exactly the op sequence of the reference (residues
+// unchanged); only the issue order across independent branches differs.
+
+// A batched op over many independent operands: sub-batches of at most
+// C.batch run as concurrent branches, so one sub-batch's pipeline tails
+// overlap another's kernels.
+static G rot_many(Eval& ev, const G& xs, int64_t r, bool add_self = false) {
+    Ctx& C = ev.c;
+    const int SB = std::max(1, C.batch), nsub = ((int)xs.size() + SB - 1) / SB;
+    if (nsub <= 1) return ev.lrot_batch(xs, r, add_self);
+    G out(xs.size());
+    par_for(C, nsub, fork_width(C, nsub), [&](int i) {
+        const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);
+        G part = ev.lrot_batch(G(xs.begin() + lo, xs.begin() + hi), r, add_self);
+        std::copy(part.begin(), part.end(), out.begin() + lo);
+    });
+    return out;
+}
+
+static G mult_many(Eval& ev, const G& xs, const G& ys) {
+    Ctx& C = ev.c;
+    const int SB = std::max(1, C.batch), nsub = ((int)xs.size() + SB - 1) / SB;
+    if (nsub <= 1) return ev.mult_batch(xs, ys);
+    G out(xs.size());
+    par_for(C, nsub, fork_width(C, nsub), [&](int i) {
+        const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);
+        G part = ev.mult_batch(G(xs.begin() + lo, xs.begin() + hi), G(ys.begin() + lo, ys.begin() + hi));
+        std::copy(part.begin(), part.end(), out.begin() + lo);
+    });
+    return out;
+}
+
+static G concat(const std::vector<G>& parts) {
+    G o;
+    for (auto& p : parts) o.insert(o.end(), p.begin(), p.end());
+    return o;
+}
+
+static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, const G& B, int c, double scale,
+                                          const Geo& g) {
+    const int K = c / 2;
+    // packing prologue: B + i * RU(B, c/2), all block columns in one batch
+    const int kk0 = (c / 2) % g.s0;
+    G rolled = kk0 ? ev.lrot_batch(B, (int64_t)kk0 * g.s1) : B;
+    G packed(n);
+    for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], ev.mul_i(rolled[q]));
+    // RU(packed, k) per pass (one batch per k: its own Galois element)
+    std::vector<G> shifted(K);
+    for (int k = 0; k < K; k++) {
+        const int kk = k % g.s0;
+        shifted[k] = kk ? ev.lrot_batch(packed, (int64_t)kk * g.s1) : packed;
+    }
+    // all passes' products in one batch
+    G xs, ys;
+    for (int k = 0; k < K; k++)
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) {
+                xs.push_back(A[(size_t)p * n + q]);
+                ys.push_back(shifted[k][q]);
+            }
+    G prod = mult_many(ev, xs, ys);
+    // col_sums of every (pass, block row): pre-add, then the ladders in lockstep
+    G acc((size_t)K * m);
+    for (int k = 0; k < K; k++)
+        for (int p = 0; p < m; p++) {
+            const size_t base = ((size_t)k * m + p) * n;
+            CtP a = prod[base];
+            for (int q = 1; q < n; q++) a = ev.add(a, prod[base + q]);
+            acc[(size_t)k * m + p] = a;
+        }
+    for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, 1 << t, true);
+    const Pattern c0 = col0(g);
+    for (auto& a : acc) a = ev.mult_p(a, c0);
+    for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, -(1 << t), true);
+    std::vector<G> terms(K, G(m));
+    for (int k = 0; k < K; k++) {
+        const Pattern mask = diag_mask(g, k, c, true, scale);
+        for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(acc[(size_t)k * m + p], mask);
+    }
+    G out = terms[0];
+    for (int k = 1; k < K; k++)
+        for (int p = 0; p < m; p++) out[p] = ev.add(out[p], terms[k][p]);
+    G cj = ev.conj_batch(out);
+    for (int p = 0; p < m; p++) out[p] = ev.add(out[p], cj[p]);
+    return out;
+}
+
+// rot_left of every block of E by k (encoding.py:291-311); the rrot(s1) of
+// several calls can be gathered by the caller: returns (head, tail) pairs
+static void rot_left_split(Eval& ev, const G& E, int k, const Geo& g, G& head, G& tail) {
+    const Pattern keep = keep_head(g, g.s1 - k);
+    G a1 = ev.lrot_batch(E, k);
+    head.resize(E.size());
+    tail.resize(E.size());
+    for (size_t i = 0; i < E.size(); i++) {
+        head[i] = ev.mult_p(a1[i], keep);
+        tail[i] = ev.sub(a1[i], head[i]);
+    }
+}
+
+static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& B, int n, int c, double scale,
+                                          const Geo& g, const Reducer& red) {
+    const int K = c / 2;
+    const int s1 = g.s1;
+    const bool partial = grid_level(A) < grid_level(B);
+    // packing prologue: A + i * RL(A, c/2)
+    G packed(m);
+    {
+        const int k = (c / 2) % s1;
+        G one = A;
+        if (k) {
+            G head, tail;
+            rot_left_split(ev, A, k, g, head, tail);
+            G back = ev.lrot_batch(tail, -(int64_t)s1);
+            for (int p = 0; p < m; p++) one[p] = ev.add(head[p], back[p]);
+        }
+        for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], ev.mul_i(one[p]));
+    }
+    // left operands of every pass
+    std::vector<G> left(K);
+    if (partial) {
+        for (int k = 0; k < K; k++) left[k] = ev.lrot_batch(packed, k);
+    } else {
+        std::vector<G> heads(K), tails(K);
+        std::vector<int> moving;
+        for (int k = 0; k < K; k++) {
+            if (k % s1 == 0) { left[k] = packed; continue; }
+            rot_left_split(ev, packed, k % s1, g, heads[k], tails[k]);
+            moving.push_back(k);
+        }
+        std::vector<G> tparts;
+        for (int k : moving) tparts.push_back(tails[k]);
+        G back = rot_many(ev, concat(tparts), -(int64_t)s1);
+        size_t o = 0;
+        for (int k : moving) {
+            left[k].resize(m);
+            for (int p = 0; p < m; p++) left[k][p] = ev.add(heads[k][p], back[o++]);
+        }
+    }
+    // right operands: B, or PRU(B, k) on the partial branch (all lrot(s1) in one batch)
+    std::vector<G> right(K, B);
+    if (partial) {
+        std::vector<G> heads(K), tails(K);
+        std::vector<int> moving;
+        for (int k = 0; k < K; k++) {
+            const int kk = k % s1;
+            if (!kk) continue;
+            const Pattern keep = keep_head(g, s1 - kk);
+            heads[k].resize(B.size());
+            tails[k].resize(B.size());
+            for (size_t i = 0; i < B.size(); i++) {
+                heads[k][i] = ev.mult_p(B[i], keep);
+                tails[k][i] = ev.sub(B[i], heads[k][i]);
+            }
+            moving.push_back(k);
+        }
+        std::vector<G> tparts;
+        for (int k : moving) tparts.push_back(tails[k]);
+        G up = rot_many(ev, concat(tparts), (int64_t)s1);
+        size_t o = 0;
+        for (int k : moving)
+            for (size_t i = 0; i < B.size(); i++) right[k][i] = ev.add(heads[k][i], up[o++]);
+    }
+    // all passes' products in one batch
+    G xs, ys;
+    for (int k = 0; k < K; k++)
+        for (int p = 0; p < m; p++)
+            for (int q = 0; q < n; q++) {
+                xs.push_back(left[k][p]);
+                ys.push_back(right[k][(size_t)p * n + q]);
+            }
+    G prod = mult_many(ev, xs, ys);
+    // row_sums: block-row pre-adds (cross-rank reduction point, in pass order),
+    // then the ladders of every (pass, block column) in lockstep
+    G acc((size_t)K * n);
+    for (int k = 0; k < K; k++) {
+        G pre(n);
+        for (int q = 0; q < n; q++) {
+            CtP a = prod[((size_t)k * m) * n + q];
+            for (int p = 1; p < m; p++) a = ev.add(a, prod[((size_t)k * m + p) * n + q]);
+            pre[q] = a;
+        }
+        if (red) red(pre);
+        for (int q = 0; q < n; q++) acc[(size_t)k * n + q] = pre[q];
+    }
+    for (int t = 0; t < ilog2(g.s0); t++) acc = rot_many(ev, acc, (int64_t)(1 << t) * s1, true);
+    std::vector<G> terms(K, G(n));
+    for (int k = 0; k < K; k++) {
+        const Pattern mask = diag_mask(g, -k, c, true, scale);
+        for (int q = 0; q < n; q++) terms[k][q] = ev.mult_p(acc[(size_t)k * n + q], mask);
+    }
+    G out = terms[0];
+    for (int k = 1; k < K; k++)
+        for (int q = 0; q < n; q++) out[q] = ev.add(out[q], terms[k][q]);
+    G cj = ev.conj_batch(out);
+    for (int q = 0; q < n; q++) out[q] = ev.add(out[q], cj[q]);
+    return out;
 }
 
 // ---- DiagABT (matmul.py:74-110) --------------------------------------------
@@ -294,10 +504,11 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
         return sums;
     }
     Ctx& C = ev.c;
-    // Branches may run concurrently only when no auto-bootstrap can fire
-    // inside (DiagABT consumes 3 levels), so the refresh-nonce order is the
-    // reference's sequential one.
+    // Branches may run concurrently (or in lockstep) only when no
+    // auto-bootstrap can fire inside (DiagABT consumes 3 levels), so the
+    // refresh-nonce order is the reference's sequential one.
     const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
+    if (par && C.lockstep) return diag_abt_lockstep(ev, A, m, n, B, c, scale, g);
     auto W = [&](int w) { return par ? w : 1; };
     // packing prologue, one branch per block column: B + i * RU(B, c/2)
     G packed(n);
@@ -359,6 +570,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     // cross-rank reducer is fine: the host still reaches the k-th pre-sum's
     // collective in k order on every rank, and only that branch waits for it.
     const bool ser = ev.auto_boot && std::min(grid_level(A), grid_level(B)) < 5;
+    if (!ser && C.lockstep) return diag_atb_lockstep(ev, A, m, B, n, c, scale, g, red);
     const int width = ser ? 1 : fork_width(C, c / 2);
     // packing prologue per block row: A + i * RL(A, c/2)
     G packed(m);

@@ -32,7 +32,7 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
 // A: m x 1 horizontally tiled column, B: m x n grid (row-major)
 std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, const std::vector<CtP>& B, int n, int c,
                                 double scale, const Reducer& red);
-int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps);
+int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps, int batch = 1);
 // Table-4 baselines (matmul.py:160-237)
 std::vector<CtP> sched_col_major_abt(Eval& ev, const std::vector<CtP>& A, int m, int n, const std::vector<CtP>& B,
                                      int c, double scale);

@@ -71,6 +71,20 @@ def throughput(params="cfg1", level=12, reps=8):
     return out
 
 
+def batch_throughput(params="cfg1", level=12, reps=4):
+    """Key switches per second: `s` concurrent chains, each rotating a batch of `b` operands per step."""
+    ctx = P.CKKSContext(params, None, seed=3)
+    x = ctx.encrypt(np.random.default_rng(0).uniform(-1, 1, ctx.slot_count), level)
+    L = N.lib()
+    out = {}
+    for s in (1, 2, 4):
+        for b in (1, 2, 4, 8, 16):
+            ms = C.c_float()
+            N.check(L.hc_bench_keyswitch_batch(ctx._h, x._h, s, b, reps, C.byref(ms)))
+            out[f"s{s}_b{b}"] = round(s * b * reps / (ms.value * 1e-3))
+    return out
+
+
 def ntt_throughput(params="cfg1"):
     """Batched NTT: limb-transforms/s and GB/s (algorithmic 16N bytes per limb) vs limb count."""
     ctx = P.CKKSContext(params, None, seed=3)
@@ -88,7 +102,9 @@ def ntt_throughput(params="cfg1"):
 
 
 if __name__ == "__main__":
-    if "--ntt" in sys.argv:
+    if "--batch" in sys.argv:
+        print(json.dumps({"keyswitch_per_s_streams_batch": batch_throughput(), "level": 12}))
+    elif "--ntt" in sys.argv:
         print(json.dumps({"ntt": ntt_throughput()}))
     elif "--throughput" in sys.argv:
         lv = 12

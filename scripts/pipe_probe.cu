@@ -17,7 +17,7 @@ constexpr int ACC = 8;
             _Pragma("unroll") for (int j = 0; j < ACC; j++) { BODY; }         \
         }                                                                     \
         TYPE s = 0;                                                           \
-        _Pragma("unroll") for (int j = 0; j < ACC; j++) s ^= a[j];            \
+        _Pragma("unroll") for (int j = 0; j < ACC; j++) s += a[j];            \
         out[blockIdx.x * blockDim.x + threadIdx.x] = s;                       \
     }
 
@@ -53,6 +53,31 @@ __device__ __forceinline__ uint64_t shoup3(uint64_t x, uint64_t w, uint64_t ws, 
 KERNEL(k_shoup, uint64_t, a[j] = shoup(a[j], (uint64_t)m0 << 28 | m1, (uint64_t)m1 << 40 | m0, ((uint64_t)m0 << 40) + 1))
 KERNEL(k_shoup3, uint64_t, a[j] = shoup3(a[j], (uint64_t)m0 << 28 | m1, (uint64_t)m1 << 40 | m0, ((uint64_t)m0 << 40) + 1))
 
+// FP64 pipe: dependent-free DFMA chains
+KERNEL(k_dfma, double, asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(a[j]) : "d"((double)m0), "d"((double)m1)))
+// FP64 modular product of integers held in doubles (q < 2^50): h + l = x*w exactly,
+// quotient by rint(h * qinv), remainder in (-2q, 2q)
+__device__ __forceinline__ double fmodmul(double x, double w, double q, double qinv) {
+    const double h = x * w;
+    const double l = fma(x, w, -h);
+    const double qt = rint(h * qinv);
+    return fma(-qt, q, h) + l;
+}
+// same with the rounding by the 1.5 * 2^52 magic constant (no FRND)
+__device__ __forceinline__ double fmodmul2(double x, double w, double q, double qinv) {
+    const double h = x * w;
+    const double l = fma(x, w, -h);
+    const double qt = fma(h, qinv, 6755399441055744.0) - 6755399441055744.0;
+    return fma(-qt, q, h) + l;
+}
+KERNEL(k_fmodmul2, double, a[j] = fmodmul2(a[j], (double)m0 * 1e6, 4398046511093.0, 1.0 / 4398046511093.0))
+KERNEL(k_fbfly2, double, { double t = fmodmul2(a[(j + 1) % ACC], (double)m1 * 1e6, 4398046511093.0, 1.0 / 4398046511093.0); double x = a[j]; a[j] = x + t; a[(j + 1) % ACC] = x - t; })
+KERNEL(k_fmodmul, double, a[j] = fmodmul(a[j], (double)m0 * 1e6, 4398046511093.0, 1.0 / 4398046511093.0))
+// FP64 CT butterfly pair (X + T, X - T) on signed lazy values
+KERNEL(k_fbfly, double, { double t = fmodmul(a[(j + 1) % ACC], (double)m1 * 1e6, 4398046511093.0, 1.0 / 4398046511093.0); double x = a[j]; a[j] = x + t; a[(j + 1) % ACC] = x - t; })
+// integer Harvey CT butterfly pair for comparison
+KERNEL(k_ibfly, uint64_t, { uint64_t q = ((uint64_t)m0 << 40) + 1; uint64_t X = a[j]; X = X >= 2 * q ? X - 2 * q : X; uint64_t T = shoup(a[(j + 1) % ACC], (uint64_t)m0 << 28 | m1, (uint64_t)m1 << 40 | m0, q); a[j] = X + T; a[(j + 1) % ACC] = X + 2 * q - T; })
+
 int main() {
     int blocks = 148 * 8, threads = 256;
     uint64_t* out;
@@ -71,6 +96,12 @@ int main() {
         {"IMAD+IADD3", [](uint64_t* o) { k_mix2<<<148 * 8, 256>>>((uint32_t*)o, 3, 5); }},
         {"shoup (exact hi)", [](uint64_t* o) { k_shoup<<<148 * 8, 256>>>(o, 3, 5); }},
         {"shoup3 (approx hi)", [](uint64_t* o) { k_shoup3<<<148 * 8, 256>>>(o, 3, 5); }},
+        {"DFMA", [](uint64_t* o) { k_dfma<<<148 * 8, 256>>>((double*)o, 3, 5); }},
+        {"fp64 modmul", [](uint64_t* o) { k_fmodmul<<<148 * 8, 256>>>((double*)o, 3, 5); }},
+        {"fp64 butterfly", [](uint64_t* o) { k_fbfly<<<148 * 8, 256>>>((double*)o, 3, 5); }},
+        {"fp64 modmul (magic rint)", [](uint64_t* o) { k_fmodmul2<<<148 * 8, 256>>>((double*)o, 3, 5); }},
+        {"fp64 butterfly (magic rint)", [](uint64_t* o) { k_fbfly2<<<148 * 8, 256>>>((double*)o, 3, 5); }},
+        {"int butterfly", [](uint64_t* o) { k_ibfly<<<148 * 8, 256>>>(o, 3, 5); }},
         {"mul.lo.u64", [](uint64_t* o) { k_mul64<<<148 * 8, 256>>>(o, 3, 5); }},
         {"mul.hi.u64", [](uint64_t* o) { k_mulhi64<<<148 * 8, 256>>>(o, 3, 5); }},
     };

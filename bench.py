@@ -340,6 +340,10 @@ def run_b200(args, world, rank, local):
     top = max(prof.items(), key=lambda kv: kv[1][1])
     name, (n_launch, k_ms, k_bytes) = top
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # --set full capture (a batched rotation at the top level), next to that
+    # launch's algorithmic bytes: traffic close to the algorithmic figure means
+    # no wasted re-reads (the capture's configuration is named in the file)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):

@@ -1,12 +1,13 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv): per-kernel
 launch count, total and mean device time, and share of the captured window."""
 import csv
+import gzip
 import re
 import sys
 from collections import defaultdict
 
 rows = []
-with open(sys.argv[1]) as f:
+with (gzip.open(sys.argv[1], "rt") if sys.argv[1].endswith(".gz") else open(sys.argv[1])) as f:
     lines = [ln for ln in f if ln.startswith('"')]
 for r in csv.DictReader(lines):
     if r.get("Metric Name") != "gpu__time_duration.sum":

@@ -59,6 +59,10 @@ int hc_set_grid_rows(hc_ctx *ctx, int grid_rows);
 int hc_set_streams(hc_ctx *ctx, int n);
 /* EmulatorContext.auto_bootstrap (emulator.py:132) */
 int hc_set_auto_bootstrap(hc_ctx *ctx, int on);
+/* fused schedule forms on (default) / off: hoisted rotations and one
+ * relinearisation per product sum; residues follow the
+ * oracle's matching mode, the ledger is the reference's either way */
+int hc_set_hoist(hc_ctx *ctx, int on);
 /* OpLedger.counts / reset (emulator.py:88-108); counts[HC_NCOUNTS] */
 int hc_ctx_counts(hc_ctx *ctx, int64_t *counts, int reset);
 /* encryption-randomness counter (shared with the oracle's nonce sequence) */
@@ -103,6 +107,13 @@ int hc_op_mult_scalar(hc_ctx *ctx, const hc_ct *a, double re, double im, hc_ct *
 int hc_op_mult_plain(hc_ctx *ctx, const hc_ct *a, const double *re, const double *im, const char *key, hc_ct **out);
 /* lrot (emulator.py:237-247); r mod slots must be non-zero (r == 0 is the caller's no-op) */
 int hc_op_lrot(hc_ctx *ctx, const hc_ct *a, int64_t r, hc_ct **out);
+/* lrot(a, rs[k]) for k < n with one shared ModUp (hoisted; Rot per non-zero
+ * r, r == 0 yields a handle to a itself); outs[n] */
+int hc_op_lrot_hoisted(hc_ctx *ctx, const hc_ct *a, const int64_t *rs, int n, hc_ct **outs);
+/* add(...add(mult(a0, b0), mult(a1, b1))...) over n pairs with one
+ * relinearisation + rescale (n Mult, n-1 Add); the separate ops unless all
+ * operands share one level >= 1 and n >= 2 */
+int hc_op_mult_sum(hc_ctx *ctx, const hc_ct *const *a, const hc_ct *const *b, int n, hc_ct **out);
 /* conj (emulator.py:253-257), mul_i (emulator.py:259-265, unledgered) */
 int hc_op_conj(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
 int hc_op_mul_i(hc_ctx *ctx, const hc_ct *a, hc_ct **out);

@@ -708,17 +708,17 @@ void orc_level_adjust(const orc_ctx *c, const u64 *a, int from, int to, u64 *out
 /* key switching                                                       */
 /* ------------------------------------------------------------------ */
 
-/* d: [level+1][N] NTT; out: [2][level+1][N] with (k0, k1) */
-static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *out) {
-    int N = c->N, L = c->L, K = c->K, nall = c->nall, nl = level + 1;
-    int nt = nl + K;                       /* target basis: Q_l then P */
+/* ModUp of d ([level+1][N], NTT form): up [beta][nt][N] in NTT form over
+ * the target basis (Q_l then P); for target limbs inside digit j the value is
+ * d itself.  Fast base conversion of the digit's INTT, scaled by
+ * [(Q'/q_i)^-1]_{q_i}, then the forward NTT on every non-digit target. */
+static void ks_modup(orc_ctx *c, const u64 *d, int level, u64 *up) {
+    int N = c->N, L = c->L, K = c->K, nl = level + 1;
+    int nt = nl + K;
     int *tl = malloc(sizeof(int) * nt);
     for (int i = 0; i < nl; i++) tl[i] = i;
     for (int t = 0; t < K; t++) tl[nl + t] = L + 1 + t;
     int beta = (nl + c->alpha - 1) / c->alpha;
-    size_t poly = (size_t)nt * N;
-    u64 *acc = calloc(2 * poly, sizeof(u64));
-    u64 *up = malloc(sizeof(u64) * poly);
     u64 *x = malloc(sizeof(u64) * (size_t)c->alpha * N);
     for (int j = 0; j < beta; j++) {
         int lo = j * c->alpha, hi = lo + c->alpha;
@@ -735,11 +735,12 @@ static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *ou
             u64 inv = invmod(qh, p->q);
             for (int k = 0; k < N; k++) x[(size_t)a * N + k] = mulmod(x[(size_t)a * N + k], inv, p);
         }
+        u64 *upj = up + (size_t)j * nt * N;
 #pragma omp parallel for schedule(dynamic)
         for (int t = 0; t < nt; t++) {
             int li = tl[t];
             const prime_t *p = &c->pr[li];
-            u64 *o = up + (size_t)t * N;
+            u64 *o = upj + (size_t)t * N;
             if (li >= lo && li < hi) { memcpy(o, d + (size_t)li * N, sizeof(u64) * N); continue; }
             u64 cf[MAXP];
             for (int a = 0; a < na; a++) {
@@ -754,6 +755,23 @@ static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *ou
             }
             ntt(c, p, o);
         }
+    }
+    free(x); free(tl);
+}
+
+/* Key inner product of the ModUp digits `up` with `key`, then ModDown by P:
+ * out [2][level+1][N] = (k0, k1). */
+static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *key, u64 *out) {
+    int N = c->N, L = c->L, K = c->K, nall = c->nall, nl = level + 1;
+    int nt = nl + K;
+    int *tl = malloc(sizeof(int) * nt);
+    for (int i = 0; i < nl; i++) tl[i] = i;
+    for (int t = 0; t < K; t++) tl[nl + t] = L + 1 + t;
+    int beta = (nl + c->alpha - 1) / c->alpha;
+    size_t poly = (size_t)nt * N;
+    u64 *acc = calloc(2 * poly, sizeof(u64));
+    for (int j = 0; j < beta; j++) {
+        const u64 *upj = up + (size_t)j * poly;
         /* inner product with digit j of the key */
         const u64 *kb = key->data + (size_t)(2 * j) * nall * N, *ka = kb + (size_t)nall * N;
 #pragma omp parallel for
@@ -762,8 +780,8 @@ static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *ou
             const prime_t *p = &c->pr[li];
             for (int k = 0; k < N; k++) {
                 size_t o = (size_t)t * N + k, ko = (size_t)li * N + k;
-                acc[o] = addmod(acc[o], mulmod(up[o], kb[ko], p), p->q);
-                acc[poly + o] = addmod(acc[poly + o], mulmod(up[o], ka[ko], p), p->q);
+                acc[o] = addmod(acc[o], mulmod(upj[o], kb[ko], p), p->q);
+                acc[poly + o] = addmod(acc[poly + o], mulmod(upj[o], ka[ko], p), p->q);
             }
         }
     }
@@ -804,7 +822,20 @@ static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *ou
         }
         free(y);
     }
-    free(acc); free(up); free(x); free(tl);
+    free(acc); free(tl);
+}
+
+static size_t modup_words(const orc_ctx *c, int level) {
+    int nl = level + 1, beta = (nl + c->alpha - 1) / c->alpha;
+    return (size_t)beta * (nl + c->K) * c->N;
+}
+
+/* d: [level+1][N] NTT; out: [2][level+1][N] with (k0, k1) */
+static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *out) {
+    u64 *up = malloc(sizeof(u64) * modup_words(c, level));
+    ks_modup(c, d, level, up);
+    ks_keyprod_moddown(c, up, level, key, out);
+    free(up);
 }
 
 static void automorph_ntt(const orc_ctx *c, const u64 *in, u64 g, int nl, u64 *out) {
@@ -859,6 +890,74 @@ void orc_mult(orc_ctx *c, const u64 *a, const u64 *b, int level, u64 *out) {
             d[o] = mulmod(a0, b0, p);
             d[poly + o] = reduce128((u128)a0 * b1 + (u128)a1 * b0, p);
             d[2 * poly + o] = mulmod(a1, b1, p);
+        }
+    }
+    swkey_t *key = get_key(c, 0);
+    u64 *ks = malloc(sizeof(u64) * 2 * poly);
+    keyswitch(c, d + 2 * poly, level, key, ks);
+    for (size_t o = 0; o < poly; o++) {
+        u64 q = c->pr[o / N].q;
+        d[o] = addmod(d[o], ks[o], q);
+        d[poly + o] = addmod(d[poly + o], ks[poly + o], q);
+    }
+    orc_rescale(c, d, level, 2, out);
+    free(d); free(ks);
+}
+
+/* Hoisted rotations: one ModUp of c1 shared by every
+ * Galois element g_r.  The automorphism is a permutation of NTT indices on
+ * every limb, so sigma_g applied to the extended-basis digits is a valid
+ * ModUp of sigma_g(c1) (the base-conversion overflow u*D_j becomes
+ * sigma_g(u)*D_j); the result is a different, equally valid key switch, so
+ * residues differ from orc_automorph.  out_r = (sigma(c0) + KS0, KS1). */
+void orc_rotate_hoisted(orc_ctx *c, const u64 *a, int level, const u64 *gs, int ng, u64 *outs) {
+    int N = c->N, nl = level + 1, nt = nl + c->K;
+    int beta = (nl + c->alpha - 1) / c->alpha;
+    size_t poly = (size_t)nl * N, mw = modup_words(c, level);
+    u64 *up = malloc(sizeof(u64) * mw);
+    ks_modup(c, a + poly, level, up);
+    u64 *ups = malloc(sizeof(u64) * mw);
+    u64 *c0 = malloc(sizeof(u64) * poly);
+    u64 *ks = malloc(sizeof(u64) * 2 * poly);
+    for (int r = 0; r < ng; r++) {
+        swkey_t *key = get_key(c, (int)gs[r]);
+        for (int j = 0; j < beta; j++)
+            automorph_ntt(c, up + (size_t)j * nt * N, gs[r], nt, ups + (size_t)j * nt * N);
+        ks_keyprod_moddown(c, ups, level, key, ks);
+        automorph_ntt(c, a, gs[r], nl, c0);
+        u64 *o = outs + (size_t)r * 2 * poly;
+        for (int i = 0; i < nl; i++) {
+            u64 q = c->pr[i].q;
+            for (int k = 0; k < N; k++) {
+                size_t e = (size_t)i * N + k;
+                o[e] = addmod(c0[e], ks[e], q);
+                o[poly + e] = ks[poly + e];
+            }
+        }
+    }
+    free(up); free(ups); free(c0); free(ks);
+}
+
+/* Sum of n ct x ct products with one relinearisation and one rescale:
+ * d = sum_q tensor(a_q, b_q) (component-wise mod q), then d0 + KS(d2)_0,
+ * d1 + KS(d2)_1, rescale.  as / bs: n ciphertexts [2][level+1][N] each,
+ * contiguous. */
+void orc_mult_sum(orc_ctx *c, const u64 *as, const u64 *bs, int n, int level, u64 *out) {
+    int N = c->N, nl = level + 1;
+    size_t poly = (size_t)nl * N;
+    u64 *d = calloc(3 * poly, sizeof(u64));
+    for (int q = 0; q < n; q++) {
+        const u64 *a = as + (size_t)q * 2 * poly, *b = bs + (size_t)q * 2 * poly;
+#pragma omp parallel for
+        for (int i = 0; i < nl; i++) {
+            const prime_t *p = &c->pr[i];
+            for (int k = 0; k < N; k++) {
+                size_t o = (size_t)i * N + k;
+                u64 a0 = a[o], a1 = a[poly + o], b0 = b[o], b1 = b[poly + o];
+                d[o] = addmod(d[o], mulmod(a0, b0, p), p->q);
+                d[poly + o] = addmod(d[poly + o], reduce128((u128)a0 * b1 + (u128)a1 * b0, p), p->q);
+                d[2 * poly + o] = addmod(d[2 * poly + o], mulmod(a1, b1, p), p->q);
+            }
         }
     }
     swkey_t *key = get_key(c, 0);

@@ -81,6 +81,8 @@ def lib():
         L.orc_galois_rot.restype = U
         L.orc_galois_rot.argtypes = [P, C.c_int64]
         L.orc_mult.argtypes = [P, u64p, u64p, I, u64p]
+        L.orc_rotate_hoisted.argtypes = [P, u64p, I, u64p, I, u64p]
+        L.orc_mult_sum.argtypes = [P, u64p, u64p, I, I, u64p]
         L.orc_key.argtypes = [P, I, u64p]
         L.orc_ntt_limb.argtypes = [P, I, u64p, I]
         L.orc_mulmod.restype = U
@@ -194,6 +196,17 @@ class RnsParams:
         lib().orc_mult(self.h, a, b, level, o)
         return o
 
+    def rotate_hoisted(self, a, level, gs):
+        o = np.zeros((len(gs),) + self.ct_shape(level), np.uint64)
+        lib().orc_rotate_hoisted(self.h, a, level, np.asarray(gs, np.uint64), len(gs), o)
+        return list(o)
+
+    def mult_sum(self, As, Bs, level):
+        o = self._out(level - 1)
+        lib().orc_mult_sum(self.h, np.ascontiguousarray(np.stack(As)), np.ascontiguousarray(np.stack(Bs)),
+                           len(As), level, o)
+        return o
+
     def rescale(self, a, level):
         o = self._out(level - 1)
         lib().orc_rescale(self.h, np.ascontiguousarray(a), level, a.shape[0], o)
@@ -257,8 +270,12 @@ class RnsBlock:
 class OracleCKKSContext:
     """EmulatorContext duck type (emulator.py:111-281) over RNS-CKKS residues."""
 
-    def __init__(self, params="cfg0", grid_rows=None, *, auto_bootstrap=False, seed=2024):
+    def __init__(self, params="cfg0", grid_rows=None, *, auto_bootstrap=False, seed=2024, hoist=True):
         self.p = params if isinstance(params, RnsParams) else RnsParams(params, seed=seed)
+        # fused schedule forms (hoisted rotations, one relinearisation per
+        # product sum) where the restated DiagABT / DiagATB use them; the
+        # CUDA product's `hoist` flag must match for residue parity
+        self.hoist = hoist
         self.slot_count = self.p.slots
         self.grid_rows = grid_rows or (1 << (int(np.log2(self.slot_count)) // 2))
         self.grid_cols = self.slot_count // self.grid_rows
@@ -392,6 +409,40 @@ class OracleCKKSContext:
 
     def rrot(self, x, r):
         return self.lrot(x, -int(r))
+
+    def lrot_hoisted(self, x, rs):
+        """lrot(x, r) for every r in rs with one shared ModUp (DESIGN.md §3,
+        hoisted rotations): same ledger as the separate calls, r = 0 returns x."""
+        kx, vx = self._kind(x)
+        rr = [int(r) % self.slot_count for r in rs]
+        if kx != "ct":
+            return [self.lrot(x, r) for r in rr]
+        moving = [r for r in rr if r]
+        outs = {}
+        if moving:
+            self.ledger.record("Rot", len(moving))
+            self.extra["KeySwitch"] += len(moving)
+            data = self.p.rotate_hoisted(vx.data, vx.level, [self.p.galois(r) for r in moving])
+            outs = {r: RnsBlock(self, d, vx.level) for r, d in zip(moving, data)}
+        return [outs[r] if r else x for r in rr]
+
+    def mult_sum(self, xs, ys):
+        """add(...add(mult(x0, y0), mult(x1, y1))...) with one relinearisation
+        and one rescale for the whole sum: the ledger records
+        the n Mult and n - 1 Add of the separate ops.  Operands must be
+        ciphertexts at one level >= 1; anything else takes the separate ops."""
+        blocks = list(xs) + list(ys)
+        if (len(xs) < 2 or not all(isinstance(b, RnsBlock) for b in blocks)
+                or len({b.level for b in blocks}) != 1 or blocks[0].level < 1):
+            acc = self.mult(xs[0], ys[0])
+            for x, y in zip(xs[1:], ys[1:]):
+                acc = self.add(acc, self.mult(x, y))
+            return acc
+        lv = blocks[0].level
+        self.ledger.record("Mult", len(xs))
+        self.ledger.record("Add", len(xs) - 1)
+        self.extra["KeySwitch"] += 1
+        return RnsBlock(self, self.p.mult_sum([x.data for x in xs], [y.data for y in ys], lv), lv - 1)
 
     def conj(self, x):
         kx, vx = self._kind(x)

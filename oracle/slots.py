@@ -409,7 +409,9 @@ def rot_up(E, k):                                                   # encoding.p
     return E if k == 0 else E.lrot(k * E.ctx.grid_cols)
 
 
-def rot_left(E, k):                                                 # encoding.py:291-311
+def rot_left(E, k, first=None):                                     # encoding.py:291-311
+    """``first(b)`` (default ``lrot(b, k)``) supplies the leading rotation,
+    so a caller can hoist it across several k (fused form, ``diag_atb``)."""
     ctx, s1 = E.ctx, E.ctx.grid_cols
     k = int(k) % s1
     if k == 0:
@@ -417,7 +419,7 @@ def rot_left(E, k):                                                 # encoding.p
     keep = ctx.pack(keep_head_pattern(ctx.grid_rows, s1, s1 - k).ravel())
 
     def fix(b):
-        a1 = ctx.lrot(b, k)
+        a1 = ctx.lrot(b, k) if first is None else first(b)
         head = ctx.cmult(a1, keep)
         tail = ctx.sub(a1, head)
         return ctx.add(head, ctx.rrot(tail, s1))
@@ -438,24 +440,30 @@ def prot_up(E, k):                                                  # encoding.p
     return E.each(fix)
 
 
-def col_sums(E):                                                    # encoding.py:335-360
-    ctx, s1 = E.ctx, E.ctx.grid_cols
-    gr, gc = E.grid
+def col_ladder(ctx, acc):
+    """encoding.py:354-359 — lrot ladder, column-0 mask, rrot ladder."""
+    s1 = ctx.grid_cols
     c0 = np.zeros((ctx.grid_rows, s1))
     c0[:, 0] = 1.0
     c0b = ctx.pack(c0.ravel())
+    for t in range(lg(s1)):
+        acc = ctx.add(acc, ctx.lrot(acc, 1 << t))
+    acc = ctx.cmult(acc, c0b)
+    for t in range(lg(s1)):
+        acc = ctx.add(acc, ctx.rrot(acc, 1 << t))
+    return acc
+
+
+def col_sums(E):                                                    # encoding.py:335-360
+    ctx = E.ctx
+    gr, gc = E.grid
     rows = []
     for p in range(gr):
         acc = E.blocks[p][0]
         for q in range(1, gc):
             acc = ctx.add(acc, E.blocks[p][q])
-        for t in range(lg(s1)):
-            acc = ctx.add(acc, ctx.lrot(acc, 1 << t))
-        acc = ctx.cmult(acc, c0b)
-        for t in range(lg(s1)):
-            acc = ctx.add(acc, ctx.rrot(acc, 1 << t))
-        rows.append((acc,))
-    return Grid(ctx, rows, (E.shape[0], s1))
+        rows.append((col_ladder(ctx, acc),))
+    return Grid(ctx, rows, (E.shape[0], ctx.grid_cols))
 
 
 def row_presum(E, q):
@@ -497,6 +505,15 @@ def _colwise(C, B):
                       for p in range(B.grid[0])], B.shape)
 
 
+def fused(ctx, depth, *grids):
+    """Whether the fused schedule forms apply: the context
+    offers them (the RNS oracle or the CUDA product with ``hoist`` on) and no
+    auto-bootstrap can fire inside the product, which consumes ``depth - 1``
+    levels — the CUDA product's lockstep condition (csrc/schedules.cu)."""
+    return (getattr(ctx, "hoist", False) and hasattr(ctx, "lrot_hoisted")
+            and (not ctx.auto_bootstrap or min(g.level for g in grids) >= depth))
+
+
 def diag_abt(A, B, scale=1.0):                                      # matmul.py:74-110
     if A.tiling != "none" or B.tiling != "vertical" or A.shape[1] != B.shape[1]:
         raise ShapeMismatch("diag_abt layout")
@@ -508,6 +525,19 @@ def diag_abt(A, B, scale=1.0):                                      # matmul.py:
     rolled = rot_up(B, c // 2)
     packed = B.add(rolled.each(ctx.mul_i))
     acc = None
+    if fused(ctx, 4, A, B) and packed.grid[0] == 1:
+        # fused form: the c/2 rotations RU(packed, k) of a block column share
+        # one ModUp, and each block row's product sum (the col_sums pre-add of
+        # the rowwise products) is relinearised and rescaled once
+        s0, s1, n = ctx.grid_rows, ctx.grid_cols, packed.grid[1]
+        rots = [ctx.lrot_hoisted(packed.blocks[0][q], [(k % s0) * s1 for k in range(c // 2)]) for q in range(n)]
+        for k in range(c // 2):
+            rows = [(col_ladder(ctx, ctx.mult_sum(list(A.blocks[p]), [rots[q][k] for q in range(n)])),)
+                    for p in range(m)]
+            sums = Grid(ctx, rows, (A.shape[0], s1))
+            term = sums.mul(make_mask(ctx, k, c, (m, 1), True, scale))
+            acc = term if acc is None else acc.add(term)
+        return acc.add(acc.conj()).meta(out_shape, "horizontal", c)
     for k in range(c // 2):
         sums = col_sums(_rowwise(A, rot_up(packed, k)))
         term = sums.mul(make_mask(ctx, k, c, (m, 1), True, scale))
@@ -526,8 +556,21 @@ def diag_atb(A, B, scale=1.0, presum=row_presum):                   # matmul.py:
     partial = A.level < B.level
     packed = A.add(rot_left(A, c // 2).each(ctx.mul_i))
     acc = None
+    hoisted = None
+    if fused(ctx, 5, A, B):
+        # fused form: the per-pass leading rotations lrot(packed, k) of a block
+        # share one ModUp
+        s1 = ctx.grid_cols
+        amounts = [k if partial else k % s1 for k in range(c // 2)]
+        hoisted = {id(b): ctx.lrot_hoisted(b, amounts) for r in packed.blocks for b in r}
     for k in range(c // 2):
-        if partial:
+        if hoisted is not None:
+            pick = (lambda kk: (lambda b: hoisted[id(b)][kk]))(k)
+            if partial:
+                left, right = packed.each(pick), prot_up(B, k)
+            else:
+                left, right = rot_left(packed, k, first=pick), B
+        elif partial:
             left, right = packed.lrot(k), prot_up(B, k)
         else:
             left, right = rot_left(packed, k), B

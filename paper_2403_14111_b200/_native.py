@@ -41,6 +41,7 @@ SIGNATURES = {
     "hc_set_grid_rows": (I, [P, I]),
     "hc_set_auto_bootstrap": (I, [P, I]),
     "hc_set_streams": (I, [P, I]),
+    "hc_set_hoist": (I, [P, I]),
     "hc_ctx_counts": (I, [P, I64P, I]),
     "hc_ctx_nonce": (I, [P, U64P, U64P]),
     "hc_sync": (I, [P]),
@@ -65,6 +66,8 @@ SIGNATURES = {
     "hc_op_mult_scalar": (I, [P, P, D, D, PP]),
     "hc_op_mult_plain": (I, [P, P, DP, DP, C.c_char_p, PP]),
     "hc_op_lrot": (I, [P, P, I64, PP]),
+    "hc_op_lrot_hoisted": (I, [P, P, C.POINTER(C.c_int64), I, PP]),
+    "hc_op_mult_sum": (I, [P, PP, PP, I, PP]),
     "hc_op_conj": (I, [P, P, PP]),
     "hc_op_mul_i": (I, [P, P, PP]),
     "hc_op_bootstrap": (I, [P, P, PP]),

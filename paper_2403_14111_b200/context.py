@@ -165,7 +165,7 @@ class CKKSContext:
 
     def __init__(self, params: str | int = "cfg1", grid_rows: int | None = None, *, max_level=None,
                  auto_bootstrap: bool = False, seed: int = 2024, sigma: float = 3.2, device: int = 0,
-                 op_weights=None):
+                 op_weights=None, hoist: bool = True):
         if isinstance(params, (int, np.integer)):
             params = params_for(int(params), 12 if max_level is None else max_level)
         logn, qb, pb, alpha, logs, hw = PARAMS[params]
@@ -193,6 +193,8 @@ class CKKSContext:
         N.check(N.lib().hc_set_grid_rows(self._h, grid_rows))
         self._auto = False
         self.auto_bootstrap = auto_bootstrap
+        self._hoist = True
+        self.hoist = hoist
         self.ledger = NativeLedger(self, op_weights)
         self.decode_events: list = []
         n = len(qb) + len(pb)
@@ -222,6 +224,19 @@ class CKKSContext:
     def auto_bootstrap(self, on: bool) -> None:
         self._auto = bool(on)
         N.check(N.lib().hc_set_auto_bootstrap(self._h, int(self._auto)))
+
+    @property
+    def hoist(self) -> bool:
+        """Fused schedule forms: hoisted rotations and one
+        relinearisation per product sum, in the native schedules and through
+        ``lrot_hoisted`` / ``mult_sum``.  The oracle context's ``hoist`` must
+        match for residue parity; the ledger is the reference's either way."""
+        return self._hoist
+
+    @hoist.setter
+    def hoist(self, on: bool) -> None:
+        self._hoist = bool(on)
+        N.check(N.lib().hc_set_hoist(self._h, int(self._hoist)))
 
     @property
     def extra(self):
@@ -404,6 +419,41 @@ class CKKSContext:
 
     def rrot(self, x, r: int):
         return self.lrot(x, -int(r))
+
+    def lrot_hoisted(self, x, rs):
+        """[lrot(x, r) for r in rs] with one shared ModUp (hoisted rotations):
+        one Rot per non-zero r, r = 0 returns x itself."""
+        kx, vx = self._kind(x)
+        rr = [int(r) % self.slot_count for r in rs]
+        if kx != "ct" or not self._hoist:
+            return [self.lrot(x, r) for r in rr]
+        arr = (C.c_int64 * len(rr))(*rr)
+        outs = (C.c_void_p * len(rr))()
+        N.check(N.lib().hc_op_lrot_hoisted(self._h, vx._h, arr, len(rr), outs))
+        res = []
+        for r, h in zip(rr, outs):
+            if r == 0:
+                N.lib().hc_ct_free(h)
+                res.append(x)
+            else:
+                res.append(Ciphertext(self, C.c_void_p(h)))
+        return res
+
+    def mult_sum(self, xs, ys):
+        """add(...add(mult(x0, y0), mult(x1, y1))...) with one relinearisation
+        and rescale (n Mult + n - 1 Add on the ledger) when every operand is a
+        ciphertext at one level >= 1 and n >= 2; the separate ops otherwise."""
+        xs, ys = list(xs), list(ys)
+        blocks = xs + ys
+        if (not self._hoist or len(xs) < 2 or not all(isinstance(b, Ciphertext) for b in blocks)
+                or len({b.level for b in blocks}) != 1 or blocks[0].level < 1):
+            acc = self.mult(xs[0], ys[0])
+            for x, y in zip(xs[1:], ys[1:]):
+                acc = self.add(acc, self.mult(x, y))
+            return acc
+        A = (C.c_void_p * len(xs))(*[x._h for x in xs])
+        B = (C.c_void_p * len(ys))(*[y._h for y in ys])
+        return self._new(N.lib().hc_op_mult_sum, A, B, len(xs))
 
     def conj(self, x):
         kx, vx = self._kind(x)

@@ -100,6 +100,11 @@ int hc_set_auto_bootstrap(hc_ctx* ctx, int on) {
     return 0;
 }
 
+int hc_set_hoist(hc_ctx* ctx, int on) {
+    ctx->c->hoist = on != 0;
+    return 0;
+}
+
 int hc_ctx_counts(hc_ctx* ctx, int64_t* counts, int reset) {
     std::lock_guard<std::mutex> g(ctx->c->mu);
     for (int i = 0; i < HC_NCOUNTS; i++) {
@@ -246,6 +251,24 @@ int hc_op_mult_plain(hc_ctx* ctx, const hc_ct* a, const double* re, const double
 
 int hc_op_lrot(hc_ctx* ctx, const hc_ct* a, int64_t r, hc_ct** out) {
     return guard([&] { *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).lrot(a->p, r)); });
+}
+
+int hc_op_lrot_hoisted(hc_ctx* ctx, const hc_ct* a, const int64_t* rs, int n, hc_ct** outs) {
+    return guard([&] {
+        if (n < 0) throw hc::Error(HC_EPARAM, "negative rotation count");
+        std::vector<int64_t> r(rs, rs + n);
+        auto o = hc::Eval(*ctx->c, ctx->auto_boot).lrot_hoisted({a->p}, r);
+        for (int k = 0; k < n; k++) outs[k] = wrap(o[0][k]);
+    });
+}
+
+int hc_op_mult_sum(hc_ctx* ctx, const hc_ct* const* a, const hc_ct* const* b, int n, hc_ct** out) {
+    return guard([&] {
+        if (n < 1) throw hc::Error(HC_EPARAM, "empty product sum");
+        std::vector<hc::CtP> xs(n), ys(n);
+        for (int q = 0; q < n; q++) { xs[q] = a[q]->p; ys[q] = b[q]->p; }
+        *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).mult_sum_batch({xs}, {ys})[0]);
+    });
 }
 
 int hc_op_conj(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {

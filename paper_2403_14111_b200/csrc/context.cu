@@ -217,6 +217,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     if (const char* e = std::getenv("HC_STREAMS")) c->fork_cap = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HC_NTT_FP")) c->ntt_fp = std::atoi(e) != 0;
     if (const char* e = std::getenv("HC_LOCKSTEP")) c->lockstep = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HC_HOIST")) c->hoist = std::atoi(e) != 0;
     if (const char* e = std::getenv("HC_BATCH")) c->batch = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("HC_RUNAHEAD")) c->ra_depth = std::max(1, std::atoi(e));
     cudaMemPoolProps props = {};

@@ -167,8 +167,8 @@ CtP ev_level_adjust(Ctx& c, const Ct& a, int to) {
 
 static inline int tprime(const Ctx& c, int level, int t) { return t <= level ? t : c.L + 1 + (t - level - 1); }
 
-// d: [level+1][N] (NTT).  out [2][level+1][N] = KS(d) + addend (first add_npoly polys)
-void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+// ModUp of d ([level+1][N], NTT) -> UP [beta][nt][N] (NTT form, allocated here)
+static u64* ks_modup(Ctx& c, const u64* d, int level) {
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
     const int beta = (nl + c.alpha - 1) / c.alpha;
     u64* X = c.alloc((size_t)nl * N);
@@ -191,9 +191,16 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
         }
         ntt_forward(c, j);
     }
+    c.free(X);
+    return UP;
+}
+
+// key product of the ModUp digits UP with `key`, ModDown, + addend
+static void ks_tail(Ctx& c, const u64* UP, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+    const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
+    const int beta = (nl + c.alpha - 1) / c.alpha;
     u64* ACC = c.alloc((size_t)2 * nt * N);
     k_keyprod(c, ACC, UP, key.d, level, beta);
-    c.free(UP);
     {
         JobList j;
         j.n = 0;
@@ -206,7 +213,6 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
             }
         ntt_inverse(c, j);
     }
-    c.free(X);
     u64* W = c.alloc((size_t)2 * nl * N);
     k_moddown_conv(c, W, ACC, level);
     ntt_limbs(c, W, 0, nl, false);
@@ -215,6 +221,13 @@ void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const 
     c.free(W);
     c.free(ACC);
     c.counts[OP_KS]++;
+}
+
+// d: [level+1][N] (NTT).  out [2][level+1][N] = KS(d) + addend (first add_npoly polys)
+void keyswitch(Ctx& c, const u64* d, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+    u64* UP = ks_modup(c, d, level);
+    ks_tail(c, UP, level, key, out, addend, add_npoly);
+    c.free(UP);
 }
 
 CtP ev_automorph(Ctx& c, const Ct& a, u64 g) {
@@ -305,6 +318,88 @@ std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, co
     }
     if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) throw Error(-2, "batched relinearisation");
     c.counts[OP_KS] += (int64_t)B;
+    for (size_t b = 0; b < B; b++) {
+        out[b] = new_ct(c, level - 1);
+        rescale_raw(c, T + 2 * poly * b, level, 2, out[b]->d);
+    }
+    return out;
+}
+
+// Hoisted rotations: rotation r of input i shares the ModUp
+// of c1(i) with every other rotation of it; the digits are permuted by each
+// Galois element inside the key product.  All inputs at one level.
+// out[i][r] = sigma_{g_r}(x_i) with the hoisted key switch.
+std::vector<std::vector<CtP>> ev_rot_hoisted(Ctx& c, const std::vector<const Ct*>& xs, const std::vector<u64>& gals) {
+    const size_t nx = xs.size(), ng = gals.size();
+    std::vector<std::vector<CtP>> out(nx, std::vector<CtP>(ng));
+    if (nx == 0 || ng == 0) return out;
+    const int level = xs[0]->level;
+    for (auto* x : xs)
+        if (x->level != level) throw Error(-4, "hoisted rotation: inputs at different levels");
+    std::vector<const Key*> keys(ng);
+    for (size_t r = 0; r < ng; r++) keys[r] = &get_key(c, (int)gals[r]);
+    for (size_t i = 0; i < nx; i++)
+        for (size_t r = 0; r < ng; r++) out[i][r] = new_ct(c, level);
+    if (c.logN >= 14) {
+        std::vector<const u64*> c0s(nx), c1s(nx);
+        for (size_t i = 0; i < nx; i++) { c0s[i] = xs[i]->poly(0); c1s[i] = xs[i]->poly(1); }
+        std::vector<KsHoist> e;
+        for (size_t i = 0; i < nx; i++)
+            for (size_t r = 0; r < ng; r++) e.push_back(KsHoist{(int)i, gals[r], keys[r]->d, out[i][r]->d});
+        if (!keyswitch_hoisted(c, c0s.data(), c1s.data(), level, (int)e.size(), e.data()))
+            throw Error(-2, "hoisted rotation");
+        c.counts[OP_KS] += (int64_t)e.size();
+        return out;
+    }
+    // small rings: the unfused pipeline, digits permuted by an explicit automorphism
+    const int nl = level + 1, nt = nl + c.K, beta = (nl + c.alpha - 1) / c.alpha;
+    for (size_t i = 0; i < nx; i++) {
+        u64* UP = ks_modup(c, xs[i]->poly(1), level);
+        u64* UPg = c.alloc((size_t)beta * nt * c.N);
+        u64* S0 = c.alloc((size_t)nl * c.N);
+        for (size_t r = 0; r < ng; r++) {
+            k_automorph(c, UPg, UP, beta * nt, gals[r]);
+            k_automorph(c, S0, xs[i]->poly(0), nl, gals[r]);
+            ks_tail(c, UPg, level, *keys[r], out[i][r]->d, S0, 1);
+        }
+        c.free(S0);
+        c.free(UPg);
+        c.free(UP);
+    }
+    return out;
+}
+
+// Product sums with one relinearisation each:
+// out_b = rescale(d0 + KS(d2)_0, d1 + KS(d2)_1), d = sum_q tensor(a_bq, b_bq).
+// Every operand of every group at one level >= 1.
+std::vector<CtP> ev_mult_sum_batch(Ctx& c, const std::vector<std::vector<std::pair<const Ct*, const Ct*>>>& groups) {
+    const size_t B = groups.size();
+    std::vector<CtP> out(B);
+    if (B == 0) return out;
+    const int level = groups[0][0].first->level;
+    for (auto& gr : groups)
+        for (auto& pr : gr)
+            if (pr.first->level != level || pr.second->level != level) throw Error(-4, "product sum: level mismatch");
+    if (level < 1) throw Error(-3, "multiply at level 0");
+    const Key& key = get_key(c, 0);
+    const int nl = level + 1;
+    const size_t poly = (size_t)nl * c.N;
+    Scratch sc(c);
+    u64* D = sc.take(3 * poly * B);
+    u64* T = sc.take(2 * poly * B);
+    std::vector<KsIn> in(B);
+    for (size_t b = 0; b < B; b++) {
+        u64* Db = D + 3 * poly * b;
+        std::vector<const u64*> as, bs;
+        for (auto& pr : groups[b]) { as.push_back(pr.first->d); bs.push_back(pr.second->d); }
+        k_tensor_sum(c, Db, as.data(), bs.data(), (int)as.size(), nl);
+        in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
+    }
+    if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) {
+        for (size_t b = 0; b < B; b++) keyswitch(c, in[b].d, level, key, in[b].out, in[b].add, 2);
+    } else {
+        c.counts[OP_KS] += (int64_t)B;
+    }
     for (size_t b = 0; b < B; b++) {
         out[b] = new_ct(c, level - 1);
         rescale_raw(c, T + 2 * poly * b, level, 2, out[b]->d);
@@ -481,6 +576,80 @@ std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs, const std::vector<
             }
         std::vector<CtP> r = ev_mult_batch(c, ab);
         for (size_t k = 0; k < idx.size(); k++) out[idx[k]] = r[k];
+    }
+    return out;
+}
+
+std::vector<std::vector<CtP>> Eval::lrot_hoisted(const std::vector<CtP>& xs, const std::vector<int64_t>& rs) {
+    const int64_t S = c.N / 2;
+    std::vector<int64_t> rr(rs.size());
+    std::vector<u64> gals;
+    std::vector<int> slot(rs.size(), -1);
+    for (size_t k = 0; k < rs.size(); k++) {
+        rr[k] = ((rs[k] % S) + S) % S;
+        if (!rr[k]) continue;
+        for (size_t j = 0; j < k; j++)
+            if (rr[j] == rr[k]) slot[k] = slot[j];
+        if (slot[k] < 0) { slot[k] = (int)gals.size(); gals.push_back(galois_rot(c, rr[k])); }
+    }
+    std::vector<std::vector<CtP>> out(xs.size(), std::vector<CtP>(rs.size()));
+    int moving = 0;
+    for (auto v : rr) moving += v != 0;
+    rec(OP_ROT, moving * (int)xs.size());
+    // one hoisted pipeline per level present
+    std::vector<char> done(xs.size(), 0);
+    for (size_t i = 0; i < xs.size(); i++) {
+        if (done[i]) continue;
+        std::vector<size_t> idx;
+        std::vector<const Ct*> a;
+        for (size_t j = i; j < xs.size(); j++)
+            if (!done[j] && xs[j]->level == xs[i]->level) {
+                idx.push_back(j);
+                a.push_back(xs[j].get());
+                done[j] = 1;
+            }
+        std::vector<std::vector<CtP>> h = ev_rot_hoisted(c, a, gals);
+        for (size_t t = 0; t < idx.size(); t++)
+            for (size_t k = 0; k < rs.size(); k++) out[idx[t]][k] = rr[k] ? h[t][slot[k]] : xs[idx[t]];
+    }
+    return out;
+}
+
+std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, const std::vector<std::vector<CtP>>& bs) {
+    std::vector<CtP> out(as.size());
+    std::vector<size_t> fused;
+    for (size_t i = 0; i < as.size(); i++) {
+        const size_t n = as[i].size();
+        bool ok = n >= 2 && bs[i].size() == n;
+        const int l = as[i][0]->level;
+        for (size_t q = 0; ok && q < n; q++) ok = as[i][q]->level == l && bs[i][q]->level == l;
+        ok = ok && l >= 1;
+        if (ok) { fused.push_back(i); continue; }
+        // the separate ops, in the reference's order
+        CtP acc = mult(as[i][0], bs[i][0]);
+        for (size_t q = 1; q < n; q++) acc = add(acc, mult(as[i][q], bs[i][q]));
+        out[i] = acc;
+    }
+    // one batched relinearisation per level present
+    std::vector<char> done(fused.size(), 0);
+    for (size_t u = 0; u < fused.size(); u++) {
+        if (done[u]) continue;
+        std::vector<size_t> idx;
+        std::vector<std::vector<std::pair<const Ct*, const Ct*>>> groups;
+        const int l = as[fused[u]][0]->level;
+        for (size_t v = u; v < fused.size(); v++) {
+            const size_t i = fused[v];
+            if (done[v] || as[i][0]->level != l) continue;
+            done[v] = 1;
+            idx.push_back(i);
+            std::vector<std::pair<const Ct*, const Ct*>> gr;
+            for (size_t q = 0; q < as[i].size(); q++) gr.emplace_back(as[i][q].get(), bs[i][q].get());
+            groups.push_back(gr);
+            rec(OP_MULT, (int)as[i].size());
+            rec(OP_ADD, (int)as[i].size() - 1);
+        }
+        std::vector<CtP> r = ev_mult_sum_batch(c, groups);
+        for (size_t t = 0; t < idx.size(); t++) out[idx[t]] = r[t];
     }
     return out;
 }

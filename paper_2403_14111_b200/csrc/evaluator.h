@@ -28,6 +28,15 @@ struct KsIn {
     const u64* key;
 };
 bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal);
+// hoisted key switches (keyswitch.cu): entry b rotates input src (c0s / c1s)
+// by Galois element gal with `key` into out; one ModUp per distinct input
+struct KsHoist {
+    int src;
+    u64 gal;
+    const u64* key;
+    u64* out;
+};
+bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int level, int B, const KsHoist* e);
 // out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
 bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
@@ -85,6 +94,13 @@ struct Eval {
     std::vector<CtP> lrot_batch(const std::vector<CtP>& xs, int64_t r, bool add_self = false);
     std::vector<CtP> conj_batch(const std::vector<CtP>& xs);
     std::vector<CtP> mult_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys);
+    // fused forms (residues differ from the separate ops, the
+    // ledger does not): lrot of every x by every r with one ModUp per x
+    // (out[x][r]; r = 0 returns x), and add(...add(mult(a0, b0), mult(a1, b1))...)
+    // with one relinearisation and rescale per group (separate ops unless
+    // every operand is at one level >= 1 and the group has >= 2 products)
+    std::vector<std::vector<CtP>> lrot_hoisted(const std::vector<CtP>& xs, const std::vector<int64_t>& rs);
+    std::vector<CtP> mult_sum_batch(const std::vector<std::vector<CtP>>& as, const std::vector<std::vector<CtP>>& bs);
     CtP mul_i(const CtP& a);
     CtP bootstrap(const CtP& a);
     PtP encoded(const Pattern& p, int level);

@@ -121,6 +121,42 @@ void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl) {
     HC_CUDA(cudaGetLastError());
 }
 
+// sum of n tensor products (fused product sums): each
+// component accumulated in 128 bits (at most 2 * TS_MAXN products of
+// 61-bit residues) and reduced once
+constexpr int TS_MAXN = 8;
+struct TensorSrc {
+    const u64* a[TS_MAXN];
+    const u64* b[TS_MAXN];
+};
+__global__ void tensor_sum_kernel(u64* __restrict__ d, TensorSrc src, int n, const PrimeDev* __restrict__ primes,
+                                  int nl, int N) {
+    const size_t poly = (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        U128 s0 = {0, 0}, s1 = {0, 0}, s2 = {0, 0};
+        for (int q = 0; q < n; q++) {
+            const u64 a0 = src.a[q][e], a1 = src.a[q][poly + e], b0 = src.b[q][e], b1 = src.b[q][poly + e];
+            mac128(s0, a0, b0);
+            mac128(s1, a0, b1);
+            mac128(s1, a1, b0);
+            mac128(s2, a1, b1);
+        }
+        d[e] = reduce128(s0.hi, s0.lo, P);
+        d[poly + e] = reduce128(s1.hi, s1.lo, P);
+        d[2 * poly + e] = reduce128(s2.hi, s2.lo, P);
+    }
+}
+
+void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int n, int nl) {
+    if (n < 1 || n > TS_MAXN) throw Error(-1, "tensor sum: bad operand count");
+    TensorSrc src;
+    for (int q = 0; q < n; q++) { src.a[q] = a[q]; src.b[q] = b[q]; }
+    Launch scope(c, "tensor", 8.0 * c.N * (4.0 * n + 3) * nl);
+    tensor_sum_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(d, src, n, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------------------
 // Galois automorphism in the NTT domain: out[j] = in[src(j)]
 // ---------------------------------------------------------------------------

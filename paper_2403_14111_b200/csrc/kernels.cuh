@@ -13,6 +13,8 @@ struct ConstTab {
 void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const ConstTab* consts, int nl, int npoly,
                    int bpoly);
 void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl);
+// d = sum_q tensor(a[q], b[q]), n <= 8
+void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int n, int nl);
 void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g);
 void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta);
 void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta);

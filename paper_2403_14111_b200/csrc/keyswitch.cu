@@ -50,13 +50,20 @@ struct KsGeo {
 // The key switches of one batched pipeline: all at the same level and read
 // through the same Galois element; each has its own input, output, addends
 // and switching key (equal keys are read once by the key product).
+//
+// Hoisted form (several Galois elements applied to one input): the ModUp
+// stage runs once per distinct input (no gather), and entry b of the tail
+// reads its input's digits and c1 through its own element ugal[b].
 struct KsBatch {
     int nb;
-    const u64* d[KS_MAXB];      // c1 source (NTT form), read through gal
+    const u64* d[KS_MAXB];      // c1 source (NTT form), read through ugal[b] or the pipeline's gal
+    const u64* up[KS_MAXB];     // ModUp digits of this entry's input ([beta][nt][N])
     u64* out[KS_MAXB];          // [2][nl][N]
-    const u64* add[KS_MAXB];    // [add_npoly][nl][N] addend (read through add_gal) or null
+    const u64* add[KS_MAXB];    // [add_npoly][nl][N] addend (read through agal[b]) or null
     const u64* add2[KS_MAXB];   // [2][nl][N] second addend (ladder step) or null
     const u64* key[KS_MAXB];    // [dnum][2][nall][N]
+    u64 ugal[KS_MAXB];          // hoisted: Galois element gathered over up[b] and d[b] (0 = none)
+    u64 agal[KS_MAXB];          // Galois element the addend is read through (0 = none)
 };
 
 // ---- A: ModUp conversion fused into the column pass --------------------------
@@ -125,7 +132,7 @@ constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
 // thread, 16-byte accesses, one Barrett reduction per output.
 
 __global__ void __launch_bounds__(256, 3) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
-                                                            const u64* __restrict__ UP, u64 gal, KsBatch kb,
+                                                            u64 gal, KsBatch kb,
                                                             u64* __restrict__ acc, int tlimit) {
     const size_t N = (size_t)1 << g.logN;
     const size_t total = (size_t)tlimit << g.logN;
@@ -150,8 +157,11 @@ __global__ void __launch_bounds__(256, 3) ks_keyprod_stream(KsGeo g, const Prime
                     kav[j] = kp[kstride];
                 }
             }
-            const u64* up = UP + b * g.i_stride();
+            const u64* up = kb.up[b];
             const u64* d = kb.d[b];
+            const u64 ug = kb.ugal[b];
+            const size_t ku = ug ? galois_src((unsigned)k, g.logN, ug) : k;
+            const u64 dg = ug ? 0 : gal;
             // issue every digit load before the first product
             u64 x[KP_MAXB];
 #pragma unroll
@@ -160,9 +170,9 @@ __global__ void __launch_bounds__(256, 3) ks_keyprod_stream(KsGeo g, const Prime
                 const int lo = j * g.alpha, hi = min(lo + g.alpha, g.nl);
                 if (t >= lo && t < hi) {
                     const u64* src = d + (size_t)t * N;
-                    x[j] = gal ? src[galois_src((unsigned)k, g.logN, gal)] : src[k];
+                    x[j] = dg ? src[galois_src((unsigned)k, g.logN, dg)] : src[ku];
                 } else {
-                    x[j] = up[((size_t)j * g.nt + t) * N + k];
+                    x[j] = up[((size_t)j * g.nt + t) * N + ku];
                 }
             }
             u64 ob, oa;
@@ -261,7 +271,7 @@ struct StModdown {
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
-                      const u64* __restrict__ pinv, int add_npoly, u64 add_gal, KsBatch kb) {
+                      const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
     StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
                  (s < add_npoly && addend) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
-                 add_gal, g.logN, addend2 ? addend2 + ((size_t)s * g.nl + i) * N : nullptr};
+                 kb.agal[b], g.logN, addend2 ? addend2 + ((size_t)s * g.nl + i) * N : nullptr};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
     G.init(g.N1);
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
@@ -383,8 +393,24 @@ template <> struct ColCfg<15> { static constexpr int LOGSZ = 6, SUBS = 32; };
 template <> struct ColCfg<16> { static constexpr int LOGSZ = 7, SUBS = 16; };
 template <> struct ColCfg<17> { static constexpr int LOGSZ = 8, SUBS = 8; };
 
+// One key-switch tail entry: which ModUp input it consumes and, hoisted, the
+// Galois element applied to that input's digits.
+struct KsTail {
+    int src;
+    u64 ugal;
+    const u64* d;   // c1 of the input (NTT form)
+    u64* out;
+    const u64* add;
+    const u64* add2;
+    const u64* key;
+    u64 agal;
+};
+
+// The fused pipeline: ModUp stage over `nin` inputs din[] (read through gal),
+// then key product + ModDown over `B` tail entries.
 template <int LOGN>
-static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal) {
+static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int level, int B, const KsTail* in,
+                          int add_npoly) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
@@ -393,26 +419,19 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     KsBatch kb;
     kb.nb = B;
-    for (int b = 0; b < B; b++) {
-        kb.d[b] = in[b].d;
-        kb.out[b] = in[b].out;
-        kb.add[b] = in[b].add;
-        kb.add2[b] = in[b].add2;
-        kb.key[b] = in[b].key;
-    }
 
     Scratch sc(c);
     // 1. Y = INTT(sigma(d)) * (Q'/q_i)^-1
-    u64* Y = sc.take((size_t)B * g.y_stride());
+    u64* Y = sc.take((size_t)nin * g.y_stride());
     {
         JobList j;
         j.n = nl;
         j.custom = 1;
         j.galois = gal;
-        j.nb = B;
-        for (int b = 0; b < B; b++) {
+        j.nb = nin;
+        for (int b = 0; b < nin; b++) {
             j.boff[b] = (long long)(b * g.y_stride());
-            j.sboff[b] = (long long)(in[b].d - in[0].d);
+            j.sboff[b] = (long long)(din[b] - din[0]);
         }
         for (int i = 0; i < nl; i++) {
             const int dj = i / c.alpha, lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
@@ -422,14 +441,14 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
             const u64 sc = mulm(c.pr[i].ninv, powm(qh, qi - 2, qi), qi);
             j.prime[i] = i;
             j.ptr[i] = Y + (size_t)i * N;
-            j.src[i] = in[0].d + (size_t)i * N;
+            j.src[i] = din[0] + (size_t)i * N;
             j.scale[i] = sc;
             j.scale_s[i] = shoup_of(sc, qi);
         }
         ntt_inverse(c, j);
     }
     // 2. A: conversion + column pass for every (digit, non-digit target)
-    u64* I = sc.take((size_t)B * g.i_stride());
+    u64* I = sc.take((size_t)nin * g.i_stride());
     {
         KsJobs jobs;
         jobs.n = 0;
@@ -444,8 +463,8 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
         }
         static bool at = false;
         // algorithmic: the digit limbs Y read once, one intermediate limb written per job
-        Launch scope(c, "ks_modup_cols", 8.0 * N * B * (nl + (double)jobs.n));
-        dim3 grid((N >> CL) / CS, jobs.n, B);
+        Launch scope(c, "ks_modup_cols", 8.0 * N * nin * (nl + (double)jobs.n));
+        dim3 grid((N >> CL) / CS, jobs.n, nin);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);
             kern<<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
@@ -464,8 +483,8 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
     {
         JobList j;
         j.n = 0;
-        j.nb = B;
-        for (int b = 0; b < B; b++) j.boff[b] = (long long)(b * g.i_stride());
+        j.nb = nin;
+        for (int b = 0; b < nin; b++) j.boff[b] = (long long)(b * g.i_stride());
         for (int dj = 0; dj < g.beta; dj++) {
             const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
             for (int t = 0; t < nt; t++) {
@@ -477,14 +496,24 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
             }
         }
         ntt_forward_chunks(c, j);
+        for (int b = 0; b < B; b++) {
+            kb.d[b] = in[b].d;
+            kb.up[b] = I + (size_t)in[b].src * g.i_stride();
+            kb.out[b] = in[b].out;
+            kb.add[b] = in[b].add;
+            kb.add2[b] = in[b].add2;
+            kb.key[b] = in[b].key;
+            kb.ugal[b] = in[b].ugal;
+            kb.agal[b] = in[b].agal;
+        }
         int nkeys = 1;
         for (int b = 1; b < B; b++) nkeys += in[b].key != in[b - 1].key;
         const size_t work = (size_t)nt * N;
-        // algorithmic: the digit limbs and ACC per key switch, each distinct key run once
+        // algorithmic: the digit limbs (once per input) and ACC per key switch, each distinct key run once
         Launch scope(c, "ks_keyprod_stream",
-                     8.0 * N * ((double)B * (g.beta * nt + 2.0 * nt) + 2.0 * nkeys * g.beta * nt));
+                     8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
         int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 32);
-        ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, I, gal, kb, ACC, nt);
+        ks_keyprod_stream<<<blocks, 256, 0, c.stream>>>(g, c.d_primes, gal, kb, ACC, nt);
         HC_CUDA(cudaGetLastError());
     }
     // 4. INTT of the P limbs, final scale N^-1 (P/p_t)^-1 (in place)
@@ -537,21 +566,57 @@ static void keyswitch_batch_t(Ctx& c, int B, const KsIn* in, u64 gal, int level,
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
         dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl, B);
         ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
-                                                                add_npoly, add_gal, kb);
+                                                                add_npoly, kb);
         HC_CUDA(cudaGetLastError());
     }
 }
 
+static bool fusable(const Ctx& c, int level) {
+    return (level + c.alpha) / c.alpha <= KP_MAXB && c.K <= 4 && c.alpha <= 4 && c.logN >= 14 && c.logN <= 17;
+}
+
+static void ks_pipeline(Ctx& c, int nin, const u64* const* din, u64 gal, int level, int B, const KsTail* in,
+                        int add_npoly) {
+    switch (c.logN) {
+        case 14: ks_pipeline_t<14>(c, nin, din, gal, level, B, in, add_npoly); break;
+        case 15: ks_pipeline_t<15>(c, nin, din, gal, level, B, in, add_npoly); break;
+        case 16: ks_pipeline_t<16>(c, nin, din, gal, level, B, in, add_npoly); break;
+        default: ks_pipeline_t<17>(c, nin, din, gal, level, B, in, add_npoly); break;
+    }
+}
+
 bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal) {
-    if ((level + c.alpha) / c.alpha > KP_MAXB || c.K > 4 || c.alpha > 4 || c.logN < 14 || c.logN > 17) return false;
+    if (!fusable(c, level)) return false;
     for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
         const int nb = std::min(KS_MAXB, B - b0);
-        switch (c.logN) {
-            case 14: keyswitch_batch_t<14>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
-            case 15: keyswitch_batch_t<15>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
-            case 16: keyswitch_batch_t<16>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
-            default: keyswitch_batch_t<17>(c, nb, in + b0, gal, level, add_npoly, add_gal); break;
+        const u64* din[KS_MAXB];
+        KsTail tl[KS_MAXB];
+        for (int b = 0; b < nb; b++) {
+            const KsIn& x = in[b0 + b];
+            din[b] = x.d;
+            tl[b] = KsTail{b, 0, x.d, x.out, x.add, x.add2, x.key, add_gal};
         }
+        ks_pipeline(c, nb, din, gal, level, nb, tl, add_npoly);
+    }
+    return true;
+}
+
+bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int level, int B, const KsHoist* e) {
+    if (!fusable(c, level)) return false;
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        // this chunk's distinct inputs, in first-use order
+        int srcs[KS_MAXB], nsrc = 0;
+        const u64* din[KS_MAXB];
+        KsTail tl[KS_MAXB];
+        for (int b = 0; b < nb; b++) {
+            const KsHoist& x = e[b0 + b];
+            int m = -1;
+            for (int i = 0; i < nsrc; i++) if (srcs[i] == x.src) m = i;
+            if (m < 0) { m = nsrc; srcs[nsrc] = x.src; din[nsrc++] = c1s[x.src]; }
+            tl[b] = KsTail{m, x.gal, c1s[x.src], x.out, c0s[x.src], nullptr, x.key, x.gal};
+        }
+        ks_pipeline(c, nsrc, din, 0, level, nb, tl, 1);
     }
     return true;
 }

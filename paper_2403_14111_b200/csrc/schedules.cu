@@ -334,30 +334,49 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     G rolled = kk0 ? ev.lrot_batch(B, (int64_t)kk0 * g.s1) : B;
     G packed(n);
     for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], ev.mul_i(rolled[q]));
-    // RU(packed, k) per pass (one batch per k: its own Galois element)
     std::vector<G> shifted(K);
-    for (int k = 0; k < K; k++) {
-        const int kk = k % g.s0;
-        shifted[k] = kk ? ev.lrot_batch(packed, (int64_t)kk * g.s1) : packed;
-    }
-    // all passes' products in one batch
-    G xs, ys;
-    for (int k = 0; k < K; k++)
-        for (int p = 0; p < m; p++)
-            for (int q = 0; q < n; q++) {
-                xs.push_back(A[(size_t)p * n + q]);
-                ys.push_back(shifted[k][q]);
-            }
-    G prod = mult_many(ev, xs, ys);
-    // col_sums of every (pass, block row): pre-add, then the ladders in lockstep
     G acc((size_t)K * m);
-    for (int k = 0; k < K; k++)
-        for (int p = 0; p < m; p++) {
-            const size_t base = ((size_t)k * m + p) * n;
-            CtP a = prod[base];
-            for (int q = 1; q < n; q++) a = ev.add(a, prod[base + q]);
-            acc[(size_t)k * m + p] = a;
+    if (ev.c.hoist) {
+        // fused form (oracle/slots.py diag_abt): RU(packed, k)
+        // of every pass with one ModUp per block column, and each (pass, block
+        // row) product sum -- the col_sums pre-add of the rowwise products --
+        // relinearised and rescaled once
+        std::vector<int64_t> amounts(K);
+        for (int k = 0; k < K; k++) amounts[k] = (int64_t)(k % g.s0) * g.s1;
+        std::vector<G> H = ev.lrot_hoisted(packed, amounts);
+        std::vector<G> as, bs;
+        for (int k = 0; k < K; k++)
+            for (int p = 0; p < m; p++) {
+                as.emplace_back(A.begin() + (size_t)p * n, A.begin() + (size_t)(p + 1) * n);
+                G b(n);
+                for (int q = 0; q < n; q++) b[q] = H[q][k];
+                bs.push_back(b);
+            }
+        acc = ev.mult_sum_batch(as, bs);
+    } else {
+        // RU(packed, k) per pass (one batch per k: its own Galois element)
+        for (int k = 0; k < K; k++) {
+            const int kk = k % g.s0;
+            shifted[k] = kk ? ev.lrot_batch(packed, (int64_t)kk * g.s1) : packed;
         }
+        // all passes' products in one batch
+        G xs, ys;
+        for (int k = 0; k < K; k++)
+            for (int p = 0; p < m; p++)
+                for (int q = 0; q < n; q++) {
+                    xs.push_back(A[(size_t)p * n + q]);
+                    ys.push_back(shifted[k][q]);
+                }
+        G prod = mult_many(ev, xs, ys);
+        // col_sums of every (pass, block row): pre-add, then the ladders in lockstep
+        for (int k = 0; k < K; k++)
+            for (int p = 0; p < m; p++) {
+                const size_t base = ((size_t)k * m + p) * n;
+                CtP a = prod[base];
+                for (int q = 1; q < n; q++) a = ev.add(a, prod[base + q]);
+                acc[(size_t)k * m + p] = a;
+            }
+    }
     for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, 1 << t, true);
     const Pattern c0 = col0(g);
     for (auto& a : acc) a = ev.mult_p(a, c0);
@@ -376,10 +395,11 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
 }
 
 // rot_left of every block of E by k (encoding.py:291-311); the rrot(s1) of
-// several calls can be gathered by the caller: returns (head, tail) pairs
-static void rot_left_split(Eval& ev, const G& E, int k, const Geo& g, G& head, G& tail) {
+// several calls can be gathered by the caller: returns (head, tail) pairs.
+// `first`, when given, holds lrot(E, k) already (hoisted by the caller).
+static void rot_left_split(Eval& ev, const G& E, int k, const Geo& g, G& head, G& tail, const G* first = nullptr) {
     const Pattern keep = keep_head(g, g.s1 - k);
-    G a1 = ev.lrot_batch(E, k);
+    G a1 = first ? *first : ev.lrot_batch(E, k);
     head.resize(E.size());
     tail.resize(E.size());
     for (size_t i = 0; i < E.size(); i++) {
@@ -406,16 +426,27 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
         }
         for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], ev.mul_i(one[p]));
     }
-    // left operands of every pass
+    // left operands of every pass; fused form (oracle/slots.py
+    // diag_atb): the leading rotations lrot(packed, k) share one ModUp per block
     std::vector<G> left(K);
+    std::vector<G> first(K);
+    if (ev.c.hoist) {
+        std::vector<int64_t> amounts(K);
+        for (int k = 0; k < K; k++) amounts[k] = partial ? k : k % s1;
+        std::vector<G> H = ev.lrot_hoisted(packed, amounts);
+        for (int k = 0; k < K; k++) {
+            first[k].resize(m);
+            for (int p = 0; p < m; p++) first[k][p] = H[p][k];
+        }
+    }
     if (partial) {
-        for (int k = 0; k < K; k++) left[k] = ev.lrot_batch(packed, k);
+        for (int k = 0; k < K; k++) left[k] = ev.c.hoist ? first[k] : ev.lrot_batch(packed, k);
     } else {
         std::vector<G> heads(K), tails(K);
         std::vector<int> moving;
         for (int k = 0; k < K; k++) {
             if (k % s1 == 0) { left[k] = packed; continue; }
-            rot_left_split(ev, packed, k % s1, g, heads[k], tails[k]);
+            rot_left_split(ev, packed, k % s1, g, heads[k], tails[k], ev.c.hoist ? &first[k] : nullptr);
             moving.push_back(k);
         }
         std::vector<G> tparts;
@@ -508,7 +539,8 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     // auto-bootstrap can fire inside (DiagABT consumes 3 levels), so the
     // refresh-nonce order is the reference's sequential one.
     const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
-    if (par && C.lockstep) return diag_abt_lockstep(ev, A, m, n, B, c, scale, g);
+    // the fused forms exist only in lockstep form: hoist implies lockstep
+    if (par && (C.lockstep || C.hoist)) return diag_abt_lockstep(ev, A, m, n, B, c, scale, g);
     auto W = [&](int w) { return par ? w : 1; };
     // packing prologue, one branch per block column: B + i * RU(B, c/2)
     G packed(n);
@@ -570,7 +602,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     // cross-rank reducer is fine: the host still reaches the k-th pre-sum's
     // collective in k order on every rank, and only that branch waits for it.
     const bool ser = ev.auto_boot && std::min(grid_level(A), grid_level(B)) < 5;
-    if (!ser && C.lockstep) return diag_atb_lockstep(ev, A, m, B, n, c, scale, g, red);
+    if (!ser && (C.lockstep || C.hoist)) return diag_atb_lockstep(ev, A, m, B, n, c, scale, g, red);
     const int width = ser ? 1 : fork_width(C, c / 2);
     // packing prologue per block row: A + i * RL(A, c/2)
     G packed(m);

@@ -105,6 +105,62 @@ def test_per_op_residues(pair):
     np.testing.assert_array_equal(rs.residues(), o.p.rescale(ox.data, ox.level))
 
 
+def _fused_ops(g, o, seed, tol=1e-5):
+    """hoisted rotations and product sums: residues, levels, ledgers"""
+    rng = np.random.default_rng(seed)
+    n = g.slot_count
+    xs = [rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n) for _ in range(3)]
+    ys = [rng.uniform(-1, 1, n) for _ in range(3)]
+    g.nonce, o.nonce = 0, 0
+    gx, gy = [g.encrypt(v) for v in xs], [g.encrypt(v) for v in ys]
+    ox, oy = [o.encrypt(v) for v in xs], [o.encrypt(v) for v in ys]
+    g.ledger.reset()
+    o.ledger.reset()
+    rs = (1, 5, 0, n - 3, n // 2)
+    for r, a, b in zip(rs, g.lrot_hoisted(gx[0], rs), o.lrot_hoisted(ox[0], rs)):
+        np.testing.assert_array_equal(a.residues(), b.data)
+        assert np.max(np.abs(a.slots - np.roll(xs[0], -r))) < tol
+        if r == 0:
+            assert a is gx[0]
+    gs, os_ = g.mult_sum(gx, gy), o.mult_sum(ox, oy)
+    np.testing.assert_array_equal(gs.residues(), os_.data)
+    assert gs.level == os_.level == g.max_level - 1
+    assert np.max(np.abs(gs.slots - sum(a * b for a, b in zip(xs, ys)))) < tol
+    assert _ledger(g) == _ledger(o) == [2, 0, 3, 4, 0, 0]
+
+
+def test_fused_ops_residues(pair):
+    _fused_ops(*pair, seed=6)
+
+
+@pytest.mark.slow
+def test_fused_ops_residues_cfg1():
+    """the same through the fused N = 2^16 pipeline (keyswitch_hoisted, batched relinearisation)"""
+    P = _prod()
+    # key-switch noise at cfg1: the first digit's modulus (58 + 3 x 42 bits)
+    # exceeds P (3 x 60 bits), so one switch leaves ~1e-4 in the worst slot
+    _fused_ops(P.CKKSContext("cfg1", 128, seed=3), R.OracleCKKSContext("cfg1", 128, seed=3), seed=7, tol=1e-3)
+
+
+@pytest.mark.parametrize("hoist", [True, False])
+def test_native_multi_column_diag_abt_small12(hoist):
+    """DiagABT with 3 block columns (the product sums fuse when hoist is on):
+    native schedule == restated schedule over the oracle in the same mode."""
+    P = _prod()
+    rng = np.random.default_rng(4)
+    A, B = rng.uniform(-1, 1, (10, 40)), rng.uniform(-1, 1, (4, 40))
+    g = P.CKKSContext("small12", 16, seed=5, hoist=hoist)
+    o = R.OracleCKKSContext("small12", 16, seed=5, hoist=hoist)
+    GA, OA = _enc_pair(g, o, A)
+    g.nonce = o.nonce = 40
+    GB, OB = P.encode(g, B, "vertical"), S.encode(o, B, "vertical")
+    out = P.diag_abt(GA, GB, scale=0.5)
+    ref = S.diag_abt(OA, OB, scale=0.5)
+    _same_grid(out, ref)
+    assert _ledger(g) == _ledger(o)
+    assert np.max(np.abs(P.decode(out, tol=1e-3) - 0.5 * A @ B.T)) < 1e-4
+
+
 def _enc_pair(g, o, arr, tiling="none", level=None):
     from paper_2403_14111_b200 import encode
     g.nonce = o.nonce = 0

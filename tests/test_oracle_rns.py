@@ -182,3 +182,48 @@ def test_restated_training_small12(golden):
     led = np.array([ctx.ledger.counts()[k] for k in OPS])
     np.testing.assert_array_equal(led, golden["small_train_led"])
     assert np.max(np.abs(np.stack(snaps) - golden["small_train_snaps"])) < 1e-4
+
+
+def test_hoisted_rotations_and_product_sums(small):
+    """Fused forms: a hoisted rotation is a different but valid
+    key switch (same slots, different residues); a product sum decrypts to the
+    sum of products and equals orc_mult for a single pair."""
+    rng = np.random.default_rng(3)
+    n, L = small.slots, small.L
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    cx = small.encrypt(x, L, 0)
+    rs = (1, 7, n - 2, n // 2)
+    outs = small.rotate_hoisted(cx, L, [small.galois(r) for r in rs])
+    differ = 0
+    for r, o in zip(rs, outs):
+        assert np.max(np.abs(small.decrypt(o, L) - np.roll(x, -r))) < TOL
+        differ += not np.array_equal(o, small.automorph(cx, L, small.galois(r)))
+    assert differ == len(rs)
+    ys = [rng.uniform(-1, 1, n) for _ in range(3)]
+    xs = [rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n) for _ in range(3)]
+    cxs = [small.encrypt(v, L, 10 + i) for i, v in enumerate(xs)]
+    cys = [small.encrypt(v, L, 20 + i) for i, v in enumerate(ys)]
+    s = small.mult_sum(cxs, cys, L)
+    assert np.max(np.abs(small.decrypt(s, L - 1) - sum(a * b for a, b in zip(xs, ys)))) < TOL
+    np.testing.assert_array_equal(small.mult_sum(cxs[:1], cys[:1], L), small.mult(cxs[0], cys[0], L))
+
+
+@pytest.mark.parametrize("hoist", [True, False])
+def test_fused_schedules_keep_the_reference_ledger(golden, hoist):
+    """DiagABT with several block columns (product sums fuse) and DiagATB in
+    both branches: the fused forms keep the reference ledger and values."""
+    rng = np.random.default_rng(4)
+    A, B = rng.uniform(-1, 1, (10, 40)), rng.uniform(-1, 1, (4, 40))
+    ctx = R.OracleCKKSContext("small12", 16, seed=5, hoist=hoist)
+    r = S.diag_abt(S.encode(ctx, A), S.encode(ctx, B, "vertical"), scale=0.5)
+    slot = S.SlotBackend(256, 16, max_level=12)
+    S.diag_abt(S.encode(slot, A), S.encode(slot, B, "vertical"), scale=0.5)
+    assert ctx.ledger.counts() == slot.ledger.counts()
+    assert np.max(np.abs(S.decode(r, tol=1e-3) - 0.5 * A @ B.T)) < 1e-4
+    for branch, alev in (("rl", None), ("pru", 11)):
+        ctx = R.OracleCKKSContext("small12", 16, seed=8, hoist=hoist)
+        r = S.diag_atb(S.encode(ctx, golden["small_atb_A"], "horizontal", level=alev),
+                       S.encode(ctx, golden["small_atb_B"]), scale=2.0)
+        led = np.array([ctx.ledger.counts()[k] for k in OPS])
+        np.testing.assert_array_equal(led, golden[f"small_atb_{branch}_led"])
+        assert np.max(np.abs(S.decode(r, tol=1e-4) - golden[f"small_atb_{branch}_out"])) < 1e-4

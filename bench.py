@@ -439,14 +439,69 @@ def run_train_step(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+def run_softmax(args, world, rank, local):
+    """BASELINE config 3: the encrypted softmax approximation of one 128x16
+    logit block (10 active classes) at N=2^16, the reference's SoftmaxConfig
+    defaults (approx.py:51-57) and per-operand auto-bootstrap (refresh
+    surrogate).  One dependent ciphertext chain: replicas only for N > 1."""
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+    from paper_2403_14111_b200 import workloads as wl
+
+    L = N.lib()
+    Z = wl.config3()
+    ctx = P.CKKSContext("cfg1", 128, seed=3, device=local, auto_bootstrap=True)
+    EZ = P.encode(ctx, Z, "horizontal")
+    nonce0 = ctx.nonce
+
+    def step():
+        ctx.nonce = nonce0   # same refresh nonces every step
+        return P.a_softmax(EZ)
+
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.wait_ready()
+    for _ in range(args.warmup):
+        out = step()
+    ctx.sync()
+    ez = np.exp(Z - Z.max(axis=1, keepdims=True))
+    err = float(np.max(np.abs(P.decode(out, tol=1e-2) - ez / ez.sum(axis=1, keepdims=True))))
+    quiet_gc()
+    c0 = ctx.ledger.counts()
+    launches0 = L.hc_launch_count(ctx._h)
+    barrier(world)
+    ms = C.c_float()
+    N.check(L.hc_timer_begin(ctx._h))
+    for _ in range(args.steps):
+        out = step()
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    barrier(world)
+    clk = clocks.stop()
+    total = all_max(ms.value, world)
+    counts = {k: (v - c0[k]) // args.steps for k, v in ctx.ledger.counts().items()}
+    line = {"metric": "encrypted softmax ms, config 3 (128x16 logits, 10 classes, N=2^16)",
+            "value": total / args.steps, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded U[-128,128] logits, BASELINE config 3)",
+            "config": {"workload": "a_softmax (domain extension R=8 L=2 n=5, a_max, a_exp, a_inv) on one block; "
+                                   "replicas only for N > 1",
+                       "refresh": "surrogate (decrypt/re-encrypt), not CKKS bootstrapping"},
+            "max_abs_err_vs_float64": err, "ledger_per_step": counts,
+            "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="pair", choices=["pair", "train"],
-                    help="pair: DiagABT+DiagATB (BASELINE metric); train: config-4 data-parallel NAG step")
+    ap.add_argument("--workload", default="pair", choices=["pair", "train", "softmax"],
+                    help="pair: DiagABT+DiagATB (BASELINE metric); train: config-4 data-parallel NAG step; "
+                         "softmax: config-3 encrypted softmax")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
@@ -459,6 +514,8 @@ def main():
     world, rank, local = dist_setup(args.gpus)
     if args.workload == "train":
         run_train_step(args, world, rank, local)
+    elif args.workload == "softmax":
+        run_softmax(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
     if world > 1:

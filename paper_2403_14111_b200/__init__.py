@@ -36,12 +36,26 @@ from .encoding import (
 from .errors import (
     DepthExhausted,
     HefitError,
+    ProtocolError,
     ResidualImaginary,
     ShapeMismatch,
     SlotCountMismatch,
     TilingError,
 )
 from .matmul import ALGORITHMS, col_major_abt, count_formula, diag_abt, diag_atb, rotation_steps, row_major_atb
-from .training import TrainState, init_weights, nag_step, one_hot, run_steps
+from .protocol import ChannelEndpoint, channel_pair, pack_matrix, unpack_matrix
+from .training import (
+    Client,
+    FitResult,
+    Server,
+    TrainState,
+    batch_slices,
+    fit,
+    init_weights,
+    log_loss,
+    nag_step,
+    one_hot,
+    run_steps,
+)
 
 __version__ = "0.1.0"

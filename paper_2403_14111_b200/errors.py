@@ -23,3 +23,9 @@ class TilingError(HefitError):
 
 class ResidualImaginary(HefitError):
     code = "encoding.imaginary"
+
+
+class ProtocolError(HefitError):
+    """A channel message could not be parsed or arrived out of order (errors.py:56-59)."""
+
+    code = "protocol.message"

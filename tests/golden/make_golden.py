@@ -147,6 +147,27 @@ def main():
     out["cfg4_led"] = led(c4.ledger.counts())
 
     path = os.path.join(HERE, "hefit_golden.npz")
+    # -- the two-party protocol end to end (training.py:159-338): fit with
+    # validation logits and early stopping on unlearnable labels, so the
+    # run exercises improved / continue / stop decisions (margins >= 4e-3)
+    frng = np.random.default_rng(78)
+
+    def draw(n):
+        y = frng.integers(0, 3, n)
+        x = frng.standard_normal((n, 12))
+        return x / np.linalg.norm(x, axis=1, keepdims=True), y
+
+    fxt, fyt = draw(48)
+    fxv, fyv = draw(16)
+    fctx = EmulatorContext(256, 16, max_level=12, auto_bootstrap=True)
+    fr = training.fit(fxt, fyt, fxv, fyv, 3, ctx=fctx, lr=1.0, batch_size=16, epochs=8, patience=2, seed=1)
+    out["fit_xt"], out["fit_yt"], out["fit_xv"], out["fit_yv"] = fxt, fyt, fxv, fyv
+    out["fit_weights"] = fr.weights
+    out["fit_val_losses"] = np.array(fr.val_losses)
+    out["fit_train_losses"] = np.array(fr.train_losses)
+    out["fit_meta"] = np.array([fr.epochs_run, fr.best_epoch, int(fr.stopped_early)])
+    out["fit_led"] = led(fr.ledger_counts)
+
     np.savez_compressed(path, **out)
     print("wrote", path, "hefit", hefit.__version__, "numpy", np.__version__)
 

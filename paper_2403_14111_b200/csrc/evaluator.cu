@@ -8,6 +8,7 @@
 //   INTT of the P limbs -> ModDown conversion -> NTT -> (acc - conv) * P^-1
 //   with the automorphism's c0 / the tensor's (d0, d1) added in the same pass.
 #include <cmath>
+#include <map>
 
 #include "evaluator.h"
 #include "kernels.cuh"
@@ -556,11 +557,22 @@ std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs, const std::vector<
         return out;
     }
     rec(OP_MULT, (int)xs.size());
+    // level adjustments are deterministic: an operand shared by several
+    // products (DiagATB's B blocks, one per pass) is adjusted once
+    std::map<std::pair<const Ct*, int>, CtP> adj;
+    auto at_once = [&](const CtP& a, int l) {
+        if (a->level == l) return a;
+        auto it = adj.find({a.get(), l});
+        if (it != adj.end()) return it->second;
+        CtP o = at(a, l);
+        adj[{a.get(), l}] = o;
+        return o;
+    };
     std::vector<CtP> ax(xs.size()), ay(xs.size());
     for (size_t i = 0; i < xs.size(); i++) {
         const int l = std::min(xs[i]->level, ys[i]->level);
-        ax[i] = at(xs[i], l);
-        ay[i] = at(ys[i], l);
+        ax[i] = at_once(xs[i], l);
+        ay[i] = at_once(ys[i], l);
     }
     // one fused pipeline per level present
     std::vector<char> done(xs.size(), 0);

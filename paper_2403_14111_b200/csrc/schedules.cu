@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <map>
+
 #include "schedules.h"
 
 namespace hc {
@@ -307,10 +309,31 @@ static G rot_many(Eval& ev, const G& xs, int64_t r, bool add_self = false) {
     return out;
 }
 
-static G mult_many(Eval& ev, const G& xs, const G& ys) {
+static G mult_many(Eval& ev, const G& xs_in, const G& ys_in) {
     Ctx& C = ev.c;
-    const int SB = std::max(1, C.batch), nsub = ((int)xs.size() + SB - 1) / SB;
-    if (nsub <= 1) return ev.mult_batch(xs, ys);
+    const int SB = std::max(1, C.batch), nsub = ((int)xs_in.size() + SB - 1) / SB;
+    if (nsub <= 1) return ev.mult_batch(xs_in, ys_in);
+    // operands shared across sub-batches (DiagATB's B blocks, one use per
+    // pass) are level-adjusted once here, before the fan-out; residues are
+    // those of the per-product adjustment (deterministic)
+    G xs = xs_in, ys = ys_in;
+    bool boot = false;
+    for (size_t i = 0; i < xs.size(); i++) boot |= xs[i]->level < 1 || ys[i]->level < 1;
+    if (!boot) {
+        std::map<std::pair<const Ct*, int>, CtP> adj;
+        auto once = [&](CtP& a, int l) {
+            if (a->level == l) return;
+            auto key = std::make_pair((const Ct*)a.get(), l);
+            auto it = adj.find(key);
+            if (it == adj.end()) it = adj.emplace(key, ev.at(a, l)).first;
+            a = it->second;
+        };
+        for (size_t i = 0; i < xs.size(); i++) {
+            const int l = std::min(xs[i]->level, ys[i]->level);
+            once(xs[i], l);
+            once(ys[i], l);
+        }
+    }
     G out(xs.size());
     par_for(C, nsub, fork_width(C, nsub), [&](int i) {
         const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);

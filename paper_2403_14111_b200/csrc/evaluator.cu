@@ -102,6 +102,20 @@ static void rescale_raw(Ctx& c, const u64* a, int level, int npoly, u64* out) {
     c.free(Y);
 }
 
+// out[b] = rescale of the 2-poly input T + 2 * poly * b (level -> level - 1)
+static void rescale_many(Ctx& c, const u64* T, size_t poly, int level, std::vector<CtP>& out) {
+    const size_t B = out.size();
+    std::vector<const u64*> a(B);
+    std::vector<u64*> o(B);
+    for (size_t b = 0; b < B; b++) {
+        out[b] = new_ct(c, level - 1);
+        a[b] = T + 2 * poly * b;
+        o[b] = out[b]->d;
+    }
+    if (rescale_fused_batch(c, (int)B, a.data(), level, 2, o.data())) return;
+    for (size_t b = 0; b < B; b++) rescale_raw(c, a[b], level, 2, o[b]);
+}
+
 CtP ev_rescale(Ctx& c, const Ct& a) {
     if (a.level < 1) throw Error(-3, "rescale at level 0");
     CtP o = new_ct(c, a.level - 1);
@@ -319,10 +333,7 @@ std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, co
     }
     if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) throw Error(-2, "batched relinearisation");
     c.counts[OP_KS] += (int64_t)B;
-    for (size_t b = 0; b < B; b++) {
-        out[b] = new_ct(c, level - 1);
-        rescale_raw(c, T + 2 * poly * b, level, 2, out[b]->d);
-    }
+    rescale_many(c, T, poly, level, out);
     return out;
 }
 
@@ -401,10 +412,7 @@ std::vector<CtP> ev_mult_sum_batch(Ctx& c, const std::vector<std::vector<std::pa
     } else {
         c.counts[OP_KS] += (int64_t)B;
     }
-    for (size_t b = 0; b < B; b++) {
-        out[b] = new_ct(c, level - 1);
-        rescale_raw(c, T + 2 * poly * b, level, 2, out[b]->d);
-    }
+    rescale_many(c, T, poly, level, out);
     return out;
 }
 
@@ -663,6 +671,27 @@ std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, c
         std::vector<CtP> r = ev_mult_sum_batch(c, groups);
         for (size_t t = 0; t < idx.size(); t++) out[idx[t]] = r[t];
     }
+    return out;
+}
+
+std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs, const std::vector<const Pattern*>& ps) {
+    std::vector<CtP> out(xs.size());
+    bool ok = c.logN >= 14 && xs.size() > 1;
+    for (auto& x : xs) ok = ok && x->level >= 1 && x->level == xs[0]->level;
+    if (!ok) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = mult_p(xs[i], *ps[i]);
+        return out;
+    }
+    rec(OP_CMULT, (int)xs.size());
+    const int level = xs[0]->level;
+    const size_t poly = (size_t)(level + 1) * c.N;
+    Scratch sc(c);
+    u64* T = sc.take(2 * poly * xs.size());
+    for (size_t i = 0; i < xs.size(); i++) {
+        PtP pt = encoded(*ps[i], level);
+        k_elementwise(c, EWP_PT_MUL, T + 2 * poly * i, xs[i]->d, pt->d, nullptr, level + 1, 2, 1);
+    }
+    rescale_many(c, T, poly, level, out);
     return out;
 }
 

@@ -40,6 +40,8 @@ bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int
 // out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
 bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);
+// B rescales of npoly-poly inputs at one level in one pipeline (4 launches)
+bool rescale_fused_batch(Ctx& c, int B, const u64* const* a, int level, int npoly, u64* const* out);
 
 // a plaintext slot pattern with a cache key (content-addressed by the caller).
 // Values are either given (vals) or produced by gen() only on a cache miss,
@@ -99,6 +101,9 @@ struct Eval {
     // (out[x][r]; r = 0 returns x), and add(...add(mult(a0, b0), mult(a1, b1))...)
     // with one relinearisation and rescale per group (separate ops unless
     // every operand is at one level >= 1 and the group has >= 2 products)
+    // mult_p over independent operands (pattern ps[i] for xs[i]) with one
+    // batched rescale; same ledger and residues as the separate calls
+    std::vector<CtP> mult_p_batch(const std::vector<CtP>& xs, const std::vector<const Pattern*>& ps);
     std::vector<std::vector<CtP>> lrot_hoisted(const std::vector<CtP>& xs, const std::vector<int64_t>& rs);
     std::vector<CtP> mult_sum_batch(const std::vector<std::vector<CtP>>& as, const std::vector<std::vector<CtP>>& bs);
     CtP mul_i(const CtP& a);

@@ -309,13 +309,21 @@ struct LdBcast {
     }
 };
 
+// batched rescales (grid z = ciphertext): inputs / outputs per ciphertext
+struct RsBatch {
+    const u64* a[KS_MAXB];
+    u64* out[KS_MAXB];
+};
+
 template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
-            u64* __restrict__ Yt) {
+            u64* __restrict__ Yt, int npoly) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
+    X += (size_t)blockIdx.z * npoly * N;
+    Yt += (size_t)blockIdx.z * npoly * level * N;
     const PrimeDev P = primes[i];
     const u64 q = P.q;
     LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2]};
@@ -345,11 +353,14 @@ struct StRescale {
 };
 
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
-    rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, const u64* __restrict__ a,
-              const u64* __restrict__ tab, u64* __restrict__ out) {
+    rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, RsBatch rb,
+              const u64* __restrict__ tab, int npoly) {
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
+    Yt += (size_t)blockIdx.z * npoly * level * N;
+    const u64* __restrict__ a = rb.a[blockIdx.z];
+    u64* __restrict__ out = rb.out[blockIdx.z];
     const PrimeDev P = primes[i];
     const u64 q = P.q;
     LdPlain ld{Yt + ((size_t)s * level + i) * N};
@@ -628,53 +639,64 @@ bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u
 }
 
 template <int LOGN>
-static void rescale_fused_t(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int npoly, u64* const* out) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     const int N = c.N;
     Scratch sc(c);
-    u64* X = sc.take((size_t)npoly * N);
+    u64* X = sc.take((size_t)B * npoly * N);
     JobList j;
-    j.n = npoly;
-    for (int s = 0; s < npoly; s++) {
-        j.prime[s] = level;
-        j.ptr[s] = X + (size_t)s * N;
-        j.src[s] = a + ((size_t)s * (level + 1) + level) * N;
-    }
+    j.n = B * npoly;
+    for (int b = 0; b < B; b++)
+        for (int s = 0; s < npoly; s++) {
+            j.prime[b * npoly + s] = level;
+            j.ptr[b * npoly + s] = X + ((size_t)b * npoly + s) * N;
+            j.src[b * npoly + s] = a[b] + ((size_t)s * (level + 1) + level) * N;
+        }
     ntt_inverse(c, j);
-    u64* Yt = sc.take((size_t)npoly * level * N);
+    u64* Yt = sc.take((size_t)B * npoly * level * N);
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     const int N1 = N >> CH_LOG;
     {
         static bool at = false;
         set_smem(rs_cols<CL, CS>, csm, at);
-        Launch scope(c, "rs_cols", 8.0 * N * npoly * (1.0 + level));
-        dim3 grid((N >> CL) / CS, npoly * level);
+        Launch scope(c, "rs_cols", 8.0 * N * B * npoly * (1.0 + level));
+        dim3 grid((N >> CL) / CS, npoly * level, B);
         rs_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), X,
-                                                              tab, Yt);
+                                                              tab, Yt, npoly);
         HC_CUDA(cudaGetLastError());
     }
     {
         static bool at = false;
         set_smem(rs_chunks, hsm, at);
-        Launch scope(c, "rs_chunks", 8.0 * N * npoly * 3.0 * level);
-        dim3 grid((N >> CH_LOG) / CH_SUBS, npoly * level);
-        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), Yt, a, tab,
-                                                        out);
+        RsBatch rb;
+        for (int b = 0; b < B; b++) { rb.a[b] = a[b]; rb.out[b] = out[b]; }
+        Launch scope(c, "rs_chunks", 8.0 * N * B * npoly * 3.0 * level);
+        dim3 grid((N >> CH_LOG) / CH_SUBS, npoly * level, B);
+        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), Yt, rb, tab,
+                                                        npoly);
         HC_CUDA(cudaGetLastError());
     }
 }
 
-bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out) {
-    switch (c.logN) {
-        case 14: rescale_fused_t<14>(c, a, level, npoly, out); return true;
-        case 15: rescale_fused_t<15>(c, a, level, npoly, out); return true;
-        case 16: rescale_fused_t<16>(c, a, level, npoly, out); return true;
-        case 17: rescale_fused_t<17>(c, a, level, npoly, out); return true;
-        default: return false;
+bool rescale_fused_batch(Ctx& c, int B, const u64* const* a, int level, int npoly, u64* const* out) {
+    if (c.logN < 14 || c.logN > 17) return false;
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        switch (c.logN) {
+            case 14: rescale_fused_t<14>(c, nb, a + b0, level, npoly, out + b0); break;
+            case 15: rescale_fused_t<15>(c, nb, a + b0, level, npoly, out + b0); break;
+            case 16: rescale_fused_t<16>(c, nb, a + b0, level, npoly, out + b0); break;
+            default: rescale_fused_t<17>(c, nb, a + b0, level, npoly, out + b0); break;
+        }
     }
+    return true;
+}
+
+bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out) {
+    return rescale_fused_batch(c, 1, &a, level, npoly, &out);
 }
 
 }  // namespace hc

@@ -402,12 +402,18 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     }
     for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, 1 << t, true);
     const Pattern c0 = col0(g);
-    for (auto& a : acc) a = ev.mult_p(a, c0);
+    acc = ev.mult_p_batch(acc, std::vector<const Pattern*>(acc.size(), &c0));
     for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, -(1 << t), true);
     std::vector<G> terms(K, G(m));
-    for (int k = 0; k < K; k++) {
-        const Pattern mask = diag_mask(g, k, c, true, scale);
-        for (int p = 0; p < m; p++) terms[k][p] = ev.mult_p(acc[(size_t)k * m + p], mask);
+    {
+        std::vector<Pattern> masks;
+        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, k, c, true, scale));
+        std::vector<const Pattern*> ps;
+        for (int k = 0; k < K; k++)
+            for (int p = 0; p < m; p++) ps.push_back(&masks[k]);
+        G t = ev.mult_p_batch(acc, ps);
+        for (int k = 0; k < K; k++)
+            for (int p = 0; p < m; p++) terms[k][p] = t[(size_t)k * m + p];
     }
     G out = terms[0];
     for (int k = 1; k < K; k++)
@@ -465,20 +471,34 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     if (partial) {
         for (int k = 0; k < K; k++) left[k] = ev.c.hoist ? first[k] : ev.lrot_batch(packed, k);
     } else {
-        std::vector<G> heads(K), tails(K);
+        // RL per pass (encoding.py:291-311): head = lrot(packed, k) * keep_k,
+        // tail = lrot - head, left = head + rrot(tail, s1); the keep masks of
+        // every pass in one batch, the rrot(s1) of every tail in one batch
         std::vector<int> moving;
         for (int k = 0; k < K; k++) {
-            if (k % s1 == 0) { left[k] = packed; continue; }
-            rot_left_split(ev, packed, k % s1, g, heads[k], tails[k], ev.c.hoist ? &first[k] : nullptr);
-            moving.push_back(k);
+            if (k % s1 == 0) left[k] = packed;
+            else moving.push_back(k);
         }
-        std::vector<G> tparts;
-        for (int k : moving) tparts.push_back(tails[k]);
-        G back = rot_many(ev, concat(tparts), -(int64_t)s1);
+        std::vector<Pattern> keeps;
+        for (int k : moving) keeps.push_back(keep_head(g, s1 - k % s1));
+        G a1s;
+        std::vector<const Pattern*> ps;
+        for (size_t u = 0; u < moving.size(); u++) {
+            const int k = moving[u];
+            const G a1 = ev.c.hoist ? first[k] : ev.lrot_batch(packed, k % s1);
+            for (int p = 0; p < m; p++) {
+                a1s.push_back(a1[p]);
+                ps.push_back(&keeps[u]);
+            }
+        }
+        G heads = ev.mult_p_batch(a1s, ps);
+        G tails(a1s.size());
+        for (size_t i = 0; i < a1s.size(); i++) tails[i] = ev.sub(a1s[i], heads[i]);
+        G back = rot_many(ev, tails, -(int64_t)s1);
         size_t o = 0;
         for (int k : moving) {
             left[k].resize(m);
-            for (int p = 0; p < m; p++) left[k][p] = ev.add(heads[k][p], back[o++]);
+            for (int p = 0; p < m; p++, o++) left[k][p] = ev.add(heads[o], back[o]);
         }
     }
     // right operands: B, or PRU(B, k) on the partial branch (all lrot(s1) in one batch)
@@ -529,9 +549,15 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     }
     for (int t = 0; t < ilog2(g.s0); t++) acc = rot_many(ev, acc, (int64_t)(1 << t) * s1, true);
     std::vector<G> terms(K, G(n));
-    for (int k = 0; k < K; k++) {
-        const Pattern mask = diag_mask(g, -k, c, true, scale);
-        for (int q = 0; q < n; q++) terms[k][q] = ev.mult_p(acc[(size_t)k * n + q], mask);
+    {
+        std::vector<Pattern> masks;
+        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, -k, c, true, scale));
+        std::vector<const Pattern*> ps;
+        for (int k = 0; k < K; k++)
+            for (int q = 0; q < n; q++) ps.push_back(&masks[k]);
+        G t = ev.mult_p_batch(acc, ps);
+        for (int k = 0; k < K; k++)
+            for (int q = 0; q < n; q++) terms[k][q] = t[(size_t)k * n + q];
     }
     G out = terms[0];
     for (int k = 1; k < K; k++)

@@ -79,6 +79,14 @@ int hc_ct_level(const hc_ct *ct);
 int hc_ct_download(const hc_ct *ct, uint64_t *out);
 int hc_ct_upload(hc_ctx *ctx, const uint64_t *in, int level, hc_ct **out);
 int hc_ct_device_ptr(const hc_ct *ct, uint64_t **dptr);
+/* Asynchronous transfers for serving loops: the copy runs on the context's
+ * copy stream and overlaps compute.  An upload returns at once; every op
+ * issued afterwards sees the data (the context stream waits for the copy).
+ * A download is ordered after all work issued so far and completes by the
+ * next hc_sync / hc_timer_end; `in` / `out` must stay valid (pinned host
+ * memory for full overlap) until then. */
+int hc_ct_upload_async(hc_ctx *ctx, const uint64_t *in, int level, hc_ct **out);
+int hc_ct_download_async(const hc_ct *ct, uint64_t *out);
 
 /* plaintexts: encoded at scales[level] in NTT form */
 int hc_pt_free(hc_pt *pt);

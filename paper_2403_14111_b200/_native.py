@@ -42,6 +42,8 @@ SIGNATURES = {
     "hc_set_auto_bootstrap": (I, [P, I]),
     "hc_set_streams": (I, [P, I]),
     "hc_set_hoist": (I, [P, I]),
+    "hc_ct_upload_async": (I, [P, U64P, I, PP]),
+    "hc_ct_download_async": (I, [P, U64P]),
     "hc_ctx_counts": (I, [P, I64P, I]),
     "hc_ctx_nonce": (I, [P, U64P, U64P]),
     "hc_sync": (I, [P]),

@@ -121,7 +121,38 @@ int hc_ctx_nonce(hc_ctx* ctx, uint64_t* get, const uint64_t* set) {
     return 0;
 }
 
-int hc_sync(hc_ctx* ctx) { return guard([&] { HC_CUDA(cudaStreamSynchronize(ctx->c->stream)); }); }
+static void io_drain(hc::Ctx& c) {
+    if (!c.copy_stream) return;
+    HC_CUDA(cudaStreamSynchronize(c.copy_stream));
+    HC_CUDA(cudaStreamSynchronize(c.d2h_stream));
+    c.io_pending.clear();
+}
+
+// make the context stream wait for every transfer issued so far
+static void io_join(hc::Ctx& c) {
+    if (!c.copy_stream) return;
+    for (cudaStream_t s : {c.copy_stream, c.d2h_stream}) {
+        cudaEvent_t e = c.get_event();
+        HC_CUDA(cudaEventRecord(e, s));
+        HC_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+        c.ev_free.push_back(e);
+    }
+}
+
+static void io_stream(hc::Ctx& c) {
+    if (!c.copy_stream) {
+        HC_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        HC_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
+    }
+}
+
+int hc_sync(hc_ctx* ctx) {
+    return guard([&] {
+        io_join(*ctx->c);
+        HC_CUDA(cudaStreamSynchronize(ctx->c->stream));
+        io_drain(*ctx->c);
+    });
+}
 
 int hc_keygen(hc_ctx* ctx, int g) { return guard([&] { hc::get_key(*ctx->c, g); }); }
 
@@ -159,6 +190,44 @@ int hc_ct_upload(hc_ctx* ctx, const uint64_t* in, int level, hc_ct** out) {
         HC_CUDA(cudaMemcpyAsync(p->d, in, p->words() * 8, cudaMemcpyHostToDevice, c.stream));
         HC_CUDA(cudaStreamSynchronize(c.stream));
         *out = wrap(p);
+    });
+}
+
+int hc_ct_upload_async(hc_ctx* ctx, const uint64_t* in, int level, hc_ct** out) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (level < 0 || level > c.L) throw hc::Error(HC_EPARAM, "level out of range");
+        io_stream(c);
+        // allocated on the copy stream, so the copy does not queue behind compute
+        cudaStream_t saved = c.stream;
+        c.stream = c.copy_stream;
+        hc::CtP p;
+        try {
+            p = hc::new_ct(c, level);
+        } catch (...) {
+            c.stream = saved;
+            throw;
+        }
+        c.stream = saved;
+        HC_CUDA(cudaMemcpyAsync(p->d, in, p->words() * 8, cudaMemcpyHostToDevice, c.copy_stream));
+        cudaEvent_t e = c.get_event();
+        HC_CUDA(cudaEventRecord(e, c.copy_stream));
+        HC_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+        c.ev_free.push_back(e);
+        *out = wrap(p);
+    });
+}
+
+int hc_ct_download_async(const hc_ct* ct, uint64_t* out) {
+    return guard([&] {
+        hc::Ctx& c = *ct->p->ctx;
+        io_stream(c);
+        cudaEvent_t e = c.get_event();
+        HC_CUDA(cudaEventRecord(e, c.stream));
+        HC_CUDA(cudaStreamWaitEvent(c.d2h_stream, e, 0));
+        c.ev_free.push_back(e);
+        HC_CUDA(cudaMemcpyAsync(out, ct->p->d, ct->p->words() * 8, cudaMemcpyDeviceToHost, c.d2h_stream));
+        c.io_pending.push_back(ct->p);
     });
 }
 
@@ -308,9 +377,11 @@ int hc_timer_begin(hc_ctx* ctx) {
 int hc_timer_end(hc_ctx* ctx, float* ms) {
     return guard([&] {
         hc::Ctx& c = *ctx->c;
+        io_join(c);   // pending downloads are inside the timed region
         HC_CUDA(cudaEventRecord(c.t1, c.stream));
         HC_CUDA(cudaEventSynchronize(c.t1));
         HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
+        io_drain(c);
     });
 }
 

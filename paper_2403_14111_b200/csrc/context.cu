@@ -433,6 +433,9 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
 
 void ctx_destroy(Ctx* c) {
     if (!c) return;
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
+    c->io_pending.clear();
     cudaStreamSynchronize(c->stream);
     for (auto& kv : c->arenas) cudaFree(kv.second.base);
     for (auto* p : c->arena_graveyard) cudaFree(p);

@@ -105,6 +105,12 @@ struct Ctx {
     int ra_idx = 0;                   // waits for the one ra_depth calls back to finish
     int ra_depth = 8;                 // HC_RUNAHEAD (2 measured host-jitter-bound steps)
     cudaMemPool_t pool = nullptr;
+    // host <-> device transfers of the asynchronous C-ABI (hc_ct_upload_async /
+    // hc_ct_download_async) run on their own stream, overlapping compute;
+    // ciphertexts being downloaded stay alive until hc_sync / hc_timer_end
+    cudaStream_t copy_stream = nullptr;   // uploads
+    cudaStream_t d2h_stream = nullptr;    // downloads (a download waits for compute; uploads must not queue behind it)
+    std::vector<std::shared_ptr<struct Ct>> io_pending;
     PrimeHost pr[MAXP];
     double scale[MAXP];
     // device tables

@@ -52,3 +52,28 @@ def test_fit_matches_reference_run(golden):
     np.testing.assert_allclose(r.weights, golden["fit_weights"], atol=1e-3)
     assert g.decodes_by("server") == []
     assert len(g.decodes_by("client")) == r.epochs_run + 1
+
+
+def test_async_transfers_match_sync_path():
+    """hc_ct_upload_async / hc_ct_download_async (copy streams) give the
+    residues of the synchronous path, with work issued in between."""
+    import ctypes as C
+
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+    g = P.CKKSContext("small12", 16, seed=41)
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, g.slot_count)
+    ct = g.encrypt(x)
+    res = np.ascontiguousarray(ct.residues())
+    L = N.lib()
+    h = C.c_void_p()
+    N.check(L.hc_ct_upload_async(g._h, res.ctypes.data_as(N.U64P), ct.level, C.byref(h)))
+    up = P.Ciphertext(g, h)
+    sq = g.mult(up, up)
+    out = np.zeros((2, sq.level + 1, g.N), np.uint64)
+    N.check(L.hc_ct_download_async(sq._h, out.ctypes.data_as(N.U64P)))
+    ref = g.mult(ct, ct)
+    g.sync()
+    np.testing.assert_array_equal(out, ref.residues())
+    np.testing.assert_array_equal(up.residues(), res)

@@ -435,6 +435,14 @@ def run_train_step(args, world, rank, local):
     clk = clocks.stop()
     total = all_max(ms.value, world)
     counts = {k: (v - c0[k]) // args.steps for k, v in ctx.ledger.counts().items()}
+    # one profiled step (kernel time per kernel, streams serialised)
+    ctx.set_streams(1)
+    N.check(L.hc_prof_begin(ctx._h))
+    step()
+    buf = C.create_string_buffer(1 << 16)
+    N.check(L.hc_prof_end(ctx._h, buf, len(buf)))
+    prof = json.loads(buf.value.decode())
+    ctx.set_streams(8)
     hbm, _ = peaks()
     line = {"metric": "NAG training step ms, config 4 (1024 rows x 768, 10 classes, N=2^16)",
             "value": total / args.steps, "unit": "ms", "n_gpus": world, "steps": args.steps,
@@ -445,6 +453,7 @@ def run_train_step(args, world, rank, local):
                                    "DiagATB with cross-rank mod-sum, NAG update, refresh)",
                        "rows": int(X.shape[0]), "block_rows_per_rank": len(sharding.partition(8, world, rank))},
             "ledger_per_step": counts, "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0),
+            "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)

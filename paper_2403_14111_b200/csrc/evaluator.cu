@@ -556,13 +556,20 @@ std::vector<CtP> Eval::conj_batch(const std::vector<CtP>& xs) {
     return ev_automorph_batch(c, a, 2 * (u64)c.N - 1, false);
 }
 
-std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys) {
-    bool boot = false;
-    for (size_t i = 0; i < xs.size(); i++) boot |= xs[i]->level < 1 || ys[i]->level < 1;
+std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs_in, const std::vector<CtP>& ys_in) {
+    std::vector<CtP> xs = xs_in, ys = ys_in;
     std::vector<CtP> out(xs.size());
-    if (boot) {   // refreshes: the reference's op-by-op order fixes their nonces
-        for (size_t i = 0; i < xs.size(); i++) out[i] = mult(xs[i], ys[i]);
-        return out;
+    // per-operand auto-bootstrap (emulator.py:218-221) in the reference's
+    // op-by-op order -- x before y, product by product -- so every refresh
+    // draws the nonce the sequential order gives it; then one batch
+    for (size_t i = 0; i < xs.size(); i++) {
+        const int r = (xs[i]->level < 1 ? 1 : 0) + (ys[i]->level < 1 ? 1 : 0);
+        if (!r) continue;
+        if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
+        int j = 0;
+        if (xs[i]->level < 1) xs[i] = refresh_planned(xs[i], j++, r);
+        if (ys[i]->level < 1) ys[i] = refresh_planned(ys[i], j++, r);
+        plan.events += r;
     }
     rec(OP_MULT, (int)xs.size());
     // level adjustments are deterministic: an operand shared by several
@@ -671,6 +678,28 @@ std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, c
         std::vector<CtP> r = ev_mult_sum_batch(c, groups);
         for (size_t t = 0; t < idx.size(); t++) out[idx[t]] = r[t];
     }
+    return out;
+}
+
+std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs, std::complex<double> s) {
+    std::vector<CtP> out(xs.size());
+    bool ok = c.logN >= 14 && xs.size() > 1;
+    for (auto& x : xs) ok = ok && x->level >= 1 && x->level == xs[0]->level;
+    if (!ok) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = mult_c(xs[i], s);
+        return out;
+    }
+    rec(OP_CMULT, (int)xs.size());
+    const int level = xs[0]->level;
+    const size_t poly = (size_t)(level + 1) * c.N;
+    const double sc = c.scale[level];
+    ConstTab t;
+    const_pairs(c, std::llrint(s.real() * sc), std::llrint(s.imag() * sc), level + 1, t);
+    Scratch scr(c);
+    u64* T = scr.take(2 * poly * xs.size());
+    for (size_t i = 0; i < xs.size(); i++)
+        k_elementwise(c, EWP_CONST_MUL, T + 2 * poly * i, xs[i]->d, nullptr, &t, level + 1, 2, 0);
+    rescale_many(c, T, poly, level, out);
     return out;
 }
 

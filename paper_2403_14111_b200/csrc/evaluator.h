@@ -104,6 +104,8 @@ struct Eval {
     // mult_p over independent operands (pattern ps[i] for xs[i]) with one
     // batched rescale; same ledger and residues as the separate calls
     std::vector<CtP> mult_p_batch(const std::vector<CtP>& xs, const std::vector<const Pattern*>& ps);
+    // mult_c over independent operands by one scalar, one batched rescale
+    std::vector<CtP> mult_c_batch(const std::vector<CtP>& xs, std::complex<double> s);
     std::vector<std::vector<CtP>> lrot_hoisted(const std::vector<CtP>& xs, const std::vector<int64_t>& rs);
     std::vector<CtP> mult_sum_batch(const std::vector<std::vector<CtP>>& as, const std::vector<std::vector<CtP>>& bs);
     CtP mul_i(const CtP& a);

@@ -799,11 +799,9 @@ struct SM {
     Geo g;
     int classes, period;
 
-    G scale(const G& x, double t) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult_c(x[i], t);
-        return o;
-    }
+    // the products run as batches over the blocks (one key-switch /
+    // rescale pipeline per op); refreshes keep the block-by-block order
+    G scale(const G& x, double t) { return ev.mult_c_batch(x, t); }
     G addc(const G& x, double s) {
         G o(x.size());
         for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_c(x[i], s);
@@ -829,21 +827,9 @@ struct SM {
         for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_p(x[i], p, true, false);
         return o;
     }
-    G mul(const G& x, const G& y) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult(x[i], y[i]);
-        return o;
-    }
-    G mulp(const G& x, const Pattern& p) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.mult_p(x[i], p);
-        return o;
-    }
-    G lrot(const G& x, int r) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.lrot(x[i], r);
-        return o;
-    }
+    G mul(const G& x, const G& y) { return ev.mult_batch(x, y); }
+    G mulp(const G& x, const Pattern& p) { return ev.mult_p_batch(x, std::vector<const Pattern*>(x.size(), &p)); }
+    G lrot(const G& x, int r) { return ev.lrot_batch(x, r); }
     G rrot(const G& x, int r) {
         G o(x.size());
         for (size_t i = 0; i < x.size(); i++) o[i] = ev.rrot(x[i], r);
@@ -886,8 +872,7 @@ struct SM {
             best = add(x1, x3);
         }
         best = mulp(best, col0(g));
-        for (int t = 0; t < ilog2(g.s1); t++)
-            for (auto& b : best) b = ev.add_rrot(b, 1 << t);
+        for (int t = 0; t < ilog2(g.s1); t++) best = ev.lrot_batch(best, -(1 << t), true);
         return scale(best, two_r);
     }
     G domain_extend(G M, const SoftmaxCfg& cfg) {
@@ -953,7 +938,9 @@ std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes,
     const int m = (int)M.size();
     bool uniform = m > 1 && !ev.plan.on;
     for (auto& b : M) uniform = uniform && b->level == M[0]->level;
-    if (!uniform || ev.c.fork_cap <= 1) return softmax_serial(ev, M, classes, period, cfg);
+    // lockstep (default): the blocks advance op by op, each op one batch --
+    // the reference's own order, so refreshes draw the sequential nonces
+    if (!uniform || ev.c.fork_cap <= 1 || ev.c.lockstep) return softmax_serial(ev, M, classes, period, cfg);
     // Block rows are independent: one branch per block row, each with the
     // nonce plan that reproduces the sequential (block-interleaved) order.
     u64 base;
@@ -992,12 +979,15 @@ static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int 
     if (cfg.precise) norm = sm.dep_comp(norm, cfg);
     G e = sm.exp(norm, cfg);
     G expd = sm.mulp(e, keep);
-    G total = col_sums(ev, expd, (int)expd.size(), 1, g);
+    // col_sums of every block (encoding.py:335-360) in lockstep
+    G total = expd;
+    for (int t = 0; t < ilog2(g.s1); t++) total = ev.lrot_batch(total, 1 << t, true);
+    total = sm.mulp(total, col0(g));
+    for (int t = 0; t < ilog2(g.s1); t++) total = ev.lrot_batch(total, -(1 << t), true);
     G recip = sm.inv(total, cfg);
     G out = sm.mul(expd, recip);
     const int reps = g.s1 / period;
-    for (int t = 0; t < ilog2(reps); t++)
-        for (auto& b : out) b = ev.add_rrot(b, period * (1 << t));
+    for (int t = 0; t < ilog2(reps); t++) out = ev.lrot_batch(out, -(int64_t)period * (1 << t), true);
     return out;
 }
 

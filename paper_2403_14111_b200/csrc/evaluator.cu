@@ -326,11 +326,16 @@ std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, co
     u64* D = sc.take(3 * poly * B);
     u64* T = sc.take(2 * poly * B);
     std::vector<KsIn> in(B);
+    std::vector<u64*> dd(B);
+    std::vector<const u64*> aa(B), bb(B);
     for (size_t b = 0; b < B; b++) {
         u64* Db = D + 3 * poly * b;
-        k_tensor(c, Db, ab[b].first->d, ab[b].second->d, nl);
+        dd[b] = Db;
+        aa[b] = ab[b].first->d;
+        bb[b] = ab[b].second->d;
         in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
     }
+    k_tensor_batch(c, (int)B, dd.data(), aa.data(), bb.data(), nl);
     if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) throw Error(-2, "batched relinearisation");
     c.counts[OP_KS] += (int64_t)B;
     rescale_many(c, T, poly, level, out);
@@ -678,6 +683,80 @@ std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, c
         std::vector<CtP> r = ev_mult_sum_batch(c, groups);
         for (size_t t = 0; t < idx.size(); t++) out[idx[t]] = r[t];
     }
+    return out;
+}
+
+// ---- batched element-wise ops (one launch over the blocks of a lockstep op)
+
+std::vector<CtP> Eval::add_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys, bool sub) {
+    std::vector<CtP> out(xs.size());
+    bool ok = xs.size() > 1;
+    for (size_t i = 0; ok && i < xs.size(); i++) ok = xs[i]->level == xs[0]->level && ys[i]->level == xs[0]->level;
+    if (!ok) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = add(xs[i], ys[i], sub);
+        return out;
+    }
+    rec(OP_ADD, (int)xs.size());
+    const int level = xs[0]->level;
+    std::vector<u64*> o(xs.size());
+    std::vector<const u64*> a(xs.size()), b(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) {
+        out[i] = new_ct(c, level);
+        o[i] = out[i]->d;
+        a[i] = xs[i]->d;
+        b[i] = ys[i]->d;
+    }
+    k_elementwise_batch(c, sub ? EWP_SUB : EWP_ADD, (int)xs.size(), o.data(), a.data(), b.data(), nullptr, level + 1,
+                        2, 2);
+    return out;
+}
+
+std::vector<CtP> Eval::add_c_batch(const std::vector<CtP>& xs, std::complex<double> s, bool sub, bool reversed) {
+    std::vector<CtP> out(xs.size());
+    bool ok = xs.size() > 1;
+    for (auto& x : xs) ok = ok && x->level == xs[0]->level;
+    if (!ok) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = add_c(xs[i], s, sub, reversed);
+        return out;
+    }
+    rec(OP_ADD, (int)xs.size());
+    const int level = xs[0]->level;
+    if (!reversed && sub) s = -s;
+    const double sc = c.scale[level];
+    ConstTab t;
+    const_pairs(c, std::llrint(s.real() * sc), std::llrint(s.imag() * sc), level + 1, t);
+    std::vector<u64*> o(xs.size());
+    std::vector<const u64*> a(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) {
+        out[i] = new_ct(c, level);
+        o[i] = out[i]->d;
+        a[i] = xs[i]->d;
+    }
+    k_elementwise_batch(c, reversed ? EWP_CONST_RADD : EWP_CONST_ADD, (int)xs.size(), o.data(), a.data(), nullptr,
+                        &t, level + 1, 2, 0);
+    return out;
+}
+
+std::vector<CtP> Eval::add_p_batch(const std::vector<CtP>& xs, const Pattern& p, bool sub, bool reversed) {
+    std::vector<CtP> out(xs.size());
+    bool ok = xs.size() > 1;
+    for (auto& x : xs) ok = ok && x->level == xs[0]->level;
+    if (!ok) {
+        for (size_t i = 0; i < xs.size(); i++) out[i] = add_p(xs[i], p, sub, reversed);
+        return out;
+    }
+    rec(OP_ADD, (int)xs.size());
+    const int level = xs[0]->level;
+    PtP pt = encoded(p, level);
+    std::vector<u64*> o(xs.size());
+    std::vector<const u64*> a(xs.size()), b(xs.size(), pt->d);
+    for (size_t i = 0; i < xs.size(); i++) {
+        out[i] = new_ct(c, level);
+        o[i] = out[i]->d;
+        a[i] = xs[i]->d;
+    }
+    const int op = reversed ? EWP_PT_RSUB : (sub ? EWP_PT_SUB : EWP_PT_ADD);
+    k_elementwise_batch(c, op, (int)xs.size(), o.data(), a.data(), b.data(), nullptr, level + 1, 2, 1);
     return out;
 }
 

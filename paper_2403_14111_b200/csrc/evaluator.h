@@ -104,6 +104,13 @@ struct Eval {
     // mult_p over independent operands (pattern ps[i] for xs[i]) with one
     // batched rescale; same ledger and residues as the separate calls
     std::vector<CtP> mult_p_batch(const std::vector<CtP>& xs, const std::vector<const Pattern*>& ps);
+    // add / sub, + - scalar, + - plaintext over independent operands at one
+    // level: one launch (the separate ops otherwise); same ledger and residues
+    std::vector<CtP> add_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys, bool sub = false);
+    std::vector<CtP> add_c_batch(const std::vector<CtP>& xs, std::complex<double> s, bool sub = false,
+                                 bool reversed = false);
+    std::vector<CtP> add_p_batch(const std::vector<CtP>& xs, const Pattern& p, bool sub = false,
+                                 bool reversed = false);
     // mult_c over independent operands by one scalar, one batched rescale
     std::vector<CtP> mult_c_batch(const std::vector<CtP>& xs, std::complex<double> s);
     std::vector<std::vector<CtP>> lrot_hoisted(const std::vector<CtP>& xs, const std::vector<int64_t>& rs);

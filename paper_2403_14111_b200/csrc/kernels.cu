@@ -5,6 +5,8 @@
 // accesses) and use a grid sized in multiples of the SM count; they are
 // HBM-bound by construction.  Base conversion (ModUp / ModDown) and the key
 // inner product are the integer-heavy parts of key switching.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace hc {
@@ -22,11 +24,18 @@ static inline int nblocks(size_t work, int threads) {
 enum EwOp { EW_ADD, EW_SUB, EW_NEG, EW_PT_ADD, EW_PT_SUB, EW_PT_RSUB, EW_PT_MUL, EW_CONST_MUL, EW_CONST_ADD,
             EW_CONST_RADD };
 
-// consts: per limb {lo, lo_shoup, hi, hi_shoup}
-__global__ void ew_kernel(int op, u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ b,
-                          const ConstTab consts, const PrimeDev* __restrict__ primes, int nl, int npoly,
-                          int N, int bpoly) {
+// consts: per limb {lo, lo_shoup, hi, hi_shoup}; grid z = ciphertext of a batch
+struct EwPtrs {
+    u64* out[KS_MAXB];
+    const u64* a[KS_MAXB];
+    const u64* b[KS_MAXB];
+};
+__global__ void ew_kernel(int op, EwPtrs ptr, const ConstTab consts, const PrimeDev* __restrict__ primes, int nl,
+                          int npoly, int N, int bpoly) {
     // grid.y = poly * nl + limb: no integer division on the hot path
+    u64* __restrict__ out = ptr.out[blockIdx.z];
+    const u64* __restrict__ a = ptr.a[blockIdx.z];
+    const u64* __restrict__ b = ptr.b[blockIdx.z];
     const size_t half = (size_t)N / 2;
     const int limb = blockIdx.y % nl;
     const int s = blockIdx.y / nl;
@@ -83,25 +92,39 @@ __global__ void ew_kernel(int op, u64* __restrict__ out, const u64* __restrict__
     }
 }
 
-void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const ConstTab* consts, int nl, int npoly,
-                   int bpoly) {
-    const size_t work = (size_t)npoly * nl * c.N / 2;
+void k_elementwise_batch(Ctx& c, int op, int B, u64* const* out, const u64* const* a, const u64* const* b,
+                         const ConstTab* consts, int nl, int npoly, int bpoly) {
     static const ConstTab zero = {};
     const bool pt_b = op >= EW_PT_ADD && op <= EW_PT_MUL;
     const double rd = (double)npoly * nl + (pt_b ? nl : (op <= EW_SUB ? bpoly * nl : 0));
-    Launch scope(c, "elementwise", 8.0 * c.N * (rd + (double)npoly * nl));
-    (void)work;
-    dim3 grid((unsigned)((c.N / 2 + 255) / 256), (unsigned)(npoly * nl));
-    ew_kernel<<<grid, 256, 0, c.stream>>>(op, out, a, b, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
-    HC_CUDA(cudaGetLastError());
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        EwPtrs p;
+        for (int i = 0; i < nb; i++) {
+            p.out[i] = out[b0 + i];
+            p.a[i] = a[b0 + i];
+            p.b[i] = b ? b[b0 + i] : nullptr;
+        }
+        Launch scope(c, "elementwise", 8.0 * c.N * nb * (rd + (double)npoly * nl));
+        dim3 grid((unsigned)((c.N / 2 + 255) / 256), (unsigned)(npoly * nl), nb);
+        ew_kernel<<<grid, 256, 0, c.stream>>>(op, p, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
+        HC_CUDA(cudaGetLastError());
+    }
+}
+
+void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const ConstTab* consts, int nl, int npoly,
+                   int bpoly) {
+    k_elementwise_batch(c, op, 1, &out, &a, b ? &b : nullptr, consts, nl, npoly, bpoly);
 }
 
 // ---------------------------------------------------------------------------
 // tensor product: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
 // ---------------------------------------------------------------------------
 
-__global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, const u64* __restrict__ b,
-                              const PrimeDev* __restrict__ primes, int nl, int N) {
+__global__ void tensor_kernel(EwPtrs ptr, const PrimeDev* __restrict__ primes, int nl, int N) {
+    u64* __restrict__ d = ptr.out[blockIdx.y];
+    const u64* __restrict__ a = ptr.a[blockIdx.y];
+    const u64* __restrict__ b = ptr.b[blockIdx.y];
     const size_t poly = (size_t)nl * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
@@ -115,11 +138,23 @@ __global__ void tensor_kernel(u64* __restrict__ d, const u64* __restrict__ a, co
     }
 }
 
-void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl) {
-    Launch scope(c, "tensor", 8.0 * c.N * 7 * nl);
-    tensor_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(d, a, b, c.d_primes, nl, c.N);
-    HC_CUDA(cudaGetLastError());
+void k_tensor_batch(Ctx& c, int B, u64* const* d, const u64* const* a, const u64* const* b, int nl) {
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        EwPtrs p;
+        for (int i = 0; i < nb; i++) {
+            p.out[i] = d[b0 + i];
+            p.a[i] = a[b0 + i];
+            p.b[i] = b[b0 + i];
+        }
+        Launch scope(c, "tensor", 8.0 * c.N * 7 * nl * nb);
+        dim3 grid((unsigned)std::max(1, nblocks((size_t)nl * c.N, 256) / nb), nb);
+        tensor_kernel<<<grid, 256, 0, c.stream>>>(p, c.d_primes, nl, c.N);
+        HC_CUDA(cudaGetLastError());
+    }
 }
+
+void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl) { k_tensor_batch(c, 1, &d, &a, &b, nl); }
 
 // sum of n tensor products (fused product sums): each
 // component accumulated in 128 bits (at most 2 * TS_MAXN products of

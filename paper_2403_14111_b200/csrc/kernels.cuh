@@ -13,6 +13,10 @@ struct ConstTab {
 void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const ConstTab* consts, int nl, int npoly,
                    int bpoly);
 void k_tensor(Ctx& c, u64* d, const u64* a, const u64* b, int nl);
+void k_tensor_batch(Ctx& c, int B, u64* const* d, const u64* const* a, const u64* const* b, int nl);
+// the element-wise op over B ciphertexts (b may be null when unused)
+void k_elementwise_batch(Ctx& c, int op, int B, u64* const* out, const u64* const* a, const u64* const* b,
+                         const ConstTab* consts, int nl, int npoly, int bpoly);
 // d = sum_q tensor(a[q], b[q]), n <= 8
 void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int n, int nl);
 void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g);

@@ -802,31 +802,11 @@ struct SM {
     // the products run as batches over the blocks (one key-switch /
     // rescale pipeline per op); refreshes keep the block-by-block order
     G scale(const G& x, double t) { return ev.mult_c_batch(x, t); }
-    G addc(const G& x, double s) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_c(x[i], s);
-        return o;
-    }
-    G rsubc(const G& x, double s) {   // s - x
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_c(x[i], s, false, true);
-        return o;
-    }
-    G add(const G& x, const G& y) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add(x[i], y[i]);
-        return o;
-    }
-    G sub(const G& x, const G& y) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.sub(x[i], y[i]);
-        return o;
-    }
-    G subp(const G& x, const Pattern& p) {
-        G o(x.size());
-        for (size_t i = 0; i < x.size(); i++) o[i] = ev.add_p(x[i], p, true, false);
-        return o;
-    }
+    G addc(const G& x, double s) { return ev.add_c_batch(x, s); }
+    G rsubc(const G& x, double s) { return ev.add_c_batch(x, s, false, true); }   // s - x
+    G add(const G& x, const G& y) { return ev.add_batch(x, y); }
+    G sub(const G& x, const G& y) { return ev.add_batch(x, y, true); }
+    G subp(const G& x, const Pattern& p) { return ev.add_p_batch(x, p, true, false); }
     G mul(const G& x, const G& y) { return ev.mult_batch(x, y); }
     G mulp(const G& x, const Pattern& p) { return ev.mult_p_batch(x, std::vector<const Pattern*>(x.size(), &p)); }
     G lrot(const G& x, int r) { return ev.lrot_batch(x, r); }

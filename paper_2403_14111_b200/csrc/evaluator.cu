@@ -168,12 +168,40 @@ CtP ev_drop(Ctx& c, const Ct& a, int to) {
     return o;
 }
 
+static void rescale_many(Ctx& c, const u64* T, size_t poly, int level, std::vector<CtP>& out);
+
+// Level adjustment of several ciphertexts from one level to `to`: the first
+// to + 2 limbs of each poly times llrint(Δ_{to+1}²/Δ_from) (read in place, one
+// launch), then one batched rescale
+std::vector<CtP> ev_level_adjust_batch(Ctx& c, const std::vector<const Ct*>& xs, int to) {
+    std::vector<CtP> out(xs.size());
+    if (xs.empty()) return out;
+    const int from = xs[0]->level;
+    for (auto* x : xs)
+        if (x->level != from || to >= from) throw Error(-4, "level adjust needs one source level above the target");
+    const int nl2 = to + 2;
+    const double s1 = c.scale[to + 1];
+    const int64_t cst = std::llrint(s1 * (s1 / c.scale[from]));
+    ConstTab t;
+    const_pairs(c, cst, 0, nl2, t);
+    const size_t poly = (size_t)nl2 * c.N;
+    Scratch sc(c);
+    u64* T = sc.take(2 * poly * xs.size());
+    std::vector<u64*> o(2 * xs.size());
+    std::vector<const u64*> a(2 * xs.size());
+    for (size_t b = 0; b < xs.size(); b++)
+        for (int s = 0; s < 2; s++) {
+            o[2 * b + s] = T + (2 * b + s) * poly;
+            a[2 * b + s] = xs[b]->poly(s);
+        }
+    k_elementwise_batch(c, EWP_CONST_MUL, (int)o.size(), o.data(), a.data(), nullptr, &t, nl2, 1, 0);
+    rescale_many(c, T, poly, to + 1, out);
+    return out;
+}
+
 CtP ev_level_adjust(Ctx& c, const Ct& a, int to) {
     if (to >= a.level) throw Error(-4, "level adjust needs a lower target");
-    CtP d = ev_drop(c, a, to + 1);
-    const double s1 = c.scale[to + 1];
-    const int64_t cst = std::llrint(s1 * (s1 / c.scale[a.level]));
-    return mul_int_rescale(c, d->d, to + 1, cst, 0);
+    return ev_level_adjust_batch(c, {&a}, to)[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -577,23 +605,13 @@ std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs_in, const std::vect
         plan.events += r;
     }
     rec(OP_MULT, (int)xs.size());
-    // level adjustments are deterministic: an operand shared by several
-    // products (DiagATB's B blocks, one per pass) is adjusted once
-    std::map<std::pair<const Ct*, int>, CtP> adj;
-    auto at_once = [&](const CtP& a, int l) {
-        if (a->level == l) return a;
-        auto it = adj.find({a.get(), l});
-        if (it != adj.end()) return it->second;
-        CtP o = at(a, l);
-        adj[{a.get(), l}] = o;
-        return o;
-    };
-    std::vector<CtP> ax(xs.size()), ay(xs.size());
-    for (size_t i = 0; i < xs.size(); i++) {
-        const int l = std::min(xs[i]->level, ys[i]->level);
-        ax[i] = at_once(xs[i], l);
-        ay[i] = at_once(ys[i], l);
-    }
+    // level adjustments in batches; an operand shared by several products
+    // (DiagATB's B blocks, one per pass) is adjusted once (deterministic)
+    std::vector<int> ls(xs.size());
+    for (size_t i = 0; i < xs.size(); i++) ls[i] = std::min(xs[i]->level, ys[i]->level);
+    std::vector<CtP> ax = xs, ay = ys;
+    at_batch(ax, ls);
+    at_batch(ay, ls);
     // one fused pipeline per level present
     std::vector<char> done(xs.size(), 0);
     for (size_t i = 0; i < xs.size(); i++) {
@@ -688,10 +706,47 @@ std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, c
 
 // ---- batched element-wise ops (one launch over the blocks of a lockstep op)
 
-std::vector<CtP> Eval::add_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys, bool sub) {
-    std::vector<CtP> out(xs.size());
+std::vector<CtP> Eval::at_batch(std::vector<CtP>& xs, const std::vector<int>& ls) {
+    // group the needed adjustments by (source level, target): one batch each;
+    // a ciphertext needed by several slots is adjusted once (deterministic)
+    std::map<std::pair<int, int>, std::vector<const Ct*>> groups;
+    std::map<std::pair<const Ct*, int>, CtP> done;
+    for (size_t i = 0; i < xs.size(); i++) {
+        if (xs[i]->level == ls[i]) continue;
+        auto key = std::make_pair((const Ct*)xs[i].get(), ls[i]);
+        if (done.count(key)) continue;
+        done[key] = nullptr;
+        groups[{xs[i]->level, ls[i]}].push_back(xs[i].get());
+    }
+    for (auto& kv : groups) {
+        rec(OP_ADJUST, (int)kv.second.size());
+        std::vector<CtP> r = ev_level_adjust_batch(c, kv.second, kv.first.second);
+        for (size_t u = 0; u < r.size(); u++) done[{kv.second[u], kv.first.second}] = r[u];
+    }
+    for (size_t i = 0; i < xs.size(); i++)
+        if (xs[i]->level != ls[i]) xs[i] = done[{xs[i].get(), ls[i]}];
+    return xs;
+}
+
+std::vector<CtP> Eval::add_batch(const std::vector<CtP>& xs_in, const std::vector<CtP>& ys_in, bool sub) {
+    std::vector<CtP> out(xs_in.size());
+    std::vector<CtP> xs = xs_in, ys = ys_in;
     bool ok = xs.size() > 1;
-    for (size_t i = 0; ok && i < xs.size(); i++) ok = xs[i]->level == xs[0]->level && ys[i]->level == xs[0]->level;
+    int lmin = ok ? xs[0]->level : 0;
+    for (size_t i = 0; ok && i < xs.size(); i++) lmin = std::min(lmin, std::min(xs[i]->level, ys[i]->level));
+    if (ok) {
+        // result level min(levels) per pair (emulator.py:195-210); one batch
+        // when every pair lands on one level
+        std::vector<int> ls(xs.size());
+        for (size_t i = 0; i < xs.size(); i++) {
+            ls[i] = std::min(xs[i]->level, ys[i]->level);
+            ok = ok && ls[i] == lmin;
+        }
+        if (ok) {
+            at_batch(xs, ls);
+            at_batch(ys, ls);
+        }
+    }
     if (!ok) {
         for (size_t i = 0; i < xs.size(); i++) out[i] = add(xs[i], ys[i], sub);
         return out;

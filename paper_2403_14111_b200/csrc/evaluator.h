@@ -75,6 +75,8 @@ struct Eval {
     void rec(int kind, int n = 1);
     u64 next_nonce();
     CtP at(const CtP& a, int level);
+    // at() over a vector (in place, slot i to level ls[i]), batched per (source, target) level
+    std::vector<CtP> at_batch(std::vector<CtP>& xs, const std::vector<int>& ls);
     CtP ready(const CtP& a);
 
     CtP add(const CtP& a, const CtP& b, bool sub = false);

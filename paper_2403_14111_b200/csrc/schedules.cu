@@ -416,11 +416,9 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
             for (int p = 0; p < m; p++) terms[k][p] = t[(size_t)k * m + p];
     }
     G out = terms[0];
-    for (int k = 1; k < K; k++)
-        for (int p = 0; p < m; p++) out[p] = ev.add(out[p], terms[k][p]);
+    for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
     G cj = ev.conj_batch(out);
-    for (int p = 0; p < m; p++) out[p] = ev.add(out[p], cj[p]);
-    return out;
+    return ev.add_batch(out, cj);
 }
 
 // rot_left of every block of E by k (encoding.py:291-311); the rrot(s1) of
@@ -537,16 +535,20 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     // row_sums: block-row pre-adds (cross-rank reduction point, in pass order),
     // then the ladders of every (pass, block column) in lockstep
     G acc((size_t)K * n);
-    for (int k = 0; k < K; k++) {
-        G pre(n);
-        for (int q = 0; q < n; q++) {
-            CtP a = prod[((size_t)k * m) * n + q];
-            for (int p = 1; p < m; p++) a = ev.add(a, prod[((size_t)k * m + p) * n + q]);
-            pre[q] = a;
-        }
-        if (red) red(pre);
-        for (int q = 0; q < n; q++) acc[(size_t)k * n + q] = pre[q];
+    for (int k = 0; k < K; k++)
+        for (int q = 0; q < n; q++) acc[(size_t)k * n + q] = prod[((size_t)k * m) * n + q];
+    for (int p = 1; p < m; p++) {   // one batched add per block row, every (pass, column) at once
+        G rhs((size_t)K * n);
+        for (int k = 0; k < K; k++)
+            for (int q = 0; q < n; q++) rhs[(size_t)k * n + q] = prod[((size_t)k * m + p) * n + q];
+        acc = ev.add_batch(acc, rhs);
     }
+    if (red)
+        for (int k = 0; k < K; k++) {
+            G pre(acc.begin() + (size_t)k * n, acc.begin() + (size_t)(k + 1) * n);
+            red(pre);
+            for (int q = 0; q < n; q++) acc[(size_t)k * n + q] = pre[q];
+        }
     for (int t = 0; t < ilog2(g.s0); t++) acc = rot_many(ev, acc, (int64_t)(1 << t) * s1, true);
     std::vector<G> terms(K, G(n));
     {
@@ -560,11 +562,9 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
             for (int q = 0; q < n; q++) terms[k][q] = t[(size_t)k * n + q];
     }
     G out = terms[0];
-    for (int k = 1; k < K; k++)
-        for (int q = 0; q < n; q++) out[q] = ev.add(out[q], terms[k][q]);
+    for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
     G cj = ev.conj_batch(out);
-    for (int q = 0; q < n; q++) out[q] = ev.add(out[q], cj[q]);
-    return out;
+    return ev.add_batch(out, cj);
 }
 
 // ---- DiagABT (matmul.py:74-110) --------------------------------------------

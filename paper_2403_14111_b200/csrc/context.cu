@@ -635,6 +635,57 @@ void decrypt(Ctx& c, const Ct& a, double* zr, double* zi) {
     decode_host(c, md.data(), zr, zi);
 }
 
+// B refreshes of ciphertexts at one level (the surrogate above, batched)
+std::vector<CtP> refresh_batch(Ctx& c, const std::vector<const Ct*>& a, const std::vector<u64>& nonces) {
+    std::vector<CtP> out(a.size());
+    for (size_t b0 = 0; b0 < a.size(); b0 += KS_MAXB) {
+        const int B = (int)std::min<size_t>(KS_MAXB, a.size() - b0);
+        const int level = a[b0]->level;
+        for (int b = 0; b < B; b++)
+            if (a[b0 + b]->level != level) throw Error(-4, "batched refresh needs one level");
+        const int two = level >= 1 ? 1 : 0, nl = c.L + 1;
+        Scratch sc(c);
+        u64* X = sc.take((size_t)B * (1 + two) * c.N);
+        std::vector<const u64*> c0(B), c1(B);
+        std::vector<u64*> xb(B), o(B);
+        for (int b = 0; b < B; b++) {
+            c0[b] = a[b0 + b]->poly(0);
+            c1[b] = a[b0 + b]->poly(1);
+            xb[b] = X + (size_t)b * (1 + two) * c.N;
+            out[b0 + b] = new_ct(c, c.L);
+            o[b] = out[b0 + b]->d;
+        }
+        const u64* nn = nonces.data() + b0;
+        k_refresh_batch(c, B, c0.data(), c1.data(), xb.data(), nullptr, nn, 0, two, 0, 0);
+        {
+            JobList j;
+            j.n = B * (1 + two);
+            for (int b = 0; b < B; b++)
+                for (int i = 0; i <= two; i++) {
+                    j.prime[b * (1 + two) + i] = i;
+                    j.ptr[b * (1 + two) + i] = xb[b] + (size_t)i * c.N;
+                    j.src[b * (1 + two) + i] = nullptr;
+                }
+            ntt_inverse(c, j);
+        }
+        const u64 inv01 = two ? invmod(c.pr[0].q % c.pr[1].q, c.pr[1].q) : 0;
+        k_refresh_batch(c, B, nullptr, nullptr, xb.data(), o.data(), nn, 1, two, inv01, c.scale[c.L] / c.scale[level]);
+        for (int base = 0; base < B * nl; base += MAXJ) {
+            JobList j;
+            j.n = std::min(MAXJ, B * nl - base);
+            for (int u = 0; u < j.n; u++) {
+                const int b = (base + u) / nl, i = (base + u) % nl;
+                j.prime[u] = i;
+                j.ptr[u] = o[b] + (size_t)i * c.N;
+                j.src[u] = nullptr;
+            }
+            ntt_forward(c, j);
+        }
+        k_refresh_batch(c, B, nullptr, nullptr, xb.data(), o.data(), nn, 2, two, 0, 0);
+    }
+    return out;
+}
+
 CtP refresh(Ctx& c, const Ct& a, u64 nonce) {
     const int two = a.level >= 1 ? 1 : 0;
     u64* x = dec_limbs(c, a, 1 + two);

@@ -486,10 +486,40 @@ CtP Eval::at(const CtP& a, int level) {
     return ev_level_adjust(c, *a, level);
 }
 
-CtP Eval::refresh_planned(const CtP& a, int j, int r) {
+u64 Eval::boot_nonce(int j, int r) {
     rec(OP_BOOT);
-    const u64 n = plan.on ? plan.base + (u64)plan.m * plan.events + (u64)plan.p * r + j : next_nonce();
-    return refresh(c, *a, n);
+    return plan.on ? plan.base + (u64)plan.m * plan.events + (u64)plan.p * r + j : next_nonce();
+}
+
+CtP Eval::refresh_planned(const CtP& a, int j, int r) { return refresh(c, *a, boot_nonce(j, r)); }
+
+// refresh the given operands with their nonces, batched per level
+static void refresh_many(Ctx& c, std::vector<CtP*>& slots, const std::vector<u64>& nonces) {
+    std::map<int, std::vector<size_t>> by_level;
+    for (size_t u = 0; u < slots.size(); u++) by_level[(*slots[u])->level].push_back(u);
+    for (auto& kv : by_level) {
+        std::vector<const Ct*> a;
+        std::vector<u64> n;
+        for (size_t u : kv.second) {
+            a.push_back(slots[u]->get());
+            n.push_back(nonces[u]);
+        }
+        std::vector<CtP> r = refresh_batch(c, a, n);
+        for (size_t t = 0; t < kv.second.size(); t++) *slots[kv.second[t]] = r[t];
+    }
+}
+
+void Eval::ready_batch(std::vector<CtP>& xs) {
+    std::vector<CtP*> slots;
+    std::vector<u64> nonces;
+    for (auto& x : xs) {
+        if (x->level >= 1) continue;
+        if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
+        nonces.push_back(boot_nonce(0, 1));
+        plan.events += 1;
+        slots.push_back(&x);
+    }
+    if (!slots.empty()) refresh_many(c, slots, nonces);
 }
 
 CtP Eval::ready(const CtP& a) {
@@ -595,15 +625,18 @@ std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs_in, const std::vect
     // per-operand auto-bootstrap (emulator.py:218-221) in the reference's
     // op-by-op order -- x before y, product by product -- so every refresh
     // draws the nonce the sequential order gives it; then one batch
+    std::vector<CtP*> slots;
+    std::vector<u64> nonces;
     for (size_t i = 0; i < xs.size(); i++) {
         const int r = (xs[i]->level < 1 ? 1 : 0) + (ys[i]->level < 1 ? 1 : 0);
         if (!r) continue;
         if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
         int j = 0;
-        if (xs[i]->level < 1) xs[i] = refresh_planned(xs[i], j++, r);
-        if (ys[i]->level < 1) ys[i] = refresh_planned(ys[i], j++, r);
+        if (xs[i]->level < 1) { nonces.push_back(boot_nonce(j++, r)); slots.push_back(&xs[i]); }
+        if (ys[i]->level < 1) { nonces.push_back(boot_nonce(j++, r)); slots.push_back(&ys[i]); }
         plan.events += r;
     }
+    if (!slots.empty()) refresh_many(c, slots, nonces);
     rec(OP_MULT, (int)xs.size());
     // level adjustments in batches; an operand shared by several products
     // (DiagATB's B blocks, one per pass) is adjusted once (deterministic)
@@ -815,7 +848,9 @@ std::vector<CtP> Eval::add_p_batch(const std::vector<CtP>& xs, const Pattern& p,
     return out;
 }
 
-std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs, std::complex<double> s) {
+std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs_in, std::complex<double> s) {
+    std::vector<CtP> xs = xs_in;
+    if (xs.size() > 1) ready_batch(xs);   // refreshes in block order, batched
     std::vector<CtP> out(xs.size());
     bool ok = c.logN >= 14 && xs.size() > 1;
     for (auto& x : xs) ok = ok && x->level >= 1 && x->level == xs[0]->level;
@@ -837,7 +872,9 @@ std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs, std::complex<dou
     return out;
 }
 
-std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs, const std::vector<const Pattern*>& ps) {
+std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs_in, const std::vector<const Pattern*>& ps) {
+    std::vector<CtP> xs = xs_in;
+    if (xs.size() > 1) ready_batch(xs);   // refreshes in block order, batched
     std::vector<CtP> out(xs.size());
     bool ok = c.logN >= 14 && xs.size() > 1;
     for (auto& x : xs) ok = ok && x->level >= 1 && x->level == xs[0]->level;

@@ -71,6 +71,10 @@ struct Eval {
     NoncePlan plan;
     Eval(Ctx& ctx, bool ab) : c(ctx), auto_boot(ab) {}
     CtP refresh_planned(const CtP& a, int j, int r);
+    // records a Bootstrap and returns the nonce of the j-th of r refreshes of an op
+    u64 boot_nonce(int j, int r);
+    // ready() over a vector: level-0 operands refreshed (block order, batched)
+    void ready_batch(std::vector<CtP>& xs);
 
     void rec(int kind, int n = 1);
     u64 next_nonce();

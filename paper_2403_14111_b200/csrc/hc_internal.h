@@ -229,6 +229,7 @@ CtP encrypt_coef_dev(Ctx& c, const int64_t* d_m, int level, u64 nonce);
 CtP encrypt(Ctx& c, const double* zr, const double* zi, int level, u64 nonce);
 void decrypt(Ctx& c, const Ct& a, double* zr, double* zi);
 CtP refresh(Ctx& c, const Ct& a, u64 nonce);
+std::vector<CtP> refresh_batch(Ctx& c, const std::vector<const Ct*>& a, const std::vector<u64>& nonces);
 u64 galois_rot(const Ctx& c, int64_t r);
 
 // ---- evaluator (evaluator.cu): exact CKKS ops, DESIGN.md §3 ----

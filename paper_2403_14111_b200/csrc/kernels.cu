@@ -558,6 +558,101 @@ void k_refresh_msg(Ctx& c, i64* m, const u64* x, int two, u64 inv01, double rati
     HC_CUDA(cudaGetLastError());
 }
 
+// ---- batched refresh surrogate (grid y = ciphertext): the same words as
+// dec_kernel / refresh_msg_kernel / cdt_kernel / coef_to_rns_kernel /
+// uniform_kernel / enc_combine_kernel applied one ciphertext at a time
+struct RefreshBatch {
+    const u64* c0[KS_MAXB];
+    const u64* c1[KS_MAXB];
+    u64* x[KS_MAXB];        // [1 + two][N] decryption limbs
+    u64* out[KS_MAXB];      // [2][nl][N]
+    u64 key_a[KS_MAXB], key_e[KS_MAXB];
+};
+
+__global__ void dec_batch_kernel(RefreshBatch rb, const u64* __restrict__ s, const PrimeDev* __restrict__ primes,
+                                 int nl, int N) {
+    const int b = blockIdx.y;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        rb.x[b][e] = add_mod(rb.c0[b][e], mul_mod(rb.c1[b][e], s[e], P), P.q);
+    }
+}
+
+// message (refresh_msg_kernel), error (cdt_kernel), residues of m + e
+// (coef_to_rns_kernel) and the uniform mask a (uniform_kernel), per coefficient
+__global__ void refresh_encode_kernel(RefreshBatch rb, const PrimeDev* __restrict__ primes, const u64* __restrict__ cdt,
+                                      int cdt_n, int cdt_b, int two, u64 inv_q0_mod_q1, double ratio, int nl, int N) {
+    const int b = blockIdx.y;
+    const PrimeDev P0 = primes[0];
+    const PrimeDev P1 = primes[1];
+    const u64* x = rb.x[b];
+    u64* c0 = rb.out[b];
+    u64* c1 = rb.out[b] + (size_t)nl * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const u64 v0 = x[k];
+        const i64 x0 = v0 > (P0.q - 1) / 2 ? (i64)v0 - (i64)P0.q : (i64)v0;
+        double md;
+        if (!two) {
+            md = __ll2double_rn(x0);
+        } else {
+            const u64 d = sub_mod(x[N + k], from_i64(x0, P1.q), P1.q);
+            const u64 kk = mul_mod(d, inv_q0_mod_q1, P1);
+            const i64 kc = kk > (P1.q - 1) / 2 ? (i64)kk - (i64)P1.q : (i64)kk;
+            md = __dadd_rn(__ll2double_rn(x0), __dmul_rn(__ull2double_rn(P0.q), __ll2double_rn(kc)));
+        }
+        const i64 m = __double2ll_rn(__dmul_rn(md, ratio));
+        const u64 r = rng_at(rb.key_e[b], (u64)k);
+        int cnt = 0;
+        for (int i = 0; i < cdt_n; i++) cnt += (cdt[i] <= r);
+        const i64 v = m + ((i64)cnt - cdt_b);
+        for (int i = 0; i < nl; i++) {
+            const u64 q = primes[i].q;
+            c0[(size_t)i * N + k] = from_i64(v, q);
+            c1[(size_t)i * N + k] = __umul64hi(rng_at(rb.key_a[b], (u64)i * N + k), q);
+        }
+    }
+}
+
+__global__ void enc_combine_batch_kernel(RefreshBatch rb, const u64* __restrict__ s, const PrimeDev* __restrict__ primes,
+                                         int nl, int N) {
+    const int b = blockIdx.y;
+    u64* c0 = rb.out[b];
+    const u64* c1 = rb.out[b] + (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
+        const PrimeDev P = primes[e / N];
+        c0[e] = sub_mod(c0[e], mul_mod(c1[e], s[e], P), P.q);
+    }
+}
+
+void k_refresh_batch(Ctx& c, int B, const u64* const* c0, const u64* const* c1, u64* const* xbuf, u64* const* out,
+                     const u64* nonces, int stage, int two, u64 inv01, double ratio) {
+    RefreshBatch rb;
+    for (int b = 0; b < B; b++) {
+        rb.c0[b] = c0 ? c0[b] : nullptr;
+        rb.c1[b] = c1 ? c1[b] : nullptr;
+        rb.x[b] = xbuf[b];
+        rb.out[b] = out ? out[b] : nullptr;
+        rb.key_a[b] = rng_key(c.seed, stream_id(DOM_ENC_A, nonces[b], 0));
+        rb.key_e[b] = rng_key(c.seed, stream_id(DOM_ENC_E, nonces[b], 0));
+    }
+    const int nl = c.L + 1;
+    if (stage == 0) {
+        Launch scope(c, "decrypt_limbs", 8.0 * c.N * 4 * (1 + two) * B);
+        dim3 grid((unsigned)std::max(1, nblocks((size_t)(1 + two) * c.N, 256) / B), B);
+        dec_batch_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_sk, c.d_primes, 1 + two, c.N);
+    } else if (stage == 1) {
+        Launch scope(c, "refresh_encode", 8.0 * c.N * (1.0 + two + 2.0 * nl) * B);
+        dim3 grid((unsigned)((c.N + 255) / 256), B);
+        refresh_encode_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_primes, c.d_cdt, c.cdt_n, c.cdt_b, two, inv01, ratio,
+                                                          nl, c.N);
+    } else {
+        Launch scope(c, "enc_combine", 8.0 * c.N * 4 * nl * B);
+        dim3 grid((unsigned)std::max(1, nblocks((size_t)nl * c.N, 256) / B), B);
+        enc_combine_batch_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_sk, c.d_primes, nl, c.N);
+    }
+    HC_CUDA(cudaGetLastError());
+}
+
 // c0 = c0 - c1 * s (c0 holds NTT(m + e) on entry)
 __global__ void enc_combine_kernel(u64* __restrict__ c0, const u64* __restrict__ c1, const u64* __restrict__ s,
                                    const PrimeDev* __restrict__ primes, int nl, int N) {

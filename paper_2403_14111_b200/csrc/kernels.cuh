@@ -36,6 +36,10 @@ void k_dec(Ctx& c, u64* x, const u64* c0, const u64* c1, int nl);
 void k_refresh_msg(Ctx& c, i64* m, const u64* x, int two, u64 inv01, double ratio);
 void k_enc_combine(Ctx& c, u64* c0, const u64* c1, int nl);
 void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly);
+// batched refresh surrogate stages (B <= KS_MAXB): 0 = decryption limbs into
+// xbuf, 1 = message + error + mask into out (c0 in coefficient form), 2 = c0 -= c1 s
+void k_refresh_batch(Ctx& c, int B, const u64* const* c0, const u64* const* c1, u64* const* xbuf, u64* const* out,
+                     const u64* nonces, int stage, int two, u64 inv01, double ratio);
 
 // batched NTT helpers over contiguous limbs with primes [p0, p0 + n)
 void ntt_limbs(Ctx& c, u64* d, int p0, int n, bool inverse, const u64* src = nullptr);

@@ -846,10 +846,11 @@ struct SM {
         for (int t = 0; t < ilog2(period); t++) {
             G rival = lrot(best, 1 << t);
             G w = comp(best, rival);
-            G x1 = mul(best, w);
             G x2 = rsubc(w, 1.0);
-            G x3 = mul(rival, x2);
-            best = add(x1, x3);
+            // best * w and rival * (1 - w) are independent: one batch, the
+            // first product's blocks before the second's (the reference order)
+            G xy = mul(cat(best, rival), cat(w, x2));
+            best = add(G(xy.begin(), xy.begin() + best.size()), G(xy.begin() + best.size(), xy.end()));
         }
         best = mulp(best, col0(g));
         for (int t = 0; t < ilog2(g.s1); t++) best = ev.lrot_batch(best, -(1 << t), true);
@@ -897,12 +898,30 @@ struct SM {
         G y = scale(M, 1.0 / cfg.inv_range);
         G a = rsubc(y, 2.0);
         G b = rsubc(y, 1.0);
+        // Goldschmidt: b_{i+1} = b_i^2, a_{i+1} = a_i (b_{i+1} + 1).  The
+        // update of a in iteration i and the squaring of iteration i + 1 both
+        // need only b_{i+1}: one batch (a's products first, as in the
+        // reference's op order), so the chain is iters + 1 products long
+        const size_t n = M.size();
+        if (cfg.inv_iters < 1) return scale(a, 1.0 / cfg.inv_range);
+        b = mul(b, b);
+        G t = addc(b, 1.0);
         for (int i = 0; i < cfg.inv_iters; i++) {
-            b = mul(b, b);
-            G t = addc(b, 1.0);
-            a = mul(a, t);
+            if (i + 1 < cfg.inv_iters) {
+                G r = mul(cat(a, b), cat(t, b));
+                a = G(r.begin(), r.begin() + n);
+                b = G(r.begin() + n, r.end());
+                t = addc(b, 1.0);
+            } else {
+                a = mul(a, t);
+            }
         }
         return scale(a, 1.0 / cfg.inv_range);
+    }
+    static G cat(const G& x, const G& y) {
+        G o = x;
+        o.insert(o.end(), y.begin(), y.end());
+        return o;
     }
 };
 

@@ -92,6 +92,14 @@ void Ctx::free(u64* p) {
     if (p) HC_CUDA(cudaFreeAsync(p, stream));
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HC_PDL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 Scratch::Scratch(Ctx& ctx) : c(ctx) {
     a = &c.arenas[c.stream];
     mark = a->top;

@@ -1,5 +1,6 @@
 // Internal declarations of the B200 RNS-CKKS library (not part of the C-ABI).
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -198,6 +199,31 @@ struct HostTrace {
     explicit HostTrace(const char* w);
     ~HostTrace();
 };
+
+// Programmatic dependent launch (sm_90+): every kernel is launched with
+// programmatic stream serialisation and starts with pdl_enter(): it lets the
+// next kernel of the stream begin launching, then waits until the previous
+// kernel has completed and its writes are visible -- ordering identical to
+// plain stream order, minus the launch gap.  HC_PDL=0 launches plainly.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    HC_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // RAII scope around one kernel launch: counts it and, when profiling,
 // brackets it with CUDA events on the context stream.  `bytes` is the

@@ -32,6 +32,7 @@ struct EwPtrs {
 };
 __global__ void ew_kernel(int op, EwPtrs ptr, const ConstTab consts, const PrimeDev* __restrict__ primes, int nl,
                           int npoly, int N, int bpoly) {
+    pdl_enter();
     // grid.y = poly * nl + limb: no integer division on the hot path
     u64* __restrict__ out = ptr.out[blockIdx.z];
     const u64* __restrict__ a = ptr.a[blockIdx.z];
@@ -107,7 +108,7 @@ void k_elementwise_batch(Ctx& c, int op, int B, u64* const* out, const u64* cons
         }
         Launch scope(c, "elementwise", 8.0 * c.N * nb * (rd + (double)npoly * nl));
         dim3 grid((unsigned)((c.N / 2 + 255) / 256), (unsigned)(npoly * nl), nb);
-        ew_kernel<<<grid, 256, 0, c.stream>>>(op, p, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
+        launch_k(c, ew_kernel, grid, 256, 0, op, p, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
         HC_CUDA(cudaGetLastError());
     }
 }
@@ -122,6 +123,7 @@ void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const C
 // ---------------------------------------------------------------------------
 
 __global__ void tensor_kernel(EwPtrs ptr, const PrimeDev* __restrict__ primes, int nl, int N) {
+    pdl_enter();
     u64* __restrict__ d = ptr.out[blockIdx.y];
     const u64* __restrict__ a = ptr.a[blockIdx.y];
     const u64* __restrict__ b = ptr.b[blockIdx.y];
@@ -149,7 +151,7 @@ void k_tensor_batch(Ctx& c, int B, u64* const* d, const u64* const* a, const u64
         }
         Launch scope(c, "tensor", 8.0 * c.N * 7 * nl * nb);
         dim3 grid((unsigned)std::max(1, nblocks((size_t)nl * c.N, 256) / nb), nb);
-        tensor_kernel<<<grid, 256, 0, c.stream>>>(p, c.d_primes, nl, c.N);
+        launch_k(c, tensor_kernel, grid, 256, 0, p, c.d_primes, nl, c.N);
         HC_CUDA(cudaGetLastError());
     }
 }
@@ -166,6 +168,7 @@ struct TensorSrc {
 };
 __global__ void tensor_sum_kernel(u64* __restrict__ d, TensorSrc src, int n, const PrimeDev* __restrict__ primes,
                                   int nl, int N) {
+    pdl_enter();
     const size_t poly = (size_t)nl * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
@@ -188,7 +191,7 @@ void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int 
     TensorSrc src;
     for (int q = 0; q < n; q++) { src.a[q] = a[q]; src.b[q] = b[q]; }
     Launch scope(c, "tensor", 8.0 * c.N * (4.0 * n + 3) * nl);
-    tensor_sum_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(d, src, n, c.d_primes, nl, c.N);
+    launch_k(c, tensor_sum_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, d, src, n, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
@@ -197,6 +200,7 @@ void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int 
 // ---------------------------------------------------------------------------
 
 __global__ void automorph_kernel(u64* __restrict__ out, const u64* __restrict__ in, int nlimbs, int logN, u64 g) {
+    pdl_enter();
     const int N = 1 << logN;
     const u64 mask = 2 * (u64)N - 1;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nlimbs * N;
@@ -212,7 +216,7 @@ __global__ void automorph_kernel(u64* __restrict__ out, const u64* __restrict__ 
 
 void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g) {
     Launch scope(c, "automorph", 16.0 * c.N * nlimbs);
-    automorph_kernel<<<nblocks((size_t)nlimbs * c.N, 256), 256, 0, c.stream>>>(out, in, nlimbs, c.logN, g);
+    launch_k(c, automorph_kernel, nblocks((size_t)nlimbs * c.N, 256), 256, 0, out, in, nlimbs, c.logN, g);
     HC_CUDA(cudaGetLastError());
 }
 
@@ -228,6 +232,7 @@ __global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, co
                              const u64* __restrict__ tab, const u64* __restrict__ tab_inv,
                              const PrimeDev* __restrict__ primes, int level, int L, int K, int alpha, int dnum,
                              int nall, int N) {
+    pdl_enter();
     const int j = blockIdx.y;
     const int lo = j * alpha;
     int hi = lo + alpha;
@@ -268,7 +273,7 @@ void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
     dim3 grid((c.N + 255) / 256, beta);
     const int nl = level + 1, nt = nl + c.K;
     Launch scope(c, "modup", 8.0 * c.N * (2.0 * nl + (double)beta * nt));
-    modup_kernel<<<grid, 256, 0, c.stream>>>(up, X, D, c.d_modup, c.d_modup_inv, c.d_primes, level, c.L, c.K,
+    launch_k(c, modup_kernel, grid, 256, 0, up, X, D, c.d_modup, c.d_modup_inv, c.d_primes, level, c.L, c.K,
                                               c.alpha, c.dnum, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -280,6 +285,7 @@ void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
 __global__ void keyprod_kernel(u64* __restrict__ acc, const u64* __restrict__ up, const u64* __restrict__ key,
                                const PrimeDev* __restrict__ primes, int level, int L, int K, int beta, int nall,
                                int N) {
+    pdl_enter();
     const int nt = level + 1 + K;
     const size_t poly = (size_t)nt * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
@@ -304,7 +310,7 @@ void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int b
     const size_t poly = (size_t)(level + 1 + c.K) * c.N;
     const double nt = level + 1 + c.K;
     Launch scope(c, "keyprod", 8.0 * c.N * (3.0 * beta * nt + 2.0 * nt));
-    keyprod_kernel<<<nblocks(poly, 256), 256, 0, c.stream>>>(acc, up, key, c.d_primes, level, c.L, c.K, beta,
+    launch_k(c, keyprod_kernel, nblocks(poly, 256), 256, 0, acc, up, key, c.d_primes, level, c.L, c.K, beta,
                                                               c.nall, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -317,6 +323,7 @@ void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int b
 __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__ acc, const u64* __restrict__ tab,
                                     const u64* __restrict__ tab_inv, const PrimeDev* __restrict__ primes, int level,
                                     int L, int K, int nall, int N) {
+    pdl_enter();
     const int s = blockIdx.y;
     const int nt = level + 1 + K;
     const u64* A = acc + (size_t)s * nt * N;
@@ -345,7 +352,7 @@ __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__
 void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
     dim3 grid((c.N + 255) / 256, 2);
     Launch scope(c, "moddown_conv", 8.0 * c.N * (2.0 * c.K + 2.0 * (level + 1)));
-    moddown_conv_kernel<<<grid, 256, 0, c.stream>>>(W, acc, c.d_moddown, c.d_moddown_inv, c.d_primes, level, c.L,
+    launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_moddown, c.d_moddown_inv, c.d_primes, level, c.L,
                                                      c.K, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -354,6 +361,7 @@ void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
 __global__ void moddown_combine_kernel(u64* __restrict__ out, const u64* __restrict__ acc, const u64* __restrict__ W,
                                        const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly,
                                        const PrimeDev* __restrict__ primes, int level, int K, int N) {
+    pdl_enter();
     const int nl = level + 1, nt = nl + K;
     const size_t poly = (size_t)nl * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < 2 * poly; e += (size_t)gridDim.x * blockDim.x) {
@@ -372,7 +380,7 @@ void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64
                        int level) {
     const size_t work = 2 * (size_t)(level + 1) * c.N;
     Launch scope(c, "moddown_combine", 8.0 * c.N * (level + 1) * (6.0 + add_npoly));
-    moddown_combine_kernel<<<nblocks(work, 256), 256, 0, c.stream>>>(out, acc, W, c.d_pinv, addend, add_npoly,
+    launch_k(c, moddown_combine_kernel, nblocks(work, 256), 256, 0, out, acc, W, c.d_pinv, addend, add_npoly,
                                                                       c.d_primes, level, c.K, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -383,6 +391,7 @@ void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64
 
 __global__ void rescale_bcast_kernel(u64* __restrict__ Y, const u64* __restrict__ X, const u64* __restrict__ tab,
                                      const PrimeDev* __restrict__ primes, int level, int npoly, int N) {
+    pdl_enter();
     const u64 ql = primes[level].q;
     const size_t per = (size_t)level * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * per; e += (size_t)gridDim.x * blockDim.x) {
@@ -401,6 +410,7 @@ __global__ void rescale_bcast_kernel(u64* __restrict__ Y, const u64* __restrict_
 __global__ void rescale_combine_kernel(u64* __restrict__ out, const u64* __restrict__ a, const u64* __restrict__ Y,
                                        const u64* __restrict__ tab, const PrimeDev* __restrict__ primes, int level,
                                        int npoly, int N) {
+    pdl_enter();
     const size_t per = (size_t)level * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * per; e += (size_t)gridDim.x * blockDim.x) {
         const int s = (int)(e / per);
@@ -415,7 +425,7 @@ __global__ void rescale_combine_kernel(u64* __restrict__ out, const u64* __restr
 void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly) {
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
     Launch scope(c, "rescale_bcast", 8.0 * c.N * npoly * (1.0 + level));
-    rescale_bcast_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(Y, X, tab, c.d_primes,
+    launch_k(c, rescale_bcast_kernel, nblocks((size_t)npoly * level * c.N, 256), 256, 0, Y, X, tab, c.d_primes,
                                                                                           level, npoly, c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -423,7 +433,7 @@ void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly) {
 void k_rescale_combine(Ctx& c, u64* out, const u64* a, const u64* Y, int level, int npoly) {
     const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
     Launch scope(c, "rescale_combine", 8.0 * c.N * npoly * 3.0 * level);
-    rescale_combine_kernel<<<nblocks((size_t)npoly * level * c.N, 256), 256, 0, c.stream>>>(out, a, Y, tab,
+    launch_k(c, rescale_combine_kernel, nblocks((size_t)npoly * level * c.N, 256), 256, 0, out, a, Y, tab,
                                                                                             c.d_primes, level, npoly,
                                                                                             c.N);
     HC_CUDA(cudaGetLastError());
@@ -436,6 +446,7 @@ void k_rescale_combine(Ctx& c, u64* out, const u64* a, const u64* Y, int level, 
 // out[i][k] = uniform mod prime(first + i), counter (prime index)*N + k
 __global__ void uniform_kernel(u64* __restrict__ out, const PrimeDev* __restrict__ primes, int first, int nl, int N,
                                u64 key) {
+    pdl_enter();
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
         const int i = (int)(e / N);
         const int pi = first + i;
@@ -446,12 +457,13 @@ __global__ void uniform_kernel(u64* __restrict__ out, const PrimeDev* __restrict
 
 void k_uniform(Ctx& c, u64* out, int first_prime, int nl, u64 stream) {
     Launch scope(c, "sample_uniform", 8.0 * c.N * nl);
-    uniform_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, c.d_primes, first_prime, nl, c.N,
+    launch_k(c, uniform_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, out, c.d_primes, first_prime, nl, c.N,
                                                                           rng_key(c.seed, stream));
     HC_CUDA(cudaGetLastError());
 }
 
 __global__ void cdt_kernel(i64* __restrict__ e, const u64* __restrict__ cdt, int n, int b, int N, u64 key) {
+    pdl_enter();
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         const u64 r = rng_at(key, (u64)k);
         int cnt = 0;
@@ -462,13 +474,14 @@ __global__ void cdt_kernel(i64* __restrict__ e, const u64* __restrict__ cdt, int
 
 void k_cdt(Ctx& c, i64* e, u64 stream) {
     Launch scope(c, "sample_gauss", 8.0 * c.N);
-    cdt_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(e, c.d_cdt, c.cdt_n, c.cdt_b, c.N, rng_key(c.seed, stream));
+    launch_k(c, cdt_kernel, nblocks(c.N, 256), 256, 0, e, c.d_cdt, c.cdt_n, c.cdt_b, c.N, rng_key(c.seed, stream));
     HC_CUDA(cudaGetLastError());
 }
 
 // out[i][k] = (m[k] + e[k]) mod q_i for primes 0..nl-1 (e optional)
 __global__ void coef_to_rns_kernel(u64* __restrict__ out, const i64* __restrict__ m, const i64* __restrict__ e,
                                    const PrimeDev* __restrict__ primes, int first, int nl, int N) {
+    pdl_enter();
     for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x) {
         const int i = (int)(x / N);
         const size_t k = x - (size_t)i * N;
@@ -480,7 +493,7 @@ __global__ void coef_to_rns_kernel(u64* __restrict__ out, const i64* __restrict_
 
 void k_coef_to_rns(Ctx& c, u64* out, const i64* m, const i64* e, int first_prime, int nl) {
     Launch scope(c, "coef_to_rns", 8.0 * c.N * (2.0 + nl));
-    coef_to_rns_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, m, e, c.d_primes, first_prime, nl,
+    launch_k(c, coef_to_rns_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, out, m, e, c.d_primes, first_prime, nl,
                                                                               c.N);
     HC_CUDA(cudaGetLastError());
 }
@@ -489,6 +502,7 @@ void k_coef_to_rns(Ctx& c, u64* out, const i64* m, const i64* e, int first_prime
 __global__ void key_combine_kernel(u64* __restrict__ b, const u64* __restrict__ a, const u64* __restrict__ s,
                                    const u64* __restrict__ s2, const u64* __restrict__ pm,
                                    const PrimeDev* __restrict__ primes, int nl, int dlo, int dhi, int N) {
+    pdl_enter();
     for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x) {
         const int i = (int)(x / N);
         const PrimeDev P = primes[i];
@@ -500,25 +514,27 @@ __global__ void key_combine_kernel(u64* __restrict__ b, const u64* __restrict__ 
 
 void k_key_combine(Ctx& c, u64* b, const u64* a, const u64* s, const u64* s2, const u64* pm, int nl, int dlo,
                    int dhi) {
-    key_combine_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(b, a, s, s2, pm, c.d_primes, nl, dlo,
+    launch_k(c, key_combine_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, b, a, s, s2, pm, c.d_primes, nl, dlo,
                                                                               dhi, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
 __global__ void square_kernel(u64* __restrict__ out, const u64* __restrict__ a, const PrimeDev* __restrict__ primes,
                               int nl, int N) {
+    pdl_enter();
     for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < (size_t)nl * N; x += (size_t)gridDim.x * blockDim.x)
         out[x] = mul_mod(a[x], a[x], primes[x / N]);
 }
 
 void k_square(Ctx& c, u64* out, const u64* a, int nl) {
-    square_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(out, a, c.d_primes, nl, c.N);
+    launch_k(c, square_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, out, a, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
 // x[i] = c0[i] + c1[i] * s[i] for limbs 0..nl-1
 __global__ void dec_kernel(u64* __restrict__ x, const u64* __restrict__ c0, const u64* __restrict__ c1,
                            const u64* __restrict__ s, const PrimeDev* __restrict__ primes, int nl, int N) {
+    pdl_enter();
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
         x[e] = add_mod(c0[e], mul_mod(c1[e], s[e], P), P.q);
@@ -527,13 +543,14 @@ __global__ void dec_kernel(u64* __restrict__ x, const u64* __restrict__ c0, cons
 
 void k_dec(Ctx& c, u64* x, const u64* c0, const u64* c1, int nl) {
     Launch scope(c, "decrypt_limbs", 8.0 * c.N * 4 * nl);
-    dec_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(x, c0, c1, c.d_sk, c.d_primes, nl, c.N);
+    launch_k(c, dec_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, x, c0, c1, c.d_sk, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
 // refresh surrogate message: m'[k] = rint(m_d * ratio), m_d = x0c + q0 * kc
 __global__ void refresh_msg_kernel(i64* __restrict__ m, const u64* __restrict__ x, const PrimeDev* __restrict__ primes,
                                    int two, u64 inv_q0_mod_q1, double ratio, int N) {
+    pdl_enter();
     const PrimeDev P0 = primes[0];
     const PrimeDev P1 = primes[1];
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
@@ -554,7 +571,7 @@ __global__ void refresh_msg_kernel(i64* __restrict__ m, const u64* __restrict__ 
 
 void k_refresh_msg(Ctx& c, i64* m, const u64* x, int two, u64 inv01, double ratio) {
     Launch scope(c, "refresh_msg", 8.0 * c.N * 3);
-    refresh_msg_kernel<<<nblocks(c.N, 256), 256, 0, c.stream>>>(m, x, c.d_primes, two, inv01, ratio, c.N);
+    launch_k(c, refresh_msg_kernel, nblocks(c.N, 256), 256, 0, m, x, c.d_primes, two, inv01, ratio, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
@@ -571,6 +588,7 @@ struct RefreshBatch {
 
 __global__ void dec_batch_kernel(RefreshBatch rb, const u64* __restrict__ s, const PrimeDev* __restrict__ primes,
                                  int nl, int N) {
+    pdl_enter();
     const int b = blockIdx.y;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
@@ -582,6 +600,7 @@ __global__ void dec_batch_kernel(RefreshBatch rb, const u64* __restrict__ s, con
 // (coef_to_rns_kernel) and the uniform mask a (uniform_kernel), per coefficient
 __global__ void refresh_encode_kernel(RefreshBatch rb, const PrimeDev* __restrict__ primes, const u64* __restrict__ cdt,
                                       int cdt_n, int cdt_b, int two, u64 inv_q0_mod_q1, double ratio, int nl, int N) {
+    pdl_enter();
     const int b = blockIdx.y;
     const PrimeDev P0 = primes[0];
     const PrimeDev P1 = primes[1];
@@ -615,6 +634,7 @@ __global__ void refresh_encode_kernel(RefreshBatch rb, const PrimeDev* __restric
 
 __global__ void enc_combine_batch_kernel(RefreshBatch rb, const u64* __restrict__ s, const PrimeDev* __restrict__ primes,
                                          int nl, int N) {
+    pdl_enter();
     const int b = blockIdx.y;
     u64* c0 = rb.out[b];
     const u64* c1 = rb.out[b] + (size_t)nl * N;
@@ -639,16 +659,16 @@ void k_refresh_batch(Ctx& c, int B, const u64* const* c0, const u64* const* c1, 
     if (stage == 0) {
         Launch scope(c, "decrypt_limbs", 8.0 * c.N * 4 * (1 + two) * B);
         dim3 grid((unsigned)std::max(1, nblocks((size_t)(1 + two) * c.N, 256) / B), B);
-        dec_batch_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_sk, c.d_primes, 1 + two, c.N);
+        launch_k(c, dec_batch_kernel, grid, 256, 0, rb, c.d_sk, c.d_primes, 1 + two, c.N);
     } else if (stage == 1) {
         Launch scope(c, "refresh_encode", 8.0 * c.N * (1.0 + two + 2.0 * nl) * B);
         dim3 grid((unsigned)((c.N + 255) / 256), B);
-        refresh_encode_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_primes, c.d_cdt, c.cdt_n, c.cdt_b, two, inv01, ratio,
+        launch_k(c, refresh_encode_kernel, grid, 256, 0, rb, c.d_primes, c.d_cdt, c.cdt_n, c.cdt_b, two, inv01, ratio,
                                                           nl, c.N);
     } else {
         Launch scope(c, "enc_combine", 8.0 * c.N * 4 * nl * B);
         dim3 grid((unsigned)std::max(1, nblocks((size_t)nl * c.N, 256) / B), B);
-        enc_combine_batch_kernel<<<grid, 256, 0, c.stream>>>(rb, c.d_sk, c.d_primes, nl, c.N);
+        launch_k(c, enc_combine_batch_kernel, grid, 256, 0, rb, c.d_sk, c.d_primes, nl, c.N);
     }
     HC_CUDA(cudaGetLastError());
 }
@@ -656,6 +676,7 @@ void k_refresh_batch(Ctx& c, int B, const u64* const* c0, const u64* const* c1, 
 // c0 = c0 - c1 * s (c0 holds NTT(m + e) on entry)
 __global__ void enc_combine_kernel(u64* __restrict__ c0, const u64* __restrict__ c1, const u64* __restrict__ s,
                                    const PrimeDev* __restrict__ primes, int nl, int N) {
+    pdl_enter();
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)nl * N; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
         c0[e] = sub_mod(c0[e], mul_mod(c1[e], s[e], P), P.q);
@@ -664,12 +685,13 @@ __global__ void enc_combine_kernel(u64* __restrict__ c0, const u64* __restrict__
 
 void k_enc_combine(Ctx& c, u64* c0, const u64* c1, int nl) {
     Launch scope(c, "enc_combine", 8.0 * c.N * 4 * nl);
-    enc_combine_kernel<<<nblocks((size_t)nl * c.N, 256), 256, 0, c.stream>>>(c0, c1, c.d_sk, c.d_primes, nl, c.N);
+    launch_k(c, enc_combine_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, c0, c1, c.d_sk, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
 // cross-rank reduction finish: x mod q_i (x is a sum of R < 16 residues)
 __global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restrict__ primes, int nl, int npoly, int N) {
+    pdl_enter();
     const size_t poly = (size_t)nl * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * poly; e += (size_t)gridDim.x * blockDim.x) {
         const int i = (int)((e % poly) / N);
@@ -679,7 +701,7 @@ __global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restric
 
 void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly) {
     Launch scope(c, "mod_reduce", 16.0 * c.N * npoly * nl);
-    mod_reduce_kernel<<<nblocks((size_t)npoly * nl * c.N, 256), 256, 0, c.stream>>>(x, c.d_primes, nl, npoly, c.N);
+    launch_k(c, mod_reduce_kernel, nblocks((size_t)npoly * nl * c.N, 256), 256, 0, x, c.d_primes, nl, npoly, c.N);
     HC_CUDA(cudaGetLastError());
 }
 

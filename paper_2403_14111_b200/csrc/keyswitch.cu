@@ -93,6 +93,7 @@ template <int LOGSZ, int SUBS, int NA>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int job = blockIdx.y;
     const int j = jobs.digit[job], t = jobs.t[job];
@@ -151,6 +152,7 @@ __device__ __forceinline__ void kp_load2(const u64* __restrict__ base, size_t k,
 __global__ void __launch_bounds__(256, KP_MINB) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
                                                             u64 gal, KsBatch kb,
                                                             u64* __restrict__ acc, int tlimit) {
+    pdl_enter();
     const size_t N = (size_t)1 << g.logN;
     const size_t kstride = (size_t)g.nall * N;
     const int t = blockIdx.y;
@@ -229,6 +231,7 @@ template <int LOGSZ, int SUBS, int NK>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -287,6 +290,7 @@ struct StModdown {
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -334,6 +338,7 @@ template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
             u64* __restrict__ Yt, int npoly) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
@@ -370,6 +375,7 @@ struct StRescale {
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, RsBatch rb,
               const u64* __restrict__ tab, int npoly) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
@@ -493,7 +499,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         dim3 grid((N >> CL) / CS, jobs.n, nin);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);
-            kern<<<grid, CG::THREADS, csm, c.stream>>>(jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
+            launch_k(c, kern, grid, CG::THREADS, csm, jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
         };
         switch (c.alpha) {
             case 1: go(ks_modup_cols<CL, CS, 1>); break;
@@ -539,7 +545,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         Launch scope(c, "ks_keyprod_stream",
                      8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
         dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
-        ks_keyprod_stream<<<grid, 256, 0, c.stream>>>(g, c.d_primes, gal, kb, ACC, nt);
+        launch_k(c, ks_keyprod_stream, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
         HC_CUDA(cudaGetLastError());
     }
     // 4. INTT of the P limbs, final scale N^-1 (P/p_t)^-1 (in place)
@@ -573,7 +579,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         dim3 grid((N >> CL) / CS, 2 * nl, B);
         auto go = [&](auto kern) {
             set_smem(kern, csm, at);
-            kern<<<grid, CG::THREADS, csm, c.stream>>>(g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
+            launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
         };
         switch (K) {
             case 1: go(ks_moddown_cols<CL, CS, 1>); break;
@@ -591,7 +597,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         for (int b = 0; b < B; b++) nadd2 += in[b].add2 != nullptr;
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
         dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl, B);
-        ks_moddown_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
+        launch_k(c, ks_moddown_chunks, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
                                                                 add_npoly, kb);
         HC_CUDA(cudaGetLastError());
     }
@@ -679,7 +685,7 @@ static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int n
         set_smem(rs_cols<CL, CS>, csm, at);
         Launch scope(c, "rs_cols", 8.0 * N * B * npoly * (1.0 + level));
         dim3 grid((N >> CL) / CS, npoly * level, B);
-        rs_cols<CL, CS><<<grid, CG::THREADS, csm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), X,
+        launch_k(c, rs_cols<CL, CS>, grid, CG::THREADS, csm, level, c.logN, N1, c.d_primes, c.twp(0, false), X,
                                                               tab, Yt, npoly);
         HC_CUDA(cudaGetLastError());
     }
@@ -690,7 +696,7 @@ static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int n
         for (int b = 0; b < B; b++) { rb.a[b] = a[b]; rb.out[b] = out[b]; }
         Launch scope(c, "rs_chunks", 8.0 * N * B * npoly * 3.0 * level);
         dim3 grid((N >> CH_LOG) / CH_SUBS, npoly * level, B);
-        rs_chunks<<<grid, HG::THREADS, hsm, c.stream>>>(level, c.logN, N1, c.d_primes, c.twp(0, false), Yt, rb, tab,
+        launch_k(c, rs_chunks, grid, HG::THREADS, hsm, level, c.logN, N1, c.d_primes, c.twp(0, false), Yt, rb, tab,
                                                         npoly);
         HC_CUDA(cudaGetLastError());
     }

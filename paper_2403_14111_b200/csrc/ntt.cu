@@ -30,6 +30,7 @@ template <int LOGSZ, int MODE, int SUBS, bool INV>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS)
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
+    pdl_enter();
     extern __shared__ u64 sm[];
     const int job = blockIdx.y, b = blockIdx.z;
     const int pidx = jobs.prime[job];
@@ -79,10 +80,10 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
     }
     Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n * jobs.nb);
     if (inv)
-        ntt_kernel<LOGSZ, MODE, SUBS, true><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes, c.twp(0, true),
+        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, true>, grid, PG::THREADS, smem, jobs, c.d_primes, c.twp(0, true),
                                                                                   c.logN, N1, use_src, last);
     else
-        ntt_kernel<LOGSZ, MODE, SUBS, false><<<grid, PG::THREADS, smem, c.stream>>>(jobs, c.d_primes,
+        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, false>, grid, PG::THREADS, smem, jobs, c.d_primes,
                                                                                    c.twp(0, false), c.logN, N1,
                                                                                    use_src, last);
     HC_CUDA(cudaGetLastError());

@@ -205,9 +205,11 @@ struct HostTrace {
 // next kernel of the stream begin launching, then waits until the previous
 // kernel has completed and its writes are visible -- ordering identical to
 // plain stream order, minus the launch gap.  HC_PDL=0 launches plainly.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_trigger();
+    pdl_wait();
 }
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>

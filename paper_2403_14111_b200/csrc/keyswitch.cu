@@ -93,7 +93,7 @@ template <int LOGSZ, int SUBS, int NA>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int job = blockIdx.y;
     const int j = jobs.digit[job], t = jobs.t[job];
@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)pi << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
+    pdl_wait();   // everything above reads context-lifetime tables only
     ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
@@ -231,7 +232,7 @@ template <int LOGSZ, int SUBS, int NK>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
+    pdl_wait();   // everything above reads context-lifetime tables only
     ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NK, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
@@ -290,7 +292,7 @@ struct StModdown {
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
     const size_t N = (size_t)1 << g.logN;
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
+    pdl_wait();   // everything above reads context-lifetime tables only
     ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StModdown::MD_OUTB>(G, sm, TW, P, ld, st, twsm, true);
 }
 
@@ -338,7 +341,7 @@ template <int LOGSZ, int SUBS>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
             u64* __restrict__ Yt, int npoly) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
@@ -353,6 +356,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
+    pdl_wait();   // everything above reads context-lifetime tables only
     ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
@@ -375,7 +379,7 @@ struct StRescale {
 __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
     rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, RsBatch rb,
               const u64* __restrict__ tab, int npoly) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / level, i = blockIdx.y % level;
     const size_t N = (size_t)1 << logN;
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     const ulonglong2* TW = tw + ((size_t)i << logN);
     ulonglong2* twsm = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, N1);
+    pdl_wait();   // everything above reads context-lifetime tables only
     ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StRescale::RS_OUTB>(G, sm, TW, P, ld, st, twsm, true);
 }
 

@@ -30,7 +30,7 @@ template <int LOGSZ, int MODE, int SUBS, bool INV>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS)
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
-    pdl_enter();
+    pdl_trigger();
     extern __shared__ u64 sm[];
     const int job = blockIdx.y, b = blockIdx.z;
     const int pidx = jobs.prime[job];
@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<L
     ulonglong2* twsm = PG::twsm_of(sm);
     if (twsm) stage_twiddles<LOGSZ, MODE, SUBS>(G, twsm, TW, N1);
     const bool pend = twsm != nullptr;
+    pdl_wait();   // above: context-lifetime tables (primes, twiddles) only
     const u64 gal = use_src ? jobs.galois : 0;
     u64 c = P.ninv, cs = P.ninv_s;
     if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }

@@ -29,7 +29,10 @@
 
 namespace hc {
 
-constexpr int CH_LOG = 9, CH_SUBS = 4;       // chunk pass: 512-point, 4 per CTA
+#ifndef HC_CH_SUBS
+#define HC_CH_SUBS 2   // 128-thread CTAs: finer last wave (measured 4 -> 2: -3 % kernel time)
+#endif
+constexpr int CH_LOG = 9, CH_SUBS = HC_CH_SUBS;   // chunk pass: 512-point, CH_SUBS per CTA
 
 struct KsJobs {
     int n;
@@ -289,7 +292,7 @@ struct StModdown {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::MIN_BLOCKS)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
     pdl_trigger();
@@ -376,7 +379,7 @@ struct StRescale {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PASS_MIN_BLOCKS)
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::MIN_BLOCKS)
     rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, RsBatch rb,
               const u64* __restrict__ tab, int npoly) {
     pdl_trigger();
@@ -427,7 +430,10 @@ template <int LOGN>
 struct ColCfg;
 template <> struct ColCfg<14> { static constexpr int LOGSZ = 5, SUBS = 64; };
 template <> struct ColCfg<15> { static constexpr int LOGSZ = 6, SUBS = 32; };
-template <> struct ColCfg<16> { static constexpr int LOGSZ = 7, SUBS = 16; };
+#ifndef HC_COL_SUBS16
+#define HC_COL_SUBS16 16
+#endif
+template <> struct ColCfg<16> { static constexpr int LOGSZ = 7, SUBS = HC_COL_SUBS16; };
 template <> struct ColCfg<17> { static constexpr int LOGSZ = 8, SUBS = 8; };
 
 // One key-switch tail entry: which ModUp input it consumes and, hoisted, the

@@ -124,9 +124,12 @@ static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src
     }
 }
 
+#ifndef HC_NTT_CH_SUBS
+#define HC_NTT_CH_SUBS 2   // 128-thread CTAs (measured 4 -> 2: -0.8 % per pair)
+#endif
 static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
-    if (small_grid(jobs, N1 / 4)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
-    else launch_t<9, MODE_CHUNKS, 4>(c, jobs, inv, N1, use_src, last);
+    if (small_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
+    else launch_t<9, MODE_CHUNKS, HC_NTT_CH_SUBS>(c, jobs, inv, N1, use_src, last);
 }
 
 // second half of a split forward NTT (in place), for callers that ran the

@@ -860,8 +860,13 @@ struct SM {
         const double delta = 4.0 / (27.0 * std::pow(cfg.base_range, 2.0));
         for (int i = cfg.extension_steps - 1; i >= 0; i--) {
             const double di = delta * std::pow(cfg.extension_base, (double)(-2 * i));
-            G sq = mul(M, M);
-            G sc = scale(M, di);
+            // the square and the scaling are independent: two branches on
+            // side streams, issued in the reference's order (nonces unchanged)
+            G sq, sc;
+            par_for(ev.c, 2, 2, [&](int i) {
+                if (i == 0) sq = mul(M, M);
+                else sc = scale(M, di);
+            });
             G pr = mul(sq, sc);
             M = sub(M, pr);
         }
@@ -876,8 +881,11 @@ struct SM {
         const double c5 = 1.0 * (4.0 / 27.0) * K / std::pow(R, 4.0);
         G sq = mul(M, M);
         G cube = mul(sq, M);
-        G fifth = mul(cube, sq);
-        G t3 = scale(cube, c3);
+        G fifth, t3;
+        par_for(ev.c, 2, 2, [&](int i) {   // independent: side streams, reference issue order
+            if (i == 0) fifth = mul(cube, sq);
+            else t3 = scale(cube, c3);
+        });
         G t5 = scale(fifth, c5);
         G d = sub(t3, t5);
         return add(M, d);

@@ -512,6 +512,11 @@ def run_softmax(args, world, rank, local):
     clk = clocks.stop()
     total = all_max(ms.value, world)
     counts = {k: (v - c0[k]) // args.steps for k, v in ctx.ledger.counts().items()}
+    N.check(L.hc_prof_begin(ctx._h))
+    step()
+    buf = C.create_string_buffer(1 << 16)
+    N.check(L.hc_prof_end(ctx._h, buf, len(buf)))
+    prof = json.loads(buf.value.decode())
     line = {"metric": "encrypted softmax ms, config 3 (128x16 logits, 10 classes, N=2^16)",
             "value": total / args.steps, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False,
@@ -521,6 +526,7 @@ def run_softmax(args, world, rank, local):
                                    "replicas only for N > 1",
                        "refresh": "surrogate (decrypt/re-encrypt), not CKKS bootstrapping"},
             "max_abs_err_vs_float64": err, "ledger_per_step": counts,
+            "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)

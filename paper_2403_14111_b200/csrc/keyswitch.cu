@@ -141,32 +141,36 @@ constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
 // a pair of coefficients (16-byte accesses) for every key switch of the
 // batch, with the key words held in registers while the key does not change.
 
-__device__ __forceinline__ void kp_load2(const u64* __restrict__ base, size_t k, u64 gal_or_zero, int logN, u64& v0,
-                                         u64& v1) {
+// E coefficients per thread (1 or 2; pairs use 16-byte accesses)
+template <int E>
+__device__ __forceinline__ void kp_load(const u64* __restrict__ base, size_t k, u64 gal_or_zero, int logN, u64* v) {
     if (gal_or_zero) {
-        v0 = base[galois_src((unsigned)k, logN, gal_or_zero)];
-        v1 = base[galois_src((unsigned)(k + 1), logN, gal_or_zero)];
-    } else {
+#pragma unroll
+        for (int e = 0; e < E; e++) v[e] = base[galois_src((unsigned)(k + e), logN, gal_or_zero)];
+    } else if (E == 2) {
         const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(base + k);
-        v0 = w.x;
-        v1 = w.y;
+        v[0] = w.x;
+        v[E - 1] = w.y;
+    } else {
+        v[0] = base[k];
     }
 }
 
-__global__ void __launch_bounds__(256, KP_MINB) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
-                                                            u64 gal, KsBatch kb,
-                                                            u64* __restrict__ acc, int tlimit) {
+template <int E>
+__global__ void __launch_bounds__(256, E == 2 ? KP_MINB : 3) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
+                                                                      u64 gal, KsBatch kb,
+                                                                      u64* __restrict__ acc, int tlimit) {
     pdl_enter();
     const size_t N = (size_t)1 << g.logN;
     const size_t kstride = (size_t)g.nall * N;
     const int t = blockIdx.y;
     const int pi = g.prime(t);
     const PrimeDev P = primes[pi];
-    const size_t k = 2 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+    const size_t k = E * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (k >= N) return;
     int dig = -1;   // the digit that contains limb t (uniform), or -1 for a P limb
     if (t < g.nl) dig = t / g.alpha;
-    u64 kb0[KP_MAXB], kb1[KP_MAXB], ka0[KP_MAXB], ka1[KP_MAXB];
+    u64 kbv[KP_MAXB][E], kav[KP_MAXB][E];
     const u64* kprev = nullptr;
     for (int b = 0; b < kb.nb; b++) {
         if (kb.key[b] != kprev) {
@@ -175,56 +179,59 @@ __global__ void __launch_bounds__(256, KP_MINB) ks_keyprod_stream(KsGeo g, const
             for (int j = 0; j < KP_MAXB; j++) {
                 if (j >= g.beta) break;
                 const u64* kp = kprev + ((size_t)(2 * j) * g.nall + pi) * N;
-                kp_load2(kp, k, 0, g.logN, kb0[j], kb1[j]);
-                kp_load2(kp + kstride, k, 0, g.logN, ka0[j], ka1[j]);
+                kp_load<E>(kp, k, 0, g.logN, kbv[j]);
+                kp_load<E>(kp + kstride, k, 0, g.logN, kav[j]);
             }
         }
         const u64* up = kb.up[b];
         const u64 ug = kb.ugal[b];
         // issue every digit load before the first product
-        u64 x0[KP_MAXB], x1[KP_MAXB];
+        u64 x[KP_MAXB][E];
 #pragma unroll
         for (int j = 0; j < KP_MAXB; j++) {
             if (j >= g.beta) break;
-            if (j == dig) kp_load2(kb.d[b] + (size_t)t * N, k, ug ? ug : gal, g.logN, x0[j], x1[j]);
-            else kp_load2(up + ((size_t)j * g.nt + t) * N, k, ug, g.logN, x0[j], x1[j]);
+            if (j == dig) kp_load<E>(kb.d[b] + (size_t)t * N, k, ug ? ug : gal, g.logN, x[j]);
+            else kp_load<E>(up + ((size_t)j * g.nt + t) * N, k, ug, g.logN, x[j]);
         }
-        u64 ob0, oa0, ob1, oa1;
+        u64 ob[E], oa[E];
         if (P.fp) {
             // FP64 products (q < 2^46): each term exact and centered (|r| < 0.6q),
             // the sum of <= 4 reduced once; digits are lazy words below 2q
-            double sb0 = 0, sa0 = 0, sb1 = 0, sa1 = 0;
 #pragma unroll
-            for (int j = 0; j < KP_MAXB; j++) {
-                if (j >= g.beta) break;
-                const double y0 = fp_word(x0[j]), y1 = fp_word(x1[j]);
-                sb0 = __dadd_rn(sb0, fp_mulmod(y0, fp_word(kb0[j]), P.qd, P.qinv));
-                sa0 = __dadd_rn(sa0, fp_mulmod(y0, fp_word(ka0[j]), P.qd, P.qinv));
-                sb1 = __dadd_rn(sb1, fp_mulmod(y1, fp_word(kb1[j]), P.qd, P.qinv));
-                sa1 = __dadd_rn(sa1, fp_mulmod(y1, fp_word(ka1[j]), P.qd, P.qinv));
+            for (int e = 0; e < E; e++) {
+                double sb = 0, sa = 0;
+#pragma unroll
+                for (int j = 0; j < KP_MAXB; j++) {
+                    if (j >= g.beta) break;
+                    const double y = fp_word(x[j][e]);
+                    sb = __dadd_rn(sb, fp_mulmod(y, fp_word(kbv[j][e]), P.qd, P.qinv));
+                    sa = __dadd_rn(sa, fp_mulmod(y, fp_word(kav[j][e]), P.qd, P.qinv));
+                }
+                ob[e] = fp_canon(sb, P.qd, P.qinv);
+                oa[e] = fp_canon(sa, P.qd, P.qinv);
             }
-            ob0 = fp_canon(sb0, P.qd, P.qinv);
-            oa0 = fp_canon(sa0, P.qd, P.qinv);
-            ob1 = fp_canon(sb1, P.qd, P.qinv);
-            oa1 = fp_canon(sa1, P.qd, P.qinv);
         } else {
-            U128 b0 = {0, 0}, a0 = {0, 0}, b1 = {0, 0}, a1 = {0, 0};
 #pragma unroll
-            for (int j = 0; j < KP_MAXB; j++) {
-                if (j >= g.beta) break;
-                mac128(b0, x0[j], kb0[j]);
-                mac128(a0, x0[j], ka0[j]);
-                mac128(b1, x1[j], kb1[j]);
-                mac128(a1, x1[j], ka1[j]);
+            for (int e = 0; e < E; e++) {
+                U128 b0 = {0, 0}, a0 = {0, 0};
+#pragma unroll
+                for (int j = 0; j < KP_MAXB; j++) {
+                    if (j >= g.beta) break;
+                    mac128(b0, x[j][e], kbv[j][e]);
+                    mac128(a0, x[j][e], kav[j][e]);
+                }
+                ob[e] = reduce128(b0.hi, b0.lo, P);
+                oa[e] = reduce128(a0.hi, a0.lo, P);
             }
-            ob0 = reduce128(b0.hi, b0.lo, P);
-            oa0 = reduce128(a0.hi, a0.lo, P);
-            ob1 = reduce128(b1.hi, b1.lo, P);
-            oa1 = reduce128(a1.hi, a1.lo, P);
         }
         u64* ab = acc + b * g.acc_stride();
-        *reinterpret_cast<ulonglong2*>(ab + (size_t)t * N + k) = make_ulonglong2(ob0, ob1);
-        *reinterpret_cast<ulonglong2*>(ab + ((size_t)g.nt + t) * N + k) = make_ulonglong2(oa0, oa1);
+        if (E == 2) {
+            *reinterpret_cast<ulonglong2*>(ab + (size_t)t * N + k) = make_ulonglong2(ob[0], ob[E - 1]);
+            *reinterpret_cast<ulonglong2*>(ab + ((size_t)g.nt + t) * N + k) = make_ulonglong2(oa[0], oa[E - 1]);
+        } else {
+            ab[(size_t)t * N + k] = ob[0];
+            ab[((size_t)g.nt + t) * N + k] = oa[0];
+        }
     }
 }
 
@@ -551,12 +558,18 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         }
         int nkeys = 1;
         for (int b = 1; b < B; b++) nkeys += in[b].key != in[b - 1].key;
-        const size_t work = (size_t)nt * N;
         // algorithmic: the digit limbs (once per input) and ACC per key switch, each distinct key run once
         Launch scope(c, "ks_keyprod_stream",
                      8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
-        dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
-        launch_k(c, ks_keyprod_stream, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
+        // a lone key switch (chains) takes one coefficient per thread for
+        // parallelism; batches take pairs (16-byte accesses, fewer index ops)
+        if (B >= 2) {
+            dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
+            launch_k(c, ks_keyprod_stream<2>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
+        } else {
+            dim3 grid((unsigned)((N + 255) / 256), nt);
+            launch_k(c, ks_keyprod_stream<1>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
+        }
         HC_CUDA(cudaGetLastError());
     }
     // 4. INTT of the P limbs, final scale N^-1 (P/p_t)^-1 (in place)

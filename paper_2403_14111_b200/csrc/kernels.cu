@@ -402,7 +402,7 @@ __global__ void rescale_bcast_kernel(u64* __restrict__ Y, const u64* __restrict_
         const u64 q = primes[i].q;
         const u64 v = X[(size_t)s * N + k];
         const u64 qlm = tab[3 * i + 2];
-        const u64 vm = v % q;
+        const u64 vm = mul_shoup(v, 1, primes[i].mu_hi, q);   // v mod q without a 64-bit division
         Y[e] = v > (ql - 1) / 2 ? sub_mod(vm, qlm, q) : vm;
     }
 }

@@ -332,8 +332,9 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
 struct LdBcast {
     const u64* __restrict__ X;   // INTT of the dropped limb
     u64 ql, q, qlm;
+    u64 r1;                      // floor(2^64 / q): Shoup companion of 1 (= PrimeDev::mu_hi)
     __device__ __forceinline__ u64 operator()(size_t k) const {
-        const u64 v = X[k], vm = v % q;
+        const u64 v = X[k], vm = mul_shoup(v, 1, r1, q);   // v mod q without a 64-bit division
         return v > (ql - 1) / 2 ? sub_mod(vm, qlm, q) : vm;
     }
     __device__ __forceinline__ void load8(size_t k, u64* x) const {
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
     Yt += (size_t)blockIdx.z * npoly * level * N;
     const PrimeDev P = primes[i];
     const u64 q = P.q;
-    LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2]};
+    LdBcast ld{X + (size_t)s * N, primes[level].q, q, tab[3 * i + 2], P.mu_hi};
     StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(N1);

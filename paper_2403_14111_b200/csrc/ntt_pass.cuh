@@ -458,10 +458,11 @@ struct StPlain {
 
 // NTT-domain Galois permutation: out[j] = in[src(j)]
 __device__ __forceinline__ unsigned galois_src(unsigned j, int logN, u64 g) {
-    const u64 mask = (2ull << logN) - 1;
-    const u64 ex = 2 * (u64)(__brev(j) >> (32 - logN)) + 1;
-    const u64 e2 = (ex * g) & mask;
-    return __brev((unsigned)((e2 - 1) >> 1)) >> (32 - logN);
+    // only the low logN + 1 bits of the product matter: 32-bit arithmetic
+    const unsigned mask = (2u << logN) - 1;
+    const unsigned ex = 2 * (__brev(j) >> (32 - logN)) + 1;
+    const unsigned e2 = (ex * (unsigned)g) & mask;
+    return __brev((e2 - 1) >> 1) >> (32 - logN);
 }
 
 // gather loader for the automorphism fused into a pass

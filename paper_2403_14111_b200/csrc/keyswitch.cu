@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS
 }
 
 constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
+#ifndef KP_PAIRB
+#define KP_PAIRB 2           // batches of at least this many key switches take coefficient pairs
+#endif
 #ifndef KP_MINB
-#define KP_MINB 2            // resident 256-thread CTAs per SM the key product is register-budgeted for
+#define KP_MINB 3            // resident 256-thread CTAs per SM the key product is register-budgeted for (2: 30.95, 3: 30.82, 4: 31.10 ms/pair)
 #endif
 
 // ---- B (split form): streaming key inner product over NTT-form digits -----
@@ -564,7 +567,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
                      8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
         // a lone key switch (chains) takes one coefficient per thread for
         // parallelism; batches take pairs (16-byte accesses, fewer index ops)
-        if (B >= 2) {
+        if (B >= KP_PAIRB) {
             dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
             launch_k(c, ks_keyprod_stream<2>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
         } else {

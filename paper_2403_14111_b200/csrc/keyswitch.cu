@@ -9,11 +9,13 @@
 //   2. A: column pass of the forward NTT of every non-digit limb, whose
 //      first-round loads compute the fast base conversion
 //      sum_a Y_a * [Q'/q_a]_{p_t} on the fly          -> I    (1 launch)
-//   3. B: chunk pass of those NTTs, one CTA per (chunk tile, target limb t),
-//      looping over the digits: each digit's NTT output (or, for t inside
-//      the digit, sigma(d) itself) is multiplied with the key in registers
-//      and accumulated in 128 bits; one Barrett reduction per output
-//                                                      -> ACC  (1 launch)
+//   3. B: chunk pass of those NTTs (batched, lazy outputs), then the
+//      streaming key product: one thread per coefficient (pair) of target
+//      limb t reads every digit's NTT output (or, for t inside the digit,
+//      sigma(d) itself), multiplies with the key words held in registers and
+//      accumulates (128-bit integer or exact FP64); one reduction per output.
+//      (A form with the key product inside the chunk pass's stores was
+//      measured slower and removed.)               -> ACC  (2 launches)
 //   4. INTT of ACC's P limbs, final scale N^-1 * (P/p)^-1  (2 launches)
 //   5. D: column pass of the ModDown NTT with the P->Q conversion in its
 //      loads                                           -> Wt   (1 launch)

@@ -304,7 +304,14 @@ struct StModdown {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::MIN_BLOCKS)
+// ModDown chunk pass: 5 resident 128-thread CTAs per SM (96 registers) instead
+// of the passes' 8 (64): its stores read three operands per word and the
+// extra registers let them issue early (kernel 6.71 -> 6.42 ms per pair,
+// 42 -> 44 % of the HBM peak; 6 CTAs: 6.65 ms)
+#ifndef MD_MINB
+#define MD_MINB (5 * 128 / PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
+#endif
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, MD_MINB)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
     pdl_trigger();
@@ -353,8 +360,11 @@ struct RsBatch {
     u64* out[KS_MAXB];
 };
 
+#ifndef RS_PMB
+#define RS_PMB PASS_MIN_BLOCKS   // register budget of the rescale passes (as PASS_MIN_BLOCKS)
+#endif
 template <int LOGSZ, int SUBS>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, RS_PMB)
     rs_cols(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ X, const u64* __restrict__ tab,
             u64* __restrict__ Yt, int npoly) {
     pdl_trigger();
@@ -392,7 +402,8 @@ struct StRescale {
     }
 };
 
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::MIN_BLOCKS)
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS,
+                                  PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::MIN_BLOCKS * RS_PMB / PASS_MIN_BLOCKS)
     rs_chunks(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Yt, RsBatch rb,
               const u64* __restrict__ tab, int npoly) {
     pdl_trigger();

@@ -26,8 +26,13 @@
 
 namespace hc {
 
+#ifndef NTT_PMB
+#define NTT_PMB PASS_MIN_BLOCKS   // register budget of the generic NTT kernel (as PASS_MIN_BLOCKS)
+#endif
 template <int LOGSZ, int MODE, int SUBS, bool INV>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS, PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS)
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS,
+                                  (PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * NTT_PMB / PASS_MIN_BLOCKS) > 0
+                                      ? PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * NTT_PMB / PASS_MIN_BLOCKS : 1)
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
     pdl_trigger();

@@ -29,10 +29,13 @@ namespace hc {
 #ifndef NTT_PMB
 #define NTT_PMB PASS_MIN_BLOCKS   // register budget of the generic NTT kernel (as PASS_MIN_BLOCKS)
 #endif
-template <int LOGSZ, int MODE, int SUBS, bool INV>
+#ifndef NTT_PMB_SMALL
+#define NTT_PMB_SMALL 2           // register budget of the sub-wave chain launches of the split passes
+#endif
+template <int LOGSZ, int MODE, int SUBS, bool INV, int PMB = NTT_PMB>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS,
-                                  (PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * NTT_PMB / PASS_MIN_BLOCKS) > 0
-                                      ? PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * NTT_PMB / PASS_MIN_BLOCKS : 1)
+                                  (PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * PMB / PASS_MIN_BLOCKS) > 0
+                                      ? PassGeo<LOGSZ, MODE, SUBS>::MIN_BLOCKS * PMB / PASS_MIN_BLOCKS : 1)
     ntt_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
                int N1, int use_src, int last) {
     pdl_trigger();
@@ -68,7 +71,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS,
     }
 }
 
-template <int LOGSZ, int MODE, int SUBS>
+template <int LOGSZ, int MODE, int SUBS, int PMB = NTT_PMB>
 static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
     using PG = PassGeo<LOGSZ, MODE, SUBS>;
     const size_t smem = PG::smem_bytes();
@@ -78,18 +81,18 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
                                       {"ntt_inv_full", "ntt_inv_cols", "ntt_inv_chunks"}};
     static bool attr[2] = {false, false};
     if (!attr[inv ? 1 : 0]) {
-        if (inv) HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, true>,
+        if (inv) HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, true, PMB>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        else HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, false>,
+        else HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, false, PMB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr[inv ? 1 : 0] = true;
     }
     Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n * jobs.nb);
     if (inv)
-        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, true>, grid, PG::THREADS, smem, jobs, c.d_primes, c.twp(0, true),
+        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, true, PMB>, grid, PG::THREADS, smem, jobs, c.d_primes, c.twp(0, true),
                                                                                   c.logN, N1, use_src, last);
     else
-        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, false>, grid, PG::THREADS, smem, jobs, c.d_primes,
+        launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, false, PMB>, grid, PG::THREADS, smem, jobs, c.d_primes,
                                                                                    c.twp(0, false), c.logN, N1,
                                                                                    use_src, last);
     HC_CUDA(cudaGetLastError());
@@ -112,18 +115,27 @@ static void full_pass(Ctx& c, const JobList& jobs, bool inv) {
 // takes the 64-thread variant: 4x the CTAs for the same work, so latency and
 // instruction fetch are spread over every SM.
 static bool small_grid(const JobList& jobs, int ctas_per_job) { return ctas_per_job * jobs.n * jobs.nb < 148 * 4; }
+// a sub-wave launch of a lone ciphertext (grid z = 1: the chains of softmax /
+// inversion) is latency-bound, so it takes a larger register budget
+// (NTT_PMB_SMALL=2: softmax 22.70 -> 22.16 ms); batched sub-wave launches keep
+// NTT_PMB (the larger budget measured +0.3 % per pair there)
+static bool chain_grid(const JobList& jobs, int ctas_per_job) { return jobs.nb == 1 && small_grid(jobs, ctas_per_job); }
 
 static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
     const int big_subs = 1 << (20 - c.logN);   // 64, 32, 16, 8 columns per CTA for 2^14 .. 2^17
-    const bool sm = small_grid(jobs, 512 / big_subs);
+    const bool sm = small_grid(jobs, 512 / big_subs), ch = sm && jobs.nb == 1;
     switch (c.logN) {
-        case 14: if (sm) launch_t<5, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last);
+        case 14: if (ch) launch_t<5, MODE_COLS, 16, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
+                 else if (sm) launch_t<5, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last);
                  else launch_t<5, MODE_COLS, 64>(c, jobs, inv, N1, use_src, last); break;
-        case 15: if (sm) launch_t<6, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last);
+        case 15: if (ch) launch_t<6, MODE_COLS, 8, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
+                 else if (sm) launch_t<6, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last);
                  else launch_t<6, MODE_COLS, 32>(c, jobs, inv, N1, use_src, last); break;
-        case 16: if (sm) launch_t<7, MODE_COLS, 4>(c, jobs, inv, N1, use_src, last);
+        case 16: if (ch) launch_t<7, MODE_COLS, 4, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
+                 else if (sm) launch_t<7, MODE_COLS, 4>(c, jobs, inv, N1, use_src, last);
                  else launch_t<7, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last); break;
-        case 17: if (sm) launch_t<8, MODE_COLS, 2>(c, jobs, inv, N1, use_src, last);
+        case 17: if (ch) launch_t<8, MODE_COLS, 2, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
+                 else if (sm) launch_t<8, MODE_COLS, 2>(c, jobs, inv, N1, use_src, last);
                  else launch_t<8, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last); break;
         default: throw Error(-1, "unsupported ring degree");
     }
@@ -133,7 +145,8 @@ static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src
 #define HC_NTT_CH_SUBS 2   // 128-thread CTAs (measured 4 -> 2: -0.8 % per pair)
 #endif
 static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
-    if (small_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
+    if (chain_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
+    else if (small_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
     else launch_t<9, MODE_CHUNKS, HC_NTT_CH_SUBS>(c, jobs, inv, N1, use_src, last);
 }
 

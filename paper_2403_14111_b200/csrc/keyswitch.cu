@@ -25,6 +25,7 @@
 //
 // Every step is exact modular arithmetic, so the residues equal the
 // unfused path and the oracle bit for bit.
+#include <unordered_set>
 #include "evaluator.h"
 #include "kernels.cuh"
 #include "ntt_pass.cuh"
@@ -94,8 +95,11 @@ struct LdModup {
     }
 };
 
-template <int LOGSZ, int SUBS, int NA>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
+#ifndef KS_PMB_CHAIN
+#define KS_PMB_CHAIN PASS_MIN_BLOCKS   // register budget of the column passes of a lone key switch (grid z = 1)
+#endif
+template <int LOGSZ, int SUBS, int NA, int PMB = PASS_MIN_BLOCKS>
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
                   u64* __restrict__ I) {
     pdl_trigger();
@@ -243,8 +247,8 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : 3) ks_keyprod_stream(K
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
 // (the P -> Q conversion has the ModUp loader's shape: K inputs, one target)
-template <int LOGSZ, int SUBS, int NK>
-__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PASS_MIN_BLOCKS)
+template <int LOGSZ, int SUBS, int NK, int PMB = PASS_MIN_BLOCKS>
+__global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
                     u64* __restrict__ Wt) {
     pdl_trigger();
@@ -441,12 +445,14 @@ static u64 powm(u64 b, u64 e, u64 q) {
     return r;
 }
 
+// the call-site flag skips the lookup after the first call; the per-kernel set
+// covers call sites that pick one of several instantiations (alpha, K, chain)
 template <class K>
 static void set_smem(K kern, size_t bytes, bool& done) {
-    if (!done) {
+    static std::unordered_set<const void*> seen;
+    (void)done;
+    if (seen.insert((const void*)kern).second)
         HC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        done = true;
-    }
 }
 
 // column-pass geometry per ring degree
@@ -537,10 +543,10 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             launch_k(c, kern, grid, CG::THREADS, csm, jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
         };
         switch (c.alpha) {
-            case 1: go(ks_modup_cols<CL, CS, 1>); break;
-            case 2: go(ks_modup_cols<CL, CS, 2>); break;
-            case 3: go(ks_modup_cols<CL, CS, 3>); break;
-            default: go(ks_modup_cols<CL, CS, 4>); break;
+            case 1: if (nin == 1) go(ks_modup_cols<CL, CS, 1, KS_PMB_CHAIN>); else go(ks_modup_cols<CL, CS, 1>); break;
+            case 2: if (nin == 1) go(ks_modup_cols<CL, CS, 2, KS_PMB_CHAIN>); else go(ks_modup_cols<CL, CS, 2>); break;
+            case 3: if (nin == 1) go(ks_modup_cols<CL, CS, 3, KS_PMB_CHAIN>); else go(ks_modup_cols<CL, CS, 3>); break;
+            default: if (nin == 1) go(ks_modup_cols<CL, CS, 4, KS_PMB_CHAIN>); else go(ks_modup_cols<CL, CS, 4>); break;
         }
         HC_CUDA(cudaGetLastError());
     }
@@ -623,10 +629,10 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
         };
         switch (K) {
-            case 1: go(ks_moddown_cols<CL, CS, 1>); break;
-            case 2: go(ks_moddown_cols<CL, CS, 2>); break;
-            case 3: go(ks_moddown_cols<CL, CS, 3>); break;
-            default: go(ks_moddown_cols<CL, CS, 4>); break;
+            case 1: if (B == 1) go(ks_moddown_cols<CL, CS, 1, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 1>); break;
+            case 2: if (B == 1) go(ks_moddown_cols<CL, CS, 2, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 2>); break;
+            case 3: if (B == 1) go(ks_moddown_cols<CL, CS, 3, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 3>); break;
+            default: if (B == 1) go(ks_moddown_cols<CL, CS, 4, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 4>); break;
         }
         HC_CUDA(cudaGetLastError());
     }

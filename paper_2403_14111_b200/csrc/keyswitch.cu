@@ -315,7 +315,11 @@ struct StModdown {
 #ifndef MD_MINB
 #define MD_MINB (5 * 128 / PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS)
 #endif
-__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, MD_MINB)
+#ifndef MD_MINB_CHAIN
+#define MD_MINB_CHAIN MD_MINB   // the same for a lone key switch (grid z = 1)
+#endif
+template <int MINB = MD_MINB>
+__global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS, MINB)
     ks_moddown_chunks(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Wt, const u64* __restrict__ acc,
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
     pdl_trigger();
@@ -639,13 +643,18 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
     // 6. E: chunk pass + (ACC - W) P^-1 + addend
     {
         static bool at = false;
-        set_smem(ks_moddown_chunks, hsm, at);
+        set_smem(ks_moddown_chunks<>, hsm, at);
+        set_smem(ks_moddown_chunks<MD_MINB_CHAIN>, hsm, at);
         int nadd2 = 0;
         for (int b = 0; b < B; b++) nadd2 += in[b].add2 != nullptr;
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
         dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl, B);
-        launch_k(c, ks_moddown_chunks, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt, ACC, c.d_pinv,
-                                                                add_npoly, kb);
+        if (B == 1)
+            launch_k(c, ks_moddown_chunks<MD_MINB_CHAIN>, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt,
+                     ACC, c.d_pinv, add_npoly, kb);
+        else
+            launch_k(c, ks_moddown_chunks<>, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt, ACC,
+                     c.d_pinv, add_npoly, kb);
         HC_CUDA(cudaGetLastError());
     }
 }

@@ -3,19 +3,25 @@
 One step = DiagABT (config 1: X 128x768 times W^T, W 10x768 vertically tiled,
 period 16) followed by DiagATB (config 2: (P-Y)^T X, RL branch), RNS-CKKS at
 N = 2^16, 58 + 12x42 | 3x60 bits, dnum 4, Delta 2^42, on one 128-row block
-pair per GPU (weak scaling: every rank owns its own block pair, no collective
-on the data path).  Inputs are encrypted (client side) before timing and stay
-resident in HBM; the switching keys alone (2.3 GB) exceed L2, so no flush is
-needed between steps.
+pair.  With N GPUs the pair's c/2 = 8 independent diagonal passes are
+sharded round-robin over the ranks; each rank's partial accumulators are
+mod-summed over NCCL (all-reduce + hc_mod_reduce on the library stream)
+before the replicated conj epilogue -- strong scaling, bit-exact to 1 GPU.
+Inputs are encrypted (client side) before timing and stay resident in HBM;
+the switching keys alone (2.3 GB) exceed L2, so no flush is needed between
+steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload pair|train|softmax|table4]
 
-value = ms per DiagABT+DiagATB pair for the whole job (step time / pairs in
-flight across ranks; lower is better).  e2e = the same through the public
-API with host buffers: the step's input ciphertexts are copied host->device
-from pinned memory and its outputs device->host inside the timed region.
---impl reference times the CPU RNS-CKKS oracle (the reference has no CKKS
-implementation of its own) on the host cores.
+value = ms per DiagABT+DiagATB pair for the whole job (lower is better).
+roofline = the step's algorithmic HBM bytes under SURVEY §8(d)'s per-op
+model (accumulated by the library op by op) over the step time, against the
+measured HBM peak.  e2e = the same through the public API with host buffers:
+the step's input ciphertexts are copied host->device from pinned memory and
+its outputs device->host inside the timed region.  --impl reference times
+whole pairs on the C RNS-CKKS oracle (the reference itself has no CKKS; its
+float64 slot emulator is timed beside it) on the host cores.
 """
 
 from __future__ import annotations
@@ -174,58 +180,128 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
+def all_sum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=_coll_device(), dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def keyswitch_rate(ctx, ct, streams=4, batch=16, reps=4):
+    """Key switches per second of batched level-12 rotations (hc_bench_keyswitch_batch)."""
+    from paper_2403_14111_b200 import _native as N
+    ms = C.c_float()
+    N.check(N.lib().hc_bench_keyswitch_batch(ctx._h, ct._h, streams, batch, 1, C.byref(ms)))   # warm
+    N.check(N.lib().hc_bench_keyswitch_batch(ctx._h, ct._h, streams, batch, reps, C.byref(ms)))
+    return streams * batch * reps / (ms.value * 1e-3)
+
+
+def ncu_evidence():
+    """DRAM traffic and issue utilisation of the key-switch pipeline from the
+    committed ncu --set full capture (profiles/r2/ncu_keyswitch.json)."""
+    path = os.path.join(ROOT, "profiles", "r2", "ncu_keyswitch.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
-# CPU legs (oracle): a bounded sample of the same workload
+# CPU legs: the C RNS-CKKS oracle (the same CKKS computation, all host
+# threads) and the reference's own float64 slot emulator (hefit, 1 core, no
+# cryptography).  Timed on whole DiagABT + DiagATB-RL pairs.
 # ---------------------------------------------------------------------------
 
 
-def oracle_pass_sample(reps=1):
-    """Time one diagonal pass (k = 1 of c/2 = 8) of DiagABT and of DiagATB-RL
-    on the C RNS-CKKS oracle, all host threads; returns ms per pair
-    extrapolated x8 (prologue/epilogue key switches, ~3% of the pair, are
-    not counted, which flatters the CPU)."""
+def oracle_pairs(budget_s, max_pairs):
+    """Whole pairs (DiagABT cfg1 + DiagATB-RL cfg2, every pass, prologue and
+    conj epilogue) on the C RNS-CKKS oracle with OpenMP over all host
+    threads.  The switching keys are generated before timing (the GPU arm's
+    keys are resident too); pairs are timed until `budget_s` or `max_pairs`.
+    Returns (per-pair ms list, setup s)."""
     # torchrun exports OMP_NUM_THREADS=1; the CPU leg uses every host thread
     # (read by libgomp when the oracle library loads)
     os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     from oracle import rns as R
     from oracle import slots as S
     from paper_2403_14111_b200 import workloads as wl
+    from paper_2403_14111_b200.matmul import rotation_steps
 
+    t0 = time.perf_counter()
     X, W = wl.config1()
     PY, _ = wl.config2()
     o = R.OracleCKKSContext("cfg1", 128, seed=1)
     OX, OW, OP = S.encode(o, X), S.encode(o, W, "vertical"), S.encode(o, PY, "horizontal")
-    c = OW.period
-    packed_b = OW.add(S.rot_up(OW, c // 2).each(o.mul_i))
-    packed_a = OP.add(S.rot_left(OP, c // 2).each(o.mul_i))
+    steps = set(rotation_steps(o, "diag_abt", 16)) | set(rotation_steps(o, "diag_atb", 16))
+    for r in sorted(steps):
+        o.p.key(o.p.galois(r))
+    o.p.key(0)
+    o.p.key(2 * o.p.N - 1)
+    setup = time.perf_counter() - t0
     ms = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        sums = S.col_sums(S._rowwise(OX, S.rot_up(packed_b, 1)))
-        sums.mul(S.make_mask(o, 1, c, (1, 1), True, 1.0))
+    t_start = time.perf_counter()
+    while len(ms) < max_pairs and (not ms or time.perf_counter() - t_start + ms[-1] / 1e3 < budget_s):
         t1 = time.perf_counter()
-        left = S.rot_left(packed_a, 1)
-        sums = S.row_sums(S._colwise(left, OX))
-        sums.mul(S.make_mask(o, -1, c, (1, 3), True, 1.0))
-        t2 = time.perf_counter()
-        ms.append(((t1 - t0) + (t2 - t1)) * 1e3 * (c // 2))
-    return ms, o.extra["KeySwitch"]
+        S.diag_abt(OX, OW)
+        S.diag_atb(OP, OX)
+        ms.append((time.perf_counter() - t1) * 1e3)
+    return ms, setup
+
+
+def emulator_pair(reps=3):
+    """The reference's own CPU path: hefit's float64 slot emulator (no
+    cryptography; numpy element-wise complex ops, single-threaded) running
+    the same pair at the same shapes.  None when hefit is not installed
+    (baseline/_ref)."""
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(k, "1")
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "hefit")) and p not in sys.path:
+        sys.path.append(p)
+    try:
+        import hefit
+    except Exception:
+        return None
+    from paper_2403_14111_b200 import workloads as wl
+    X, W = wl.config1()
+    PY, _ = wl.config2()
+    ms = []
+    for _ in range(reps + 1):
+        e = hefit.EmulatorContext(32768, 128, max_level=12)
+        EX, EW = hefit.encode(e, X), hefit.encode(e, W, "vertical")
+        EP = hefit.encode(e, PY, "horizontal")
+        t0 = time.perf_counter()
+        hefit.diag_abt(EX, EW)
+        hefit.diag_atb(EP, EX)
+        ms.append((time.perf_counter() - t0) * 1e3)
+    return {"value": statistics.median(ms[1:]), "unit": "ms", "cores": 1, "kind": "reference",
+            "sample": f"hefit {getattr(hefit, '__version__', '?')} float64 slot emulator (the reference's own CPU "
+                      f"path, no cryptography), whole pair, median of {reps} after 1 warm-up"}
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
     cores = os.cpu_count()
-    samples, _ = oracle_pass_sample(args.warmup + args.steps)
-    timed = samples[args.warmup:]
-    v = statistics.median(timed)
+    # a few minutes at most: whole pairs until ~90 s of timed CPU work
+    ms, setup = oracle_pairs(budget_s=float(os.environ.get("HC_REF_BUDGET_S", "90")), max_pairs=max(1, args.steps))
+    v = statistics.median(ms)
+    emu = emulator_pair()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "steps": len(ms), "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": v, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": CONFIG,
+            "timed_s": round(sum(ms) / 1e3, 1), "setup_s": round(setup, 1), "runs_ms": [round(x, 1) for x in ms],
             "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "port",
-                             "sample": "one of the 8 diagonal passes of DiagABT cfg1 and of DiagATB-RL cfg2 per "
-                                       "step on the C RNS-CKKS oracle (OpenMP, all host threads), x8"},
+                             "sample": f"{len(ms)} whole DiagABT cfg1 + DiagATB-RL cfg2 pairs (all 8 passes, "
+                                       "prologue and conj epilogue) on the C RNS-CKKS oracle, OpenMP over all "
+                                       "host threads; switching keys generated before timing; median"},
+            "reference_emulator": emu,
             "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -243,7 +319,13 @@ def run_b200(args, world, rank, local):
     from paper_2403_14111_b200 import workloads as wl
 
     L = N.lib()
-    ctx = P.CKKSContext("cfg1", 128, seed=1 + rank, device=local)
+    # every rank holds the same keys and inputs; with N > 1 the pair's c/2 = 8
+    # diagonal passes are sharded round-robin over the ranks and the partial
+    # accumulators are mod-summed over NCCL (SURVEY §8(e) k-diagonal sharding)
+    ctx = P.CKKSContext("cfg1", 128, seed=1, device=local)
+    if world > 1:
+        from paper_2403_14111_b200 import sharding
+        ctx.set_pass_shard(world, rank, sharding.NcclModReducer())
     X, W = wl.config1()
     PY, _ = wl.config2()
     EX, EW, EP = P.encode(ctx, X), P.encode(ctx, W, "vertical"), P.encode(ctx, PY, "horizontal")
@@ -262,6 +344,7 @@ def run_b200(args, world, rank, local):
     quiet_gc()
     counts0 = ctx.ledger.counts()
     extra0 = ctx.extra
+    model0 = ctx.model_bytes()
     launches0 = L.hc_launch_count(ctx._h)
     barrier(world)
     N.check(L.hc_timer_begin(ctx._h))
@@ -281,8 +364,10 @@ def run_b200(args, world, rank, local):
     launches = L.hc_launch_count(ctx._h) - launches0
     counts = {k: v - counts0[k] for k, v in ctx.ledger.counts().items()}
     ks = ctx.extra["KeySwitch"] - extra0["KeySwitch"]
+    model_step = all_sum(ctx.model_bytes() - model0, world) / args.steps
+    ks = int(all_sum(ks, world))
     ms_step = total_ms / args.steps
-    value = ms_step / world            # whole job: `world` pairs per step
+    value = ms_step                    # whole job: one pair per step (passes sharded over the ranks)
 
     # one profiled step, serialised on one stream so each kernel's CUDA-event
     # duration is its own (concurrent branches would overlap the intervals)
@@ -351,40 +436,52 @@ def run_b200(args, world, rank, local):
             e2e_step()
         N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
         barrier(world)
-        e2e_runs.append(all_max(ms.value, world) / e2e_steps / world)
+        e2e_runs.append(all_max(ms.value, world) / e2e_steps)
     e2e_ms = statistics.median(e2e_runs)
     # the end-to-end results are the resident run's, bit for bit
     e2e_exact = all(np.array_equal(t.numpy().view(np.uint64), blk.residues().ravel())
                     for blk, t in zip(lg.flat() + gr.flat(), host_out))
 
     hbm, peak_kind = peaks()
+    # level-12 key-switch throughput (batched rotations of one top-level
+    # ciphertext; the §8(d) per-op model charges 94.37 MB per switch)
+    ks_rate = keyswitch_rate(ctx, EX.flat()[0])
+    ks_model = 94.37e6
+    # the dominant kernel of the profiled step (its own algorithmic bytes per
+    # launch over its CUDA-event time), for the breakdown
     top = max(prof.items(), key=lambda kv: kv[1][1])
     name, (n_launch, k_ms, k_bytes) = top
-    achieved = k_bytes / (k_ms * 1e-3) / 1e9
-    # DRAM bytes per launch of the dominant kernel from the committed ncu
-    # --set full capture (a batched rotation at the top level), next to that
-    # launch's algorithmic bytes: traffic close to the algorithmic figure means
-    # no wasted re-reads (the capture's configuration is named in the file)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(name)
-        except Exception:
-            traffic = None
     step_prof_ms = sum(v[1] for v in prof.values())
+    ncu = ncu_evidence()
+    achieved = model_step / (ms_step * 1e-3) / 1e9
+    peak_all = hbm * world
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, BASELINE configs 1-2)",
-        "config": CONFIG,
+        "config": dict(CONFIG, parallelism=f"diagonal passes sharded over {world} rank(s), NCCL mod-sum"
+                       if world > 1 else "1 GPU"),
         "diag_abt_ms": abt_ms, "diag_atb_ms": atb_ms,
-        "keyswitch_per_s": ks * world / (total_ms * 1e-3),
+        "keyswitch_per_s": ks / (total_ms * 1e-3),
         "ledger_per_step": {k: v // args.steps for k, v in counts.items()},
         "keyswitches_per_step": ks // args.steps,
-        "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": traffic,
-                     "launches_per_step": int(n_launch), "kernel_share_of_step": k_ms / step_prof_ms},
+        # algorithmic bytes of the step under the per-op model
+        # (inputs read once, outputs written once, key-switch intermediates on
+        # chip), accumulated by the library op by op at each op's level
+        "roofline": {"bound": "hbm", "basis": "SURVEY 8(d) per-op model of the whole step",
+                     "achieved": achieved, "peak": peak_all, "unit": "GB/s", "frac": achieved / peak_all,
+                     "peak_kind": peak_kind, "model_bytes_per_step": model_step,
+                     "traffic": ncu.get("dram_bytes_per_keyswitch") if ncu else None,
+                     "traffic_ratio": ncu.get("traffic_ratio") if ncu else None,
+                     "traffic_basis": ncu.get("basis") if ncu else None},
+        "keyswitch_level12": {"per_s": ks_rate, "model_bytes": ks_model,
+                              "achieved_gbs": ks_rate * ks_model / 1e9,
+                              "frac": ks_rate * ks_model / 1e9 / hbm,
+                              "sample": "4 streams x batches of 16 rotations of one level-12 ciphertext"},
+        "issue_active_pct": ncu.get("issue_active_pct") if ncu else None,
+        "dominant_kernel": {"name": name, "launches_per_step": int(n_launch), "ms_per_step": k_ms,
+                            "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9,
+                            "share_of_step": k_ms / step_prof_ms},
         "kernel_breakdown_ms": {k: round(v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "transfers": "async copy streams (hc_ct_upload_async / hc_ct_download_async)",
@@ -396,10 +493,12 @@ def run_b200(args, world, rank, local):
     if os.environ.get("HC_BENCH_TRACE"):
         line["host_issue_ms_per_step"] = trace
     if world == 1 and not args.no_cpu:
-        samples, _ = oracle_pass_sample(1)
-        line["cpu_baseline"] = {"value": samples[0], "unit": "ms", "cores": os.cpu_count(), "kind": "port",
-                                "sample": "one of the 8 diagonal passes of DiagABT cfg1 and DiagATB-RL cfg2 on the "
-                                          "C RNS-CKKS oracle (OpenMP, all host threads), x8"}
+        ms_cpu, _ = oracle_pairs(budget_s=1.0, max_pairs=1)
+        line["cpu_baseline"] = {"value": ms_cpu[0], "unit": "ms", "cores": os.cpu_count(), "kind": "port",
+                                "sample": "one whole DiagABT cfg1 + DiagATB-RL cfg2 pair (all 8 passes, prologue, "
+                                          "conj epilogue) on the C RNS-CKKS oracle, OpenMP over all host threads, "
+                                          "keys generated before timing",
+                                "reference_emulator": emulator_pair()}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

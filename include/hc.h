@@ -157,10 +157,44 @@ int hc_row_major_atb(hc_ctx *ctx, const hc_ct *const *A, int m, const hc_ct *con
 int hc_softmax(hc_ctx *ctx, const hc_ct *const *A, int m, int classes, int period, const double *cfg, hc_ct **out,
                int64_t *counts);
 
-/* finish a cross-rank uint64 sum: residues mod q_i in place (K8) */
+/* building blocks of the softmax (hefit/__init__.py:22-28 exports them):
+ * fn = HC_APPROX_COMP a_comp(A, B) (approx.py:205-213), HC_APPROX_MAX
+ * a_max (approx.py:216-238; A one horizontally tiled block column of period
+ * `period`, `classes` active), HC_APPROX_DOMAIN_EXTEND (approx.py:241-253),
+ * HC_APPROX_DEP_COMP (approx.py:256-273), HC_APPROX_EXP (approx.py:276-292),
+ * HC_APPROX_INV (approx.py:295-309).  A[m] (and B[m]) any blocks; out[m];
+ * cfg as for hc_softmax; op order, ledger and refresh points as the reference */
+enum { HC_APPROX_COMP = 0, HC_APPROX_MAX, HC_APPROX_DOMAIN_EXTEND, HC_APPROX_DEP_COMP, HC_APPROX_EXP, HC_APPROX_INV };
+int hc_approx(hc_ctx *ctx, int fn, const hc_ct *const *A, const hc_ct *const *B, int m, int classes, int period,
+              const double *cfg, hc_ct **out, int64_t *counts);
+
+/* finish a cross-rank uint64 sum: residues mod q_i in place (K8); any
+ * 64-bit word is accepted (a sum of R canonical residues with R * q < 2^64) */
 int hc_mod_reduce(hc_ctx *ctx, hc_ct *ct);
+/* block-row sharding: this context holds block rows
+ * [first_block, first_block + m) of a batch of total_blocks (0 = off).  The
+ * batched softmax then draws every refresh nonce the single-context run of
+ * the whole batch would draw (training.py:66-100 data-parallel form), so the
+ * replicated weights stay bit-identical across ranks. */
+int hc_set_shard(hc_ctx *ctx, int total_blocks, int first_block);
+/* diagonal-pass sharding of hc_diag_abt / hc_diag_atb: the
+ * c/2 independent passes of matmul.py:102-108 / 141-152 are split round-robin
+ * (k = rank mod world); before the conj epilogue each context calls
+ * reduce_fn(user, acc, count) on its partial accumulators, which must replace
+ * them by the modular sum over ranks (all-reduce + hc_mod_reduce).  The result
+ * equals the unsharded schedule's residues.  world = 1 turns it off. */
+int hc_set_pass_shard(hc_ctx *ctx, int world, int rank, hc_reduce_fn reduce_fn, void *user);
+/* the CUDA stream (cudaStream_t) the context issues on right now; a
+ * hc_reduce_fn orders its collective and hc_mod_reduce after the pre-sums on
+ * it (stream handoff, no host synchronisation) */
+int hc_ctx_stream(hc_ctx *ctx, void **stream);
 
 /* ---- measurement (no reference counterpart) ---- */
+/* algorithmic HBM bytes of the ledgered ops issued so far under SURVEY §8(d)'s
+ * per-op model (inputs read once, output written once, key-switch
+ * intermediates on chip; Add 6/5/4 Lq, CMult 5Lq-2 / 4Lq-2, Mult
+ * 4Lq + 2d(Lq+K) + 2(Lq-1), Rot/Conj 4Lq + 2d(Lq+K) limbs of 8N bytes) */
+int hc_ctx_model_bytes(hc_ctx *ctx, double *bytes, int reset);
 /* CUDA events on the context stream around a region */
 int hc_timer_begin(hc_ctx *ctx);
 int hc_timer_end(hc_ctx *ctx, float *ms);

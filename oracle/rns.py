@@ -32,6 +32,8 @@ PARAMS = {
     # cfg1's modulus chain on a tiny ring: deep schedules (softmax, NAG step)
     # in milliseconds; not secure, test-only
     "small12": (9, [58] + [42] * 12, [60] * 3, 4, 42, 64),
+    # the same chain at the reference's default training ring (2^13 slots x 2)
+    "n13l12": (13, [58] + [42] * 12, [60] * 3, 4, 42, 64),
     "tiny": (10, [50] + [40] * 3, [50], 1, 40, 32),
 }
 

@@ -7,7 +7,20 @@ training step — with ciphertexts resident in B200 HBM and every op a
 hand-written sm_100a CUDA kernel sequence behind the C-ABI in include/hc.h.
 """
 
-from .approx import COMP_F, COMP_G, DEFAULTS, EXP_POLY, SoftmaxConfig, a_softmax
+from .approx import (
+    COMP_F,
+    COMP_G,
+    DEFAULTS,
+    EXP_POLY,
+    SoftmaxConfig,
+    a_comp,
+    a_exp,
+    a_inv,
+    a_max,
+    a_softmax,
+    dep_compensation,
+    domain_extend,
+)
 from .context import (
     DECODE_TOL,
     DEFAULT_OP_WEIGHTS_MS,
@@ -55,6 +68,7 @@ from .training import (
     log_loss,
     nag_step,
     one_hot,
+    default_context,
     run_steps,
 )
 

@@ -78,9 +78,14 @@ SIGNATURES = {
     "hc_diag_abt": (I, [P, PP, I, I, PP, I, D, PP, I64P]),
     "hc_diag_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P, REDUCE_FN, P]),
     "hc_softmax": (I, [P, PP, I, I, I, DP, PP, I64P]),
+    "hc_approx": (I, [P, I, PP, PP, I, I, I, DP, PP, I64P]),
     "hc_col_major_abt": (I, [P, PP, I, I, PP, I, D, PP, I64P]),
     "hc_row_major_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P]),
     "hc_mod_reduce": (I, [P, P]),
+    "hc_set_shard": (I, [P, I, I]),
+    "hc_set_pass_shard": (I, [P, I, I, REDUCE_FN, P]),
+    "hc_ctx_model_bytes": (I, [P, DP, I]),
+    "hc_ctx_stream": (I, [P, PP]),
     "hc_timer_begin": (I, [P]),
     "hc_timer_end": (I, [P, C.POINTER(C.c_float)]),
     "hc_launch_count": (I64, [P]),

@@ -6,6 +6,9 @@ order: tournament max (log2(period) rounds of f∘g∘g comparisons), domain
 extension, degree-5 compensation, degree-12 exp + squarings, col_sums and
 16 Goldschmidt iterations, with the refresh surrogate at every level-0
 multiplication operand exactly where the reference auto-bootstraps.
+The building blocks ``a_comp`` / ``a_max`` / ``domain_extend`` / ``a_exp`` /
+``a_inv`` (hefit/__init__.py:22-28) are exported the same way, each one
+native call (``hc_approx``) over all blocks of its operand in lockstep.
 The float64 array carrier of the reference is its plaintext twin; it lives in
 the test oracle (oracle/slots.py), not in this package.
 """
@@ -81,3 +84,67 @@ def a_softmax(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS, classes: int | No
     N.check(N.lib().hc_softmax(ctx._h, _handles(M.flat()), m, classes, period, cfg.as_array(), out, counts))
     blocks = tuple((Ciphertext(ctx, C.c_void_p(out[p])),) for p in range(m))
     return EncodedMatrix(ctx, blocks, (M.shape[0], classes), "horizontal", period)
+
+
+# -- building blocks (approx.py:195-309), encrypted carrier ----------------------
+
+HC_APPROX_COMP, HC_APPROX_MAX, HC_APPROX_DOMAIN_EXTEND, HC_APPROX_DEP_COMP, HC_APPROX_EXP, HC_APPROX_INV = range(6)
+
+
+def _approx(fn: int, M: EncodedMatrix, cfg: SoftmaxConfig, other: EncodedMatrix | None = None, classes: int = 0,
+            period: int = 0) -> EncodedMatrix:
+    if not isinstance(M, EncodedMatrix):
+        raise TypeError("the B200 backend takes an encrypted EncodedMatrix "
+                        "(the float64 array carrier is the plaintext twin, see oracle/slots.py)")
+    ctx = _native_ctx(M) if other is None else _native_ctx(M, other)
+    if other is not None and (other.grid != M.grid):
+        raise ShapeMismatch(f"operand grids differ: {M.grid} vs {other.grid}")
+    blocks = M.flat()
+    out = (C.c_void_p * len(blocks))()
+    counts = (C.c_int64 * N.NCOUNTS)()
+    N.check(N.lib().hc_approx(ctx._h, fn, _handles(blocks), _handles(other.flat()) if other is not None else None,
+                              len(blocks), classes, period, cfg.as_array(), out, counts))
+    m, n = M.grid
+    res = tuple(tuple(Ciphertext(ctx, C.c_void_p(out[p * n + q])) for q in range(n)) for p in range(m))
+    return EncodedMatrix(ctx, res, M.shape, M.tiling, M.period)
+
+
+def a_comp(x: EncodedMatrix, y: EncodedMatrix) -> EncodedMatrix:
+    """Soft comparison (approx.py:205-213): ~1 where x > y, 1/2 at equality;
+    f o g o g of odd degree-7 polynomials on inputs in [-1/2, 1/2]."""
+    return _approx(HC_APPROX_COMP, x, DEFAULTS, other=y)
+
+
+def a_max(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS, classes: int | None = None,
+          period: int | None = None) -> EncodedMatrix:
+    """Row-wise approximate maximum broadcast over the row (approx.py:216-238)."""
+    if M.tiling != "horizontal" or M.grid[1] != 1:
+        raise ShapeMismatch("a_max expects a horizontally tiled single-block-column matrix")
+    classes = M.shape[1] if classes is None else classes
+    period = M.period if period is None else period
+    if period < classes:
+        raise ShapeMismatch(f"period {period} smaller than classes {classes}")
+    return _approx(HC_APPROX_MAX, M, cfg, classes=classes, period=period)
+
+
+def domain_extend(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS) -> EncodedMatrix:
+    """Contract [-max_range, max_range] into the exp's base range (approx.py:241-253)."""
+    return _approx(HC_APPROX_DOMAIN_EXTEND, M, cfg)
+
+
+def dep_compensation(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS) -> EncodedMatrix:
+    """Degree-5 correction of the contraction bias (approx.py:256-273, ``_dep_compensation``)."""
+    return _approx(HC_APPROX_DEP_COMP, M, cfg)
+
+
+def a_exp(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS) -> EncodedMatrix:
+    """exp on [-exp_range, exp_range]: degree-12 fit at x/B, squared log2(B) times (approx.py:276-292)."""
+    if cfg.exp_range < 1 or cfg.exp_range & (cfg.exp_range - 1):
+        raise ShapeMismatch(f"exp_range must be a power of two, got {cfg.exp_range}")
+    return _approx(HC_APPROX_EXP, M, cfg)
+
+
+def a_inv(M: EncodedMatrix, cfg: SoftmaxConfig = DEFAULTS) -> EncodedMatrix:
+    """Goldschmidt reciprocal normalised by inv_range (approx.py:295-309)."""
+    return _approx(HC_APPROX_INV, M, cfg)
+

@@ -42,6 +42,9 @@ PARAMS = {
     "cfg1": (16, [58] + [42] * 12, [60] * 3, 4, 42, 64),
     # cfg1's chain on a tiny ring (test-only, insecure)
     "small12": (9, [58] + [42] * 12, [60] * 3, 4, 42, 64),
+    # cfg1's chain at the reference's default run_steps context
+    # (EmulatorContext(4096, 64, max_level=12), training.py:361); insecure ring
+    "n13l12": (13, [58] + [42] * 12, [60] * 3, 4, 42, 64),
     "tiny": (10, [50] + [40] * 3, [50], 1, 40, 32),
 }
 
@@ -264,6 +267,41 @@ class CKKSContext:
 
     def sync(self):
         N.check(N.lib().hc_sync(self._h))
+
+    def model_bytes(self, reset: bool = False) -> float:
+        """SURVEY §8(d) per-op HBM model (bytes) of the ledgered ops so far."""
+        v = C.c_double()
+        N.check(N.lib().hc_ctx_model_bytes(self._h, C.byref(v), int(reset)))
+        return v.value
+
+    def set_shard(self, total_blocks: int, first_block: int) -> None:
+        """Block-row sharding: this context holds block rows
+        ``first_block ..`` of a batch of ``total_blocks``; the softmax's refresh
+        nonces then follow the whole batch's sequential order (``hc_set_shard``)."""
+        N.check(N.lib().hc_set_shard(self._h, int(total_blocks), int(first_block)))
+
+    def set_pass_shard(self, world: int, rank: int, reducer=None) -> None:
+        """Diagonal-pass sharding of diag_abt / diag_atb (``hc_set_pass_shard``):
+        this context runs passes k = rank (mod world); ``reducer(ctx, handles)``
+        replaces the partial accumulators by their modular sum over ranks."""
+        if world > 1 and reducer is None:
+            raise ValueError("pass sharding needs a reducer")
+        if world > 1:
+            from .matmul import _reduce_callback
+            self._pass_cb = _reduce_callback(self, reducer)
+        else:
+            self._pass_cb = N.REDUCE_FN(0)
+        N.check(N.lib().hc_set_pass_shard(self._h, int(world), int(rank), self._pass_cb, None))
+
+    def stream(self) -> int:
+        """The cudaStream_t the library issues on right now (for stream handoff)."""
+        s = C.c_void_p()
+        N.check(N.lib().hc_ctx_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
+    def mod_reduce(self, ct) -> None:
+        """Finish a cross-rank uint64 sum held in ``ct``'s residues, in place (K8)."""
+        N.check(N.lib().hc_mod_reduce(self._h, ct._h if isinstance(ct, Ciphertext) else ct))
 
     def keygen(self, galois: int):
         N.check(N.lib().hc_keygen(self._h, int(galois)))

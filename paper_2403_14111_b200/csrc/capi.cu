@@ -360,6 +360,48 @@ int hc_level_adjust(hc_ctx* ctx, const hc_ct* a, int level, hc_ct** out) {
     return guard([&] { *out = wrap(hc::ev_level_adjust(*ctx->c, *a->p, level)); });
 }
 
+int hc_ctx_model_bytes(hc_ctx* ctx, double* bytes, int reset) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(ctx->c->mu);
+        if (bytes) *bytes = ctx->c->model_bytes;
+        if (reset) ctx->c->model_bytes = 0;
+    });
+}
+
+int hc_set_shard(hc_ctx* ctx, int total_blocks, int first_block) {
+    return guard([&] {
+        if (total_blocks < 0 || first_block < 0 || (total_blocks && first_block >= total_blocks))
+            throw hc::Error(HC_EPARAM, "bad shard");
+        ctx->c->shard_total = total_blocks;
+        ctx->c->shard_first = first_block;
+    });
+}
+
+int hc_set_pass_shard(hc_ctx* ctx, int world, int rank, hc_reduce_fn reduce_fn, void* user) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw hc::Error(HC_EPARAM, "bad pass shard");
+        if (world > 1 && !reduce_fn) throw hc::Error(HC_EPARAM, "pass sharding needs a reducer");
+        hc::Ctx& c = *ctx->c;
+        c.pass_world = world;
+        c.pass_rank = rank;
+        if (world == 1) {
+            c.pass_reducer = nullptr;
+            return;
+        }
+        c.pass_reducer = [reduce_fn, user](std::vector<hc::CtP>& cts) {
+            std::vector<hc_ct*> hs(cts.size());
+            for (size_t i = 0; i < cts.size(); i++) hs[i] = wrap(cts[i]);
+            const int rc = reduce_fn(user, hs.data(), (int)hs.size());
+            for (size_t i = 0; i < cts.size(); i++) { cts[i] = hs[i]->p; delete hs[i]; }
+            if (rc) throw hc::Error(HC_ECUDA, "cross-rank pass reduction failed");
+        };
+    });
+}
+
+int hc_ctx_stream(hc_ctx* ctx, void** stream) {
+    return guard([&] { *stream = (void*)ctx->c->stream; });
+}
+
 int hc_mod_reduce(hc_ctx* ctx, hc_ct* ct) {
     return guard([&] { hc::k_mod_reduce(*ctx->c, ct->p->d, ct->p->level + 1, ct->p->npoly); });
 }
@@ -558,7 +600,8 @@ int hc_diag_atb(hc_ctx* ctx, const hc_ct* const* A, int m, const hc_ct* const* B
             red = [&](std::vector<hc::CtP>& cts) {
                 std::vector<hc_ct*> hs(cts.size());
                 for (size_t i = 0; i < cts.size(); i++) hs[i] = wrap(cts[i]);
-                HC_CUDA(cudaStreamSynchronize(ctx->c->stream));
+                // no host synchronisation: the reducer orders its collective
+                // after the pre-sums on hc_ctx_stream() (stream handoff)
                 const int rc = reduce_fn(user, hs.data(), (int)hs.size());
                 for (size_t i = 0; i < cts.size(); i++) { cts[i] = hs[i]->p; delete hs[i]; }
                 if (rc) throw hc::Error(HC_ECUDA, "cross-rank reduction failed");
@@ -606,6 +649,23 @@ int hc_softmax(hc_ctx* ctx, const hc_ct* const* A, int m, int classes, int perio
         hc::SoftmaxCfg sc;
         if (cfg) sc = hc::SoftmaxCfg::from(cfg);
         std::vector<hc::CtP> res = hc::sched_softmax(ev, unwrap(A, m), classes, period, sc);
+        for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
+        add_counts(ctx, before, counts);
+    });
+}
+
+int hc_approx(hc_ctx* ctx, int fn, const hc_ct* const* A, const hc_ct* const* B, int m, int classes, int period,
+              const double* cfg, hc_ct** out, int64_t* counts) {
+    return guard([&] {
+        int64_t before[HC_NCOUNTS];
+        snap(ctx, before);
+        RunAhead throttle(*ctx->c);
+        hc::Eval ev(*ctx->c, ctx->auto_boot);
+        hc::SoftmaxCfg sc;
+        if (cfg) sc = hc::SoftmaxCfg::from(cfg);
+        std::vector<hc::CtP> y;
+        if (fn == hc::APPROX_COMP) y = unwrap(B, m);
+        std::vector<hc::CtP> res = hc::sched_approx(ev, fn, unwrap(A, m), y, classes, period, sc);
         for (int i = 0; i < m; i++) out[i] = wrap(res[i]);
         add_counts(ctx, before, counts);
     });

@@ -4,6 +4,7 @@
 // Every choice follows the CKKS spec in DESIGN.md §3; the host encoder is
 // compiled with -ffp-contract=off so its double arithmetic is bit-identical
 // to the oracle's (oracle/ckks_oracle.c) on the same machine.
+#include <set>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -457,6 +458,7 @@ void ctx_destroy(Ctx* c) {
                      v[1] / 1e9, v[2] / 1e9, v[3] / 1e9);
     }
     c->pt_cache.clear();
+    c->pt_cache_bytes = 0;
     for (auto& kv : c->keys) cudaFree(kv.second.d);
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
@@ -704,6 +706,16 @@ CtP refresh(Ctx& c, const Ct& a, u64 nonce) {
     CtP out = encrypt_coef_dev(c, m, c.L, nonce);
     c.free((u64*)m);
     return out;
+}
+
+void set_smem_attr(const void* kern, size_t bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    HC_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert({kern, dev}).second)
+        HC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 }  // namespace hc

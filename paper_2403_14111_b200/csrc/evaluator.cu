@@ -7,6 +7,7 @@
 //   key inner product (128-bit lazy accumulation, one Barrett reduction) ->
 //   INTT of the P limbs -> ModDown conversion -> NTT -> (acc - conv) * P^-1
 //   with the automorphism's c0 / the tensor's (d0, d1) added in the same pass.
+#include <cstdlib>
 #include <cmath>
 #include <map>
 
@@ -475,6 +476,25 @@ void Eval::rec(int k, int n) {
     c.counts[k] += n;
 }
 
+double model_limbs(const Ctx& c, int kind, int variant, int level) {
+    const double Lq = level + 1, d = (level + c.alpha) / c.alpha;
+    switch (kind) {
+        case OP_ADD: return variant == MV_CT ? 6 * Lq : (variant == MV_PT ? 5 * Lq : 4 * Lq);
+        case OP_CMULT: return variant == MV_PT ? 5 * Lq - 2 : 4 * Lq - 2;
+        case OP_MULT: return 4 * Lq + 2 * d * (Lq + c.K) + 2 * (Lq - 1);
+        case OP_ROT:
+        case OP_CONJ: return 4 * Lq + 2 * d * (Lq + c.K);
+        case MODEL_MULI: return 4 * Lq;
+        default: return 0;
+    }
+}
+
+void Eval::model(int kind, int variant, int level, int n) {
+    const double b = n * model_limbs(c, kind, variant, level) * 8.0 * c.N;
+    std::lock_guard<std::mutex> g(c.mu);
+    c.model_bytes += b;
+}
+
 u64 Eval::next_nonce() {
     std::lock_guard<std::mutex> g(c.mu);
     return c.nonce++;
@@ -487,8 +507,29 @@ CtP Eval::at(const CtP& a, int level) {
 }
 
 u64 Eval::boot_nonce(int j, int r) {
+    if (plan.on && plan.mloc > 1) throw Error(-4, "single-operand refresh inside a multi-block nonce plan");
     rec(OP_BOOT);
     return plan.on ? plan.base + (u64)plan.m * plan.events + (u64)plan.p * r + j : next_nonce();
+}
+
+std::vector<u64> Eval::batch_nonces(const std::vector<int>& r) {
+    std::vector<u64> out;
+    const size_t n = r.size();
+    const size_t ml = plan.on ? (size_t)std::max(plan.mloc, 1) : 1;
+    if (n % ml) throw Error(-4, "sharded batch: items are not whole rounds over the shard's blocks");
+    for (size_t s0 = 0; s0 < n; s0 += ml) {
+        const int rs = r[s0];
+        for (size_t i = s0; i < s0 + ml; i++) {
+            if (r[i] != rs) throw Error(-4, "sharded batch: blocks of one op at different levels");
+            for (int j = 0; j < rs; j++) {
+                rec(OP_BOOT);
+                out.push_back(plan.on ? plan.base + (u64)plan.m * plan.events + (u64)(plan.p + (int)(i - s0)) * rs + j
+                                      : next_nonce());
+            }
+        }
+        plan.events += rs;
+    }
+    return out;
 }
 
 CtP Eval::refresh_planned(const CtP& a, int j, int r) { return refresh(c, *a, boot_nonce(j, r)); }
@@ -511,15 +552,16 @@ static void refresh_many(Ctx& c, std::vector<CtP*>& slots, const std::vector<u64
 
 void Eval::ready_batch(std::vector<CtP>& xs) {
     std::vector<CtP*> slots;
-    std::vector<u64> nonces;
-    for (auto& x : xs) {
-        if (x->level >= 1) continue;
+    std::vector<int> r(xs.size(), 0);
+    for (size_t i = 0; i < xs.size(); i++) {
+        if (xs[i]->level >= 1) continue;
         if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
-        nonces.push_back(boot_nonce(0, 1));
-        plan.events += 1;
-        slots.push_back(&x);
+        r[i] = 1;
+        slots.push_back(&xs[i]);
     }
-    if (!slots.empty()) refresh_many(c, slots, nonces);
+    if (slots.empty()) return;
+    std::vector<u64> nonces = batch_nonces(r);
+    refresh_many(c, slots, nonces);
 }
 
 CtP Eval::ready(const CtP& a) {
@@ -533,11 +575,13 @@ CtP Eval::ready(const CtP& a) {
 CtP Eval::add(const CtP& a, const CtP& b, bool sub) {
     rec(OP_ADD);
     const int l = std::min(a->level, b->level);
+    model(OP_ADD, MV_CT, l);
     return ev_add(c, *at(a, l), *at(b, l), sub);
 }
 
 CtP Eval::add_c(const CtP& a, std::complex<double> s, bool sub, bool reversed) {
     rec(OP_ADD);
+    model(OP_ADD, MV_SCALAR, a->level);
     // ct + s, ct - s, s - ct
     if (reversed) return ev_add_const(c, *a, s.real(), s.imag(), true);
     if (sub) s = -s;
@@ -546,6 +590,7 @@ CtP Eval::add_c(const CtP& a, std::complex<double> s, bool sub, bool reversed) {
 
 CtP Eval::add_p(const CtP& a, const Pattern& p, bool sub, bool reversed) {
     rec(OP_ADD);
+    model(OP_ADD, MV_PT, a->level);
     PtP pt = encoded(p, a->level);
     return ev_add_pt(c, *a, *pt, sub, reversed);
 }
@@ -561,18 +606,21 @@ CtP Eval::mult(const CtP& x, const CtP& y) {
     plan.events += r;
     rec(OP_MULT);
     const int l = std::min(a->level, b->level);
+    model(OP_MULT, MV_CT, l);
     return ev_mult(c, *at(a, l), *at(b, l));
 }
 
 CtP Eval::mult_c(const CtP& x, std::complex<double> s) {
     CtP a = ready(x);
     rec(OP_CMULT);
+    model(OP_CMULT, MV_SCALAR, a->level);
     return ev_mul_const(c, *a, s.real(), s.imag());
 }
 
 CtP Eval::mult_p(const CtP& x, const Pattern& p) {
     CtP a = ready(x);
     rec(OP_CMULT);
+    model(OP_CMULT, MV_PT, a->level);
     PtP pt = encoded(p, a->level);
     return ev_mul_pt(c, *a, *pt);
 }
@@ -582,6 +630,7 @@ CtP Eval::lrot(const CtP& a, int64_t r) {
     r = ((r % S) + S) % S;
     if (r == 0) return a;
     rec(OP_ROT);
+    model(OP_ROT, MV_CT, a->level);
     return ev_automorph(c, *a, galois_rot(c, r));
 }
 
@@ -591,6 +640,8 @@ CtP Eval::add_lrot(const CtP& a, int64_t r) {
     if (r == 0) return add(a, a);
     rec(OP_ROT);
     rec(OP_ADD);
+    model(OP_ROT, MV_CT, a->level);
+    model(OP_ADD, MV_CT, a->level);
     CtP o;
     if (ev_automorph_add(c, *a, galois_rot(c, r), o)) return o;
     CtP rot = ev_automorph(c, *a, galois_rot(c, r));
@@ -607,6 +658,10 @@ std::vector<CtP> Eval::lrot_batch(const std::vector<CtP>& xs, int64_t r, bool ad
     }
     rec(OP_ROT, (int)xs.size());
     if (add_self) rec(OP_ADD, (int)xs.size());
+    for (auto& x : xs) {
+        model(OP_ROT, MV_CT, x->level);
+        if (add_self) model(OP_ADD, MV_CT, x->level);
+    }
     std::vector<const Ct*> a(xs.size());
     for (size_t i = 0; i < xs.size(); i++) a[i] = xs[i].get();
     return ev_automorph_batch(c, a, galois_rot(c, r), add_self);
@@ -614,6 +669,7 @@ std::vector<CtP> Eval::lrot_batch(const std::vector<CtP>& xs, int64_t r, bool ad
 
 std::vector<CtP> Eval::conj_batch(const std::vector<CtP>& xs) {
     rec(OP_CONJ, (int)xs.size());
+    for (auto& x : xs) model(OP_CONJ, MV_CT, x->level);
     std::vector<const Ct*> a(xs.size());
     for (size_t i = 0; i < xs.size(); i++) a[i] = xs[i].get();
     return ev_automorph_batch(c, a, 2 * (u64)c.N - 1, false);
@@ -626,18 +682,21 @@ std::vector<CtP> Eval::mult_batch(const std::vector<CtP>& xs_in, const std::vect
     // op-by-op order -- x before y, product by product -- so every refresh
     // draws the nonce the sequential order gives it; then one batch
     std::vector<CtP*> slots;
-    std::vector<u64> nonces;
+    std::vector<int> rs(xs.size(), 0);
     for (size_t i = 0; i < xs.size(); i++) {
         const int r = (xs[i]->level < 1 ? 1 : 0) + (ys[i]->level < 1 ? 1 : 0);
         if (!r) continue;
         if (!auto_boot) throw Error(-3, "mult: operand at level 0 cannot be multiplied");
-        int j = 0;
-        if (xs[i]->level < 1) { nonces.push_back(boot_nonce(j++, r)); slots.push_back(&xs[i]); }
-        if (ys[i]->level < 1) { nonces.push_back(boot_nonce(j++, r)); slots.push_back(&ys[i]); }
-        plan.events += r;
+        rs[i] = r;
+        if (xs[i]->level < 1) slots.push_back(&xs[i]);
+        if (ys[i]->level < 1) slots.push_back(&ys[i]);
     }
-    if (!slots.empty()) refresh_many(c, slots, nonces);
+    if (!slots.empty()) {
+        std::vector<u64> nonces = batch_nonces(rs);
+        refresh_many(c, slots, nonces);
+    }
     rec(OP_MULT, (int)xs.size());
+    for (size_t i = 0; i < xs.size(); i++) model(OP_MULT, MV_CT, std::min(xs[i]->level, ys[i]->level));
     // level adjustments in batches; an operand shared by several products
     // (DiagATB's B blocks, one per pass) is adjusted once (deterministic)
     std::vector<int> ls(xs.size());
@@ -679,6 +738,7 @@ std::vector<std::vector<CtP>> Eval::lrot_hoisted(const std::vector<CtP>& xs, con
     int moving = 0;
     for (auto v : rr) moving += v != 0;
     rec(OP_ROT, moving * (int)xs.size());
+    for (auto& x : xs) model(OP_ROT, MV_CT, x->level, moving);
     // one hoisted pipeline per level present
     std::vector<char> done(xs.size(), 0);
     for (size_t i = 0; i < xs.size(); i++) {
@@ -730,6 +790,8 @@ std::vector<CtP> Eval::mult_sum_batch(const std::vector<std::vector<CtP>>& as, c
             groups.push_back(gr);
             rec(OP_MULT, (int)as[i].size());
             rec(OP_ADD, (int)as[i].size() - 1);
+            model(OP_MULT, MV_CT, l, (int)as[i].size());
+            model(OP_ADD, MV_CT, l - 1, (int)as[i].size() - 1);
         }
         std::vector<CtP> r = ev_mult_sum_batch(c, groups);
         for (size_t t = 0; t < idx.size(); t++) out[idx[t]] = r[t];
@@ -786,6 +848,7 @@ std::vector<CtP> Eval::add_batch(const std::vector<CtP>& xs_in, const std::vecto
     }
     rec(OP_ADD, (int)xs.size());
     const int level = xs[0]->level;
+    model(OP_ADD, MV_CT, level, (int)xs.size());
     std::vector<u64*> o(xs.size());
     std::vector<const u64*> a(xs.size()), b(xs.size());
     for (size_t i = 0; i < xs.size(); i++) {
@@ -809,6 +872,7 @@ std::vector<CtP> Eval::add_c_batch(const std::vector<CtP>& xs, std::complex<doub
     }
     rec(OP_ADD, (int)xs.size());
     const int level = xs[0]->level;
+    model(OP_ADD, MV_SCALAR, level, (int)xs.size());
     if (!reversed && sub) s = -s;
     const double sc = c.scale[level];
     ConstTab t;
@@ -835,6 +899,7 @@ std::vector<CtP> Eval::add_p_batch(const std::vector<CtP>& xs, const Pattern& p,
     }
     rec(OP_ADD, (int)xs.size());
     const int level = xs[0]->level;
+    model(OP_ADD, MV_PT, level, (int)xs.size());
     PtP pt = encoded(p, level);
     std::vector<u64*> o(xs.size());
     std::vector<const u64*> a(xs.size()), b(xs.size(), pt->d);
@@ -860,6 +925,7 @@ std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs_in, std::complex<
     }
     rec(OP_CMULT, (int)xs.size());
     const int level = xs[0]->level;
+    model(OP_CMULT, MV_SCALAR, level, (int)xs.size());
     const size_t poly = (size_t)(level + 1) * c.N;
     const double sc = c.scale[level];
     ConstTab t;
@@ -884,6 +950,7 @@ std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs_in, const std::ve
     }
     rec(OP_CMULT, (int)xs.size());
     const int level = xs[0]->level;
+    model(OP_CMULT, MV_PT, level, (int)xs.size());
     const size_t poly = (size_t)(level + 1) * c.N;
     Scratch sc(c);
     u64* T = sc.take(2 * poly * xs.size());
@@ -897,10 +964,14 @@ std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs_in, const std::ve
 
 CtP Eval::conj(const CtP& a) {
     rec(OP_CONJ);
+    model(OP_CONJ, MV_CT, a->level);
     return ev_automorph(c, *a, 2 * (u64)c.N - 1);
 }
 
-CtP Eval::mul_i(const CtP& a) { return ev_mul_i(c, *a); }
+CtP Eval::mul_i(const CtP& a) {
+    model(MODEL_MULI, MV_CT, a->level);   // unledgered (emulator.py:259-265) but charged by §8(d)
+    return ev_mul_i(c, *a);
+}
 
 CtP Eval::bootstrap(const CtP& a) {
     CtP o = refresh_planned(a, 0, 1);
@@ -913,7 +984,10 @@ PtP Eval::encoded(const Pattern& p, int level) {
     {
         std::lock_guard<std::mutex> g(c.mu);
         auto it = c.pt_cache.find(key);
-        if (it != c.pt_cache.end()) return it->second;
+        if (it != c.pt_cache.end()) {
+            it->second.used = ++c.pt_clock;
+            return it->second.pt;
+        }
     }
     std::vector<std::complex<double>> generated;
     const std::vector<std::complex<double>>* vals = &p.vals;
@@ -926,7 +1000,23 @@ PtP Eval::encoded(const Pattern& p, int level) {
     for (size_t i = 0; i < vals->size(); i++) { zr[i] = (*vals)[i].real(); zi[i] = (*vals)[i].imag(); }
     PtP pt = encode_pt(c, zr.data(), zi.data(), level, c.scale[level]);
     std::lock_guard<std::mutex> g(c.mu);
-    c.pt_cache[key] = pt;
+    if (!c.pt_cache_cap) {
+        const char* e = std::getenv("HC_PT_CACHE_MB");
+        c.pt_cache_cap = (size_t)(e ? std::atoll(e) : 4096) << 20;
+    }
+    const size_t bytes = (size_t)(level + 1) * c.N * 8;
+    auto ins = c.pt_cache.emplace(key, Ctx::PtEntry{pt, ++c.pt_clock});
+    if (!ins.second) return ins.first->second.pt;
+    c.pt_cache_bytes += bytes;
+    // evict least-recently-used entries (never the one just inserted); a
+    // schedule still holding an evicted plaintext keeps it alive (shared_ptr)
+    while (c.pt_cache_bytes > c.pt_cache_cap && c.pt_cache.size() > 1) {
+        auto lru = c.pt_cache.end();
+        for (auto it = c.pt_cache.begin(); it != c.pt_cache.end(); ++it)
+            if (it != ins.first && (lru == c.pt_cache.end() || it->second.used < lru->second.used)) lru = it;
+        c.pt_cache_bytes -= (size_t)(lru->second.pt->level + 1) * c.N * 8;
+        c.pt_cache.erase(lru);
+    }
     return pt;
 }
 

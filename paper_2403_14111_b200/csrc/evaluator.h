@@ -58,12 +58,24 @@ struct Pattern {
 //   base + m * (refreshes in its earlier ops) + p * r + j,
 // exactly the nonce the sequential order assigns (all blocks share one level
 // history, so every block refreshes the same operands in the same ops).
+//
+// A shard holding mloc consecutive blocks p .. p + mloc - 1 of m runs them in
+// lockstep: a batched op lists its items [sub-op][block] (mloc blocks per
+// sub-op), and item i of a sub-op drawing r refreshes takes
+//   base + m * events + (p + i) * r + j,
+// then events += r -- again the nonces of the whole batch's sequential run.
 struct NoncePlan {
     bool on = false;
     u64 base = 0;
-    int m = 1, p = 0;
+    int m = 1, p = 0, mloc = 1;
     u64 events = 0;
 };
+
+// operand kinds of the per-op HBM model: ct (op) ct, ct (op) plaintext, ct (op) scalar
+enum { MV_CT = 0, MV_PT, MV_SCALAR };
+constexpr int MODEL_MULI = 100;   // model kind of mul_i (not a ledger slot)
+// limbs (8N bytes each) the §8(d) model charges one op at `level`
+double model_limbs(const Ctx& c, int kind, int variant, int level);
 
 struct Eval {
     Ctx& c;
@@ -75,8 +87,14 @@ struct Eval {
     u64 boot_nonce(int j, int r);
     // ready() over a vector: level-0 operands refreshed (block order, batched)
     void ready_batch(std::vector<CtP>& xs);
+    // nonces of a batched op whose item i draws r[i] refreshes (records the
+    // Bootstraps); sequential draws, or the plan's layout above
+    std::vector<u64> batch_nonces(const std::vector<int>& r);
 
     void rec(int kind, int n = 1);
+    // SURVEY §8(d) per-op HBM model of a ledgered op at `level` (operand
+    // kind MV_*), accumulated in Ctx::model_bytes (hc_ctx_model_bytes)
+    void model(int kind, int variant, int level, int n = 1);
     u64 next_nonce();
     CtP at(const CtP& a, int level);
     // at() over a vector (in place, slot i to level ls[i]), batched per (source, target) level

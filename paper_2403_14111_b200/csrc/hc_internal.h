@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -86,6 +87,15 @@ struct Ctx {
     u64 seed;
     int device;
     int grid_rows = 0;            // s0 of the slot grid (EmulatorContext.grid_rows)
+    // block-row sharding (hc_set_shard): this context holds block rows
+    // [shard_first, shard_first + m) of a batch of shard_total; refresh nonces
+    // follow the whole batch's sequential order (evaluator.h NoncePlan)
+    int shard_total = 0, shard_first = 0;
+    // diagonal-pass sharding (hc_set_pass_shard): this context runs passes
+    // k = pass_rank (mod pass_world) of DiagABT / DiagATB and pass_reducer
+    // replaces the partial accumulators by their modular sum over ranks
+    int pass_world = 1, pass_rank = 0;
+    std::function<void(std::vector<std::shared_ptr<struct Ct>>&)> pass_reducer;
     // `stream` is the stream every launch / allocation goes to.  It is the
     // context's main stream except inside a schedule's fork region, where it
     // temporarily names one of the side streams (see schedules.cu Fork).
@@ -140,9 +150,18 @@ struct Ctx {
     // counters
     uint64_t nonce = 0;
     int64_t counts[OP_NKIND] = {0};
+    double model_bytes = 0;       // SURVEY §8(d) per-op HBM model of the ledgered ops (Eval::model)
     std::mutex mu;
-    // encoded-mask cache used by the native schedules
-    std::map<std::string, PtP> pt_cache;
+    // encoded-mask cache used by the native schedules and content-addressed
+    // Python operands: least-recently-used eviction above pt_cache_cap bytes
+    // (HC_PT_CACHE_MB, default 4096)
+    struct PtEntry {
+        PtP pt;
+        uint64_t used;
+    };
+    std::map<std::string, PtEntry> pt_cache;
+    size_t pt_cache_bytes = 0, pt_cache_cap = 0;
+    uint64_t pt_clock = 0;
 
     // the C-ABI's owning handle; every ciphertext/plaintext handle holds a
     // strong reference, so the context outlives all of them in any
@@ -225,6 +244,14 @@ inline void launch_k(Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block, size
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     HC_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per (kernel, device);
+// thread-safe (contexts may be driven from several host threads)
+void set_smem_attr(const void* kern, size_t bytes);
+template <class K>
+inline void set_smem(K kern, size_t bytes) {
+    set_smem_attr(reinterpret_cast<const void*>(kern), bytes);
 }
 
 // RAII scope around one kernel launch: counts it and, when profiling,

@@ -689,19 +689,27 @@ void k_enc_combine(Ctx& c, u64* c0, const u64* c1, int nl) {
     HC_CUDA(cudaGetLastError());
 }
 
-// cross-rank reduction finish: x mod q_i (x is a sum of R < 16 residues)
-__global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restrict__ primes, int nl, int npoly, int N) {
+// cross-rank reduction finish: x mod q_i for any 64-bit word x (a sum of R
+// residues, R * q < 2^64): a Shoup product by 1 with the Barrett word
+// floor(2^64 / q) (= PrimeDev::mu_hi) lands in [0, 2q), one conditional
+// subtraction finishes; grid y = limb, 16-byte accesses
+__global__ void mod_reduce_kernel(u64* __restrict__ x, const PrimeDev* __restrict__ primes, int nl, int N) {
     pdl_enter();
-    const size_t poly = (size_t)nl * N;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < npoly * poly; e += (size_t)gridDim.x * blockDim.x) {
-        const int i = (int)((e % poly) / N);
-        x[e] = x[e] % primes[i].q;
+    const int limb = blockIdx.y;
+    const PrimeDev P = primes[limb % nl];
+    ulonglong2* v = reinterpret_cast<ulonglong2*>(x + (size_t)limb * N);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N / 2; e += gridDim.x * blockDim.x) {
+        ulonglong2 w = v[e];
+        w.x = csub(mul_shoup_lazy(w.x, 1, P.mu_hi, P.q), P.q);
+        w.y = csub(mul_shoup_lazy(w.y, 1, P.mu_hi, P.q), P.q);
+        v[e] = w;
     }
 }
 
 void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly) {
     Launch scope(c, "mod_reduce", 16.0 * c.N * npoly * nl);
-    launch_k(c, mod_reduce_kernel, nblocks((size_t)npoly * nl * c.N, 256), 256, 0, x, c.d_primes, nl, npoly, c.N);
+    dim3 grid((unsigned)std::min<size_t>((c.N / 2 + 255) / 256, 64), npoly * nl);
+    launch_k(c, mod_reduce_kernel, grid, 256, 0, x, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 

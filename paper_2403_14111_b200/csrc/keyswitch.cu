@@ -25,7 +25,6 @@
 //
 // Every step is exact modular arithmetic, so the residues equal the
 // unfused path and the oracle bit for bit.
-#include <unordered_set>
 #include "evaluator.h"
 #include "kernels.cuh"
 #include "ntt_pass.cuh"
@@ -449,16 +448,6 @@ static u64 powm(u64 b, u64 e, u64 q) {
     return r;
 }
 
-// the call-site flag skips the lookup after the first call; the per-kernel set
-// covers call sites that pick one of several instantiations (alpha, K, chain)
-template <class K>
-static void set_smem(K kern, size_t bytes, bool& done) {
-    static std::unordered_set<const void*> seen;
-    (void)done;
-    if (seen.insert((const void*)kern).second)
-        HC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-}
-
 // column-pass geometry per ring degree
 template <int LOGN>
 struct ColCfg;
@@ -538,12 +527,11 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
                 jobs.n++;
             }
         }
-        static bool at = false;
         // algorithmic: the digit limbs Y read once, one intermediate limb written per job
         Launch scope(c, "ks_modup_cols", 8.0 * N * nin * (nl + (double)jobs.n));
         dim3 grid((N >> CL) / CS, jobs.n, nin);
         auto go = [&](auto kern) {
-            set_smem(kern, csm, at);
+            set_smem(kern, csm);
             launch_k(c, kern, grid, CG::THREADS, csm, jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup, I);
         };
         switch (c.alpha) {
@@ -625,11 +613,10 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
     // 5. D: P -> Q conversion + column pass
     u64* Wt = sc.take((size_t)B * g.w_stride());
     {
-        static bool at = false;
         Launch scope(c, "ks_moddown_cols", 8.0 * N * B * (2.0 * K + 2.0 * nl));
         dim3 grid((N >> CL) / CS, 2 * nl, B);
         auto go = [&](auto kern) {
-            set_smem(kern, csm, at);
+            set_smem(kern, csm);
             launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, c.d_moddown, Wt);
         };
         switch (K) {
@@ -642,9 +629,8 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
     }
     // 6. E: chunk pass + (ACC - W) P^-1 + addend
     {
-        static bool at = false;
-        set_smem(ks_moddown_chunks<>, hsm, at);
-        set_smem(ks_moddown_chunks<MD_MINB_CHAIN>, hsm, at);
+        set_smem(ks_moddown_chunks<>, hsm);
+        set_smem(ks_moddown_chunks<MD_MINB_CHAIN>, hsm);
         int nadd2 = 0;
         for (int b = 0; b < B; b++) nadd2 += in[b].add2 != nullptr;
         Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
@@ -737,8 +723,7 @@ static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int n
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     const int N1 = N >> CH_LOG;
     {
-        static bool at = false;
-        set_smem(rs_cols<CL, CS>, csm, at);
+        set_smem(rs_cols<CL, CS>, csm);
         Launch scope(c, "rs_cols", 8.0 * N * B * npoly * (1.0 + level));
         dim3 grid((N >> CL) / CS, npoly * level, B);
         launch_k(c, rs_cols<CL, CS>, grid, CG::THREADS, csm, level, c.logN, N1, c.d_primes, c.twp(0, false), X,
@@ -746,8 +731,7 @@ static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int n
         HC_CUDA(cudaGetLastError());
     }
     {
-        static bool at = false;
-        set_smem(rs_chunks, hsm, at);
+        set_smem(rs_chunks, hsm);
         RsBatch rb;
         for (int b = 0; b < B; b++) { rb.a[b] = a[b]; rb.out[b] = out[b]; }
         Launch scope(c, "rs_chunks", 8.0 * N * B * npoly * 3.0 * level);

@@ -79,14 +79,8 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
     dim3 grid(nsub / SUBS, jobs.n, jobs.nb);
     static const char* names[2][3] = {{"ntt_fwd_full", "ntt_fwd_cols", "ntt_fwd_chunks"},
                                       {"ntt_inv_full", "ntt_inv_cols", "ntt_inv_chunks"}};
-    static bool attr[2] = {false, false};
-    if (!attr[inv ? 1 : 0]) {
-        if (inv) HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, true, PMB>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        else HC_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGSZ, MODE, SUBS, false, PMB>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[inv ? 1 : 0] = true;
-    }
+    if (inv) set_smem(ntt_kernel<LOGSZ, MODE, SUBS, true, PMB>, smem);
+    else set_smem(ntt_kernel<LOGSZ, MODE, SUBS, false, PMB>, smem);
     Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n * jobs.nb);
     if (inv)
         launch_k(c, ntt_kernel<LOGSZ, MODE, SUBS, true, PMB>, grid, PG::THREADS, smem, jobs, c.d_primes, c.twp(0, true),

@@ -349,9 +349,31 @@ static G concat(const std::vector<G>& parts) {
     return o;
 }
 
+// Diagonal-pass sharding (hc_set_pass_shard): the c/2 passes
+// are independent; this context runs passes k = rank, rank + world, ...,
+// hands its partial accumulator (the sum of its passes' terms) to the pass
+// reducer, which replaces it by the modular sum over ranks, and every rank
+// finishes the replicated conj epilogue.  Modular sums are exact, so the
+// result equals the single-context schedule bit for bit.
+static std::vector<int> local_passes(const Ctx& C, int K) {
+    std::vector<int> ks;
+    for (int k = C.pass_rank; k < K; k += std::max(1, C.pass_world)) ks.push_back(k);
+    if (ks.empty()) throw Error(-4, "pass sharding: more ranks than diagonal passes");
+    return ks;
+}
+
+static G reduce_passes(Eval& ev, G out) {
+    if (ev.c.pass_world > 1) {
+        if (!ev.c.pass_reducer) throw Error(-4, "pass sharding without a pass reducer");
+        ev.c.pass_reducer(out);
+    }
+    return out;
+}
+
 static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, const G& B, int c, double scale,
                                           const Geo& g) {
-    const int K = c / 2;
+    const std::vector<int> ks = local_passes(ev.c, c / 2);
+    const int K = (int)ks.size();
     // packing prologue: B + i * RU(B, c/2), all block columns in one batch
     const int kk0 = (c / 2) % g.s0;
     G rolled = kk0 ? ev.lrot_batch(B, (int64_t)kk0 * g.s1) : B;
@@ -365,7 +387,7 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
         // row) product sum -- the col_sums pre-add of the rowwise products --
         // relinearised and rescaled once
         std::vector<int64_t> amounts(K);
-        for (int k = 0; k < K; k++) amounts[k] = (int64_t)(k % g.s0) * g.s1;
+        for (int u = 0; u < K; u++) amounts[u] = (int64_t)(ks[u] % g.s0) * g.s1;
         std::vector<G> H = ev.lrot_hoisted(packed, amounts);
         std::vector<G> as, bs;
         for (int k = 0; k < K; k++)
@@ -379,7 +401,7 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     } else {
         // RU(packed, k) per pass (one batch per k: its own Galois element)
         for (int k = 0; k < K; k++) {
-            const int kk = k % g.s0;
+            const int kk = ks[k] % g.s0;
             shifted[k] = kk ? ev.lrot_batch(packed, (int64_t)kk * g.s1) : packed;
         }
         // all passes' products in one batch
@@ -407,7 +429,7 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     std::vector<G> terms(K, G(m));
     {
         std::vector<Pattern> masks;
-        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, k, c, true, scale));
+        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, ks[k], c, true, scale));
         std::vector<const Pattern*> ps;
         for (int k = 0; k < K; k++)
             for (int p = 0; p < m; p++) ps.push_back(&masks[k]);
@@ -417,6 +439,7 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     }
     G out = terms[0];
     for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
+    out = reduce_passes(ev, out);
     G cj = ev.conj_batch(out);
     return ev.add_batch(out, cj);
 }
@@ -437,7 +460,8 @@ static void rot_left_split(Eval& ev, const G& E, int k, const Geo& g, G& head, G
 
 static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& B, int n, int c, double scale,
                                           const Geo& g, const Reducer& red) {
-    const int K = c / 2;
+    const std::vector<int> ks = local_passes(ev.c, c / 2);
+    const int K = (int)ks.size();
     const int s1 = g.s1;
     const bool partial = grid_level(A) < grid_level(B);
     // packing prologue: A + i * RL(A, c/2)
@@ -459,7 +483,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     std::vector<G> first(K);
     if (ev.c.hoist) {
         std::vector<int64_t> amounts(K);
-        for (int k = 0; k < K; k++) amounts[k] = partial ? k : k % s1;
+        for (int k = 0; k < K; k++) amounts[k] = partial ? ks[k] : ks[k] % s1;
         std::vector<G> H = ev.lrot_hoisted(packed, amounts);
         for (int k = 0; k < K; k++) {
             first[k].resize(m);
@@ -467,23 +491,23 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
         }
     }
     if (partial) {
-        for (int k = 0; k < K; k++) left[k] = ev.c.hoist ? first[k] : ev.lrot_batch(packed, k);
+        for (int k = 0; k < K; k++) left[k] = ev.c.hoist ? first[k] : ev.lrot_batch(packed, ks[k]);
     } else {
         // RL per pass (encoding.py:291-311): head = lrot(packed, k) * keep_k,
         // tail = lrot - head, left = head + rrot(tail, s1); the keep masks of
         // every pass in one batch, the rrot(s1) of every tail in one batch
         std::vector<int> moving;
         for (int k = 0; k < K; k++) {
-            if (k % s1 == 0) left[k] = packed;
+            if (ks[k] % s1 == 0) left[k] = packed;
             else moving.push_back(k);
         }
         std::vector<Pattern> keeps;
-        for (int k : moving) keeps.push_back(keep_head(g, s1 - k % s1));
+        for (int k : moving) keeps.push_back(keep_head(g, s1 - ks[k] % s1));
         G a1s;
         std::vector<const Pattern*> ps;
         for (size_t u = 0; u < moving.size(); u++) {
             const int k = moving[u];
-            const G a1 = ev.c.hoist ? first[k] : ev.lrot_batch(packed, k % s1);
+            const G a1 = ev.c.hoist ? first[k] : ev.lrot_batch(packed, ks[k] % s1);
             for (int p = 0; p < m; p++) {
                 a1s.push_back(a1[p]);
                 ps.push_back(&keeps[u]);
@@ -505,7 +529,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
         std::vector<G> heads(K), tails(K);
         std::vector<int> moving;
         for (int k = 0; k < K; k++) {
-            const int kk = k % s1;
+            const int kk = ks[k] % s1;
             if (!kk) continue;
             const Pattern keep = keep_head(g, s1 - kk);
             heads[k].resize(B.size());
@@ -553,7 +577,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     std::vector<G> terms(K, G(n));
     {
         std::vector<Pattern> masks;
-        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, -k, c, true, scale));
+        for (int k = 0; k < K; k++) masks.push_back(diag_mask(g, -ks[k], c, true, scale));
         std::vector<const Pattern*> ps;
         for (int k = 0; k < K; k++)
             for (int q = 0; q < n; q++) ps.push_back(&masks[k]);
@@ -563,6 +587,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     }
     G out = terms[0];
     for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
+    out = reduce_passes(ev, out);
     G cj = ev.conj_batch(out);
     return ev.add_batch(out, cj);
 }
@@ -590,6 +615,7 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
     const bool par = !ev.auto_boot || std::min(grid_level(A), grid_level(B)) >= 4;
     // the fused forms exist only in lockstep form: hoist implies lockstep
     if (par && (C.lockstep || C.hoist)) return diag_abt_lockstep(ev, A, m, n, B, c, scale, g);
+    if (C.pass_world > 1) throw Error(-4, "pass sharding needs the lockstep schedule (no refresh inside)");
     auto W = [&](int w) { return par ? w : 1; };
     // packing prologue, one branch per block column: B + i * RU(B, c/2)
     G packed(n);
@@ -652,6 +678,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
     // collective in k order on every rank, and only that branch waits for it.
     const bool ser = ev.auto_boot && std::min(grid_level(A), grid_level(B)) < 5;
     if (!ser && (C.lockstep || C.hoist)) return diag_atb_lockstep(ev, A, m, B, n, c, scale, g, red);
+    if (C.pass_world > 1) throw Error(-4, "pass sharding needs the lockstep schedule (no refresh inside)");
     const int width = ser ? 1 : fork_width(C, c / 2);
     // packing prologue per block row: A + i * RL(A, c/2)
     G packed(m);
@@ -943,6 +970,26 @@ std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes,
     if (period < classes || period > g.s1 || (period & (period - 1))) throw Error(-4, "softmax: bad period");
     if (cfg.exp_range < 1 || (cfg.exp_range & (cfg.exp_range - 1))) throw Error(-4, "exp_range must be a power of two");
     const int m = (int)M.size();
+    Ctx& C = ev.c;
+    if (C.shard_total > 0 && !ev.plan.on) {
+        // block-row shard of a larger batch: lockstep over the local blocks with
+        // the whole batch's nonce layout, so every refresh (and the context
+        // nonce afterwards) equals the single-context run of all block rows
+        if (C.shard_first + m > C.shard_total) throw Error(-4, "softmax: shard exceeds the batch");
+        Eval sev(C, ev.auto_boot);
+        {
+            std::lock_guard<std::mutex> lk(C.mu);
+            sev.plan.base = C.nonce;
+        }
+        sev.plan.on = true;
+        sev.plan.m = C.shard_total;
+        sev.plan.p = C.shard_first;
+        sev.plan.mloc = m;
+        std::vector<CtP> out = softmax_serial(sev, M, classes, period, cfg);
+        std::lock_guard<std::mutex> lk(C.mu);
+        C.nonce = sev.plan.base + (u64)C.shard_total * sev.plan.events;
+        return out;
+    }
     bool uniform = m > 1 && !ev.plan.on;
     for (auto& b : M) uniform = uniform && b->level == M[0]->level;
     // lockstep (default): the blocks advance op by op, each op one batch --
@@ -996,6 +1043,30 @@ static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int 
     const int reps = g.s1 / period;
     for (int t = 0; t < ilog2(reps); t++) out = ev.lrot_batch(out, -(int64_t)period * (1 << t), true);
     return out;
+}
+
+std::vector<CtP> sched_approx(Eval& ev, int fn, const std::vector<CtP>& X, const std::vector<CtP>& Y, int classes,
+                              int period, const SoftmaxCfg& cfg) {
+    const Geo g = geo(ev, geo_rows(ev));
+    SM sm{ev, g, classes, period};
+    switch (fn) {
+        case APPROX_COMP:
+            if (Y.size() != X.size()) throw Error(-4, "a_comp: operand grids differ");
+            return sm.comp(X, Y);
+        case APPROX_MAX: {
+            if (period < classes || period > g.s1 || (period & (period - 1))) throw Error(-4, "a_max: bad period");
+            const double full = cfg.base_range * std::pow(cfg.extension_base, (double)cfg.extension_steps);
+            return sm.amax(X, cfg, (int)std::ceil(full / 2));
+        }
+        case APPROX_DOMAIN_EXTEND: return sm.domain_extend(X, cfg);
+        case APPROX_DEP_COMP: return sm.dep_comp(X, cfg);
+        case APPROX_EXP:
+            if (cfg.exp_range < 1 || (cfg.exp_range & (cfg.exp_range - 1)))
+                throw Error(-4, "exp_range must be a power of two");
+            return sm.exp(X, cfg);
+        case APPROX_INV: return sm.inv(X, cfg);
+        default: throw Error(-1, "unknown approximation");
+    }
 }
 
 }  // namespace hc

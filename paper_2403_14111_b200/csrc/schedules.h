@@ -40,5 +40,11 @@ std::vector<CtP> sched_row_major_atb(Eval& ev, const std::vector<CtP>& A, int m,
                                      int c, double scale);
 // M: m x 1 horizontally tiled logits
 std::vector<CtP> sched_softmax(Eval& ev, const std::vector<CtP>& M, int classes, int period, const SoftmaxCfg& cfg);
+// the softmax's building blocks (approx.py:195-309) over any list of blocks,
+// lockstep (the reference's per-op block order); a_comp takes Y, a_max needs
+// a horizontally tiled single block column
+enum { APPROX_COMP = 0, APPROX_MAX, APPROX_DOMAIN_EXTEND, APPROX_DEP_COMP, APPROX_EXP, APPROX_INV };
+std::vector<CtP> sched_approx(Eval& ev, int fn, const std::vector<CtP>& X, const std::vector<CtP>& Y, int classes,
+                              int period, const SoftmaxCfg& cfg);
 
 }  // namespace hc

@@ -15,8 +15,17 @@ Two shardings, one process per GPU:
   after it (ladder, mask, conj, NAG update) is replicated and identical on
   every rank, so no broadcast is needed.
 
-Encryption randomness: ranks draw nonces from disjoint ranges
-(``rank_nonce_base``) so refreshes on different ranks never reuse a mask.
+Encryption randomness: ranks encrypt their own inputs with nonces from
+disjoint ranges (``rank_nonce_base``).  Refreshes inside the sharded step
+follow the whole batch's sequential nonce layout (``CKKSContext.set_shard``,
+``hc_set_shard``), so the softmax refreshes of block row p draw the nonces a
+single-context run of all block rows gives them, and the context nonce after
+the softmax -- hence the replicated W / V refreshes -- is the same on every
+rank: the weights stay bit-identical replicas without a broadcast.
+
+Reducers: ``NcclModReducer`` (one process per GPU; collective and
+``hc_mod_reduce`` ordered on the library stream, no host sync) and
+``LocalModReducer`` (several shard contexts in one process, tests).
 """
 
 from __future__ import annotations
@@ -58,33 +67,91 @@ class _DeviceView:
                                          "version": 3, "strides": None}
 
 
+def check_sum_fits(world: int, moduli, level: int) -> None:
+    """A sum of ``world`` canonical residues must fit a uint64 word (the
+    all-reduce adds them as int64, wrapping like uint64)."""
+    qmax = max(int(q) for q in list(moduli)[: level + 1])
+    if world * qmax >= 1 << 64:
+        raise ValueError(f"{world} ranks x {qmax.bit_length()}-bit primes overflow the uint64 sum")
+
+
+def device_residues(ctx, handle):
+    """int64 torch view of a ciphertext handle's [2][l+1][N] device residues."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native as N
+    L = N.lib()
+    level = L.hc_ct_level(handle)
+    ptr = N.U64P()
+    N.check(L.hc_ct_device_ptr(handle, C.byref(ptr)))
+    words = 2 * (level + 1) * ctx.N
+    return torch.as_tensor(_DeviceView(C.cast(ptr, C.c_void_p).value, words), device="cuda"), level
+
+
 class NcclModReducer:
     """Reducer for ``diag_atb(..., reducer=)`` / ``nag_step(..., reducer=)`` on GPUs:
-    all-reduce (NCCL, SUM) of each pre-sum ciphertext's residues in place, then
-    ``hc_mod_reduce`` on the library stream."""
+    an NCCL all-reduce (SUM) of each pre-sum ciphertext's residues in place,
+    then ``hc_mod_reduce`` -- all ordered on the library's current stream
+    (``hc_ctx_stream``): torch's NCCL stream waits for the pre-sums there and
+    the stream waits for the collective, so the host never blocks and the
+    next diagonal pass's work queues behind it."""
 
     def __init__(self, group=None):
         self.group = group
 
     def __call__(self, ctx, handles):
-        import ctypes as C
-
         import torch
         import torch.distributed as dist
 
-        from . import _native as N
+        world = dist.get_world_size(self.group)
+        stream = torch.cuda.ExternalStream(ctx.stream())
+        with torch.cuda.stream(stream):
+            for h in handles:
+                t, level = device_residues(ctx, h)
+                check_sum_fits(world, ctx.moduli, level)
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        for h in handles:
+            ctx.mod_reduce(h)
 
-        L = N.lib()
+
+class LocalModReducer:
+    """The same exchange for ``world`` contexts driven from one process (one
+    thread per shard, e.g. several shards on one GPU): each rank's pre-sums
+    are summed as uint64 on the device, every rank receives the raw sum and
+    finishes it with ``hc_mod_reduce`` (K8) -- the product's reduction kernel
+    on genuinely unreduced words.  ``reducer.rank(r)`` is rank r's callable."""
+
+    def __init__(self, world: int):
+        import threading
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._views = [None] * world
+        self._sums = None
+
+    def rank(self, r: int):
+        return lambda ctx, handles: self._reduce(r, ctx, handles)
+
+    def _reduce(self, r, ctx, handles):
+        import torch
+        ctx.sync()                                   # this rank's pre-sums are complete
+        views = [device_residues(ctx, h) for h in handles]
+        for _, level in views:
+            check_sum_fits(self.world, ctx.moduli, level)
+        self._views[r] = [v for v, _ in views]
+        self._bar.wait()
+        if r == 0:
+            self._sums = [torch.stack([self._views[k][i] for k in range(self.world)]).sum(0)
+                          for i in range(len(handles))]
+            torch.cuda.synchronize()
+        self._bar.wait()
+        for v, s in zip(self._views[r], self._sums):
+            v.copy_(s)
+        torch.cuda.synchronize()
+        self._bar.wait()                             # every rank has its copy
         for h in handles:
-            level = L.hc_ct_level(h)
-            words = 2 * (level + 1) * ctx.N
-            ptr = N.U64P()
-            N.check(L.hc_ct_device_ptr(h, C.byref(ptr)))
-            t = torch.as_tensor(_DeviceView(C.cast(ptr, C.c_void_p).value, words), device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
-        torch.cuda.current_stream().synchronize()
-        for h in handles:
-            N.check(L.hc_mod_reduce(ctx._h, h))
+            ctx.mod_reduce(h)
 
 
 def local_rows(X: np.ndarray, grid_rows: int, world: int, rank: int) -> np.ndarray:

@@ -27,3 +27,27 @@ def cuda_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def import_reference():
+    """The unmodified reference package (hefit): the driver's offline install
+    under baseline/_ref travels with the repo; /root/reference exists only in
+    the build container.  None when neither is present."""
+    import importlib
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "hefit")):
+            if p not in sys.path:
+                sys.path.append(p)
+            try:
+                return importlib.import_module("hefit")
+            except Exception:
+                return None
+    return None
+
+
+@pytest.fixture(scope="session")
+def hefit():
+    mod = import_reference()
+    if mod is None:
+        pytest.skip("reference package hefit not importable (baseline/_ref absent)")
+    return mod

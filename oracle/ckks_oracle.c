@@ -710,8 +710,12 @@ void orc_level_adjust(const orc_ctx *c, const u64 *a, int from, int to, u64 *out
 
 /* ModUp of d ([level+1][N], NTT form): up [beta][nt][N] in NTT form over
  * the target basis (Q_l then P); for target limbs inside digit j the value is
- * d itself.  Fast base conversion of the digit's INTT, scaled by
- * [(Q'/q_i)^-1]_{q_i}, then the forward NTT on every non-digit target. */
+ * d itself.  Centred fast base conversion of the digit's INTT, scaled by
+ * [(Q'/q_i)^-1]_{q_i}: each term y_a is taken in (-q_a/2, q_a/2], i.e.
+ * sum_a y_a [Q'/q_a]_p - #{a : y_a > (q_a-1)/2} [Q']_p, so the lifted digit
+ * has no constant bias (an uncentred digit's mean Q'/2 is amplified ~N-fold
+ * in the slots by the key-switching error); then the forward
+ * NTT on every non-digit target. */
 static void ks_modup(orc_ctx *c, const u64 *d, int level, u64 *up) {
     int N = c->N, L = c->L, K = c->K, nl = level + 1;
     int nt = nl + K;
@@ -742,16 +746,22 @@ static void ks_modup(orc_ctx *c, const u64 *d, int level, u64 *up) {
             const prime_t *p = &c->pr[li];
             u64 *o = upj + (size_t)t * N;
             if (li >= lo && li < hi) { memcpy(o, d + (size_t)li * N, sizeof(u64) * N); continue; }
-            u64 cf[MAXP];
+            u64 cf[MAXP], Qd = 1;
             for (int a = 0; a < na; a++) {
                 u64 v = 1;
                 for (int b = lo; b < hi; b++) if (b != lo + a) v = mulmod(v, c->pr[b].q % p->q, p);
                 cf[a] = v;
+                Qd = mulmod(Qd, c->pr[lo + a].q % p->q, p);
             }
             for (int k = 0; k < N; k++) {
                 u128 s = 0;
-                for (int a = 0; a < na; a++) s += (u128)x[(size_t)a * N + k] * cf[a];
-                o[k] = reduce128(s, p);
+                u64 cnt = 0;
+                for (int a = 0; a < na; a++) {
+                    const u64 y = x[(size_t)a * N + k];
+                    s += (u128)y * cf[a];
+                    cnt += y > (c->pr[lo + a].q - 1) / 2;
+                }
+                o[k] = submod(reduce128(s, p), mulmod(cnt, Qd, p), p->q);
             }
             ntt(c, p, o);
         }
@@ -810,10 +820,16 @@ static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *ke
             }
             u64 pinv = invmod(Pm, p->q);
             u64 *w = malloc(sizeof(u64) * N);
+            /* centred conversion of the P part (as in ks_modup) */
             for (int k = 0; k < N; k++) {
                 u128 sacc = 0;
-                for (int t = 0; t < K; t++) sacc += (u128)y[(size_t)t * N + k] * cf[t];
-                w[k] = reduce128(sacc, p);
+                u64 cnt = 0;
+                for (int t = 0; t < K; t++) {
+                    const u64 v = y[(size_t)t * N + k];
+                    sacc += (u128)v * cf[t];
+                    cnt += v > (c->pr[L + 1 + t].q - 1) / 2;
+                }
+                w[k] = submod(reduce128(sacc, p), mulmod(cnt, Pm, p), p->q);
             }
             ntt(c, p, w);
             for (int k = 0; k < N; k++)

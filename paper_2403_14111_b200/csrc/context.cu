@@ -347,6 +347,20 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
         }
     c->d_modup = upload(*c, mu_tab);
     c->d_modup_inv = upload(*c, mu_inv);
+    std::vector<u64> mu_negq((size_t)(L + 1) * c->dnum * nall, 0);
+    for (int l = 0; l <= L; l++)
+        for (int j = 0; j < c->dnum; j++) {
+            const int lo = j * alpha;
+            if (lo > l) continue;
+            const int hi = std::min(lo + alpha, l + 1);
+            for (int t = 0; t < nall; t++) {
+                const u64 pt = c->pr[t].q;
+                u64 v = 1;
+                for (int b = lo; b < hi; b++) v = mulm(v, c->pr[b].q % pt, pt);
+                mu_negq[(size_t)(l * c->dnum + j) * nall + t] = v ? pt - v : 0;
+            }
+        }
+    c->d_modup_negq = upload(*c, mu_negq);
 
     // ModDown tables
     std::vector<u64> md_tab((size_t)K * nall * 2), md_inv((size_t)K * 2), pinv((size_t)nall * 2), pm(nall);
@@ -376,6 +390,9 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     }
     c->d_moddown = upload(*c, md_tab);
     c->d_moddown_inv = upload(*c, md_inv);
+    std::vector<u64> md_negp(nall);
+    for (int i = 0; i < nall; i++) md_negp[i] = pm[i] ? c->pr[i].q - pm[i] : 0;
+    c->d_moddown_negp = upload(*c, md_negp);
     c->d_pinv = upload(*c, pinv);
     // P mod q_i for key generation lives right after the rescale table
     std::vector<u64> rs((size_t)(L + 1) * nall * 3 + nall, 0);
@@ -462,7 +479,7 @@ void ctx_destroy(Ctx* c) {
     for (auto& kv : c->keys) cudaFree(kv.second.d);
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
-    cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
+    cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_modup_negq); cudaFree(c->d_moddown_negp); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
     cudaStreamSynchronize(c->stream);
     for (auto s : c->side) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
     for (auto e : c->side_ev) cudaEventDestroy(e);

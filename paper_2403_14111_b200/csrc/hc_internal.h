@@ -145,6 +145,11 @@ struct Ctx {
     u64* d_modup_inv = nullptr;   // [L+1][dnum][alpha] (value, shoup)
     u64* d_moddown = nullptr;     // [K][nall] (value, shoup) phat_{p->i}
     u64* d_moddown_inv = nullptr; // [K] (value, shoup)
+    // centred base conversion: [-Q'_j]_{p} per (level, digit,
+    // target prime) and [-P]_{q_i} per prime -- added once per term taken
+    // from the upper half of its prime
+    u64* d_modup_negq = nullptr;  // [L+1][dnum][nall]
+    u64* d_moddown_negp = nullptr;   // [nall]
     u64* d_pinv = nullptr;        // [nall] (value, shoup) P^-1 mod q_i
     u64* d_rescale = nullptr;     // [L+1 (dropped prime l)][nall] (q_l^-1 mod q_i, shoup, q_l mod q_i)
     // counters

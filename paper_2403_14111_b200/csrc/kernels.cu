@@ -230,8 +230,8 @@ void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g) {
 
 __global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, const u64* __restrict__ D,
                              const u64* __restrict__ tab, const u64* __restrict__ tab_inv,
-                             const PrimeDev* __restrict__ primes, int level, int L, int K, int alpha, int dnum,
-                             int nall, int N) {
+                             const u64* __restrict__ negq_tab, const PrimeDev* __restrict__ primes, int level, int L,
+                             int K, int alpha, int dnum, int nall, int N) {
     pdl_enter();
     const int j = blockIdx.y;
     const int lo = j * alpha;
@@ -241,12 +241,15 @@ __global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, co
     const int nt = level + 1 + K;
     const u64* inv = tab_inv + ((size_t)(level * dnum + j) * alpha) * 2;
     const u64* cf = tab + ((size_t)(level * dnum + j) * alpha) * nall * 2;
+    const u64* negq = negq_tab + (size_t)(level * dnum + j) * nall;
     u64* out = up + (size_t)j * nt * N;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         u64 y[8];
+        u64 cnt = 0;   // centred conversion: terms from the upper half of their prime
         for (int a = 0; a < na; a++) {
             const u64 q = primes[lo + a].q;
             y[a] = mul_shoup(X[(size_t)(lo + a) * N + k], inv[2 * a], inv[2 * a + 1], q);
+            cnt += y[a] > (q - 1) / 2;
         }
         for (int t = 0; t < nt; t++) {
             const int pi = t <= level ? t : L + 1 + (t - level - 1);
@@ -255,12 +258,12 @@ __global__ void modup_kernel(u64* __restrict__ up, const u64* __restrict__ X, co
                 continue;
             }
             const u64 p = primes[pi].q;
-            u64 acc = 0;
+            u64 acc = cnt * negq[pi];
             for (int a = 0; a < na; a++) {
                 const u64* c2 = cf + ((size_t)a * nall + pi) * 2;
                 acc += mul_shoup_lazy(y[a], c2[0], c2[1], p);
+                if (acc >= 8 * p) acc -= 8 * p;   // < 8p for any alpha <= 8 (p < 2^60)
             }
-            // acc < 2 * na * p <= 8p
             if (acc >= 4 * p) acc -= 4 * p;
             if (acc >= 2 * p) acc -= 2 * p;
             if (acc >= p) acc -= p;
@@ -273,8 +276,8 @@ void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
     dim3 grid((c.N + 255) / 256, beta);
     const int nl = level + 1, nt = nl + c.K;
     Launch scope(c, "modup", 8.0 * c.N * (2.0 * nl + (double)beta * nt));
-    launch_k(c, modup_kernel, grid, 256, 0, up, X, D, c.d_modup, c.d_modup_inv, c.d_primes, level, c.L, c.K,
-                                              c.alpha, c.dnum, c.nall, c.N);
+    launch_k(c, modup_kernel, grid, 256, 0, up, X, D, c.d_modup, c.d_modup_inv, c.d_modup_negq, c.d_primes, level,
+             c.L, c.K, c.alpha, c.dnum, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
 }
 
@@ -321,8 +324,8 @@ void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int b
 // ---------------------------------------------------------------------------
 
 __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__ acc, const u64* __restrict__ tab,
-                                    const u64* __restrict__ tab_inv, const PrimeDev* __restrict__ primes, int level,
-                                    int L, int K, int nall, int N) {
+                                    const u64* __restrict__ tab_inv, const u64* __restrict__ negp,
+                                    const PrimeDev* __restrict__ primes, int level, int L, int K, int nall, int N) {
     pdl_enter();
     const int s = blockIdx.y;
     const int nt = level + 1 + K;
@@ -330,16 +333,19 @@ __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__
     u64* out = W + (size_t)s * (level + 1) * N;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         u64 y[8];
+        u64 cnt = 0;   // centred conversion (as in modup_kernel)
         for (int t = 0; t < K; t++) {
             const u64 p = primes[L + 1 + t].q;
             y[t] = mul_shoup(A[(size_t)(level + 1 + t) * N + k], tab_inv[2 * t], tab_inv[2 * t + 1], p);
+            cnt += y[t] > (p - 1) / 2;
         }
         for (int i = 0; i <= level; i++) {
             const u64 q = primes[i].q;
-            u64 v = 0;
+            u64 v = cnt * negp[i];
             for (int t = 0; t < K; t++) {
                 const u64* c2 = tab + ((size_t)t * nall + i) * 2;
                 v += mul_shoup_lazy(y[t], c2[0], c2[1], q);
+                if (v >= 8 * q) v -= 8 * q;   // < 8q for any K <= 8 (q < 2^60)
             }
             if (v >= 4 * q) v -= 4 * q;
             if (v >= 2 * q) v -= 2 * q;
@@ -352,8 +358,8 @@ __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__
 void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
     dim3 grid((c.N + 255) / 256, 2);
     Launch scope(c, "moddown_conv", 8.0 * c.N * (2.0 * c.K + 2.0 * (level + 1)));
-    launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_moddown, c.d_moddown_inv, c.d_primes, level, c.L,
-                                                     c.K, c.nall, c.N);
+    launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_moddown, c.d_moddown_inv, c.d_moddown_negp,
+             c.d_primes, level, c.L, c.K, c.nall, c.N);
     HC_CUDA(cudaGetLastError());
 }
 

@@ -362,9 +362,17 @@ static std::vector<int> local_passes(const Ctx& C, int K) {
     return ks;
 }
 
-static G reduce_passes(Eval& ev, G out) {
+// `lstar` is the level every pass's term reaches in the unsharded schedule's
+// sum (its lowest): a partial above it is adjusted first, which is the same
+// adjustment the unsharded sum applies to the higher-level pass (k = 0) when
+// the next pass is added, so the modular sum over ranks matches bit for bit.
+static G reduce_passes(Eval& ev, G out, int lstar) {
     if (ev.c.pass_world > 1) {
         if (!ev.c.pass_reducer) throw Error(-4, "pass sharding without a pass reducer");
+        for (auto& x : out) {
+            if (x->level < lstar) throw Error(-4, "pass sharding: partial below the common level");
+            x = ev.at(x, lstar);
+        }
         ev.c.pass_reducer(out);
     }
     return out;
@@ -439,7 +447,7 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     }
     G out = terms[0];
     for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
-    out = reduce_passes(ev, out);
+    out = reduce_passes(ev, out, out[0]->level);   // every pass's term at one level
     G cj = ev.conj_batch(out);
     return ev.add_batch(out, cj);
 }
@@ -476,6 +484,15 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
             for (int p = 0; p < m; p++) one[p] = ev.add(head[p], back[p]);
         }
         for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], ev.mul_i(one[p]));
+    }
+    // the level of pass k's term (all passes, for pass sharding): RL / PRU of
+    // a non-zero k costs the rotated operand one level, then the product and
+    // the mask one each
+    int lstar = 1 << 30;
+    for (int k = 0; k < c / 2; k++) {
+        int ll = grid_level(packed), lr = grid_level(B);
+        if (k % s1) (partial ? lr : ll) -= 1;
+        lstar = std::min(lstar, std::min(ll, lr) - 2);
     }
     // left operands of every pass; fused form (oracle/slots.py
     // diag_atb): the leading rotations lrot(packed, k) share one ModUp per block
@@ -587,7 +604,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
     }
     G out = terms[0];
     for (int k = 1; k < K; k++) out = ev.add_batch(out, terms[k]);
-    out = reduce_passes(ev, out);
+    out = reduce_passes(ev, out, lstar);
     G cj = ev.conj_batch(out);
     return ev.add_batch(out, cj);
 }

@@ -127,6 +127,10 @@ def _fused_ops(g, o, seed, tol=1e-5):
     assert gs.level == os_.level == g.max_level - 1
     assert np.max(np.abs(gs.slots - sum(a * b for a, b in zip(xs, ys)))) < tol
     assert _ledger(g) == _ledger(o) == [2, 0, 3, 4, 0, 0]
+    # centred base conversion: a hoisted rotation is the per-op key switch bit for bit
+    for r, a in zip(rs, g.lrot_hoisted(gx[0], rs)):
+        if r:
+            np.testing.assert_array_equal(a.residues(), g.lrot(gx[0], r).residues())
 
 
 def test_fused_ops_residues(pair):

@@ -125,8 +125,19 @@ int hc_op_mult_sum(hc_ctx *ctx, const hc_ct *const *a, const hc_ct *const *b, in
 /* conj (emulator.py:253-257), mul_i (emulator.py:259-265, unledgered) */
 int hc_op_conj(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
 int hc_op_mul_i(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
-/* bootstrap (emulator.py:267-273): refresh surrogate, NOT CKKS bootstrapping */
+/* bootstrap (emulator.py:267-273): the refresh surrogate (decrypt /
+ * re-encrypt, needs the secret key) or, after hc_set_bootstrap(ctx, 1), real
+ * CKKS bootstrapping (ModRaise, CoeffToSlot, EvalMod, SlotToCoeff; no secret
+ * key); the result lands on the application level */
 int hc_op_bootstrap(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
+/* EmulatorContext.max_level when the chain carries bootstrapping levels
+ * above it: fresh encryptions default to it, refreshes land on it */
+int hc_set_app_level(hc_ctx *ctx, int level);
+/* 0: refresh surrogate (default), 1: CKKS bootstrapping (needs a chain with
+ * 17 levels above the application level, e.g. the boot16 parameter set) */
+int hc_set_bootstrap(hc_ctx *ctx, int mode);
+/* one CKKS bootstrapping of a (any level) regardless of the mode, unledgered */
+int hc_bootstrap_ct(hc_ctx *ctx, const hc_ct *a, hc_ct **out);
 
 /* ---- exact CKKS primitives (no ledger), for residue-level parity ---- */
 int hc_rescale(hc_ctx *ctx, const hc_ct *a, hc_ct **out);

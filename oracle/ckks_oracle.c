@@ -56,6 +56,7 @@ typedef struct key_s {
 
 typedef struct {
     int logN, N, L, K, alpha, dnum, nall, hw;
+    int app_L;            /* application top level: refreshes land here */
     double sigma;
     u64 seed;
     prime_t pr[MAXP];
@@ -237,7 +238,7 @@ static u64 find_prime(int bits, int N, const u64 *used, int nused) {
 orc_ctx *orc_create(int logN, int nq, const int *qbits, int np, const int *pbits, int alpha,
                     int log_scale, int hw, double sigma, u64 seed) {
     orc_ctx *c = calloc(1, sizeof(orc_ctx));
-    c->logN = logN; c->N = 1 << logN; c->L = nq - 1; c->K = np; c->alpha = alpha;
+    c->logN = logN; c->N = 1 << logN; c->L = nq - 1; c->app_L = nq - 1; c->K = np; c->alpha = alpha;
     c->dnum = (nq + alpha - 1) / alpha; c->nall = nq + np; c->hw = hw; c->sigma = sigma;
     c->seed = seed;
     int N = c->N, M = N / 2;
@@ -288,6 +289,8 @@ orc_ctx *orc_create(int logN, int nq, const int *qbits, int np, const int *pbits
     }
     return c;
 }
+
+void orc_set_app_level(orc_ctx *c, int level) { c->app_L = level; }
 
 void orc_destroy(orc_ctx *c) {
     if (!c) return;
@@ -553,10 +556,10 @@ void orc_refresh(const orc_ctx *c, const u64 *ct, int level, u64 nonce, u64 *out
     int N = c->N;
     double *md = malloc(sizeof(double) * N);
     decrypt_coef(c, ct, level, md);
-    double ratio = c->scale[c->L] / c->scale[level];
+    double ratio = c->scale[c->app_L] / c->scale[level];
     i64 *m = malloc(sizeof(i64) * N);
     for (int k = 0; k < N; k++) m[k] = llrint(md[k] * ratio);
-    orc_encrypt_coef(c, m, c->L, nonce, out);
+    orc_encrypt_coef(c, m, c->app_L, nonce, out);
     free(md); free(m);
 }
 
@@ -678,6 +681,57 @@ void orc_mul_pt(const orc_ctx *c, const u64 *a, const u64 *pt, int level, u64 *o
             }
     orc_rescale(c, t, level, 2, out);
     free(t);
+}
+
+/* ct x pt without the rescale: [2][level+1][N] at scale scale[level]^2 */
+void orc_mul_pt_raw(const orc_ctx *c, const u64 *a, const u64 *pt, int level, u64 *out) {
+    int N = c->N, nl = level + 1;
+    for (int s = 0; s < 2; s++)
+#pragma omp parallel for
+        for (int i = 0; i < nl; i++)
+            for (int k = 0; k < N; k++) {
+                size_t o = ((size_t)s * nl + i) * N + k;
+                out[o] = mulmod(a[o], pt[(size_t)i * N + k], &c->pr[i]);
+            }
+}
+
+/* exact multiplication by a non-negative integer k (no rescale, no level) */
+void orc_mul_int(const orc_ctx *c, const u64 *a, int level, u64 k, u64 *out) {
+    int N = c->N, nl = level + 1;
+    for (int s = 0; s < 2; s++)
+        for (int i = 0; i < nl; i++) {
+            const prime_t *p = &c->pr[i];
+            u64 kk = k % p->q;
+            for (int j = 0; j < N; j++) {
+                size_t o = ((size_t)s * nl + i) * N + j;
+                out[o] = mulmod(a[o], kk, p);
+            }
+        }
+}
+
+/* ModRaise (bootstrapping): a level-0 ciphertext [2][1][N]
+ * -> [2][to+1][N]: each polynomial's coefficients, centred mod q0, lifted to
+ * every prime q_0..q_to; the result decrypts to m + q0 * I(X), I small */
+void orc_mod_raise(const orc_ctx *c, const u64 *a, int to, u64 *out) {
+    int N = c->N, nl = to + 1;
+    const prime_t *p0 = &c->pr[0];
+    u64 q0 = p0->q;
+    u64 *x = malloc(sizeof(u64) * N);
+    for (int s = 0; s < 2; s++) {
+        memcpy(x, a + (size_t)s * N, sizeof(u64) * N);
+        intt(c, p0, x);
+#pragma omp parallel for
+        for (int i = 0; i < nl; i++) {
+            const prime_t *p = &c->pr[i];
+            u64 *y = out + ((size_t)s * nl + i) * N;
+            for (int k = 0; k < N; k++) {
+                u64 v = x[k];
+                y[k] = v > (q0 - 1) / 2 ? submod(v % p->q, q0 % p->q, p->q) : v % p->q;
+            }
+            ntt(c, p, y);
+        }
+    }
+    free(x);
 }
 
 void orc_add_pt(const orc_ctx *c, const u64 *a, const u64 *pt, int level, int negate, u64 *out) {

@@ -25,6 +25,9 @@ from . import slots as S
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "build", "libckks_oracle.so")
 
+# parameter sets with bootstrapping levels above the application's top level
+APP_LEVELS = {"boot16": 12, "boot10": 12}
+
 # name -> (logN, q bits, p bits, alpha, log scale, hamming weight)
 PARAMS = {
     "cfg0": (13, [60] + [40] * 4, [60], 1, 40, 64),
@@ -34,6 +37,12 @@ PARAMS = {
     "small12": (9, [58] + [42] * 12, [60] * 3, 4, 42, 64),
     # the same chain at the reference's default training ring (2^13 slots x 2)
     "n13l12": (13, [58] + [42] * 12, [60] * 3, 4, 42, 64),
+    # bootstrappable chain: q0 60 bits, 12 application levels
+    # of 42 bits, then 58 / 60 / 15 x 55 bits for SlotToCoeff, EvalMod and
+    # CoeffToSlot; P = 4 x 60 bits; top scale 2^55 (scale 2^42 from level 12 down)
+    "boot16": (16, [60] + [42] * 12 + [58, 60] + [55] * 15, [60] * 4, 4, 55, 64),
+    # the same chain on a 2^10 ring (test-only, insecure): bootstrapping parity
+    "boot10": (10, [60] + [42] * 12 + [58, 60] + [55] * 15, [60] * 4, 4, 55, 64),
     "tiny": (10, [50] + [40] * 3, [50], 1, 40, 32),
 }
 
@@ -75,6 +84,10 @@ def lib():
         L.orc_mul_const.argtypes = [P, u64p, I, D, D, u64p]
         L.orc_mul_i.argtypes = [P, u64p, I, u64p]
         L.orc_mul_pt.argtypes = [P, u64p, u64p, I, u64p]
+        L.orc_mul_pt_raw.argtypes = [P, u64p, u64p, I, u64p]
+        L.orc_mul_int.argtypes = [P, u64p, I, U, u64p]
+        L.orc_mod_raise.argtypes = [P, u64p, I, u64p]
+        L.orc_set_app_level.argtypes = [P, I]
         L.orc_add_pt.argtypes = [P, u64p, u64p, I, I, u64p]
         L.orc_rescale.argtypes = [P, u64p, I, I, u64p]
         L.orc_drop.argtypes = [P, u64p, I, I, u64p]
@@ -104,6 +117,7 @@ class RnsParams:
         self.L, self.K, self.alpha = len(qb) - 1, len(pb), alpha
         self.dnum = -(-len(qb) // alpha)
         self.slots = self.N // 2
+        self.app_L = self.L
         qa = (C.c_int * len(qb))(*qb)
         pa = (C.c_int * len(pb))(*pb)
         self.h = lib().orc_create(logN, len(qb), qa, len(pb), pa, alpha, logs, hw, sigma, seed)
@@ -188,6 +202,21 @@ class RnsParams:
         lib().orc_mul_pt(self.h, a, np.ascontiguousarray(pt), level, o)
         return o
 
+    def mul_pt_raw(self, a, pt, level):
+        o = self._out(level)
+        lib().orc_mul_pt_raw(self.h, np.ascontiguousarray(a), np.ascontiguousarray(pt), level, o)
+        return o
+
+    def mul_int(self, a, level, k):
+        o = self._out(level)
+        lib().orc_mul_int(self.h, np.ascontiguousarray(a), level, int(k), o)
+        return o
+
+    def mod_raise(self, a, to):
+        o = self._out(to)
+        lib().orc_mod_raise(self.h, np.ascontiguousarray(a), to, o)
+        return o
+
     def mul_i(self, a, level):
         o = self._out(level)
         lib().orc_mul_i(self.h, a, level, o)
@@ -227,8 +256,12 @@ class RnsParams:
         lib().orc_automorph(self.h, a, level, g, o)
         return o
 
+    def set_app_level(self, level):
+        self.app_L = level
+        lib().orc_set_app_level(self.h, level)
+
     def refresh(self, a, level, nonce):
-        o = self._out(self.L)
+        o = self._out(self.app_L)
         lib().orc_refresh(self.h, a, level, nonce, o)
         return o
 
@@ -272,8 +305,15 @@ class RnsBlock:
 class OracleCKKSContext:
     """EmulatorContext duck type (emulator.py:111-281) over RNS-CKKS residues."""
 
-    def __init__(self, params="cfg0", grid_rows=None, *, auto_bootstrap=False, seed=2024, hoist=True):
+    def __init__(self, params="cfg0", grid_rows=None, *, auto_bootstrap=False, seed=2024, hoist=True,
+                 bootstrap="surrogate"):
         self.p = params if isinstance(params, RnsParams) else RnsParams(params, seed=seed)
+        if self.p.name in APP_LEVELS:
+            self.p.set_app_level(APP_LEVELS[self.p.name])
+        # the reference's bootstrap: the refresh surrogate, or CKKS
+        # bootstrapping restated in oracle/boot.py (a nonce is drawn either way)
+        self.bootstrap_mode = bootstrap
+        self._boot = None
         # fused schedule forms (hoisted rotations, one relinearisation per
         # product sum) where the restated DiagABT / DiagATB use them; the
         # CUDA product's `hoist` flag must match for residue parity
@@ -281,7 +321,7 @@ class OracleCKKSContext:
         self.slot_count = self.p.slots
         self.grid_rows = grid_rows or (1 << (int(np.log2(self.slot_count)) // 2))
         self.grid_cols = self.slot_count // self.grid_rows
-        self.max_level = self.p.L
+        self.max_level = self.p.app_L
         self.auto_bootstrap = auto_bootstrap
         self.ledger = S.Ledger()
         self.extra = {"LevelAdjust": 0, "KeySwitch": 0}
@@ -341,8 +381,17 @@ class OracleCKKSContext:
             return b
         if self.auto_bootstrap:
             self.ledger.record("Bootstrap")
-            return RnsBlock(self, self.p.refresh(b.data, b.level, self._next_nonce()), self.max_level)
+            return self._refresh(b)
         raise S.DepthExhausted(f"mult: operand at level {b.level}")
+
+    def _refresh(self, b):
+        nonce = self._next_nonce()
+        if self.bootstrap_mode == "ckks":
+            if self._boot is None:
+                from . import boot
+                self._boot = boot.Bootstrapper(self.p, self.max_level)
+            return RnsBlock(self, self._boot.bootstrap(b.data, b.level), self.max_level)
+        return RnsBlock(self, self.p.refresh(b.data, b.level, nonce), self.max_level)
 
     # -- arithmetic -------------------------------------------------------
     def _addsub(self, x, y, neg):
@@ -464,7 +513,7 @@ class OracleCKKSContext:
         if not isinstance(x, RnsBlock):
             return x
         self.ledger.record("Bootstrap")
-        return RnsBlock(self, self.p.refresh(x.data, x.level, self._next_nonce()), self.max_level)
+        return self._refresh(x)
 
     def note_decode(self, role, tag=None):
         self.decode_events.append((role, tag))

@@ -83,6 +83,9 @@ SIGNATURES = {
     "hc_row_major_atb": (I, [P, PP, I, PP, I, I, D, PP, I64P]),
     "hc_mod_reduce": (I, [P, P]),
     "hc_set_shard": (I, [P, I, I]),
+    "hc_set_app_level": (I, [P, I]),
+    "hc_set_bootstrap": (I, [P, I]),
+    "hc_bootstrap_ct": (I, [P, P, PP]),
     "hc_set_pass_shard": (I, [P, I, I, REDUCE_FN, P]),
     "hc_ctx_model_bytes": (I, [P, DP, I]),
     "hc_ctx_stream": (I, [P, PP]),

@@ -45,8 +45,20 @@ PARAMS = {
     # cfg1's chain at the reference's default run_steps context
     # (EmulatorContext(4096, 64, max_level=12), training.py:361); insecure ring
     "n13l12": (13, [58] + [42] * 12, [60] * 3, 4, 42, 64),
+    # bootstrappable chain: q0 60 bits, 12 application levels
+    # of 42 bits (scale 2^42), then 58 / 60 / 15 x 55 bits for SlotToCoeff,
+    # EvalMod and CoeffToSlot (top scale 2^55); P = 4 x 60 bits
+    "boot16": (16, [60] + [42] * 12 + [58, 60] + [55] * 15, [60] * 4, 4, 55, 64),
+    # the same chain on a 2^10 ring (test-only, insecure): bootstrapping parity
+    "boot10": (10, [60] + [42] * 12 + [58, 60] + [55] * 15, [60] * 4, 4, 55, 64),
     "tiny": (10, [50] + [40] * 3, [50], 1, 40, 32),
 }
+
+
+# parameter sets whose chain carries bootstrapping levels above the
+# application's: the EmulatorContext's max_level is this application level
+APP_LEVELS = {"boot16": 12, "boot10": 12}
+BOOTSTRAP_MODES = ("surrogate", "ckks")
 
 
 def params_for(slot_count: int, max_level: int) -> str:
@@ -168,7 +180,7 @@ class CKKSContext:
 
     def __init__(self, params: str | int = "cfg1", grid_rows: int | None = None, *, max_level=None,
                  auto_bootstrap: bool = False, seed: int = 2024, sigma: float = 3.2, device: int = 0,
-                 op_weights=None, hoist: bool = True):
+                 op_weights=None, hoist: bool = True, bootstrap: str = "surrogate"):
         if isinstance(params, (int, np.integer)):
             params = params_for(int(params), 12 if max_level is None else max_level)
         logn, qb, pb, alpha, logs, hw = PARAMS[params]
@@ -181,7 +193,8 @@ class CKKSContext:
             raise SlotCountMismatch(f"grid_rows must be a power of two <= slot_count, got {grid_rows}")
         self.grid_rows = grid_rows
         self.grid_cols = self.slot_count // grid_rows
-        self.max_level = len(qb) - 1
+        self.max_level = APP_LEVELS.get(params, len(qb) - 1)
+        self.chain_top = len(qb) - 1
         if max_level is not None and max_level != self.max_level:
             raise ValueError(f"parameter set {params} has max_level {self.max_level}")
         self.K, self.alpha = len(pb), alpha
@@ -194,6 +207,12 @@ class CKKSContext:
                                       C.byref(h)))
         self._h = h
         N.check(N.lib().hc_set_grid_rows(self._h, grid_rows))
+        if self.max_level != self.chain_top:
+            N.check(N.lib().hc_set_app_level(self._h, self.max_level))
+        if bootstrap not in BOOTSTRAP_MODES:
+            raise ValueError(f"bootstrap must be one of {BOOTSTRAP_MODES}")
+        self.bootstrap_mode = bootstrap
+        N.check(N.lib().hc_set_bootstrap(self._h, int(bootstrap == "ckks")))
         self._auto = False
         self.auto_bootstrap = auto_bootstrap
         self._hoist = True
@@ -511,6 +530,10 @@ class CKKSContext:
         return self._new(N.lib().hc_op_bootstrap, x._h)
 
     # exact primitives (no ledger)
+    def ckks_bootstrap(self, x: Ciphertext) -> Ciphertext:
+        """One CKKS bootstrapping, whatever ``bootstrap_mode`` is."""
+        return self._new(N.lib().hc_bootstrap_ct, x._h)
+
     def rescale(self, x: Ciphertext) -> Ciphertext:
         return self._new(N.lib().hc_rescale, x._h)
 

@@ -368,6 +368,26 @@ int hc_ctx_model_bytes(hc_ctx* ctx, double* bytes, int reset) {
     });
 }
 
+int hc_set_app_level(hc_ctx* ctx, int level) {
+    return guard([&] {
+        if (level < 1 || level > ctx->c->L) throw hc::Error(HC_EPARAM, "application level out of range");
+        ctx->c->app_L = level;
+    });
+}
+
+int hc_set_bootstrap(hc_ctx* ctx, int mode) {
+    return guard([&] {
+        if (mode < 0 || mode > 1) throw hc::Error(HC_EPARAM, "bootstrap mode is 0 (surrogate) or 1 (CKKS)");
+        if (mode == 1 && ctx->c->L - 17 != ctx->c->app_L)
+            throw hc::Error(HC_EPARAM, "CKKS bootstrapping needs 17 chain levels above the application's");
+        ctx->c->boot_mode = mode;
+    });
+}
+
+int hc_bootstrap_ct(hc_ctx* ctx, const hc_ct* a, hc_ct** out) {
+    return guard([&] { *out = wrap(hc::ev_bootstrap(*ctx->c, a->p)); });
+}
+
 int hc_set_shard(hc_ctx* ctx, int total_blocks, int first_block) {
     return guard([&] {
         if (total_blocks < 0 || first_block < 0 || (total_blocks && first_block >= total_blocks))

@@ -216,7 +216,7 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     if (logN < 4 || logN > 17 || nq < 1 || np < 1 || nq + np > MAXP || alpha < 1 || alpha > 8 || np > 8)
         throw Error(-1, "bad parameters");
     Ctx* c = new Ctx();
-    c->logN = logN; c->N = 1 << logN; c->L = nq - 1; c->K = np; c->alpha = alpha;
+    c->logN = logN; c->N = 1 << logN; c->L = nq - 1; c->K = np; c->alpha = alpha; c->app_L = nq - 1;
     c->dnum = (nq + alpha - 1) / alpha; c->nall = nq + np; c->hw = hw; c->sigma = sigma; c->seed = seed;
     c->device = device;
     const int N = c->N, M = N / 2, nall = c->nall, L = c->L, K = c->K;
@@ -670,7 +670,7 @@ std::vector<CtP> refresh_batch(Ctx& c, const std::vector<const Ct*>& a, const st
         const int level = a[b0]->level;
         for (int b = 0; b < B; b++)
             if (a[b0 + b]->level != level) throw Error(-4, "batched refresh needs one level");
-        const int two = level >= 1 ? 1 : 0, nl = c.L + 1;
+        const int two = level >= 1 ? 1 : 0, nl = c.app_L + 1;
         Scratch sc(c);
         u64* X = sc.take((size_t)B * (1 + two) * c.N);
         std::vector<const u64*> c0(B), c1(B);
@@ -679,7 +679,7 @@ std::vector<CtP> refresh_batch(Ctx& c, const std::vector<const Ct*>& a, const st
             c0[b] = a[b0 + b]->poly(0);
             c1[b] = a[b0 + b]->poly(1);
             xb[b] = X + (size_t)b * (1 + two) * c.N;
-            out[b0 + b] = new_ct(c, c.L);
+            out[b0 + b] = new_ct(c, c.app_L);
             o[b] = out[b0 + b]->d;
         }
         const u64* nn = nonces.data() + b0;
@@ -696,7 +696,7 @@ std::vector<CtP> refresh_batch(Ctx& c, const std::vector<const Ct*>& a, const st
             ntt_inverse(c, j);
         }
         const u64 inv01 = two ? invmod(c.pr[0].q % c.pr[1].q, c.pr[1].q) : 0;
-        k_refresh_batch(c, B, nullptr, nullptr, xb.data(), o.data(), nn, 1, two, inv01, c.scale[c.L] / c.scale[level]);
+        k_refresh_batch(c, B, nullptr, nullptr, xb.data(), o.data(), nn, 1, two, inv01, c.scale[c.app_L] / c.scale[level]);
         for (int base = 0; base < B * nl; base += MAXJ) {
             JobList j;
             j.n = std::min(MAXJ, B * nl - base);
@@ -718,9 +718,9 @@ CtP refresh(Ctx& c, const Ct& a, u64 nonce) {
     u64* x = dec_limbs(c, a, 1 + two);
     i64* m = (i64*)c.alloc(c.N);
     const u64 inv01 = two ? invmod(c.pr[0].q % c.pr[1].q, c.pr[1].q) : 0;
-    k_refresh_msg(c, m, x, two, inv01, c.scale[c.L] / c.scale[a.level]);
+    k_refresh_msg(c, m, x, two, inv01, c.scale[c.app_L] / c.scale[a.level]);
     c.free(x);
-    CtP out = encrypt_coef_dev(c, m, c.L, nonce);
+    CtP out = encrypt_coef_dev(c, m, c.app_L, nonce);
     c.free((u64*)m);
     return out;
 }

@@ -532,10 +532,21 @@ std::vector<u64> Eval::batch_nonces(const std::vector<int>& r) {
     return out;
 }
 
-CtP Eval::refresh_planned(const CtP& a, int j, int r) { return refresh(c, *a, boot_nonce(j, r)); }
+// the reference's bootstrap (emulator.py:267-273): the refresh surrogate, or
+// with c.boot_mode real CKKS bootstrapping (bootstrap.cu; the nonce is drawn
+// either way, so both modes keep one nonce sequence)
+static CtP do_refresh(Ctx& c, const CtP& a, u64 nonce) {
+    return c.boot_mode ? ev_bootstrap(c, a) : refresh(c, *a, nonce);
+}
+
+CtP Eval::refresh_planned(const CtP& a, int j, int r) { return do_refresh(c, a, boot_nonce(j, r)); }
 
 // refresh the given operands with their nonces, batched per level
 static void refresh_many(Ctx& c, std::vector<CtP*>& slots, const std::vector<u64>& nonces) {
+    if (c.boot_mode) {
+        for (size_t u = 0; u < slots.size(); u++) *slots[u] = do_refresh(c, *slots[u], nonces[u]);
+        return;
+    }
     std::map<int, std::vector<size_t>> by_level;
     for (size_t u = 0; u < slots.size(); u++) by_level[(*slots[u])->level].push_back(u);
     for (auto& kv : by_level) {

@@ -37,6 +37,10 @@ struct KsHoist {
     u64* out;
 };
 bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int level, int B, const KsHoist* e);
+// CKKS bootstrapping (bootstrap.cu): any level -> app_L
+CtP ev_mod_raise(Ctx& c, const Ct& a, int to);
+CtP ev_bootstrap(Ctx& c, const CtP& a);
+
 // out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
 bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);
 bool rescale_fused(Ctx& c, const u64* a, int level, int npoly, u64* out);

@@ -83,6 +83,12 @@ enum OpKind { OP_ADD = 0, OP_CMULT, OP_MULT, OP_ROT, OP_CONJ, OP_BOOT, OP_ADJUST
 
 struct Ctx {
     int logN, N, L, K, alpha, dnum, nall, hw;
+    // the application's top level (EmulatorContext.max_level): fresh
+    // encryptions default to it and the refresh / bootstrap land on it; below
+    // L when the chain carries bootstrapping levels above
+    int app_L = 0;
+    int boot_mode = 0;            // 0: refresh surrogate, 1: CKKS bootstrapping (hc_set_bootstrap)
+    std::shared_ptr<struct BootState> boot;   // bootstrapping plan and plaintexts (bootstrap.cu)
     double sigma;
     u64 seed;
     int device;

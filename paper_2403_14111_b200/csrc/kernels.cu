@@ -661,7 +661,7 @@ void k_refresh_batch(Ctx& c, int B, const u64* const* c0, const u64* const* c1, 
         rb.key_a[b] = rng_key(c.seed, stream_id(DOM_ENC_A, nonces[b], 0));
         rb.key_e[b] = rng_key(c.seed, stream_id(DOM_ENC_E, nonces[b], 0));
     }
-    const int nl = c.L + 1;
+    const int nl = c.app_L + 1;
     if (stage == 0) {
         Launch scope(c, "decrypt_limbs", 8.0 * c.N * 4 * (1 + two) * B);
         dim3 grid((unsigned)std::max(1, nblocks((size_t)(1 + two) * c.N, 256) / B), B);
@@ -716,6 +716,32 @@ void k_mod_reduce(Ctx& c, u64* x, int nl, int npoly) {
     Launch scope(c, "mod_reduce", 16.0 * c.N * npoly * nl);
     dim3 grid((unsigned)std::min<size_t>((c.N / 2 + 255) / 256, 64), npoly * nl);
     launch_k(c, mod_reduce_kernel, grid, 256, 0, x, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ModRaise lift (bootstrap.cu): X [2][N] coefficients mod q0 (canonical),
+// centred, reduced into every prime q_0 .. q_{nl-1}: out [2][nl][N]
+// (coefficient form; the caller runs the forward NTT).  grid (x, limb, poly)
+__global__ void mod_raise_kernel(u64* __restrict__ out, const u64* __restrict__ X, const PrimeDev* __restrict__ primes,
+                                 int nl, int N) {
+    pdl_enter();
+    const int i = blockIdx.y, s = blockIdx.z;
+    const PrimeDev P = primes[i];
+    const u64 q0 = primes[0].q, half = (q0 - 1) / 2;
+    const u64 q0m = csub(mul_shoup_lazy(q0, 1, P.mu_hi, P.q), P.q);
+    const u64* x = X + (size_t)s * N;
+    u64* o = out + ((size_t)s * nl + i) * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const u64 v = x[k];
+        const u64 r = csub(mul_shoup_lazy(v, 1, P.mu_hi, P.q), P.q);
+        o[k] = v > half ? sub_mod(r, q0m, P.q) : r;
+    }
+}
+
+void k_mod_raise(Ctx& c, u64* out, const u64* X, int nl) {
+    Launch scope(c, "mod_raise", 8.0 * c.N * 2 * (1.0 + nl));
+    dim3 grid((unsigned)std::min((c.N + 255) / 256, 64), nl, 2);
+    launch_k(c, mod_raise_kernel, grid, 256, 0, out, X, c.d_primes, nl, c.N);
     HC_CUDA(cudaGetLastError());
 }
 

@@ -20,6 +20,8 @@ void k_elementwise_batch(Ctx& c, int op, int B, u64* const* out, const u64* cons
 // d = sum_q tensor(a[q], b[q]), n <= 8
 void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int n, int nl);
 void k_automorph(Ctx& c, u64* out, const u64* in, int nlimbs, u64 g);
+// ModRaise lift of [2][N] level-0 coefficients to [2][nl][N] (bootstrap.cu)
+void k_mod_raise(Ctx& c, u64* out, const u64* X, int nl);
 void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta);
 void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta);
 void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level);

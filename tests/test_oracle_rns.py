@@ -226,3 +226,18 @@ def test_fused_schedules_keep_the_reference_ledger(golden, hoist):
         led = np.array([ctx.ledger.counts()[k] for k in OPS])
         np.testing.assert_array_equal(led, golden[f"small_atb_{branch}_led"])
         assert np.max(np.abs(S.decode(r, tol=1e-4) - golden[f"small_atb_{branch}_out"])) < 1e-4
+
+
+def test_oracle_ckks_bootstrapping_boot10():
+    """The restated CKKS bootstrapping (oracle/boot.py) on the 2^10 ring:
+    a level-0 ciphertext refreshed to the application level 12 without the
+    secret key, message within 1e-4."""
+    from oracle import boot as B
+    p = R.RnsParams("boot10", seed=5)
+    p.set_app_level(12)
+    bt = B.Bootstrapper(p, 12)
+    rng = np.random.default_rng(1)
+    w = rng.uniform(-1, 1, p.slots) + 1j * rng.uniform(-1, 1, p.slots)
+    out = bt.bootstrap(p.encrypt(w, 0, 7), 0)
+    assert out.shape == (2, 13, p.N)
+    assert np.max(np.abs(p.decrypt(out, 12) - w)) < 1e-4

@@ -476,6 +476,7 @@ void ctx_destroy(Ctx* c) {
     }
     c->pt_cache.clear();
     c->pt_cache_bytes = 0;
+    c->boot.reset();   // bootstrapping plaintexts return to the pool while it exists
     for (auto& kv : c->keys) cudaFree(kv.second.d);
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);

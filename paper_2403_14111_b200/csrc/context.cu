@@ -361,6 +361,23 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
             }
         }
     c->d_modup_negq = upload(*c, mu_negq);
+    std::vector<u64> mu_cc((size_t)(L + 1) * c->dnum * nall, 0);
+    for (int l = 0; l <= L; l++)
+        for (int j = 0; j < c->dnum; j++) {
+            const int lo = j * alpha;
+            if (lo > l) continue;
+            const int hi = std::min(lo + alpha, l + 1);
+            for (int t = 0; t < nall; t++) {
+                const u64 pt = c->pr[t].q;
+                u64 sacc = 0;
+                for (int a = lo; a < hi; a++) {
+                    const size_t ti = (((size_t)(l * c->dnum + j) * alpha + (a - lo)) * nall + t) * 2;
+                    sacc = (sacc + mulm(((c->pr[a].q - 1) / 2) % pt, mu_tab[ti], pt)) % pt;
+                }
+                mu_cc[(size_t)(l * c->dnum + j) * nall + t] = sacc ? pt - sacc : 0;
+            }
+        }
+    c->d_modup_cc = upload(*c, mu_cc);
 
     // ModDown tables
     std::vector<u64> md_tab((size_t)K * nall * 2), md_inv((size_t)K * 2), pinv((size_t)nall * 2), pm(nall);
@@ -393,6 +410,15 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     std::vector<u64> md_negp(nall);
     for (int i = 0; i < nall; i++) md_negp[i] = pm[i] ? c->pr[i].q - pm[i] : 0;
     c->d_moddown_negp = upload(*c, md_negp);
+    std::vector<u64> md_cc(nall, 0);
+    for (int i = 0; i < nall; i++) {
+        const u64 qi = c->pr[i].q;
+        u64 sacc = 0;
+        for (int t = 0; t < K; t++)
+            sacc = (sacc + mulm(((c->pr[L + 1 + t].q - 1) / 2) % qi, md_tab[((size_t)t * nall + i) * 2], qi)) % qi;
+        md_cc[i] = sacc ? qi - sacc : 0;
+    }
+    c->d_moddown_cc = upload(*c, md_cc);
     c->d_pinv = upload(*c, pinv);
     // P mod q_i for key generation lives right after the rescale table
     std::vector<u64> rs((size_t)(L + 1) * nall * 3 + nall, 0);
@@ -480,7 +506,7 @@ void ctx_destroy(Ctx* c) {
     for (auto& kv : c->keys) cudaFree(kv.second.d);
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
-    cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_modup_negq); cudaFree(c->d_moddown_negp); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
+    cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_modup_negq); cudaFree(c->d_moddown_negp); cudaFree(c->d_modup_cc); cudaFree(c->d_moddown_cc); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
     cudaStreamSynchronize(c->stream);
     for (auto s : c->side) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
     for (auto e : c->side_ev) cudaEventDestroy(e);

@@ -37,6 +37,7 @@ struct Error : std::runtime_error {
 struct JobList {
     int n = 0;
     int custom = 0;          // inverse only: final multiplier scale[] instead of N^-1
+    int center = 0;          // inverse only: outputs shifted by (q-1)/2 mod q (centred base conversion input)
     u64 galois = 0;          // first pass gathers the source through this automorphism
     int prime[MAXJ];
     u64* ptr[MAXJ];
@@ -156,6 +157,11 @@ struct Ctx {
     // from the upper half of its prime
     u64* d_modup_negq = nullptr;  // [L+1][dnum][nall]
     u64* d_moddown_negp = nullptr;   // [nall]
+    // the fused passes read inputs shifted by h_a = (q_a-1)/2 (y'' = y + h_a
+    // mod q_a, so the centred value is y'' - h_a) and start from the constant
+    // [-sum_a h_a [Q'/q_a]_p]_p (ModUp) / [-sum_t h_t [P/p_t]_{q_i}]_{q_i} (ModDown)
+    u64* d_modup_cc = nullptr;    // [L+1][dnum][nall]
+    u64* d_moddown_cc = nullptr;  // [nall]
     u64* d_pinv = nullptr;        // [nall] (value, shoup) P^-1 mod q_i
     u64* d_rescale = nullptr;     // [L+1 (dropped prime l)][nall] (q_l^-1 mod q_i, shoup, q_l mod q_i)
     // counters

@@ -75,25 +75,29 @@ struct KsBatch {
 
 // Conversion constants live in registers and the per-limb base pointers are
 // formed once, so each converted element costs NA Shoup products and loads.
-// Centred conversion: a term from the upper half of its prime
-// stands for y_a - q_a, i.e. adds [-Q']_p once more (q_a [Q'/q_a] = Q').
+// Centred conversion: the inputs arrive shifted, y'' = y + h_a
+// mod q_a with h_a = (q_a - 1) / 2 (the producing INTT's store adds it), so the
+// centred value is y'' - h_a and sum_a (y''_a - h_a) [Q'/q_a]_p starts from
+// the per-(digit, target) constant cc = [-sum_a h_a [Q'/q_a]_p]_p: no
+// per-term comparison.
 template <int NA>
 struct LdModup {
-    const u64* __restrict__ y[NA];   // Y limbs of the digit, coefficient form, pre-scaled by (Q'/q_a)^-1
-    u64 w[NA], ws[NA];               // [Q'/q_a]_p and Shoup companions
-    u64 half[NA];                    // (q_a - 1) / 2
-    u64 negq;                        // [-Q']_p
+    const u64* __restrict__ y[NA];   // shifted Y limbs of the digit, coefficient form, pre-scaled by (Q'/q_a)^-1
+    u64 w[NA], ws[NA];               // [Q'/q_a]_p and Shoup companions (0 for an inert term)
+    u64 cc;                          // [-sum_a h_a [Q'/q_a]_p]_p
     int na;
     u64 p;
+    // Terms a >= na are inert (w = ws = 0) and their pointer is a valid
+    // limb, so every load is unconditional: the NA loads of an element issue
+    // together instead of one load -> use chain per term.
     __device__ __forceinline__ u64 operator()(size_t k) const {
-        u64 acc = 0;
+        u64 v[NA];
 #pragma unroll
-        for (int a = 0; a < NA; a++)
-            if (a < na) {
-                const u64 v = y[a][k];
-                acc += mul_shoup_lazy(v, w[a], ws[a], p) + (v > half[a] ? negq : 0);
-            }
-        return acc;   // < 3 * NA * p: the pass's input bound (INB = 3 * NA)
+        for (int a = 0; a < NA; a++) v[a] = __ldg(y[a] + k);
+        u64 acc = cc;
+#pragma unroll
+        for (int a = 0; a < NA; a++) acc += mul_shoup_lazy(v[a], w[a], ws[a], p);
+        return acc;   // < (2 * NA + 1) * p: the pass's input bound
     }
     __device__ __forceinline__ void load8(size_t k, u64* x) const {
 #pragma unroll
@@ -104,10 +108,13 @@ struct LdModup {
 #ifndef KS_PMB_CHAIN
 #define KS_PMB_CHAIN PASS_MIN_BLOCKS   // register budget of the column passes of a lone key switch (grid z = 1)
 #endif
-template <int LOGSZ, int SUBS, int NA, int PMB = PASS_MIN_BLOCKS>
+#ifndef KS_COLS_PMB
+#define KS_COLS_PMB PASS_MIN_BLOCKS    // register budget of the batched conversion column passes
+#endif
+template <int LOGSZ, int SUBS, int NA, int PMB = KS_COLS_PMB>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ks_modup_cols(KsJobs jobs, KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ Y, const u64* __restrict__ modup_tab,
-                  const u64* __restrict__ negq_tab, u64* __restrict__ I) {
+                  const u64* __restrict__ cc_tab, u64* __restrict__ I) {
     pdl_trigger();
     extern __shared__ u64 sm[];
     const int job = blockIdx.y;
@@ -124,14 +131,14 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ld.na = hi - lo;
     ld.p = p;
     const u64* cf = modup_tab + (((size_t)(g.level * g.dnum + j) * g.alpha) * g.nall + pi) * 2;
-    ld.negq = negq_tab[(size_t)(g.level * g.dnum + j) * g.nall + pi];
+    ld.cc = cc_tab[(size_t)(g.level * g.dnum + j) * g.nall + pi];
 #pragma unroll
     for (int a = 0; a < NA; a++) {
-        const int aa = a < ld.na ? a : 0;
+        const bool on = a < ld.na;
+        const int aa = on ? a : 0;
         ld.y[a] = Y + (size_t)(lo + aa) * N;
-        ld.w[a] = cf[(size_t)aa * g.nall * 2];
-        ld.ws[a] = cf[(size_t)aa * g.nall * 2 + 1];
-        ld.half[a] = (primes[lo + aa].q - 1) / 2;
+        ld.w[a] = on ? cf[(size_t)aa * g.nall * 2] : 0;
+        ld.ws[a] = on ? cf[(size_t)aa * g.nall * 2 + 1] : 0;
     }
     StPlain<false, false> st{I + ((size_t)j * g.nt + t) * N, p, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
@@ -140,7 +147,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
     pdl_wait();   // everything above reads context-lifetime tables only
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 3 * NA, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA + 1, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
@@ -255,10 +262,10 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : 3) ks_keyprod_stream(K
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
 // (the P -> Q conversion has the ModUp loader's shape: K inputs, one target)
-template <int LOGSZ, int SUBS, int NK, int PMB = PASS_MIN_BLOCKS>
+template <int LOGSZ, int SUBS, int NK, int PMB = KS_COLS_PMB>
 __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ks_moddown_cols(KsGeo g, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, const u64* __restrict__ acc, const u64* __restrict__ md_tab,
-                    const u64* __restrict__ negp, u64* __restrict__ Wt) {
+                    const u64* __restrict__ cc_tab, u64* __restrict__ Wt) {
     pdl_trigger();
     extern __shared__ u64 sm[];
     const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
@@ -270,14 +277,14 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     LdModup<NK> ld;
     ld.na = g.K;
     ld.p = q;
-    ld.negq = negp[i];
+    ld.cc = cc_tab[i];
 #pragma unroll
     for (int t = 0; t < NK; t++) {
-        const int tt = t < g.K ? t : 0;
+        const bool on = t < g.K;
+        const int tt = on ? t : 0;
         ld.y[t] = acc + ((size_t)s * g.nt + g.nl + tt) * N;
-        ld.w[t] = md_tab[((size_t)tt * g.nall + i) * 2];
-        ld.ws[t] = md_tab[((size_t)tt * g.nall + i) * 2 + 1];
-        ld.half[t] = (primes[g.L + 1 + tt].q - 1) / 2;
+        ld.w[t] = on ? md_tab[((size_t)tt * g.nall + i) * 2] : 0;
+        ld.ws[t] = on ? md_tab[((size_t)tt * g.nall + i) * 2 + 1] : 0;
     }
     StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ulonglong2* twsm = PassGeo<LOGSZ, MODE_COLS, SUBS>::twsm_of(sm);
     stage_twiddles(G, twsm, TW, g.N1);
     pdl_wait();   // everything above reads context-lifetime tables only
-    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 3 * NK, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
+    ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NK + 1, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
 // ---- E: chunk pass with the ModDown combine in its stores ------------------
@@ -504,6 +511,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         JobList j;
         j.n = nl;
         j.custom = 1;
+        j.center = 1;   // shifted outputs for the centred conversion (LdModup)
         j.galois = gal;
         j.nb = nin;
         for (int b = 0; b < nin; b++) {
@@ -544,7 +552,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         auto go = [&](auto kern) {
             set_smem(kern, csm);
             launch_k(c, kern, grid, CG::THREADS, csm, jobs, g, c.d_primes, c.twp(0, false), Y, c.d_modup,
-                     c.d_modup_negq, I);
+                     c.d_modup_cc, I);
         };
         switch (c.alpha) {
             case 1: if (nin == 1) go(ks_modup_cols<CL, CS, 1, KS_PMB_CHAIN>); else go(ks_modup_cols<CL, CS, 1>); break;
@@ -604,6 +612,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         JobList j;
         j.n = 0;
         j.custom = 1;
+        j.center = 1;   // shifted outputs for the centred P -> Q conversion
         j.nb = B;
         for (int b = 0; b < B; b++) j.boff[b] = (long long)(b * g.acc_stride());
         for (int s = 0; s < 2; s++)
@@ -630,7 +639,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         auto go = [&](auto kern) {
             set_smem(kern, csm);
             launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, c.d_moddown,
-                     c.d_moddown_negp, Wt);
+                     c.d_moddown_cc, Wt);
         };
         switch (K) {
             case 1: if (B == 1) go(ks_moddown_cols<CL, CS, 1, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 1>); break;

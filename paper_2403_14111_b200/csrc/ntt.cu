@@ -56,17 +56,18 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE, SUBS>::THREADS,
     const u64 gal = use_src ? jobs.galois : 0;
     u64 c = P.ninv, cs = P.ninv_s;
     if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
+    const u64 off = (INV && jobs.center) ? (P.q - 1) / 2 : 0;
     // forward input bounds: canonical (or < 2q) residues for the first pass,
     // the column pass's lazy output (< 16q) for the chunk pass; final stores
     // need < 4q, lazy stores < 16q
     constexpr int INB = (MODE == MODE_CHUNKS) ? BOUND_LIM : 2;
     if (gal) {
         LdGalois ld{src, logN, gal};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs, off}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
         else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, pend); }
     } else {
         LdPlain ld{src};
-        if (last) { StPlain<INV, true> st{dst, P.q, c, cs}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs, off}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, 4>(G, sm, TW, P, ld, st, twsm, pend); }
         else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass<LOGSZ, MODE, SUBS, INV, INB, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, pend); }
     }
 }

@@ -442,9 +442,10 @@ template <bool INV, bool FINAL>
 struct StPlain {
     u64* __restrict__ p;
     u64 q, c, cs;
+    u64 off = 0;   // inverse final store: + off mod q (the centred base conversion's shift)
     __device__ __forceinline__ u64 fin(u64 v) const {
         if (!FINAL) return v;
-        if (INV) return mul_shoup(v, c, cs, q);
+        if (INV) return csub(mul_shoup(v, c, cs, q) + off, q);
         v = v >= 2 * q ? v - 2 * q : v;
         return v >= q ? v - q : v;
     }

@@ -318,10 +318,52 @@ struct StModdown {
         return v;
     }
     __device__ __forceinline__ void operator()(size_t k, u64 w) const { out[k] = one(k, w); }
+    // 8 consecutive words: every operand load (ACC, the gathered addend, the
+    // ladder addend) is issued before the first use, so the gathers overlap
+    // instead of forming a load -> use chain per element
     __device__ __forceinline__ void store8(size_t k, const u64* w) const {
+        u64 A[8], D[8], E[8];
+        const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(accq + k);
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const ulonglong2 t = ap[v];
+            A[2 * v] = t.x;
+            A[2 * v + 1] = t.y;
+        }
+        if (add) {
+            if (gal) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) D[e] = add[galois_src((unsigned)(k + e), logN, gal)];
+            } else {
+                const ulonglong2* dp = reinterpret_cast<const ulonglong2*>(add + k);
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const ulonglong2 t = dp[v];
+                    D[2 * v] = t.x;
+                    D[2 * v + 1] = t.y;
+                }
+            }
+        }
+        if (add2) {
+            const ulonglong2* ep = reinterpret_cast<const ulonglong2*>(add2 + k);
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const ulonglong2 t = ep[v];
+                E[2 * v] = t.x;
+                E[2 * v + 1] = t.y;
+            }
+        }
+        u64 r[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            u64 v = mul_shoup(A[e] + MD_OUTB * q - w[e], pinv, pinv_s, q);
+            if (add) v = add_mod(v, D[e], q);
+            if (add2) v = add_mod(v, E[e], q);
+            r[e] = v;
+        }
         ulonglong2* o = reinterpret_cast<ulonglong2*>(out + k);
 #pragma unroll
-        for (int v = 0; v < 4; v++) o[v] = make_ulonglong2(one(k + 2 * v, w[2 * v]), one(k + 2 * v + 1, w[2 * v + 1]));
+        for (int v = 0; v < 4; v++) o[v] = make_ulonglong2(r[2 * v], r[2 * v + 1]);
     }
 };
 

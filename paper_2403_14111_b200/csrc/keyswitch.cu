@@ -463,9 +463,19 @@ struct StRescale {
     }
     __device__ __forceinline__ void operator()(size_t k, u64 y) const { out[k] = one(k, y); }
     __device__ __forceinline__ void store8(size_t k, const u64* y) const {
+        u64 A[8];   // all operand loads before the first use
+        const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(a + k);
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const ulonglong2 t = ap[v];
+            A[2 * v] = t.x;
+            A[2 * v + 1] = t.y;
+        }
         ulonglong2* o = reinterpret_cast<ulonglong2*>(out + k);
 #pragma unroll
-        for (int v = 0; v < 4; v++) o[v] = make_ulonglong2(one(k + 2 * v, y[2 * v]), one(k + 2 * v + 1, y[2 * v + 1]));
+        for (int v = 0; v < 4; v++)
+            o[v] = make_ulonglong2(mul_shoup(A[2 * v] + RS_OUTB * q - y[2 * v], c, cs, q),
+                                   mul_shoup(A[2 * v + 1] + RS_OUTB * q - y[2 * v + 1], c, cs, q));
     }
 };
 

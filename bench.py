@@ -515,7 +515,8 @@ def run_train_step(args, world, rank, local):
     L = N.lib()
     X, y = wl.config4()
     Y = P.one_hot(y, wl.CLASSES)
-    ctx = P.CKKSContext("cfg1", 128, seed=4, device=local, auto_bootstrap=True)
+    ctx = P.CKKSContext("boot16" if args.boot == "ckks" else "cfg1", 128, seed=4, device=local, auto_bootstrap=True,
+                        bootstrap=args.boot)
     w0 = P.init_weights(wl.CLASSES, X.shape[1], wl.INIT_SEED)
     W = P.encode(ctx, w0, "vertical")                       # replicated, same nonces on all ranks
     ctx.nonce = sharding.rank_nonce_base(rank) + 1000
@@ -563,6 +564,8 @@ def run_train_step(args, world, rank, local):
             "data": "synthetic (seeded 10-class Gaussian mixture, BASELINE config 4)",
             "config": {"workload": "data-parallel NAG step over 8 block rows of 128 (DiagABT, softmax, "
                                    "DiagATB with cross-rank mod-sum, NAG update, refresh)",
+                       "refresh": "CKKS bootstrapping (boot16 chain)" if args.boot == "ckks"
+                       else "surrogate (decrypt/re-encrypt), not CKKS bootstrapping",
                        "rows": int(X.shape[0]), "block_rows_per_rank": len(sharding.partition(8, world, rank))},
             "ledger_per_step": counts, "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0),
             "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
@@ -582,7 +585,8 @@ def run_softmax(args, world, rank, local):
 
     L = N.lib()
     Z = wl.config3()
-    ctx = P.CKKSContext("cfg1", 128, seed=3, device=local, auto_bootstrap=True)
+    ctx = P.CKKSContext("boot16" if args.boot == "ckks" else "cfg1", 128, seed=3, device=local, auto_bootstrap=True,
+                        bootstrap=args.boot)
     EZ = P.encode(ctx, Z, "horizontal")
     nonce0 = ctx.nonce
 
@@ -623,10 +627,130 @@ def run_softmax(args, world, rank, local):
             "data": "synthetic (seeded U[-128,128] logits, BASELINE config 3)",
             "config": {"workload": "a_softmax (domain extension R=8 L=2 n=5, a_max, a_exp, a_inv) on one block; "
                                    "replicas only for N > 1",
-                       "refresh": "surrogate (decrypt/re-encrypt), not CKKS bootstrapping"},
+                       "refresh": "CKKS bootstrapping (boot16 chain)" if args.boot == "ckks"
+                       else "surrogate (decrypt/re-encrypt), not CKKS bootstrapping"},
             "max_abs_err_vs_float64": err, "ledger_per_step": counts,
             "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_bootstrap(args, world, rank, local):
+    """One CKKS bootstrapping of a level-0 ciphertext at
+    N = 2^16 on the boot16 chain (ModRaise, CoeffToSlot, EvalMod,
+    SlotToCoeff) landing at level 12; replicas only for N > 1.  The paper's
+    HEaaN bootstrapping: 159 ms on an A40."""
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+
+    L = N.lib()
+    ctx = P.CKKSContext("boot16", 128, seed=5, device=local)
+    rng = np.random.default_rng(1)
+    w = rng.uniform(-1, 1, ctx.slot_count) + 1j * rng.uniform(-1, 1, ctx.slot_count)
+    x = ctx.encrypt(w, 0)
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.wait_ready()
+    for _ in range(args.warmup):
+        y = ctx.ckks_bootstrap(x)
+    ctx.sync()
+    err = float(np.max(np.abs(y.slots - w)))
+    quiet_gc()
+    launches0 = L.hc_launch_count(ctx._h)
+    barrier(world)
+    ms = C.c_float()
+    N.check(L.hc_timer_begin(ctx._h))
+    for _ in range(args.steps):
+        y = ctx.ckks_bootstrap(x)
+    N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+    barrier(world)
+    clk = clocks.stop()
+    total = all_max(ms.value, world)
+    N.check(L.hc_prof_begin(ctx._h))
+    ctx.ckks_bootstrap(x)
+    buf = C.create_string_buffer(1 << 16)
+    N.check(L.hc_prof_end(ctx._h, buf, len(buf)))
+    prof = json.loads(buf.value.decode())
+    line = {"metric": "CKKS bootstrapping ms (N=2^16, 2^15 slots, level 0 -> 12)",
+            "value": total / args.steps, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / args.steps, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (uniform complex slots)",
+            "config": {"workload": "ModRaise + CoeffToSlot (3 BSGS levels) + EvalMod (Chebyshev 27, 4 double "
+                                   "angles, x2) + SlotToCoeff (3 levels); replicas only for N > 1",
+                       "chain": "q0 60 + 12x42 (app) + 58, 60, 15x55 bits; P 4x60; dnum 8"},
+            "max_abs_err": err, "paper_hea_an_a40_ms": 159.0,
+            "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_table4(args, world, rank, local):
+    """The paper's Table 4 (reference harness cli.py:240-356):
+    DiagABT vs the column-major baseline and DiagATB vs the row-major
+    baseline on encrypted operands at N = 2^16 with the table's shapes
+    (a, b, c) and the reference harness's grid (2^15 slots, s0 = min(next
+    pow2(a), slots) rows).  Device time per call (median of `steps` // 4 + 1
+    calls after one warm-up); replicas only.  The paper's A40 / HEaaN times
+    (seconds) are carried for comparison."""
+    import paper_2403_14111_b200 as P
+    from paper_2403_14111_b200 import _native as N
+
+    L = N.lib()
+    rng = np.random.default_rng(7)
+    # (a, b, c) and the paper's A40 seconds: ColMajor, DiagABT, RowMajor, DiagATB (PAPER.md:635-639)
+    table = [((128, 128, 4), (0.1104, 0.0601, 0.1171, 0.0415)),
+             ((256, 256, 8), (0.3203, 0.1211, 0.3167, 0.1239)),
+             ((512, 769, 4), (0.7609, 0.1223, 0.7176, 0.3343)),
+             ((1024, 769, 8), (3.0428, 0.3710, 2.8546, 1.2558)),
+             ((2048, 769, 16), (12.6251, 1.2376, 11.8220, 4.9970))]
+    if os.environ.get("HC_TABLE4_QUICK"):
+        table = table[:2]
+    rows = []
+    ms = C.c_float()
+
+    def timed(fn, reps):
+        fn()
+        N.check(L.hc_timer_begin(ctx._h))
+        for _ in range(reps):
+            fn()
+        N.check(L.hc_timer_end(ctx._h, C.byref(ms)))
+        return ms.value / reps
+
+    clocks = Clocks(local)
+    clocks.start()
+    clocks.wait_ready()
+    for (a, b, c), paper in table:
+        s0 = min(1 << (a - 1).bit_length(), 32768)
+        ctx = P.CKKSContext("cfg1", s0, seed=11, device=local)
+        A = rng.uniform(-1, 1, (a, b)) / np.sqrt(b)
+        B = rng.uniform(-1, 1, (c, b)) / np.sqrt(b)
+        Y = rng.uniform(-1, 1, (a, c))
+        EA, EBv, EB = P.encode(ctx, A), P.encode(ctx, B, "vertical"), P.encode(ctx, B)
+        EY, EYu = P.encode(ctx, Y, "horizontal"), P.encode(ctx, Y)
+        reps = max(1, args.steps // 4) if a <= 512 else 1
+        t_abt = timed(lambda: P.diag_abt(EA, EBv), reps)
+        t_cm = timed(lambda: P.col_major_abt(EA, EB), reps)
+        t_atb = timed(lambda: P.diag_atb(EY, EA), reps)
+        t_rm = timed(lambda: P.row_major_atb(EYu, EA), reps)
+        rows.append({"shape": [a, b, c], "grid_rows": s0, "diag_abt_ms": t_abt, "col_major_abt_ms": t_cm,
+                     "abt_speedup": t_cm / t_abt, "diag_atb_ms": t_atb, "row_major_atb_ms": t_rm,
+                     "atb_speedup": t_rm / t_atb,
+                     "paper_a40_s": {"col_major": paper[0], "diag_abt": paper[1], "row_major": paper[2],
+                                     "diag_atb": paper[3]},
+                     "vs_paper_a40": {"diag_abt": paper[1] * 1e3 / t_abt, "diag_atb": paper[3] * 1e3 / t_atb}})
+        del EA, EBv, EB, EY, EYu
+        ctx.close()
+    clk = clocks.stop()
+    line = {"metric": "Table 4: DiagABT / DiagATB vs column- / row-major baselines, ms per encrypted matmul "
+                      "(N=2^16)", "value": rows[-1]["diag_abt_ms"] + rows[-1]["diag_atb_ms"], "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": 1, "ms_per_step": rows[-1]["diag_abt_ms"] + rows[-1][
+                "diag_atb_ms"], "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (uniform, rows scaled 1/sqrt(b))",
+            "config": {"workload": "Table 4 shapes (a, b, c); cfg1 parameters, grid rows min(next_pow2(a), 2^15)",
+                       "shapes": [t[0] for t in table]},
+            "rows": rows, "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -637,9 +761,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="pair", choices=["pair", "train", "softmax"],
+    ap.add_argument("--workload", default="pair", choices=["pair", "train", "softmax", "bootstrap", "table4"],
                     help="pair: DiagABT+DiagATB (BASELINE metric); train: config-4 data-parallel NAG step; "
-                         "softmax: config-3 encrypted softmax")
+                         "softmax: config-3 encrypted softmax; bootstrap: one CKKS bootstrapping at N=2^16; "
+                         "table4: the paper's Table-4 matmul comparison")
+    ap.add_argument("--boot", default="surrogate", choices=["surrogate", "ckks"],
+                    help="train / softmax: the reference's bootstrap as the refresh surrogate or real CKKS "
+                         "bootstrapping (boot16 chain)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
@@ -654,6 +782,10 @@ def main():
         run_train_step(args, world, rank, local)
     elif args.workload == "softmax":
         run_softmax(args, world, rank, local)
+    elif args.workload == "bootstrap":
+        run_bootstrap(args, world, rank, local)
+    elif args.workload == "table4":
+        run_table4(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
     if world > 1:

@@ -167,12 +167,14 @@ struct TensorSrc {
     const u64* b[TS_MAXN];
 };
 __global__ void tensor_sum_kernel(u64* __restrict__ d, TensorSrc src, int n, const PrimeDev* __restrict__ primes,
-                                  int nl, int N) {
+                                  int nl, int N, int accumulate) {
     pdl_enter();
     const size_t poly = (size_t)nl * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
         const PrimeDev P = primes[e / N];
-        U128 s0 = {0, 0}, s1 = {0, 0}, s2 = {0, 0};
+        // accumulate: continue a longer sum from the previous group's canonical words
+        U128 s0 = {accumulate ? d[e] : 0, 0}, s1 = {accumulate ? d[poly + e] : 0, 0},
+             s2 = {accumulate ? d[2 * poly + e] : 0, 0};
         for (int q = 0; q < n; q++) {
             const u64 a0 = src.a[q][e], a1 = src.a[q][poly + e], b0 = src.b[q][e], b1 = src.b[q][poly + e];
             mac128(s0, a0, b0);
@@ -186,13 +188,19 @@ __global__ void tensor_sum_kernel(u64* __restrict__ d, TensorSrc src, int n, con
     }
 }
 
+// sums of more than TS_MAXN products run in groups, each continuing the
+// previous group's reduced words (exact: the result is the same integer mod q)
 void k_tensor_sum(Ctx& c, u64* d, const u64* const* a, const u64* const* b, int n, int nl) {
-    if (n < 1 || n > TS_MAXN) throw Error(-1, "tensor sum: bad operand count");
-    TensorSrc src;
-    for (int q = 0; q < n; q++) { src.a[q] = a[q]; src.b[q] = b[q]; }
-    Launch scope(c, "tensor", 8.0 * c.N * (4.0 * n + 3) * nl);
-    launch_k(c, tensor_sum_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, d, src, n, c.d_primes, nl, c.N);
-    HC_CUDA(cudaGetLastError());
+    if (n < 1 || n > 64) throw Error(-1, "tensor sum: bad operand count");
+    for (int q0 = 0; q0 < n; q0 += TS_MAXN) {
+        const int m = std::min(TS_MAXN, n - q0);
+        TensorSrc src;
+        for (int q = 0; q < m; q++) { src.a[q] = a[q0 + q]; src.b[q] = b[q0 + q]; }
+        Launch scope(c, "tensor", 8.0 * c.N * (4.0 * m + (q0 ? 6 : 3)) * nl);
+        launch_k(c, tensor_sum_kernel, nblocks((size_t)nl * c.N, 256), 256, 0, d, src, m, c.d_primes, nl, c.N,
+                 q0 ? 1 : 0);
+        HC_CUDA(cudaGetLastError());
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -146,13 +146,14 @@ def test_fused_ops_residues_cfg1():
     _fused_ops(P.CKKSContext("cfg1", 128, seed=3), R.OracleCKKSContext("cfg1", 128, seed=3), seed=7, tol=1e-3)
 
 
-@pytest.mark.parametrize("hoist", [True, False])
-def test_native_multi_column_diag_abt_small12(hoist):
-    """DiagABT with 3 block columns (the product sums fuse when hoist is on):
+@pytest.mark.parametrize("hoist,cols", [(True, 40), (False, 40), (True, 200)])
+def test_native_multi_column_diag_abt_small12(hoist, cols):
+    """DiagABT with 3 (and 13: more than one 8-product group of the fused
+    tensor sum) block columns (the product sums fuse when hoist is on):
     native schedule == restated schedule over the oracle in the same mode."""
     P = _prod()
     rng = np.random.default_rng(4)
-    A, B = rng.uniform(-1, 1, (10, 40)), rng.uniform(-1, 1, (4, 40))
+    A, B = rng.uniform(-1, 1, (10, cols)) / np.sqrt(cols / 40), rng.uniform(-1, 1, (4, cols))
     g = P.CKKSContext("small12", 16, seed=5, hoist=hoist)
     o = R.OracleCKKSContext("small12", 16, seed=5, hoist=hoist)
     GA, OA = _enc_pair(g, o, A)

@@ -229,12 +229,14 @@ CtP linear(Ctx& c, const CtP& x, Group& g) {
     const int nl = l + 1;
     CtP outer;
     for (auto& gv : g.giants) {
-        CtP acc;
+        // sum_b baby_b (x) pdiag_(g, b): one dot-product kernel (128-bit accumulation)
+        std::vector<const u64*> as, ps;
         for (auto& bp : gv.second) {
-            CtP prod = new_ct(c, l);
-            k_elementwise(c, EWP_PT_MUL, prod->d, baby[bp.first]->d, bp.second->d, nullptr, nl, 2, 1);
-            acc = acc ? ev_add(c, *acc, *prod, false) : prod;
+            as.push_back(baby[bp.first]->d);
+            ps.push_back(bp.second->d);
         }
+        CtP acc = new_ct(c, l);
+        k_pt_dot(c, acc->d, as.data(), ps.data(), (int)as.size(), nl);
         CtP inner = rot(c, ev_rescale(c, *acc), (int64_t)gv.first * g.n1 * g.s);
         outer = outer ? ev_add(c, *outer, *inner, false) : inner;
     }

@@ -753,4 +753,42 @@ void k_mod_raise(Ctx& c, u64* out, const u64* X, int nl) {
     HC_CUDA(cudaGetLastError());
 }
 
+// Plaintext dot product (bootstrapping's baby-step giant-step inner sums,
+// bootstrap.cu): out[s][i] = sum_t a_t[s][i] * p_t[i] mod q_i over T <= 16
+// terms, 128-bit accumulation and one reduction (the same words as the
+// separate products and modular adds); grid y = poly * nl + limb
+struct DotSrc {
+    const u64* a[16];
+    const u64* p[16];
+};
+__global__ void pt_dot_kernel(u64* __restrict__ out, DotSrc src, int T, const PrimeDev* __restrict__ primes, int nl,
+                              int N) {
+    pdl_enter();
+    const int limb = blockIdx.y % nl;
+    const PrimeDev P = primes[limb];
+    const size_t off = (size_t)blockIdx.y * N, poff = (size_t)limb * N;
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < (size_t)N / 2; v += (size_t)gridDim.x * blockDim.x) {
+        const size_t k = 2 * v;
+        U128 s0 = {0, 0}, s1 = {0, 0};
+        for (int t = 0; t < T; t++) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(src.a[t] + off + k);
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(src.p[t] + poff + k);
+            mac128(s0, x.x, w.x);
+            mac128(s1, x.y, w.y);
+        }
+        *reinterpret_cast<ulonglong2*>(out + off + k) =
+            make_ulonglong2(reduce128(s0.hi, s0.lo, P), reduce128(s1.hi, s1.lo, P));
+    }
+}
+
+void k_pt_dot(Ctx& c, u64* out, const u64* const* a, const u64* const* p, int T, int nl) {
+    if (T < 1 || T > 16) throw Error(-1, "pt_dot: 1..16 terms");
+    DotSrc src;
+    for (int t = 0; t < T; t++) { src.a[t] = a[t]; src.p[t] = p[t]; }
+    Launch scope(c, "pt_dot", 8.0 * c.N * nl * (3.0 * T + 2));
+    dim3 grid((unsigned)std::min((c.N / 2 + 255) / 256, 64), 2 * nl);
+    launch_k(c, pt_dot_kernel, grid, 256, 0, out, src, T, c.d_primes, nl, c.N);
+    HC_CUDA(cudaGetLastError());
+}
+
 }  // namespace hc

@@ -38,10 +38,11 @@ namespace hc {
 #endif
 constexpr int CH_LOG = 9, CH_SUBS = HC_CH_SUBS;   // chunk pass: 512-point, CH_SUBS per CTA
 
+constexpr int KS_MAXJOBS = 256;   // (digit, target) column-pass jobs of one ModUp (dnum <= 8)
 struct KsJobs {
     int n;
-    unsigned char digit[MAXJ];
-    unsigned char t[MAXJ];
+    unsigned char digit[KS_MAXJOBS];
+    unsigned char t[KS_MAXJOBS];
 };
 
 struct KsGeo {
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
     ntt_pass<LOGSZ, MODE_COLS, SUBS, false, 2 * NA + 1, BOUND_LIM>(G, sm, TW, P, ld, st, twsm, true);
 }
 
-constexpr int KP_MAXB = 4;   // digits handled by the key product (dnum <= 4)
+constexpr int KP_MAXB = 8;   // digits handled by the key product (dnum <= 8; instantiated for 4 and 8)
 #ifndef KP_PAIRB
 #define KP_PAIRB 2           // batches of at least this many key switches take coefficient pairs
 #endif
@@ -186,18 +187,18 @@ __device__ __forceinline__ void kp_load(const u64* __restrict__ base, size_t k, 
 // integer MACs; uniform per CTA): key words converted once per key, not per
 // batch entry.  (Prefetching entry b + 1's digits needs 127 registers; at two
 // resident CTAs it measured slower, 5.8 -> 6.6 ms per pair.)
-template <int E, bool FP>
+template <int E, bool FP, int MB>
 __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t, int pi, int dig, size_t k, u64 gal,
                                        const KsBatch& kb, u64* __restrict__ acc) {
     using KW = typename std::conditional<FP, double, u64>::type;
     const size_t N = (size_t)1 << g.logN;
     const size_t kstride = (size_t)g.nall * N;
-    KW kbv[KP_MAXB][E], kav[KP_MAXB][E];
-    auto load_x = [&](int b, u64 (&x)[KP_MAXB][E]) {
+    KW kbv[MB][E], kav[MB][E];
+    auto load_x = [&](int b, u64 (&x)[MB][E]) {
         const u64* up = kb.up[b];
         const u64 ug = kb.ugal[b];
 #pragma unroll
-        for (int j = 0; j < KP_MAXB; j++) {
+        for (int j = 0; j < MB; j++) {
             if (j >= g.beta) break;
             if (j == dig) kp_load<E>(kb.d[b] + (size_t)t * N, k, ug ? ug : gal, g.logN, x[j]);
             else kp_load<E>(up + ((size_t)j * g.nt + t) * N, k, ug, g.logN, x[j]);
@@ -208,7 +209,7 @@ __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t,
         if (kb.key[b] != kprev) {
             kprev = kb.key[b];
 #pragma unroll
-            for (int j = 0; j < KP_MAXB; j++) {
+            for (int j = 0; j < MB; j++) {
                 if (j >= g.beta) break;
                 const u64* kp = kprev + ((size_t)(2 * j) * g.nall + pi) * N;
                 u64 wb[E], wa[E];
@@ -226,7 +227,7 @@ __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t,
                 }
             }
         }
-        u64 xc[KP_MAXB][E];
+        u64 xc[MB][E];
         load_x(b, xc);
         u64 ob[E], oa[E];
 #pragma unroll
@@ -236,7 +237,7 @@ __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t,
                 // reduced once; digits are lazy words below 16q < 2^50
                 double sb = 0, sa = 0;
 #pragma unroll
-                for (int j = 0; j < KP_MAXB; j++) {
+                for (int j = 0; j < MB; j++) {
                     if (j >= g.beta) break;
                     const double y = fp_word(xc[j][e]);
                     sb = __dadd_rn(sb, fp_mulmod(y, kbv[j][e], P.qd, P.qinv));
@@ -247,7 +248,7 @@ __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t,
             } else {
                 U128 b0 = {0, 0}, a0 = {0, 0};
 #pragma unroll
-                for (int j = 0; j < KP_MAXB; j++) {
+                for (int j = 0; j < MB; j++) {
                     if (j >= g.beta) break;
                     mac128(b0, xc[j][e], kbv[j][e]);
                     mac128(a0, xc[j][e], kav[j][e]);
@@ -267,8 +268,8 @@ __device__ __forceinline__ void kp_run(const KsGeo& g, const PrimeDev& P, int t,
     }
 }
 
-template <int E>
-__global__ void __launch_bounds__(256, E == 2 ? KP_MINB : 3) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
+template <int E, int MB = 4>
+__global__ void __launch_bounds__(256, E == 2 ? KP_MINB : (MB > 4 ? 2 : 3)) ks_keyprod_stream(KsGeo g, const PrimeDev* __restrict__ primes,
                                                                       u64 gal, KsBatch kb,
                                                                       u64* __restrict__ acc, int tlimit) {
     pdl_enter();
@@ -279,8 +280,8 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : 3) ks_keyprod_stream(K
     const size_t k = E * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (k >= N) return;
     const int dig = t < g.nl ? t / g.alpha : -1;   // the digit that contains limb t (uniform), or -1 for a P limb
-    if (P.fp) kp_run<E, true>(g, P, t, pi, dig, k, gal, kb, acc);
-    else kp_run<E, false>(g, P, t, pi, dig, k, gal, kb, acc);
+    if (P.fp) kp_run<E, true, MB>(g, P, t, pi, dig, k, gal, kb, acc);
+    else kp_run<E, false, MB>(g, P, t, pi, dig, k, gal, kb, acc);
 }
 
 // ---- D: ModDown conversion fused into the column pass ----------------------
@@ -650,6 +651,7 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             const int lo = dj * c.alpha, hi = std::min(lo + c.alpha, nl);
             for (int t = 0; t < nt; t++) {
                 if (t >= lo && t < hi) continue;
+                if (j.n == MAXJ) { ntt_forward_chunks(c, j); j.n = 0; }
                 j.prime[j.n] = g.prime(t);
                 j.ptr[j.n] = I + ((size_t)dj * nt + t) * N;
                 j.src[j.n] = nullptr;
@@ -674,7 +676,10 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
                      8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
         // a lone key switch (chains) takes one coefficient per thread for
         // parallelism; batches take pairs (16-byte accesses, fewer index ops)
-        if (B >= KP_PAIRB) {
+        if (g.beta > 4) {   // deep chains (bootstrapping): 8 digits, one coefficient per thread
+            dim3 grid((unsigned)((N + 255) / 256), nt);
+            launch_k(c, ks_keyprod_stream<1, 8>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
+        } else if (B >= KP_PAIRB) {
             dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
             launch_k(c, ks_keyprod_stream<2>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
         } else {

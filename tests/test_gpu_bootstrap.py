@@ -97,3 +97,22 @@ def test_config4_step_with_ckks_bootstrapping(golden):
     assert [led[k] for k in OPS] == [518, 101, 164, 382, 4, 54]
     w1 = P.decode(st.weights, tol=1e-2)
     assert np.max(np.abs(w1 - golden["cfg4_snaps"][0])) < 2e-3
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("level", [29, 20])
+def test_keyswitch_eight_digits_boot16(level):
+    """The fused key switch with 8 digits (the bootstrapping chain's upper
+    levels, dnum > 4): rotation, conjugation and relinearised product
+    residues equal the oracle's at N = 2^16."""
+    P = _prod()
+    g = P.CKKSContext("boot16", 128, seed=9)
+    o = R.OracleCKKSContext("boot16", 128, seed=9)
+    rng = np.random.default_rng(level)
+    x = rng.uniform(-1, 1, g.slot_count) + 1j * rng.uniform(-1, 1, g.slot_count)
+    p = o.p   # raw oracle primitives: levels above the application's
+    ox = p.encrypt(x, level, 3)
+    gx = g.from_residues(ox, level)
+    np.testing.assert_array_equal(g.lrot(gx, 5).residues(), p.automorph(ox, level, p.galois(5)))
+    np.testing.assert_array_equal(g.conj(gx).residues(), p.automorph(ox, level, 2 * p.N - 1))
+    np.testing.assert_array_equal(g.mult(gx, gx).residues(), p.mult(ox, ox, level))

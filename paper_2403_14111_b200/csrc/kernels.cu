@@ -122,21 +122,28 @@ void k_elementwise(Ctx& c, int op, u64* out, const u64* a, const u64* b, const C
 // tensor product: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
 // ---------------------------------------------------------------------------
 
+// grid (x, limb, ciphertext of the batch): the prime is uniform per CTA and
+// every access moves two words (16 bytes)
 __global__ void tensor_kernel(EwPtrs ptr, const PrimeDev* __restrict__ primes, int nl, int N) {
     pdl_enter();
-    u64* __restrict__ d = ptr.out[blockIdx.y];
-    const u64* __restrict__ a = ptr.a[blockIdx.y];
-    const u64* __restrict__ b = ptr.b[blockIdx.y];
-    const size_t poly = (size_t)nl * N;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < poly; e += (size_t)gridDim.x * blockDim.x) {
-        const PrimeDev P = primes[e / N];
-        const u64 a0 = a[e], a1 = a[poly + e], b0 = b[e], b1 = b[poly + e];
-        d[e] = mul_mod(a0, b0, P);
-        U128 acc = {0, 0};
-        mac128(acc, a0, b1);
-        mac128(acc, a1, b0);
-        d[poly + e] = reduce128(acc.hi, acc.lo, P);
-        d[2 * poly + e] = mul_mod(a1, b1, P);
+    u64* __restrict__ d = ptr.out[blockIdx.z];
+    const u64* __restrict__ a = ptr.a[blockIdx.z];
+    const u64* __restrict__ b = ptr.b[blockIdx.z];
+    const size_t poly = (size_t)nl * N, off = (size_t)blockIdx.y * N;
+    const PrimeDev P = primes[blockIdx.y];
+    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < (size_t)N / 2; v += (size_t)gridDim.x * blockDim.x) {
+        const size_t e = off + 2 * v;
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(a + e), a1 = *reinterpret_cast<const ulonglong2*>(a + poly + e);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(b + e), b1 = *reinterpret_cast<const ulonglong2*>(b + poly + e);
+        U128 x0 = {0, 0}, x1 = {0, 0};
+        mac128(x0, a0.x, b1.x);
+        mac128(x0, a1.x, b0.x);
+        mac128(x1, a0.y, b1.y);
+        mac128(x1, a1.y, b0.y);
+        *reinterpret_cast<ulonglong2*>(d + e) = make_ulonglong2(mul_mod(a0.x, b0.x, P), mul_mod(a0.y, b0.y, P));
+        *reinterpret_cast<ulonglong2*>(d + poly + e) =
+            make_ulonglong2(reduce128(x0.hi, x0.lo, P), reduce128(x1.hi, x1.lo, P));
+        *reinterpret_cast<ulonglong2*>(d + 2 * poly + e) = make_ulonglong2(mul_mod(a1.x, b1.x, P), mul_mod(a1.y, b1.y, P));
     }
 }
 
@@ -150,7 +157,7 @@ void k_tensor_batch(Ctx& c, int B, u64* const* d, const u64* const* a, const u64
             p.b[i] = b[b0 + i];
         }
         Launch scope(c, "tensor", 8.0 * c.N * 7 * nl * nb);
-        dim3 grid((unsigned)std::max(1, nblocks((size_t)nl * c.N, 256) / nb), nb);
+        dim3 grid((unsigned)std::max(1, std::min((c.N / 2 + 255) / 256, 2 * 148 * 8 / std::max(1, nl * nb))), nl, nb);
         launch_k(c, tensor_kernel, grid, 256, 0, p, c.d_primes, nl, c.N);
         HC_CUDA(cudaGetLastError());
     }

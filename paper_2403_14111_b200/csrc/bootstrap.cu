@@ -211,41 +211,111 @@ BootState& boot_state(Ctx& c) {
     return *c.boot;
 }
 
-CtP rot(Ctx& c, const CtP& a, int64_t r) {
+// ---- batched forms: every step over the vector of ciphertexts being
+// bootstrapped together (the blocks of one lockstep op), each a batched key
+// switch / rescale / product where the library has one; residues are those
+// of the per-ciphertext ops
+
+using V = std::vector<CtP>;
+
+std::vector<const Ct*> ptrs(const V& v) {
+    std::vector<const Ct*> p(v.size());
+    for (size_t i = 0; i < v.size(); i++) p[i] = v[i].get();
+    return p;
+}
+
+V rot(Ctx& c, const V& a, int64_t r) {
     const int64_t n = c.N / 2;
     r = ((r % n) + n) % n;
     if (r == 0) return a;
-    return ev_automorph(c, *a, galois_rot(c, r));
+    return ev_automorph_batch(c, ptrs(a), galois_rot(c, r), false);
 }
 
-CtP adj(Ctx& c, const CtP& a, int to) { return a->level == to ? a : ev_level_adjust(c, *a, to); }
+V adj(Ctx& c, const V& a, int to) {
+    bool same = true;
+    for (auto& x : a) same = same && x->level == a[0]->level;
+    if (same && a[0]->level > to) return ev_level_adjust_batch(c, ptrs(a), to);
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) o[i] = a[i]->level == to ? a[i] : ev_level_adjust(c, *a[i], to);
+    return o;
+}
+
+V rescale(Ctx& c, const V& a) {
+    const int l = a[0]->level;
+    V o(a.size());
+    std::vector<const u64*> in(a.size());
+    std::vector<u64*> out(a.size());
+    for (size_t i = 0; i < a.size(); i++) {
+        o[i] = new_ct(c, l - 1);
+        in[i] = a[i]->d;
+        out[i] = o[i]->d;
+    }
+    if (!rescale_fused_batch(c, (int)a.size(), in.data(), l, 2, out.data()))
+        for (size_t i = 0; i < a.size(); i++) o[i] = ev_rescale(c, *a[i]);
+    return o;
+}
+
+V add(Ctx& c, const V& a, const V& b, bool sub = false) {
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) o[i] = ev_add(c, *a[i], *b[i], sub);
+    return o;
+}
+
+V add_const(Ctx& c, const V& a, double v) {
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) o[i] = ev_add_const(c, *a[i], v, 0.0, false);
+    return o;
+}
+
+V mul_const(Ctx& c, const V& a, double v) {
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) o[i] = ev_mul_const(c, *a[i], v, 0.0);
+    return o;
+}
+
+V mul_i(Ctx& c, const V& a) {
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) o[i] = ev_mul_i(c, *a[i]);
+    return o;
+}
+
+V mult(Ctx& c, const V& a, const V& b) {
+    std::vector<std::pair<const Ct*, const Ct*>> ab(a.size());
+    for (size_t i = 0; i < a.size(); i++) ab[i] = {a[i].get(), b[i].get()};
+    return ev_mult_batch(c, ab);
+}
+
+V conj(Ctx& c, const V& a) { return ev_automorph_batch(c, ptrs(a), 2 * (u64)c.N - 1, false); }
 
 // y = M x for one merged group (baby-step giant-step), level l -> l - 1
-CtP linear(Ctx& c, const CtP& x, Group& g) {
-    const int l = x->level;
+V linear(Ctx& c, const V& x, Group& g) {
+    const int l = x[0]->level;
     encode_group(c, g, l);
-    std::map<int, CtP> baby;
+    std::map<int, V> baby;
     for (int b : g.babies) baby[b] = rot(c, x, (int64_t)b * g.s);
     const int nl = l + 1;
-    CtP outer;
+    V outer;
     for (auto& gv : g.giants) {
-        // sum_b baby_b (x) pdiag_(g, b): one dot-product kernel (128-bit accumulation)
-        std::vector<const u64*> as, ps;
-        for (auto& bp : gv.second) {
-            as.push_back(baby[bp.first]->d);
-            ps.push_back(bp.second->d);
+        // sum_b baby_b (x) pdiag_(g, b): one dot-product kernel per ciphertext
+        V acc(x.size());
+        for (size_t i = 0; i < x.size(); i++) {
+            std::vector<const u64*> as, ps;
+            for (auto& bp : gv.second) {
+                as.push_back(baby[bp.first][i]->d);
+                ps.push_back(bp.second->d);
+            }
+            acc[i] = new_ct(c, l);
+            k_pt_dot(c, acc[i]->d, as.data(), ps.data(), (int)as.size(), nl);
         }
-        CtP acc = new_ct(c, l);
-        k_pt_dot(c, acc->d, as.data(), ps.data(), (int)as.size(), nl);
-        CtP inner = rot(c, ev_rescale(c, *acc), (int64_t)gv.first * g.n1 * g.s);
-        outer = outer ? ev_add(c, *outer, *inner, false) : inner;
+        V inner = rot(c, rescale(c, acc), (int64_t)gv.first * g.n1 * g.s);
+        outer = outer.empty() ? inner : add(c, outer, inner);
     }
     return outer;
 }
 
-CtP mul_int(Ctx& c, const CtP& a, u64 k) {
+V mul_int(Ctx& c, const V& a, u64 k) {
     ConstTab t;
-    const int nl = a->level + 1;
+    const int nl = a[0]->level + 1;
     for (int i = 0; i < nl; i++) {
         const u64 q = c.pr[i].q, v = k % q;
         t.v[4 * i] = v;
@@ -253,40 +323,43 @@ CtP mul_int(Ctx& c, const CtP& a, u64 k) {
         t.v[4 * i + 2] = v;
         t.v[4 * i + 3] = t.v[4 * i + 1];
     }
-    CtP o = new_ct(c, a->level);
-    k_elementwise(c, EWP_CONST_MUL, o->d, a->d, nullptr, &t, nl, 2, 0);
+    V o(a.size());
+    for (size_t i = 0; i < a.size(); i++) {
+        o[i] = new_ct(c, a[i]->level);
+        k_elementwise(c, EWP_CONST_MUL, o[i]->d, a[i]->d, nullptr, &t, nl, 2, 0);
+    }
     return o;
 }
 
-CtP evalmod(Ctx& c, const CtP& u) {
-    std::vector<CtP> T(CHEB_DEG + 1);
+V evalmod(Ctx& c, const V& u) {
+    std::vector<V> T(CHEB_DEG + 1);
     T[1] = u;
     for (int k = 2; k <= CHEB_DEG; k++) {
         int a = 1;
         while (a * 2 <= k) a *= 2;
         const int b = k - a;
-        CtP t;
+        V t;
         if (b == 0) {
-            t = ev_mult(c, *T[k / 2], *T[k / 2]);
+            t = mult(c, T[k / 2], T[k / 2]);
         } else {
-            const int lm = std::min(T[a]->level, T[b]->level);
-            t = ev_mult(c, *adj(c, T[a], lm), *adj(c, T[b], lm));
+            const int lm = std::min(T[a][0]->level, T[b][0]->level);
+            t = mult(c, adj(c, T[a], lm), adj(c, T[b], lm));
         }
-        t = ev_add(c, *t, *t, false);
-        T[k] = (b == 0) ? ev_add_const(c, *t, -1.0, 0.0, false) : ev_add(c, *t, *adj(c, T[a - b], t->level), true);
+        t = add(c, t, t);
+        T[k] = (b == 0) ? add_const(c, t, -1.0) : add(c, t, adj(c, T[a - b], t[0]->level), true);
     }
     int lmin = 1 << 30;
-    for (int k = 1; k <= CHEB_DEG; k++) lmin = std::min(lmin, T[k]->level);
-    CtP acc;
+    for (int k = 1; k <= CHEB_DEG; k++) lmin = std::min(lmin, T[k][0]->level);
+    V acc;
     for (int k = 1; k <= CHEB_DEG; k++) {
-        CtP term = ev_mul_const(c, *adj(c, T[k], lmin), CHEB[k], 0.0);
-        acc = acc ? ev_add(c, *acc, *term, false) : term;
+        V term = mul_const(c, adj(c, T[k], lmin), CHEB[k]);
+        acc = acc.empty() ? term : add(c, acc, term);
     }
-    acc = ev_add_const(c, *acc, CHEB[0], 0.0, false);
+    acc = add_const(c, acc, CHEB[0]);
     for (int i = 0; i < DOUBLINGS; i++) {
-        CtP t = ev_mult(c, *acc, *acc);
-        t = ev_add(c, *t, *t, false);
-        acc = ev_add_const(c, *t, -1.0, 0.0, false);
+        V t = mult(c, acc, acc);
+        t = add(c, t, t);
+        acc = add_const(c, t, -1.0);
     }
     return acc;
 }
@@ -325,20 +398,36 @@ CtP ev_mod_raise(Ctx& c, const Ct& a, int to) {
     return o;
 }
 
-CtP ev_bootstrap(Ctx& c, const CtP& a) {
+std::vector<CtP> ev_bootstrap_batch(Ctx& c, const std::vector<CtP>& in) {
+    if (in.empty()) return {};
     BootState& st = boot_state(c);
-    CtP x = ev_mod_raise(c, *adj(c, a, 0), c.L);
+    // one level per batch (the blocks of a lockstep op share their level history)
+    for (auto& x : in)
+        if (x->level != in[0]->level) {
+            std::vector<CtP> o;
+            for (auto& y : in) o.push_back(ev_bootstrap_batch(c, {y})[0]);
+            return o;
+        }
+    V a = adj(c, in, 0);
+    V x(a.size());
+    for (size_t i = 0; i < a.size(); i++) x[i] = ev_mod_raise(c, *a[i], c.L);
     for (auto& g : st.cts) x = linear(c, x, g);
-    x = ev_mul_const(c, *x, st.c_cts, 0.0);
-    CtP cj = ev_automorph(c, *x, 2 * (u64)c.N - 1);
-    CtP ure = ev_add(c, *x, *cj, false);
-    CtP uim = ev_mul_i(c, *ev_add(c, *cj, *x, true));
-    CtP sre = evalmod(c, ure);
-    CtP sim = evalmod(c, uim);
-    CtP y = ev_add(c, *mul_int(c, sre, INT_GAIN), *ev_mul_i(c, *mul_int(c, sim, INT_GAIN)), false);
+    x = mul_const(c, x, st.c_cts);
+    V cj = conj(c, x);
+    V ure = add(c, x, cj);
+    V uim = mul_i(c, add(c, cj, x, true));
+    // the real and imaginary parts through EvalMod together
+    V both = ure;
+    both.insert(both.end(), uim.begin(), uim.end());
+    V s = evalmod(c, both);
+    const size_t m = in.size();
+    V sre(s.begin(), s.begin() + m), sim(s.begin() + m, s.end());
+    V y = add(c, mul_int(c, sre, INT_GAIN), mul_i(c, mul_int(c, sim, INT_GAIN)));
     for (auto& g : st.stc) y = linear(c, y, g);
-    if (y->level != c.app_L) throw Error(-4, "bootstrap landed off the application's top level");
+    if (y[0]->level != c.app_L) throw Error(-4, "bootstrap landed off the application's top level");
     return y;
 }
+
+CtP ev_bootstrap(Ctx& c, const CtP& a) { return ev_bootstrap_batch(c, {a})[0]; }
 
 }  // namespace hc

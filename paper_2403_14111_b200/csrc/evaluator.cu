@@ -543,8 +543,15 @@ CtP Eval::refresh_planned(const CtP& a, int j, int r) { return do_refresh(c, a, 
 
 // refresh the given operands with their nonces, batched per level
 static void refresh_many(Ctx& c, std::vector<CtP*>& slots, const std::vector<u64>& nonces) {
-    if (c.boot_mode) {
-        for (size_t u = 0; u < slots.size(); u++) *slots[u] = do_refresh(c, *slots[u], nonces[u]);
+    if (c.boot_mode) {   // CKKS bootstrapping of all of them together (per level)
+        std::map<int, std::vector<size_t>> lv;
+        for (size_t u = 0; u < slots.size(); u++) lv[(*slots[u])->level].push_back(u);
+        for (auto& kv : lv) {
+            std::vector<CtP> in;
+            for (size_t u : kv.second) in.push_back(*slots[u]);
+            std::vector<CtP> out = ev_bootstrap_batch(c, in);
+            for (size_t t = 0; t < kv.second.size(); t++) *slots[kv.second[t]] = out[t];
+        }
         return;
     }
     std::map<int, std::vector<size_t>> by_level;

@@ -40,6 +40,12 @@ bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int
 // CKKS bootstrapping (bootstrap.cu): any level -> app_L
 CtP ev_mod_raise(Ctx& c, const Ct& a, int to);
 CtP ev_bootstrap(Ctx& c, const CtP& a);
+// several ciphertexts bootstrapped together: every step batched (same residues)
+std::vector<CtP> ev_bootstrap_batch(Ctx& c, const std::vector<CtP>& a);
+// batched primitives (evaluator.cu)
+std::vector<CtP> ev_level_adjust_batch(Ctx& c, const std::vector<const Ct*>& xs, int to);
+std::vector<CtP> ev_automorph_batch(Ctx& c, const std::vector<const Ct*>& a, u64 g, bool add_self);
+std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, const Ct*>>& ab);
 
 // out = sigma_g(a) + a in one key switch (rotate-and-add ladder step); false if not fusable
 bool ev_automorph_add(Ctx& c, const Ct& a, u64 g, CtP& out);

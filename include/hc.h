@@ -118,6 +118,12 @@ int hc_op_lrot(hc_ctx *ctx, const hc_ct *a, int64_t r, hc_ct **out);
 /* lrot(a, rs[k]) for k < n with one shared ModUp (hoisted; Rot per non-zero
  * r, r == 0 yields a handle to a itself); outs[n] */
 int hc_op_lrot_hoisted(hc_ctx *ctx, const hc_ct *a, const int64_t *rs, int n, hc_ct **outs);
+/* the doubling ladder of encoding.py:354-359 / 378-379 and approx.py:165-189,
+ *   for t < steps: a = add(a, lrot(a, stride * 2^t))      (stride < 0: rrot),
+ * steps Rot + steps Add on the ledger.  With the fused schedule forms on
+ * (hc_set_hoist) two steps run as one radix-4 rotate-and-sum stage
+ * a + lrot(a, s) + lrot(a, 2s) + lrot(a, 3s) with one ModUp and one ModDown. */
+int hc_op_ladder(hc_ctx *ctx, const hc_ct *a, int64_t stride, int steps, hc_ct **out);
 /* add(...add(mult(a0, b0), mult(a1, b1))...) over n pairs with one
  * relinearisation + rescale (n Mult, n-1 Add); the separate ops unless all
  * operands share one level >= 1 and n >= 2 */

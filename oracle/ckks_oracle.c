@@ -823,9 +823,9 @@ static void ks_modup(orc_ctx *c, const u64 *d, int level, u64 *up) {
     free(x); free(tl);
 }
 
-/* Key inner product of the ModUp digits `up` with `key`, then ModDown by P:
- * out [2][level+1][N] = (k0, k1). */
-static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *key, u64 *out) {
+/* Key inner product of the ModUp digits `up` with `key`, accumulated into
+ * acc [2][nt][N] (extended basis Q_l P, NTT form; the caller zeroes it). */
+static void ks_keyprod_acc(orc_ctx *c, const u64 *up, int level, swkey_t *key, u64 *acc) {
     int N = c->N, L = c->L, K = c->K, nall = c->nall, nl = level + 1;
     int nt = nl + K;
     int *tl = malloc(sizeof(int) * nt);
@@ -833,7 +833,6 @@ static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *ke
     for (int t = 0; t < K; t++) tl[nl + t] = L + 1 + t;
     int beta = (nl + c->alpha - 1) / c->alpha;
     size_t poly = (size_t)nt * N;
-    u64 *acc = calloc(2 * poly, sizeof(u64));
     for (int j = 0; j < beta; j++) {
         const u64 *upj = up + (size_t)j * poly;
         /* inner product with digit j of the key */
@@ -849,9 +848,16 @@ static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *ke
             }
         }
     }
-    /* ModDown by P */
+    free(tl);
+}
+
+/* ModDown by P of acc [2][nt][N] (NTT form): out [2][level+1][N]. */
+static void ks_moddown(orc_ctx *c, const u64 *acc, int level, u64 *out) {
+    int N = c->N, L = c->L, K = c->K, nl = level + 1;
+    int nt = nl + K;
+    size_t poly = (size_t)nt * N;
     for (int s = 0; s < 2; s++) {
-        u64 *A = acc + (size_t)s * poly;
+        const u64 *A = acc + (size_t)s * poly;
         u64 *y = malloc(sizeof(u64) * (size_t)K * N);
         for (int t = 0; t < K; t++) {
             const prime_t *p = &c->pr[L + 1 + t];
@@ -892,7 +898,16 @@ static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *ke
         }
         free(y);
     }
-    free(acc); free(tl);
+}
+
+/* Key inner product of the ModUp digits `up` with `key`, then ModDown by P:
+ * out [2][level+1][N] = (k0, k1). */
+static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *key, u64 *out) {
+    size_t poly = (size_t)(level + 1 + c->K) * c->N;
+    u64 *acc = calloc(2 * poly, sizeof(u64));
+    ks_keyprod_acc(c, up, level, key, acc);
+    ks_moddown(c, acc, level, out);
+    free(acc);
 }
 
 static size_t modup_words(const orc_ctx *c, int level) {
@@ -1006,6 +1021,50 @@ void orc_rotate_hoisted(orc_ctx *c, const u64 *a, int level, const u64 *gs, int 
         }
     }
     free(up); free(ups); free(c0); free(ks);
+}
+
+/* Rotate-and-sum stage (radix ladders): out = a + sum_r
+ * sigma_{g_r}(a) with one ModUp of c1 (digits permuted per Galois element, as
+ * in orc_rotate_hoisted), the key inner products of all ng rotations summed
+ * in the extended basis Q_l P and one ModDown:
+ *   out0 = c0 + sum_r sigma_r(c0) + ModDown(sum_r <sigma_r(up), key_r>)_0
+ *   out1 = c1 +                     ModDown(sum_r <sigma_r(up), key_r>)_1 */
+void orc_rotsum(orc_ctx *c, const u64 *a, int level, const u64 *gs, int ng, u64 *out) {
+    int N = c->N, nl = level + 1, nt = nl + c->K;
+    int beta = (nl + c->alpha - 1) / c->alpha;
+    size_t poly = (size_t)nl * N, mw = modup_words(c, level);
+    u64 *up = malloc(sizeof(u64) * mw);
+    ks_modup(c, a + poly, level, up);
+    u64 *ups = malloc(sizeof(u64) * mw);
+    u64 *c0 = malloc(sizeof(u64) * poly);
+    u64 *acc = calloc(2 * (size_t)nt * N, sizeof(u64));
+    u64 *s0 = malloc(sizeof(u64) * poly);
+    memcpy(s0, a, sizeof(u64) * poly);
+    for (int r = 0; r < ng; r++) {
+        swkey_t *key = get_key(c, (int)gs[r]);
+        for (int j = 0; j < beta; j++)
+            automorph_ntt(c, up + (size_t)j * nt * N, gs[r], nt, ups + (size_t)j * nt * N);
+        ks_keyprod_acc(c, ups, level, key, acc);
+        automorph_ntt(c, a, gs[r], nl, c0);
+        for (int i = 0; i < nl; i++) {
+            u64 q = c->pr[i].q;
+            for (int k = 0; k < N; k++) {
+                size_t e = (size_t)i * N + k;
+                s0[e] = addmod(s0[e], c0[e], q);
+            }
+        }
+    }
+    u64 *ks = malloc(sizeof(u64) * 2 * poly);
+    ks_moddown(c, acc, level, ks);
+    for (int i = 0; i < nl; i++) {
+        u64 q = c->pr[i].q;
+        for (int k = 0; k < N; k++) {
+            size_t e = (size_t)i * N + k;
+            out[e] = addmod(s0[e], ks[e], q);
+            out[poly + e] = addmod(a[poly + e], ks[poly + e], q);
+        }
+    }
+    free(up); free(ups); free(c0); free(acc); free(s0); free(ks);
 }
 
 /* Sum of n ct x ct products with one relinearisation and one rescale:

@@ -98,6 +98,7 @@ def lib():
         L.orc_mult.argtypes = [P, u64p, u64p, I, u64p]
         L.orc_rotate_hoisted.argtypes = [P, u64p, I, u64p, I, u64p]
         L.orc_mult_sum.argtypes = [P, u64p, u64p, I, I, u64p]
+        L.orc_rotsum.argtypes = [P, u64p, I, u64p, I, u64p]
         L.orc_key.argtypes = [P, I, u64p]
         L.orc_ntt_limb.argtypes = [P, I, u64p, I]
         L.orc_mulmod.restype = U
@@ -231,6 +232,11 @@ class RnsParams:
         o = np.zeros((len(gs),) + self.ct_shape(level), np.uint64)
         lib().orc_rotate_hoisted(self.h, a, level, np.asarray(gs, np.uint64), len(gs), o)
         return list(o)
+
+    def rotsum(self, a, level, gs):
+        o = self._out(level)
+        lib().orc_rotsum(self.h, a, level, np.asarray(gs, np.uint64), len(gs), o)
+        return o
 
     def mult_sum(self, As, Bs, level):
         o = self._out(level - 1)
@@ -476,6 +482,21 @@ class OracleCKKSContext:
             data = self.p.rotate_hoisted(vx.data, vx.level, [self.p.galois(r) for r in moving])
             outs = {r: RnsBlock(self, d, vx.level) for r, d in zip(moving, data)}
         return [outs[r] if r else x for r in rr]
+
+    def rotsum(self, x, rs, steps):
+        """x + sum_r lrot(x, r) as one rotate-and-sum stage (DESIGN.md §3,
+        radix ladders): one ModUp, the rotations' key products summed in the
+        extended basis, one ModDown.  It stands for `steps` doubling steps
+        add(x, lrot(x, .)) of the reference's ladder, whose `steps` Rot and
+        `steps` Add the ledger records."""
+        kx, vx = self._kind(x)
+        rr = [int(r) % self.slot_count for r in rs]
+        if kx != "ct" or not all(rr):
+            raise TypeError("rotsum expects a ciphertext and non-zero rotations")
+        self.ledger.record("Rot", steps)
+        self.ledger.record("Add", steps)
+        self.extra["KeySwitch"] += 1
+        return RnsBlock(self, self.p.rotsum(vx.data, vx.level, [self.p.galois(r) for r in rr]), vx.level)
 
     def mult_sum(self, xs, ys):
         """add(...add(mult(x0, y0), mult(x1, y1))...) with one relinearisation

@@ -440,17 +440,40 @@ def prot_up(E, k):                                                  # encoding.p
     return E.each(fix)
 
 
+LADDER_RADIX_LOG = 2    # doubling steps merged into one rotate-and-sum stage (radix 4)
+
+
+def ladder(ctx, acc, stride, steps):
+    """The reference's doubling ladder ``for t < steps: acc = add(acc,
+    lrot(acc, stride * 2^t))`` (stride < 0: rrot) -- encoding.py:354-359,
+    378-379, approx.py:165-189.  On a context with the fused schedule forms
+     two steps become one radix-4 rotate-and-sum stage
+    ``acc + lrot(acc, s) + lrot(acc, 2s) + lrot(acc, 3s)``, s = stride * 4^i:
+    the same slot values and ledger, half the ModUp / ModDown passes."""
+    if getattr(ctx, "hoist", False) and hasattr(ctx, "ladder") and ctx._kind(acc)[0] == "ct":
+        return ctx.ladder(acc, stride, steps)       # the CUDA product's own ladder (same stages)
+    if getattr(ctx, "hoist", False) and hasattr(ctx, "rotsum") and ctx._kind(acc)[0] == "ct":
+        t = 0
+        while t < steps:
+            w = min(LADDER_RADIX_LOG, steps - t)
+            base = stride * (1 << t)
+            acc = ctx.rotsum(acc, [base * u for u in range(1, 1 << w)], w)
+            t += w
+        return acc
+    for t in range(steps):
+        acc = ctx.add(acc, ctx.lrot(acc, stride * (1 << t)))
+    return acc
+
+
 def col_ladder(ctx, acc):
     """encoding.py:354-359 — lrot ladder, column-0 mask, rrot ladder."""
     s1 = ctx.grid_cols
     c0 = np.zeros((ctx.grid_rows, s1))
     c0[:, 0] = 1.0
     c0b = ctx.pack(c0.ravel())
-    for t in range(lg(s1)):
-        acc = ctx.add(acc, ctx.lrot(acc, 1 << t))
+    acc = ladder(ctx, acc, 1, lg(s1))
     acc = ctx.cmult(acc, c0b)
-    for t in range(lg(s1)):
-        acc = ctx.add(acc, ctx.rrot(acc, 1 << t))
+    acc = ladder(ctx, acc, -1, lg(s1))
     return acc
 
 
@@ -477,9 +500,7 @@ def row_presum(E, q):
 
 def row_ladder(ctx, acc):
     """encoding.py:378-379 — log2(s0) row-rotation doubling ladder."""
-    for t in range(lg(ctx.grid_rows)):
-        acc = ctx.add(acc, ctx.lrot(acc, (1 << t) * ctx.grid_cols))
-    return acc
+    return ladder(ctx, acc, ctx.grid_cols, lg(ctx.grid_rows))
 
 
 def row_sums(E, presum=row_presum):                                 # encoding.py:363-381
@@ -598,16 +619,14 @@ def col_major_abt(A, B, scale=1.0):                                 # matmul.py:
         rowj = np.zeros((s0, s1))
         rowj[j, :] = 1.0
         picked = B.mul(pattern(ctx, rowj, B.grid))
-        for t in range(lg(s0)):
-            picked = picked.add(picked.lrot((1 << t) * s1))
+        picked = picked.each(lambda b: ladder(ctx, b, s1, lg(s0)))
         prod = _rowwise(A, picked)
         folded = []
         for p in range(m):
             blk = prod.blocks[p][0]
             for q in range(1, n):
                 blk = ctx.add(blk, prod.blocks[p][q])
-            for t in range(lg(s1)):
-                blk = ctx.add(blk, ctx.lrot(blk, 1 << t))
+            blk = ladder(ctx, blk, 1, lg(s1))
             blk = ctx.cmult(blk, c0b)
             blk = ctx.rrot(blk, j)
             folded.append((blk,))
@@ -633,8 +652,7 @@ def row_major_atb(A, B, scale=1.0):                                 # matmul.py:
     for j in range(c):
         picked = A.lrot(j)
         picked = picked.each(lambda b: ctx.cmult(b, c0b))
-        for t in range(lg(s1)):
-            picked = picked.add(picked.rrot(1 << t))
+        picked = picked.each(lambda b: ladder(ctx, b, -1, lg(s1)))
         sums = row_sums(_colwise(picked, B))
         rowj = np.zeros((s0, s1))
         rowj[j, :] = scale
@@ -757,9 +775,7 @@ class _Layout:
 
     def bcast0(self, x):
         if self.enc:
-            for t in range(lg(self.ctx.grid_cols)):
-                x = x.add(x.rrot(1 << t))
-            return x
+            return x.each(lambda b: ladder(self.ctx, b, -1, lg(self.ctx.grid_cols)))
         return np.repeat(x[:, :1], self.period, axis=1)
 
     def rowsum(self, x):
@@ -773,9 +789,7 @@ class _Layout:
     def retile(self, x):
         if not self.enc:
             return x
-        for t in range(lg(self.ctx.grid_cols // self.period)):
-            x = x.add(x.rrot(self.period * (1 << t)))
-        return x
+        return x.each(lambda b: ladder(self.ctx, b, -self.period, lg(self.ctx.grid_cols // self.period)))
 
 
 def _odd7(x, a):                                                    # approx.py:195-202

@@ -69,6 +69,7 @@ SIGNATURES = {
     "hc_op_mult_plain": (I, [P, P, DP, DP, C.c_char_p, PP]),
     "hc_op_lrot": (I, [P, P, I64, PP]),
     "hc_op_lrot_hoisted": (I, [P, P, C.POINTER(C.c_int64), I, PP]),
+    "hc_op_ladder": (I, [P, P, C.c_int64, I, PP]),
     "hc_op_mult_sum": (I, [P, PP, PP, I, PP]),
     "hc_op_conj": (I, [P, P, PP]),
     "hc_op_mul_i": (I, [P, P, PP]),

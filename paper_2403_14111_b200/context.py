@@ -496,6 +496,18 @@ class CKKSContext:
                 res.append(Ciphertext(self, C.c_void_p(h)))
         return res
 
+    def ladder(self, x, stride: int, steps: int):
+        """The reference's doubling ladder ``for t < steps: x = add(x, lrot(x,
+        stride * 2^t))`` (encoding.py:354-359, 378-379; stride < 0: rrot):
+        steps Rot + steps Add on the ledger.  With ``hoist`` on, two steps run
+        as one radix-4 rotate-and-sum stage (one ModUp, one ModDown)."""
+        kx, vx = self._kind(x)
+        if kx != "ct":
+            for t in range(int(steps)):
+                x = self.add(x, self.lrot(x, int(stride) * (1 << t)))
+            return x
+        return self._new(N.lib().hc_op_ladder, vx._h, int(stride), int(steps))
+
     def mult_sum(self, xs, ys):
         """add(...add(mult(x0, y0), mult(x1, y1))...) with one relinearisation
         and rescale (n Mult + n - 1 Add on the ledger) when every operand is a

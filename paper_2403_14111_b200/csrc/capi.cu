@@ -331,6 +331,13 @@ int hc_op_lrot_hoisted(hc_ctx* ctx, const hc_ct* a, const int64_t* rs, int n, hc
     });
 }
 
+int hc_op_ladder(hc_ctx* ctx, const hc_ct* a, int64_t stride, int steps, hc_ct** out) {
+    return guard([&] {
+        if (steps < 0 || steps > 30) throw hc::Error(HC_EPARAM, "ladder: bad step count");
+        *out = wrap(hc::Eval(*ctx->c, ctx->auto_boot).ladder(a->p, stride, steps));
+    });
+}
+
 int hc_op_mult_sum(hc_ctx* ctx, const hc_ct* const* a, const hc_ct* const* b, int n, hc_ct** out) {
     return guard([&] {
         if (n < 1) throw hc::Error(HC_EPARAM, "empty product sum");

@@ -239,12 +239,9 @@ static u64* ks_modup(Ctx& c, const u64* d, int level) {
     return UP;
 }
 
-// key product of the ModUp digits UP with `key`, ModDown, + addend
-static void ks_tail(Ctx& c, const u64* UP, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+// ModDown of the key products ACC [2][nt][N] (its P limbs are overwritten), + addend
+static void ks_tail_acc(Ctx& c, u64* ACC, int level, u64* out, const u64* addend, int add_npoly) {
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
-    const int beta = (nl + c.alpha - 1) / c.alpha;
-    u64* ACC = c.alloc((size_t)2 * nt * N);
-    k_keyprod(c, ACC, UP, key.d, level, beta);
     {
         JobList j;
         j.n = 0;
@@ -263,8 +260,17 @@ static void ks_tail(Ctx& c, const u64* UP, int level, const Key& key, u64* out, 
     ntt_limbs(c, W + (size_t)nl * N, 0, nl, false);
     k_moddown_combine(c, out, ACC, W, addend, add_npoly, level);
     c.free(W);
-    c.free(ACC);
     c.counts[OP_KS]++;
+}
+
+// key product of the ModUp digits UP with `key`, ModDown, + addend
+static void ks_tail(Ctx& c, const u64* UP, int level, const Key& key, u64* out, const u64* addend, int add_npoly) {
+    const int nl = level + 1, nt = nl + c.K;
+    const int beta = (nl + c.alpha - 1) / c.alpha;
+    u64* ACC = c.alloc((size_t)2 * nt * c.N);
+    k_keyprod(c, ACC, UP, key.d, level, beta);
+    ks_tail_acc(c, ACC, level, out, addend, add_npoly);
+    c.free(ACC);
 }
 
 // d: [level+1][N] (NTT).  out [2][level+1][N] = KS(d) + addend (first add_npoly polys)
@@ -409,6 +415,53 @@ std::vector<std::vector<CtP>> ev_rot_hoisted(Ctx& c, const std::vector<const Ct*
             ks_tail(c, UPg, level, *keys[r], out[i][r]->d, S0, 1);
         }
         c.free(S0);
+        c.free(UPg);
+        c.free(UP);
+    }
+    return out;
+}
+
+// Rotate-and-sum stage (radix ladders): out_i = x_i + sum_r
+// sigma_{g_r}(x_i); one ModUp of c1(i), the rotations' key products summed in
+// the extended basis, one ModDown.  All inputs at one level.
+std::vector<CtP> ev_rotsum_batch(Ctx& c, const std::vector<const Ct*>& xs, const std::vector<u64>& gals) {
+    const size_t nx = xs.size(), ng = gals.size();
+    std::vector<CtP> out(nx);
+    if (nx == 0) return out;
+    const int level = xs[0]->level;
+    for (auto* x : xs)
+        if (x->level != level) throw Error(-4, "rotate-and-sum: inputs at different levels");
+    std::vector<const u64*> keys(ng);
+    for (size_t r = 0; r < ng; r++) keys[r] = get_key(c, (int)gals[r]).d;
+    for (size_t i = 0; i < nx; i++) out[i] = new_ct(c, level);
+    if (c.logN >= 14) {
+        std::vector<const u64*> in(nx);
+        std::vector<u64*> o(nx);
+        for (size_t i = 0; i < nx; i++) { in[i] = xs[i]->d; o[i] = out[i]->d; }
+        if (!keyswitch_rotsum(c, (int)nx, in.data(), o.data(), level, (int)ng, gals.data(), keys.data()))
+            throw Error(-2, "rotate-and-sum stage");
+        c.counts[OP_KS] += (int64_t)nx;
+        return out;
+    }
+    // small rings: the unfused pipeline, digits permuted by an explicit automorphism
+    const int nl = level + 1, nt = nl + c.K, beta = (nl + c.alpha - 1) / c.alpha;
+    for (size_t i = 0; i < nx; i++) {
+        u64* UP = ks_modup(c, xs[i]->poly(1), level);
+        u64* UPg = c.alloc((size_t)beta * nt * c.N);
+        u64* ACC = c.alloc((size_t)2 * nt * c.N);
+        u64* S = c.alloc((size_t)2 * nl * c.N);    // addend: x + (sum_r sigma_r(c0), 0)
+        u64* T = c.alloc((size_t)nl * c.N);
+        HC_CUDA(cudaMemcpyAsync(S, xs[i]->d, sizeof(u64) * 2 * nl * c.N, cudaMemcpyDeviceToDevice, c.stream));
+        for (size_t r = 0; r < ng; r++) {
+            k_automorph(c, UPg, UP, beta * nt, gals[r]);
+            k_keyprod(c, ACC, UPg, keys[r], level, beta, r > 0);
+            k_automorph(c, T, xs[i]->poly(0), nl, gals[r]);
+            k_elementwise(c, EWP_ADD, S, S, T, nullptr, nl, 1, 1);
+        }
+        ks_tail_acc(c, ACC, level, out[i]->d, S, 2);
+        c.free(T);
+        c.free(S);
+        c.free(ACC);
         c.free(UPg);
         c.free(UP);
     }
@@ -683,6 +736,55 @@ std::vector<CtP> Eval::lrot_batch(const std::vector<CtP>& xs, int64_t r, bool ad
     std::vector<const Ct*> a(xs.size());
     for (size_t i = 0; i < xs.size(); i++) a[i] = xs[i].get();
     return ev_automorph_batch(c, a, galois_rot(c, r), add_self);
+}
+
+constexpr int LADDER_RADIX_LOG = 2;   // doubling steps per rotate-and-sum stage (radix 4; oracle/slots.py ladder)
+
+std::vector<CtP> Eval::ladder(const std::vector<CtP>& xs_in, int64_t stride, int steps) {
+    std::vector<CtP> xs = xs_in;
+    if (!c.hoist) {
+        for (int t = 0; t < steps; t++) xs = lrot_batch(xs, stride * ((int64_t)1 << t), true);
+        return xs;
+    }
+    const int64_t S = c.N / 2;
+    for (int t = 0; t < steps;) {
+        const int w = std::min(LADDER_RADIX_LOG, steps - t);
+        const int64_t base = stride * ((int64_t)1 << t);
+        t += w;
+        std::vector<u64> gals;
+        bool zero = false;
+        for (int u = 1; u < (1 << w); u++) {
+            const int64_t r = (((base * u) % S) + S) % S;
+            zero |= r == 0;
+            gals.push_back(galois_rot(c, r));
+        }
+        if (zero) throw Error(-4, "ladder: rotation by a multiple of the slot count");
+        // the ledger and the §8(d) model record the w doubling steps this stage stands for
+        rec(OP_ROT, w * (int)xs.size());
+        rec(OP_ADD, w * (int)xs.size());
+        for (auto& x : xs) {
+            model(OP_ROT, MV_CT, x->level, w);
+            model(OP_ADD, MV_CT, x->level, w);
+        }
+        // one stage per level present
+        std::vector<CtP> out(xs.size());
+        std::vector<char> done(xs.size(), 0);
+        for (size_t i = 0; i < xs.size(); i++) {
+            if (done[i]) continue;
+            std::vector<size_t> idx;
+            std::vector<const Ct*> a;
+            for (size_t j = i; j < xs.size(); j++)
+                if (!done[j] && xs[j]->level == xs[i]->level) {
+                    idx.push_back(j);
+                    a.push_back(xs[j].get());
+                    done[j] = 1;
+                }
+            std::vector<CtP> r = ev_rotsum_batch(c, a, gals);
+            for (size_t k = 0; k < idx.size(); k++) out[idx[k]] = r[k];
+        }
+        xs = out;
+    }
+    return xs;
 }
 
 std::vector<CtP> Eval::conj_batch(const std::vector<CtP>& xs) {

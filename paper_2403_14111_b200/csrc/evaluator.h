@@ -37,6 +37,11 @@ struct KsHoist {
     u64* out;
 };
 bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int level, int B, const KsHoist* e);
+// rotate-and-sum stage (keyswitch.cu, DESIGN.md §3 radix ladders): out_b = x_b +
+// sum_r sigma_{gals[r]}(x_b), one ModUp and one ModDown per input; nrot <= 3
+bool keyswitch_rotsum(Ctx& c, int B, const u64* const* xs, u64* const* outs, int level, int nrot, const u64* gals,
+                      const u64* const* keys);
+std::vector<CtP> ev_rotsum_batch(Ctx& c, const std::vector<const Ct*>& xs, const std::vector<u64>& gals);
 // CKKS bootstrapping (bootstrap.cu): any level -> app_L
 CtP ev_mod_raise(Ctx& c, const Ct& a, int to);
 CtP ev_bootstrap(Ctx& c, const CtP& a);
@@ -128,6 +133,14 @@ struct Eval {
     // key-switch pipeline per level): lrot (add_self: add(a, lrot(a, r))),
     // conj and ct x ct over vectors of independent operands
     std::vector<CtP> lrot_batch(const std::vector<CtP>& xs, int64_t r, bool add_self = false);
+    // the reference's doubling ladder over independent operands,
+    //   for t < steps: x = add(x, lrot(x, stride * 2^t))      (stride < 0: rrot)
+    // (encoding.py:354-359, 378-379, approx.py:165-189).  With the fused
+    // schedule forms (Ctx::hoist) two steps run as one radix-4
+    // rotate-and-sum stage x + lrot(x, s) + lrot(x, 2s) + lrot(x, 3s): same
+    // slot values and ledger (steps Rot + steps Add), half the ModUp / ModDown
+    std::vector<CtP> ladder(const std::vector<CtP>& xs, int64_t stride, int steps);
+    CtP ladder(const CtP& x, int64_t stride, int steps) { return ladder(std::vector<CtP>{x}, stride, steps)[0]; }
     std::vector<CtP> conj_batch(const std::vector<CtP>& xs);
     std::vector<CtP> mult_batch(const std::vector<CtP>& xs, const std::vector<CtP>& ys);
     // fused forms (residues differ from the separate ops, the

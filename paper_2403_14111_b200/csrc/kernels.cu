@@ -302,7 +302,7 @@ void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta) {
 
 __global__ void keyprod_kernel(u64* __restrict__ acc, const u64* __restrict__ up, const u64* __restrict__ key,
                                const PrimeDev* __restrict__ primes, int level, int L, int K, int beta, int nall,
-                               int N) {
+                               int N, int accumulate) {
     pdl_enter();
     const int nt = level + 1 + K;
     const size_t poly = (size_t)nt * N;
@@ -319,17 +319,22 @@ __global__ void keyprod_kernel(u64* __restrict__ acc, const u64* __restrict__ up
             mac128(s0, u, *kb);
             mac128(s1, u, *ka);
         }
-        acc[e] = reduce128(s0.hi, s0.lo, P);
-        acc[poly + e] = reduce128(s1.hi, s1.lo, P);
+        u64 r0 = reduce128(s0.hi, s0.lo, P), r1 = reduce128(s1.hi, s1.lo, P);
+        if (accumulate) {
+            r0 = add_mod(r0, acc[e], P.q);
+            r1 = add_mod(r1, acc[poly + e], P.q);
+        }
+        acc[e] = r0;
+        acc[poly + e] = r1;
     }
 }
 
-void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta) {
+void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta, bool accumulate) {
     const size_t poly = (size_t)(level + 1 + c.K) * c.N;
     const double nt = level + 1 + c.K;
     Launch scope(c, "keyprod", 8.0 * c.N * (3.0 * beta * nt + 2.0 * nt));
     launch_k(c, keyprod_kernel, nblocks(poly, 256), 256, 0, acc, up, key, c.d_primes, level, c.L, c.K, beta,
-                                                              c.nall, c.N);
+                                                              c.nall, c.N, accumulate ? 1 : 0);
     HC_CUDA(cudaGetLastError());
 }
 

@@ -25,7 +25,8 @@ void k_mod_raise(Ctx& c, u64* out, const u64* X, int nl);
 // out [2][nl][N] = sum_t a_t (x) p_t (ciphertexts times NTT plaintexts, no rescale), T <= 16
 void k_pt_dot(Ctx& c, u64* out, const u64* const* a, const u64* const* p, int T, int nl);
 void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta);
-void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta);
+// accumulate: acc += the products (rotate-and-sum stages)
+void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta, bool accumulate = false);
 void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level);
 void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly, int level);
 void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly);

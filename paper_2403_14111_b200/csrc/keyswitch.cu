@@ -284,6 +284,167 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : (MB > 4 ? 2 : 3)) ks_k
     else kp_run<E, false, MB>(g, P, t, pi, dig, k, gal, kb, acc);
 }
 
+// ---- B (rotate-and-sum form): key products of several rotations of one input,
+// summed in the extended basis -------------------------------------------------
+// out = x + sum_r sigma_r(x) (radix ladders): entry b's digits
+// UP_b are read through each Galois element g_r and multiplied with key_r;
+// the 2 * R * beta products of a coefficient accumulate in registers, and
+// [P]_q * sigma_r(c0) joins poly 0's Q limbs, so the single ModDown that
+// follows (exact division by P) returns sum_r sigma_r(c0) + the key-switched
+// part; x itself is the ModDown store's second addend.  A thread owns one
+// coefficient pair of target limb t for up to RS_NBT entries: the key words
+// of rotation r are loaded once and reused by the entries.  Aligned index
+// pairs map to aligned pairs under every Galois element (src(k + 1) =
+// src(k) ^ 1), so each gather is one 16-byte load.
+constexpr int RS_MAXR = 3;   // rotations per stage (radix 4); bounds the 128-bit sums: 3 * (4 + 1) terms below 2^124
+constexpr int RS_NBT = 4;    // entries per thread
+struct KsRotsum {
+    int nb, nrot;
+    const u64* c0[KS_MAXB];    // x_b poly 0 [nl][N]
+    const u64* c1[KS_MAXB];    // x_b poly 1 [nl][N]
+    const u64* up[KS_MAXB];    // ModUp digits of c1_b [beta][nt][N]
+    u64 gal[RS_MAXR];
+    const u64* key[RS_MAXR];   // [dnum][2][nall][N]
+};
+
+__device__ __forceinline__ void rs_gather2(const u64* __restrict__ base, unsigned src, u64* v) {
+    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(base + (src & ~1u));
+    const bool sw = src & 1u;
+    v[0] = sw ? w.y : w.x;
+    v[1] = sw ? w.x : w.y;
+}
+
+template <bool FP, int MB, int NBT>
+__device__ __forceinline__ void rs_run(const KsGeo& g, const PrimeDev& P, int t, int pi, int dig, unsigned k, int b0,
+                                       int nb, const KsRotsum& rb, u64 pq, u64* __restrict__ acc) {
+    using KW = typename std::conditional<FP, double, u64>::type;
+    const size_t N = (size_t)1 << g.logN;
+    const size_t kstride = (size_t)g.nall * N;
+    double fb[NBT][2], fa[NBT][2];
+    U128 ib[NBT][2], ia[NBT][2];
+#pragma unroll
+    for (int i = 0; i < NBT; i++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            if constexpr (FP) { fb[i][e] = 0; fa[i][e] = 0; }
+            else { ib[i][e] = U128{0, 0}; ia[i][e] = U128{0, 0}; }
+        }
+    const bool qlimb = t < g.nl;
+    const double pqd = FP ? fp_word(pq) : 0.0;
+    // 128-bit sums hold 15 products of a lazy digit (< 16q) and a key word
+    // (q < 2^60); deeper sums (8 digits) are folded after each rotation
+    const bool fold = !FP && (g.beta + 1) * rb.nrot > 15;
+    for (int r = 0; r < rb.nrot; r++) {
+        const unsigned src = galois_src(k, g.logN, rb.gal[r]);
+        KW kbv[MB][2], kav[MB][2];
+#pragma unroll
+        for (int j = 0; j < MB; j++) {
+            if (j >= g.beta) break;
+            const u64* kp = rb.key[r] + ((size_t)(2 * j) * g.nall + pi) * N + k;
+            const ulonglong2 wb = *reinterpret_cast<const ulonglong2*>(kp);
+            const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(kp + kstride);
+            if constexpr (FP) {
+                kbv[j][0] = fp_word(wb.x); kbv[j][1] = fp_word(wb.y);
+                kav[j][0] = fp_word(wa.x); kav[j][1] = fp_word(wa.y);
+            } else {
+                kbv[j][0] = wb.x; kbv[j][1] = wb.y;
+                kav[j][0] = wa.x; kav[j][1] = wa.y;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NBT; i++) {
+            if (i >= nb) break;
+            const int b = b0 + i;
+            u64 x[MB][2], z[2];
+#pragma unroll
+            for (int j = 0; j < MB; j++) {
+                if (j >= g.beta) break;
+                const u64* bp = (j == dig) ? rb.c1[b] + (size_t)t * N : rb.up[b] + ((size_t)j * g.nt + t) * N;
+                rs_gather2(bp, src, x[j]);
+            }
+            if (qlimb) rs_gather2(rb.c0[b] + (size_t)t * N, src, z);
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                if constexpr (FP) {
+                    double sb = fb[i][e], sa = fa[i][e];
+#pragma unroll
+                    for (int j = 0; j < MB; j++) {
+                        if (j >= g.beta) break;
+                        const double y = fp_word(x[j][e]);
+                        sb = __dadd_rn(sb, fp_mulmod(y, kbv[j][e], P.qd, P.qinv));
+                        sa = __dadd_rn(sa, fp_mulmod(y, kav[j][e], P.qd, P.qinv));
+                    }
+                    if (qlimb) sb = __dadd_rn(sb, fp_mulmod(fp_word(z[e]), pqd, P.qd, P.qinv));
+                    fb[i][e] = sb;
+                    fa[i][e] = sa;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < MB; j++) {
+                        if (j >= g.beta) break;
+                        mac128(ib[i][e], x[j][e], kbv[j][e]);
+                        mac128(ia[i][e], x[j][e], kav[j][e]);
+                    }
+                    if (qlimb) mac128(ib[i][e], z[e], pq);
+                    if (fold && r + 1 < rb.nrot) {
+                        ib[i][e] = U128{reduce128(ib[i][e].hi, ib[i][e].lo, P), 0};
+                        ia[i][e] = U128{reduce128(ia[i][e].hi, ia[i][e].lo, P), 0};
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NBT; i++) {
+        if (i >= nb) break;
+        u64 ob[2], oa[2];
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            if constexpr (FP) {
+                ob[e] = fp_canon(fb[i][e], P.qd, P.qinv);
+                oa[e] = fp_canon(fa[i][e], P.qd, P.qinv);
+            } else {
+                ob[e] = reduce128(ib[i][e].hi, ib[i][e].lo, P);
+                oa[e] = reduce128(ia[i][e].hi, ia[i][e].lo, P);
+            }
+        }
+        u64* ab = acc + (size_t)(b0 + i) * g.acc_stride();
+        *reinterpret_cast<ulonglong2*>(ab + (size_t)t * N + k) = make_ulonglong2(ob[0], ob[1]);
+        *reinterpret_cast<ulonglong2*>(ab + ((size_t)g.nt + t) * N + k) = make_ulonglong2(oa[0], oa[1]);
+    }
+}
+
+#ifndef RS_MINB
+#define RS_MINB 2
+#endif
+// grid x = (coefficient block, entry group) with the group fastest, so the
+// groups sharing a block's key words run together (second read from L2)
+template <int MB = 4>
+__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum(KsGeo g, const PrimeDev* __restrict__ primes,
+                                                                  KsRotsum rb, const u64* __restrict__ pmodq,
+                                                                  u64* __restrict__ acc, int ngroups) {
+    pdl_enter();
+    const size_t N = (size_t)1 << g.logN;
+    const int t = blockIdx.y;
+    const int pi = g.prime(t);
+    const PrimeDev P = primes[pi];
+    const int grp = blockIdx.x % ngroups;
+    const unsigned k = 2u * ((blockIdx.x / ngroups) * blockDim.x + threadIdx.x);
+    if (k >= N) return;
+    const int b0 = grp * RS_NBT;
+    const int nb = min(RS_NBT, rb.nb - b0);
+    const int dig = t < g.nl ? t / g.alpha : -1;
+    const u64 pq = t < g.nl ? pmodq[pi] : 0;
+    // entries per pass over the rotations, by register budget: the integer
+    // path's 128-bit sums (and 8-digit key words) take fewer at a time; the
+    // later passes re-read the key words from L1 / L2
+    constexpr int NF = MB > 4 ? 2 : 4, NI = MB > 4 ? 1 : 2;
+    if (P.fp) {
+        for (int o = 0; o < nb; o += NF) rs_run<true, MB, NF>(g, P, t, pi, dig, k, b0 + o, min(NF, nb - o), rb, pq, acc);
+    } else {
+        for (int o = 0; o < nb; o += NI) rs_run<false, MB, NI>(g, P, t, pi, dig, k, b0 + o, min(NI, nb - o), rb, pq, acc);
+    }
+}
+
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
 // (the P -> Q conversion has the ModUp loader's shape: K inputs, one target)
@@ -569,9 +730,18 @@ struct KsTail {
 
 // The fused pipeline: ModUp stage over `nin` inputs din[] (read through gal),
 // then key product + ModDown over `B` tail entries.
+// Rotate-and-sum stage (ks_keyprod_rotsum): tail entry b sums the rotations
+// gal[0..nrot) of input b (c0[b], its c1 = din[b]) with keys key[].
+struct KsRotsumSpec {
+    int nrot;
+    u64 gal[RS_MAXR];
+    const u64* key[RS_MAXR];
+    const u64* const* c0;
+};
+
 template <int LOGN>
 static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int level, int B, const KsTail* in,
-                          int add_npoly) {
+                          int add_npoly, const KsRotsumSpec* rsum = nullptr) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
@@ -672,8 +842,28 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         int nkeys = 1;
         for (int b = 1; b < B; b++) nkeys += in[b].key != in[b - 1].key;
         // algorithmic: the digit limbs (once per input) and ACC per key switch, each distinct key run once
-        Launch scope(c, "ks_keyprod_stream",
-                     8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt));
+        if (rsum) nkeys = rsum->nrot;
+        Launch scope(c, rsum ? "ks_keyprod_rotsum" : "ks_keyprod_stream",
+                     8.0 * N * ((double)nin * g.beta * nt + 2.0 * B * nt + 2.0 * nkeys * g.beta * nt +
+                                (rsum ? (double)B * nl : 0.0)));
+        if (rsum) {
+            // rotate-and-sum: digits (once per input, re-read per rotation from L2),
+            // c0, ACC and every rotation's key
+            KsRotsum rb;
+            rb.nb = B;
+            rb.nrot = rsum->nrot;
+            for (int r = 0; r < rsum->nrot; r++) { rb.gal[r] = rsum->gal[r]; rb.key[r] = rsum->key[r]; }
+            for (int b = 0; b < B; b++) {
+                rb.c0[b] = rsum->c0[b];
+                rb.c1[b] = din[b];
+                rb.up[b] = I + (size_t)b * g.i_stride();
+            }
+            const int ngroups = (B + RS_NBT - 1) / RS_NBT;
+            const u64* pmodq = c.d_rescale + (size_t)(c.L + 1) * c.nall * 3;
+            dim3 grid((unsigned)((N / 2 + 255) / 256) * ngroups, nt);
+            if (g.beta > 4) launch_k(c, ks_keyprod_rotsum<8>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
+            else launch_k(c, ks_keyprod_rotsum<4>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
+        } else
         // a lone key switch (chains) takes one coefficient per thread for
         // parallelism; batches take pairs (16-byte accesses, fewer index ops)
         if (g.beta > 4) {   // deep chains (bootstrapping): 8 digits, one coefficient per thread
@@ -753,13 +943,38 @@ static bool fusable(const Ctx& c, int level) {
 }
 
 static void ks_pipeline(Ctx& c, int nin, const u64* const* din, u64 gal, int level, int B, const KsTail* in,
-                        int add_npoly) {
+                        int add_npoly, const KsRotsumSpec* rsum = nullptr) {
     switch (c.logN) {
-        case 14: ks_pipeline_t<14>(c, nin, din, gal, level, B, in, add_npoly); break;
-        case 15: ks_pipeline_t<15>(c, nin, din, gal, level, B, in, add_npoly); break;
-        case 16: ks_pipeline_t<16>(c, nin, din, gal, level, B, in, add_npoly); break;
-        default: ks_pipeline_t<17>(c, nin, din, gal, level, B, in, add_npoly); break;
+        case 14: ks_pipeline_t<14>(c, nin, din, gal, level, B, in, add_npoly, rsum); break;
+        case 15: ks_pipeline_t<15>(c, nin, din, gal, level, B, in, add_npoly, rsum); break;
+        case 16: ks_pipeline_t<16>(c, nin, din, gal, level, B, in, add_npoly, rsum); break;
+        default: ks_pipeline_t<17>(c, nin, din, gal, level, B, in, add_npoly, rsum); break;
     }
+}
+
+// out_b = x_b + sum_r sigma_{gals[r]}(x_b) for B inputs at one level (x_b = [c0 | c1] at xs[b])
+bool keyswitch_rotsum(Ctx& c, int B, const u64* const* xs, u64* const* outs, int level, int nrot, const u64* gals,
+                      const u64* const* keys) {
+    if (!fusable(c, level) || nrot < 1 || nrot > RS_MAXR) return false;
+    const size_t poly = (size_t)(level + 1) * c.N;
+    KsRotsumSpec rs;
+    rs.nrot = nrot;
+    for (int r = 0; r < nrot; r++) { rs.gal[r] = gals[r]; rs.key[r] = keys[r]; }
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        const u64* din[KS_MAXB];
+        const u64* c0s[KS_MAXB];
+        KsTail tl[KS_MAXB];
+        for (int b = 0; b < nb; b++) {
+            const u64* x = xs[b0 + b];
+            c0s[b] = x;
+            din[b] = x + poly;
+            tl[b] = KsTail{b, 0, x + poly, outs[b0 + b], nullptr, x, nullptr, 0};
+        }
+        rs.c0 = c0s;
+        ks_pipeline(c, nb, din, 0, level, nb, tl, 0, &rs);
+    }
+    return true;
 }
 
 bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, int add_npoly, u64 add_gal) {

@@ -229,9 +229,9 @@ static G col_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, int width
     par_for(ev.c, r, width, [&](int p) {
         CtP acc = E[(size_t)p * cols];
         for (int q = 1; q < cols; q++) acc = ev.add(acc, E[(size_t)p * cols + q]);
-        for (int t = 0; t < ilog2(g.s1); t++) acc = ev.add_lrot(acc, 1 << t);
+        acc = ev.ladder(acc, 1, ilog2(g.s1));
         acc = ev.mult_p(acc, c0);
-        for (int t = 0; t < ilog2(g.s1); t++) acc = ev.add_rrot(acc, 1 << t);
+        acc = ev.ladder(acc, -1, ilog2(g.s1));
         out[p] = acc;
     });
     return out;
@@ -248,9 +248,7 @@ static G row_sums(Eval& ev, const G& E, int r, int cols, const Geo& g, const Red
     }
     if (red) red(pre);
     for (int q = 0; q < cols; q++) {
-        CtP acc = pre[q];
-        for (int t = 0; t < ilog2(g.s0); t++) acc = ev.add_lrot(acc, (int64_t)(1 << t) * g.s1);
-        pre[q] = acc;
+        pre[q] = ev.ladder(pre[q], g.s1, ilog2(g.s0));
     }
     return pre;
 }
@@ -304,6 +302,21 @@ static G rot_many(Eval& ev, const G& xs, int64_t r, bool add_self = false) {
     par_for(C, nsub, fork_width(C, nsub), [&](int i) {
         const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);
         G part = ev.lrot_batch(G(xs.begin() + lo, xs.begin() + hi), r, add_self);
+        std::copy(part.begin(), part.end(), out.begin() + lo);
+    });
+    return out;
+}
+
+// the doubling ladder of many independent operands (Eval::ladder), in
+// sub-batches on concurrent branches like rot_many
+static G ladder_many(Eval& ev, const G& xs, int64_t stride, int steps) {
+    Ctx& C = ev.c;
+    const int SB = std::max(1, C.batch), nsub = ((int)xs.size() + SB - 1) / SB;
+    if (nsub <= 1) return ev.ladder(xs, stride, steps);
+    G out(xs.size());
+    par_for(C, nsub, fork_width(C, nsub), [&](int i) {
+        const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);
+        G part = ev.ladder(G(xs.begin() + lo, xs.begin() + hi), stride, steps);
         std::copy(part.begin(), part.end(), out.begin() + lo);
     });
     return out;
@@ -430,10 +443,10 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
                 acc[(size_t)k * m + p] = a;
             }
     }
-    for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, 1 << t, true);
+    acc = ladder_many(ev, acc, 1, ilog2(g.s1));
     const Pattern c0 = col0(g);
     acc = ev.mult_p_batch(acc, std::vector<const Pattern*>(acc.size(), &c0));
-    for (int t = 0; t < ilog2(g.s1); t++) acc = rot_many(ev, acc, -(1 << t), true);
+    acc = ladder_many(ev, acc, -1, ilog2(g.s1));
     std::vector<G> terms(K, G(m));
     {
         std::vector<Pattern> masks;
@@ -590,7 +603,7 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
             red(pre);
             for (int q = 0; q < n; q++) acc[(size_t)k * n + q] = pre[q];
         }
-    for (int t = 0; t < ilog2(g.s0); t++) acc = rot_many(ev, acc, (int64_t)(1 << t) * s1, true);
+    acc = ladder_many(ev, acc, s1, ilog2(g.s0));
     std::vector<G> terms(K, G(n));
     {
         std::vector<Pattern> masks;
@@ -733,8 +746,7 @@ std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, cons
         const Pattern mask = diag_mask(g, -k, c, true, scale);
         terms[k].resize(n);
         par_for(C, n, ser ? 1 :n, [&](int q) {
-            CtP a = pre[q];
-            for (int t = 0; t < ilog2(g.s0); t++) a = ev.add_lrot(a, (int64_t)(1 << t) * s1);
+            CtP a = ev.ladder(pre[q], s1, ilog2(g.s0));
             terms[k][q] = ev.mult_p(a, mask);
         });
     });
@@ -777,8 +789,7 @@ std::vector<CtP> sched_col_major_abt(Eval& ev, const std::vector<CtP>& A, int m,
         const Pattern rowj = row_select(g, j, 1.0);
         G picked(n);
         for (int q = 0; q < n; q++) picked[q] = ev.mult_p(B[q], rowj);
-        for (int t = 0; t < ilog2(g.s0); t++)
-            for (int q = 0; q < n; q++) picked[q] = ev.add_lrot(picked[q], (int64_t)(1 << t) * g.s1);
+        for (int q = 0; q < n; q++) picked[q] = ev.ladder(picked[q], g.s1, ilog2(g.s0));
         G prod((size_t)m * n);
         for (int p = 0; p < m; p++)
             for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(A[(size_t)p * n + q], picked[q]);
@@ -786,7 +797,7 @@ std::vector<CtP> sched_col_major_abt(Eval& ev, const std::vector<CtP>& A, int m,
         for (int p = 0; p < m; p++) {
             CtP blk = prod[(size_t)p * n];
             for (int q = 1; q < n; q++) blk = ev.add(blk, prod[(size_t)p * n + q]);
-            for (int t = 0; t < ilog2(g.s1); t++) blk = ev.add_lrot(blk, 1 << t);
+            blk = ev.ladder(blk, 1, ilog2(g.s1));
             blk = ev.mult_p(blk, c0);
             terms[j][p] = ev.rrot(blk, j);
         }
@@ -810,8 +821,7 @@ std::vector<CtP> sched_row_major_atb(Eval& ev, const std::vector<CtP>& A, int m,
         G picked(m);
         for (int p = 0; p < m; p++) picked[p] = ev.lrot(A[p], j);
         for (int p = 0; p < m; p++) picked[p] = ev.mult_p(picked[p], c0);
-        for (int t = 0; t < ilog2(g.s1); t++)
-            for (int p = 0; p < m; p++) picked[p] = ev.add_rrot(picked[p], 1 << t);
+        for (int p = 0; p < m; p++) picked[p] = ev.ladder(picked[p], -1, ilog2(g.s1));
         G prod((size_t)m * n);
         for (int p = 0; p < m; p++)
             for (int q = 0; q < n; q++) prod[(size_t)p * n + q] = ev.mult(picked[p], B[(size_t)p * n + q]);
@@ -897,7 +907,7 @@ struct SM {
             best = add(G(xy.begin(), xy.begin() + best.size()), G(xy.begin() + best.size(), xy.end()));
         }
         best = mulp(best, col0(g));
-        for (int t = 0; t < ilog2(g.s1); t++) best = ev.lrot_batch(best, -(1 << t), true);
+        best = ev.ladder(best, -1, ilog2(g.s1));
         return scale(best, two_r);
     }
     G domain_extend(G M, const SoftmaxCfg& cfg) {
@@ -1052,14 +1062,13 @@ static std::vector<CtP> softmax_serial(Eval& ev, const std::vector<CtP>& M, int 
     G expd = sm.mulp(e, keep);
     // col_sums of every block (encoding.py:335-360) in lockstep
     G total = expd;
-    for (int t = 0; t < ilog2(g.s1); t++) total = ev.lrot_batch(total, 1 << t, true);
+    total = ev.ladder(total, 1, ilog2(g.s1));
     total = sm.mulp(total, col0(g));
-    for (int t = 0; t < ilog2(g.s1); t++) total = ev.lrot_batch(total, -(1 << t), true);
+    total = ev.ladder(total, -1, ilog2(g.s1));
     G recip = sm.inv(total, cfg);
     G out = sm.mul(expd, recip);
     const int reps = g.s1 / period;
-    for (int t = 0; t < ilog2(reps); t++) out = ev.lrot_batch(out, -(int64_t)period * (1 << t), true);
-    return out;
+    return ev.ladder(out, -(int64_t)period, ilog2(reps));
 }
 
 std::vector<CtP> sched_approx(Eval& ev, int fn, const std::vector<CtP>& X, const std::vector<CtP>& Y, int classes,

@@ -131,6 +131,24 @@ def _fused_ops(g, o, seed, tol=1e-5):
     for r, a in zip(rs, g.lrot_hoisted(gx[0], rs)):
         if r:
             np.testing.assert_array_equal(a.residues(), g.lrot(gx[0], r).residues())
+    # doubling ladders as radix-4 rotate-and-sum stages (one ModUp / ModDown per
+    # two steps): residues vs the oracle's stages, the reference's ledger
+    g.ledger.reset()
+    o.ledger.reset()
+    ks0 = g.extra["KeySwitch"], o.extra["KeySwitch"]
+    for stride, steps, lv in ((1, 4, None), (-1, 3, None), (g.grid_cols, 2, 2), (-2, 1, 1)):
+        z = rng.uniform(-1, 1, n) * 2.0 ** -steps
+        g.nonce, o.nonce = 50, 50
+        a = g.encrypt(z) if lv is None else g.encrypt(z, lv)
+        b = o.encrypt(z) if lv is None else o.encrypt(z, lv)
+        la, lb = S.ladder(g, a, stride, steps), S.ladder(o, b, stride, steps)
+        np.testing.assert_array_equal(la.residues(), lb.data)
+        want = z
+        for t in range(steps):
+            want = want + np.roll(want, -stride * (1 << t))
+        assert np.max(np.abs(la.slots - want)) < tol
+    assert _ledger(g) == _ledger(o) == [10, 0, 0, 10, 0, 0]
+    assert g.extra["KeySwitch"] - ks0[0] == o.extra["KeySwitch"] - ks0[1] == 6
 
 
 def test_fused_ops_residues(pair):
@@ -502,5 +520,6 @@ def test_adversarial_residues(name, grid):
         np.testing.assert_array_equal(g.rescale(gb).residues(), o.p.rescale(data, lv))
         for r in (1, 5):
             np.testing.assert_array_equal(g.lrot(gb, r).residues(), o.lrot(ob, r).data)
+        np.testing.assert_array_equal(S.ladder(g, gb, 3, 3).residues(), S.ladder(o, ob, 3, 3).data)
         np.testing.assert_array_equal(g.conj(gb).residues(), o.conj(ob).data)
         np.testing.assert_array_equal(g.mult(gb, gb).residues(), o.mult(ob, ob).data)

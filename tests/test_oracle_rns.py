@@ -144,7 +144,10 @@ def test_restated_diag_abt_config0_over_oracle(golden):
     assert r.level == 1
     out = S.decode(r, tol=1e-4)
     assert np.max(np.abs(out - golden["cfg0_out"])) < 1e-4
-    assert ctx.extra["KeySwitch"] == 8 + 104 + 1
+    # key-switch pipelines run: 8 relinearisations (one per product sum), 8
+    # hoisted rotations, 16 ladders of 6 doubling steps as 3 radix-4
+    # rotate-and-sum stages each (96 of the ledger's 104 Rot), 1 conj
+    assert ctx.extra["KeySwitch"] == 8 + 8 + 48 + 1
 
 
 def test_restated_softmax_small12(golden):
@@ -205,6 +208,38 @@ def test_hoisted_rotations_and_product_sums(small):
     s = small.mult_sum(cxs, cys, L)
     assert np.max(np.abs(small.decrypt(s, L - 1) - sum(a * b for a, b in zip(xs, ys)))) < TOL
     np.testing.assert_array_equal(small.mult_sum(cxs[:1], cys[:1], L), small.mult(cxs[0], cys[0], L))
+
+
+def test_rotate_and_sum_stage(small):
+    """Radix ladders: x + sum_r lrot(x, r) with one ModUp, the
+    key products summed in the extended basis and one ModDown decrypts to the
+    value of the doubling steps it replaces; with a single rotation it is the
+    ordinary rotate-and-add up to the ModDown rounding of one pipeline, and
+    the restated ladder keeps the reference ledger."""
+    rng = np.random.default_rng(9)
+    n, L = small.slots, small.L
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    cx = small.encrypt(x, L, 0)
+    for rs in ((1, 2, 3), (n - 4, n - 8, n - 12), (5,), (16, 32, 48, 64, 80, 96, 112)):
+        o = small.rotsum(cx, L, [small.galois(r) for r in rs])
+        want = x + sum(np.roll(x, -r) for r in rs)
+        assert np.max(np.abs(small.decrypt(o, L) - want)) < TOL
+    one = small.rotsum(cx, L, [small.galois(5)])
+    np.testing.assert_array_equal(one, small.add(cx, small.automorph(cx, L, small.galois(5)), L))
+    for hoist in (True, False):
+        ctx = R.OracleCKKSContext("small12", 16, seed=5, hoist=hoist)
+        v = rng.uniform(-1, 1, ctx.slot_count)
+        b = ctx.encrypt(v)
+        got = S.ladder(ctx, b, 16, 4)            # row ladder: stride s1 = 16, 4 steps
+        got = S.ladder(ctx, got, -1, 3)          # odd step count: radix 4 then radix 2
+        want = v
+        for t in range(4):
+            want = want + np.roll(want, -16 * (1 << t))
+        for t in range(3):
+            want = want + np.roll(want, 1 << t)
+        assert np.max(np.abs(got.slots - want)) < 1e-4
+        assert ctx.ledger.counts()["Rot"] == 7 and ctx.ledger.counts()["Add"] == 7
+        assert ctx.extra["KeySwitch"] == (4 if hoist else 7)
 
 
 @pytest.mark.parametrize("hoist", [True, False])

@@ -223,6 +223,11 @@ int hc_bench_keyswitch(hc_ctx *ctx, const hc_ct *ct, int streams, int reps, floa
 /* same with `batch` rotations per step of each chain issued as one batched pipeline
  * (device time in ms over all streams*batch*reps key switches) */
 int hc_bench_keyswitch_batch(hc_ctx *ctx, const hc_ct *ct, int streams, int batch, int reps, float *ms);
+/* ladder throughput: `streams` concurrent branches, each `reps` doubling
+ * ladders (hc_op_ladder's stride / steps) over its own batch of `batch`
+ * copies of ct (device time in ms; ledger and model untouched) */
+int hc_bench_ladder(hc_ctx *ctx, const hc_ct *ct, int streams, int batch, int64_t stride, int steps, int reps,
+                    float *ms);
 /* batched NTT throughput: `reps` forward (or inverse) transforms of `nlimbs` limbs */
 int hc_bench_ntt(hc_ctx *ctx, int nlimbs, int reps, int inverse, float *ms);
 /* per-kernel event profiler: JSON {"kernel": [launches, total_ms, algorithmic_bytes], ...} */

@@ -95,6 +95,7 @@ SIGNATURES = {
     "hc_launch_count": (I64, [P]),
     "hc_bench_keyswitch": (I, [P, P, I, I, C.POINTER(C.c_float)]),
     "hc_bench_keyswitch_batch": (I, [P, P, I, I, I, C.POINTER(C.c_float)]),
+    "hc_bench_ladder": (I, [P, P, I, I, C.c_int64, I, I, C.POINTER(C.c_float)]),
     "hc_bench_ntt": (I, [P, I, I, I, C.POINTER(C.c_float)]),
     "hc_prof_begin": (I, [P]),
     "hc_prof_end": (I, [P, C.c_char_p, I]),

@@ -516,6 +516,29 @@ int hc_bench_keyswitch_batch(hc_ctx* ctx, const hc_ct* a, int streams, int batch
     });
 }
 
+int hc_bench_ladder(hc_ctx* ctx, const hc_ct* a, int streams, int batch, int64_t stride, int steps, int reps,
+                    float* ms) {
+    return guard([&] {
+        hc::Ctx& c = *ctx->c;
+        if (streams < 1 || batch < 1 || reps < 1 || steps < 1) throw hc::Error(HC_EPARAM, "bad sizes");
+        int64_t saved[HC_NCOUNTS];
+        snap(ctx, saved);
+        const double model = c.model_bytes;
+        hc::Eval ev(c, false);
+        hc::probe_ladders(ev, a->p, streams, batch, stride, steps, 1);   // warm keys and pool
+        HC_CUDA(cudaStreamSynchronize(c.stream));
+        if (!c.t0) { HC_CUDA(cudaEventCreate(&c.t0)); HC_CUDA(cudaEventCreate(&c.t1)); }
+        HC_CUDA(cudaEventRecord(c.t0, c.stream));
+        hc::probe_ladders(ev, a->p, streams, batch, stride, steps, reps);
+        HC_CUDA(cudaEventRecord(c.t1, c.stream));
+        HC_CUDA(cudaEventSynchronize(c.t1));
+        HC_CUDA(cudaEventElapsedTime(ms, c.t0, c.t1));
+        std::lock_guard<std::mutex> g(c.mu);
+        for (int i = 0; i < HC_NCOUNTS; i++) c.counts[i] = saved[i];
+        c.model_bytes = model;
+    });
+}
+
 int hc_prof_begin(hc_ctx* ctx) {
     return guard([&] {
         hc::Ctx& c = *ctx->c;

@@ -297,7 +297,6 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : (MB > 4 ? 2 : 3)) ks_k
 // pairs map to aligned pairs under every Galois element (src(k + 1) =
 // src(k) ^ 1), so each gather is one 16-byte load.
 constexpr int RS_MAXR = 3;   // rotations per stage (radix 4); bounds the 128-bit sums: 3 * (4 + 1) terms below 2^124
-constexpr int RS_NBT = 4;    // entries per thread
 struct KsRotsum {
     int nb, nrot;
     const u64* c0[KS_MAXB];    // x_b poly 0 [nl][N]
@@ -307,25 +306,43 @@ struct KsRotsum {
     const u64* key[RS_MAXR];   // [dnum][2][nall][N]
 };
 
-__device__ __forceinline__ void rs_gather2(const u64* __restrict__ base, unsigned src, u64* v) {
-    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(base + (src & ~1u));
-    const bool sw = src & 1u;
-    v[0] = sw ? w.y : w.x;
-    v[1] = sw ? w.x : w.y;
+// E words of index pair / word k read through a Galois permutation: aligned
+// pairs map to aligned pairs, possibly swapped (src(k + 1) = src(k) ^ 1)
+template <int E>
+__device__ __forceinline__ void rs_gather(const u64* __restrict__ base, unsigned src, u64* v) {
+    if (E == 2) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(base + (src & ~1u));
+        const bool sw = src & 1u;
+        v[0] = sw ? w.y : w.x;
+        v[E - 1] = sw ? w.x : w.y;
+    } else {
+        v[0] = base[src];
+    }
+}
+template <int E>
+__device__ __forceinline__ void rs_load(const u64* __restrict__ p, u64* v) {
+    if (E == 2) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(p);
+        v[0] = w.x;
+        v[E - 1] = w.y;
+    } else {
+        v[0] = p[0];
+    }
 }
 
-template <bool FP, int MB, int NBT>
+// NBT entries per pass over the rotations (register budget)
+template <bool FP, int MB, int NBT, int E>
 __device__ __forceinline__ void rs_run(const KsGeo& g, const PrimeDev& P, int t, int pi, int dig, unsigned k, int b0,
                                        int nb, const KsRotsum& rb, u64 pq, u64* __restrict__ acc) {
     using KW = typename std::conditional<FP, double, u64>::type;
     const size_t N = (size_t)1 << g.logN;
     const size_t kstride = (size_t)g.nall * N;
-    double fb[NBT][2], fa[NBT][2];
-    U128 ib[NBT][2], ia[NBT][2];
+    double fb[NBT][E], fa[NBT][E];
+    U128 ib[NBT][E], ia[NBT][E];
 #pragma unroll
     for (int i = 0; i < NBT; i++)
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
+        for (int e = 0; e < E; e++) {
             if constexpr (FP) { fb[i][e] = 0; fa[i][e] = 0; }
             else { ib[i][e] = U128{0, 0}; ia[i][e] = U128{0, 0}; }
         }
@@ -336,55 +353,64 @@ __device__ __forceinline__ void rs_run(const KsGeo& g, const PrimeDev& P, int t,
     const bool fold = !FP && (g.beta + 1) * rb.nrot > 15;
     for (int r = 0; r < rb.nrot; r++) {
         const unsigned src = galois_src(k, g.logN, rb.gal[r]);
-        KW kbv[MB][2], kav[MB][2];
+        // every load of this rotation is issued before the first use: the key
+        // words, then each entry's digits and c0
+        u64 kw[MB][2][E];
 #pragma unroll
         for (int j = 0; j < MB; j++) {
             if (j >= g.beta) break;
             const u64* kp = rb.key[r] + ((size_t)(2 * j) * g.nall + pi) * N + k;
-            const ulonglong2 wb = *reinterpret_cast<const ulonglong2*>(kp);
-            const ulonglong2 wa = *reinterpret_cast<const ulonglong2*>(kp + kstride);
-            if constexpr (FP) {
-                kbv[j][0] = fp_word(wb.x); kbv[j][1] = fp_word(wb.y);
-                kav[j][0] = fp_word(wa.x); kav[j][1] = fp_word(wa.y);
-            } else {
-                kbv[j][0] = wb.x; kbv[j][1] = wb.y;
-                kav[j][0] = wa.x; kav[j][1] = wa.y;
+            rs_load<E>(kp, kw[j][0]);
+            rs_load<E>(kp + kstride, kw[j][1]);
+        }
+        u64 x[NBT][MB + 1][E];
+#pragma unroll
+        for (int i = 0; i < NBT; i++) {
+            if (i >= nb) break;
+            const int b = b0 + i;
+#pragma unroll
+            for (int j = 0; j < MB; j++) {
+                if (j >= g.beta) break;
+                const u64* bp = (j == dig) ? rb.c1[b] + (size_t)t * N : rb.up[b] + ((size_t)j * g.nt + t) * N;
+                rs_gather<E>(bp, src, x[i][j]);
+            }
+            if (qlimb) rs_gather<E>(rb.c0[b] + (size_t)t * N, src, x[i][MB]);
+        }
+        KW kbv[MB][E], kav[MB][E];
+#pragma unroll
+        for (int j = 0; j < MB; j++) {
+            if (j >= g.beta) break;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                if constexpr (FP) { kbv[j][e] = fp_word(kw[j][0][e]); kav[j][e] = fp_word(kw[j][1][e]); }
+                else { kbv[j][e] = kw[j][0][e]; kav[j][e] = kw[j][1][e]; }
             }
         }
 #pragma unroll
         for (int i = 0; i < NBT; i++) {
             if (i >= nb) break;
-            const int b = b0 + i;
-            u64 x[MB][2], z[2];
 #pragma unroll
-            for (int j = 0; j < MB; j++) {
-                if (j >= g.beta) break;
-                const u64* bp = (j == dig) ? rb.c1[b] + (size_t)t * N : rb.up[b] + ((size_t)j * g.nt + t) * N;
-                rs_gather2(bp, src, x[j]);
-            }
-            if (qlimb) rs_gather2(rb.c0[b] + (size_t)t * N, src, z);
-#pragma unroll
-            for (int e = 0; e < 2; e++) {
+            for (int e = 0; e < E; e++) {
                 if constexpr (FP) {
                     double sb = fb[i][e], sa = fa[i][e];
 #pragma unroll
                     for (int j = 0; j < MB; j++) {
                         if (j >= g.beta) break;
-                        const double y = fp_word(x[j][e]);
+                        const double y = fp_word(x[i][j][e]);
                         sb = __dadd_rn(sb, fp_mulmod(y, kbv[j][e], P.qd, P.qinv));
                         sa = __dadd_rn(sa, fp_mulmod(y, kav[j][e], P.qd, P.qinv));
                     }
-                    if (qlimb) sb = __dadd_rn(sb, fp_mulmod(fp_word(z[e]), pqd, P.qd, P.qinv));
+                    if (qlimb) sb = __dadd_rn(sb, fp_mulmod(fp_word(x[i][MB][e]), pqd, P.qd, P.qinv));
                     fb[i][e] = sb;
                     fa[i][e] = sa;
                 } else {
 #pragma unroll
                     for (int j = 0; j < MB; j++) {
                         if (j >= g.beta) break;
-                        mac128(ib[i][e], x[j][e], kbv[j][e]);
-                        mac128(ia[i][e], x[j][e], kav[j][e]);
+                        mac128(ib[i][e], x[i][j][e], kbv[j][e]);
+                        mac128(ia[i][e], x[i][j][e], kav[j][e]);
                     }
-                    if (qlimb) mac128(ib[i][e], z[e], pq);
+                    if (qlimb) mac128(ib[i][e], x[i][MB][e], pq);
                     if (fold && r + 1 < rb.nrot) {
                         ib[i][e] = U128{reduce128(ib[i][e].hi, ib[i][e].lo, P), 0};
                         ia[i][e] = U128{reduce128(ia[i][e].hi, ia[i][e].lo, P), 0};
@@ -396,9 +422,9 @@ __device__ __forceinline__ void rs_run(const KsGeo& g, const PrimeDev& P, int t,
 #pragma unroll
     for (int i = 0; i < NBT; i++) {
         if (i >= nb) break;
-        u64 ob[2], oa[2];
+        u64 ob[E], oa[E];
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
+        for (int e = 0; e < E; e++) {
             if constexpr (FP) {
                 ob[e] = fp_canon(fb[i][e], P.qd, P.qinv);
                 oa[e] = fp_canon(fa[i][e], P.qd, P.qinv);
@@ -408,18 +434,44 @@ __device__ __forceinline__ void rs_run(const KsGeo& g, const PrimeDev& P, int t,
             }
         }
         u64* ab = acc + (size_t)(b0 + i) * g.acc_stride();
-        *reinterpret_cast<ulonglong2*>(ab + (size_t)t * N + k) = make_ulonglong2(ob[0], ob[1]);
-        *reinterpret_cast<ulonglong2*>(ab + ((size_t)g.nt + t) * N + k) = make_ulonglong2(oa[0], oa[1]);
+        if (E == 2) {
+            *reinterpret_cast<ulonglong2*>(ab + (size_t)t * N + k) = make_ulonglong2(ob[0], ob[E - 1]);
+            *reinterpret_cast<ulonglong2*>(ab + ((size_t)g.nt + t) * N + k) = make_ulonglong2(oa[0], oa[E - 1]);
+        } else {
+            ab[(size_t)t * N + k] = ob[0];
+            ab[((size_t)g.nt + t) * N + k] = oa[0];
+        }
     }
 }
 
-#ifndef RS_MINB
-#define RS_MINB 2
+// knobs (measured with scripts/ladder_probe.py, 3 streams x batches of 3
+// radix-4 stages at level 11, us per stage): coefficients per thread, entries
+// per pass over the rotations for FP64 / integer limbs, entries per thread
+// group, resident 256-thread CTAs per SM.  One coefficient of one entry per
+// thread at 5 CTAs per SM (48 registers; the entries of a coefficient block
+// run side by side and share its key words through L2) measured best: 99.5;
+// 2 entries per thread 112.8, 4 entries 111.0, coefficient pairs 117-132,
+// 4 / 6 CTAs per SM 102.7 / 109.5
+#ifndef RS_E
+#define RS_E 1
 #endif
+#ifndef RS_NF
+#define RS_NF 1
+#endif
+#ifndef RS_NI
+#define RS_NI 1
+#endif
+#ifndef RS_GROUP
+#define RS_GROUP 1
+#endif
+#ifndef RS_MINB
+#define RS_MINB 5
+#endif
+constexpr int RS_NBT = RS_GROUP;   // entries per thread
 // grid x = (coefficient block, entry group) with the group fastest, so the
 // groups sharing a block's key words run together (second read from L2)
 template <int MB = 4>
-__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum(KsGeo g, const PrimeDev* __restrict__ primes,
+__global__ void __launch_bounds__(256, MB > 4 ? 2 : RS_MINB) ks_keyprod_rotsum(KsGeo g, const PrimeDev* __restrict__ primes,
                                                                   KsRotsum rb, const u64* __restrict__ pmodq,
                                                                   u64* __restrict__ acc, int ngroups) {
     pdl_enter();
@@ -428,21 +480,106 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum(KsGeo g, const
     const int pi = g.prime(t);
     const PrimeDev P = primes[pi];
     const int grp = blockIdx.x % ngroups;
-    const unsigned k = 2u * ((blockIdx.x / ngroups) * blockDim.x + threadIdx.x);
+    const unsigned k = (unsigned)RS_E * ((blockIdx.x / ngroups) * blockDim.x + threadIdx.x);
     if (k >= N) return;
     const int b0 = grp * RS_NBT;
     const int nb = min(RS_NBT, rb.nb - b0);
     const int dig = t < g.nl ? t / g.alpha : -1;
     const u64 pq = t < g.nl ? pmodq[pi] : 0;
-    // entries per pass over the rotations, by register budget: the integer
-    // path's 128-bit sums (and 8-digit key words) take fewer at a time; the
-    // later passes re-read the key words from L1 / L2
-    constexpr int NF = MB > 4 ? 2 : 4, NI = MB > 4 ? 1 : 2;
+    // entries per pass over the rotations, by register budget: the later
+    // passes re-read the key words from L1 / L2
+    constexpr int NF = MB > 4 ? 1 : RS_NF, NI = MB > 4 ? 1 : RS_NI;
     if (P.fp) {
-        for (int o = 0; o < nb; o += NF) rs_run<true, MB, NF>(g, P, t, pi, dig, k, b0 + o, min(NF, nb - o), rb, pq, acc);
+        for (int o = 0; o < nb; o += NF) rs_run<true, MB, NF, RS_E>(g, P, t, pi, dig, k, b0 + o, min(NF, nb - o), rb, pq, acc);
     } else {
-        for (int o = 0; o < nb; o += NI) rs_run<false, MB, NI>(g, P, t, pi, dig, k, b0 + o, min(NI, nb - o), rb, pq, acc);
+        for (int o = 0; o < nb; o += NI) rs_run<false, MB, NI, RS_E>(g, P, t, pi, dig, k, b0 + o, min(NI, nb - o), rb, pq, acc);
     }
+}
+
+// The stage kernel proper: digit count and rotation count are compile-time,
+// so every loop is unrolled, the (rotation, digit) bases are scalar offsets of
+// one per-thread index and the parameter arrays are read at constant offsets
+// (the generic form above spent 88 % of its issue slots on loop control and
+// 64-bit address arithmetic: 1031 instructions per thread against ~400 here).
+// Grid (entry, coefficient block, target limb): the entries of a coefficient
+// block run side by side and share its key words through L2.
+template <int BETA, int NR>
+__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, const PrimeDev* __restrict__ primes,
+                                                                    KsRotsum rb, const u64* __restrict__ pmodq,
+                                                                    u64* __restrict__ acc) {
+    pdl_enter();
+    const int t = blockIdx.z;
+    const int pi = g.prime(t);
+    const PrimeDev P = primes[pi];
+    const int b = blockIdx.x;
+    const unsigned k = blockIdx.y * 256u + threadIdx.x;
+    const unsigned N = 1u << g.logN;
+    const bool qlimb = t < g.nl;
+    const int dig = qlimb ? t / g.alpha : -1;
+    const size_t toff = (size_t)t * N;
+    const u64* __restrict__ c1 = rb.c1[b] + toff;
+    const u64* __restrict__ c0 = rb.c0[b] + toff;
+    const u64* __restrict__ up = rb.up[b] + toff;
+    const size_t dstride = (size_t)g.nt * N;            // digit stride of UP
+    const size_t kstride = (size_t)g.nall * N;          // (b, a) stride of a key digit
+    const size_t koff = (size_t)pi * N + k;
+    const u64 pq = qlimb ? pmodq[pi] : 0;
+    u64 ob, oa;
+    if (P.fp) {
+        const double q = P.qd, qinv = P.qinv, pqd = fp_word(pq);
+        double sb = 0, sa = 0;
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            const unsigned src = galois_src(k, g.logN, rb.gal[r]);
+            const u64* __restrict__ kp = rb.key[r] + koff;
+            u64 kb[BETA], ka[BETA], x[BETA], z = 0;
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                kb[j] = __ldg(kp + (size_t)(2 * j) * kstride);
+                ka[j] = __ldg(kp + (size_t)(2 * j + 1) * kstride);
+                x[j] = (j == dig ? c1 : up + j * dstride)[src];
+            }
+            if (qlimb) z = c0[src];
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                const double y = fp_word(x[j]);
+                sb = __dadd_rn(sb, fp_mulmod(y, fp_word(kb[j]), q, qinv));
+                sa = __dadd_rn(sa, fp_mulmod(y, fp_word(ka[j]), q, qinv));
+            }
+            if (qlimb) sb = __dadd_rn(sb, fp_mulmod(fp_word(z), pqd, q, qinv));
+        }
+        ob = fp_canon(sb, q, qinv);
+        oa = fp_canon(sa, q, qinv);
+    } else {
+        // 128-bit sums hold 15 products of a lazy digit (< 16q) and a key
+        // word (q < 2^60): NR * (BETA + 1) <= 15 (static_assert below)
+        U128 ib = {0, 0}, ia = {0, 0};
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            const unsigned src = galois_src(k, g.logN, rb.gal[r]);
+            const u64* __restrict__ kp = rb.key[r] + koff;
+            u64 kb[BETA], ka[BETA], x[BETA], z = 0;
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                kb[j] = __ldg(kp + (size_t)(2 * j) * kstride);
+                ka[j] = __ldg(kp + (size_t)(2 * j + 1) * kstride);
+                x[j] = (j == dig ? c1 : up + j * dstride)[src];
+            }
+            if (qlimb) z = c0[src];
+#pragma unroll
+            for (int j = 0; j < BETA; j++) {
+                mac128(ib, x[j], kb[j]);
+                mac128(ia, x[j], ka[j]);
+            }
+            if (qlimb) mac128(ib, z, pq);
+        }
+        ob = reduce128(ib.hi, ib.lo, P);
+        oa = reduce128(ia.hi, ia.lo, P);
+    }
+    static_assert(NR * (BETA + 1) <= 15, "128-bit key-product sum bound");
+    u64* __restrict__ ab = acc + (size_t)b * g.acc_stride() + toff + k;
+    ab[0] = ob;
+    ab[dstride] = oa;
 }
 
 // ---- D: ModDown conversion fused into the column pass ----------------------
@@ -860,8 +997,15 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             }
             const int ngroups = (B + RS_NBT - 1) / RS_NBT;
             const u64* pmodq = c.d_rescale + (size_t)(c.L + 1) * c.nall * 3;
-            dim3 grid((unsigned)((N / 2 + 255) / 256) * ngroups, nt);
-            if (g.beta > 4) launch_k(c, ks_keyprod_rotsum<8>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
+            dim3 grid((unsigned)((N / RS_E + 255) / 256) * ngroups, nt);
+            dim3 tgrid((unsigned)B, (unsigned)(N / 256), (unsigned)nt);
+            const int nr = rsum->nrot;
+            auto go = [&](auto kern) { launch_k(c, kern, tgrid, 256, 0, g, c.d_primes, rb, pmodq, ACC); };
+            if (nr == 3 && g.beta == 4) go(ks_keyprod_rotsum_t<4, 3>);
+            else if (nr == 3 && g.beta == 3) go(ks_keyprod_rotsum_t<3, 3>);
+            else if (nr == 3 && g.beta == 2) go(ks_keyprod_rotsum_t<2, 3>);
+            else if (nr == 3 && g.beta == 1) go(ks_keyprod_rotsum_t<1, 3>);
+            else if (g.beta > 4) launch_k(c, ks_keyprod_rotsum<8>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
             else launch_k(c, ks_keyprod_rotsum<4>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
         } else
         // a lone key switch (chains) takes one coefficient per thread for

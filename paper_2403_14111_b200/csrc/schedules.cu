@@ -283,6 +283,16 @@ int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps, int batch
     return (int64_t)streams * reps * std::max(1, batch);
 }
 
+// `streams` independent branches, each running `reps` ladders (stride, steps)
+// over its own batch of `batch` ciphertexts (measurement only).
+void probe_ladders(Eval& ev, const CtP& x, int streams, int batch, int64_t stride, int steps, int reps) {
+    par_for(ev.c, streams, streams, [&](int) {
+        G a(batch);
+        for (int b = 0; b < batch; b++) a[b] = ev.add(x, x);   // distinct operands
+        for (int r = 0; r < reps; r++) a = ev.ladder(a, stride, steps);
+    });
+}
+
 // ---- lockstep (batched) forms ----------------------------------------------
 // When no auto-bootstrap can fire, the independent diagonal passes run in
 // lockstep: every op that the passes (and blocks) apply with the same Galois

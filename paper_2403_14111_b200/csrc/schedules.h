@@ -33,6 +33,7 @@ std::vector<CtP> sched_diag_abt(Eval& ev, const std::vector<CtP>& A, int m, int 
 std::vector<CtP> sched_diag_atb(Eval& ev, const std::vector<CtP>& A, int m, const std::vector<CtP>& B, int n, int c,
                                 double scale, const Reducer& red);
 int64_t probe_rotations(Eval& ev, const CtP& x, int streams, int reps, int batch = 1);
+void probe_ladders(Eval& ev, const CtP& x, int streams, int batch, int64_t stride, int steps, int reps);
 // Table-4 baselines (matmul.py:160-237)
 std::vector<CtP> sched_col_major_abt(Eval& ev, const std::vector<CtP>& A, int m, int n, const std::vector<CtP>& B,
                                      int c, double scale);

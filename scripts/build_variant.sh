@@ -6,7 +6,7 @@ FLAGS="$*"
 SRC=paper_2403_14111_b200/csrc
 OUT=/tmp/hcvar_$NAME
 mkdir -p $OUT exp
-for f in ntt kernels keyswitch context evaluator schedules capi; do
+for f in ntt kernels keyswitch context evaluator schedules bootstrap capi; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     -Xcompiler -ffp-contract=off -Xcompiler -fno-fast-math --expt-relaxed-constexpr $FLAGS \
     -c $SRC/$f.cu -o $OUT/$f.o &

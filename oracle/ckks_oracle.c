@@ -900,6 +900,104 @@ static void ks_moddown(orc_ctx *c, const u64 *acc, int level, u64 *out) {
     }
 }
 
+static size_t modup_words(const orc_ctx *c, int level);
+
+/* Merged ModDown + rescale: acc [2][nt][N] (NTT form) holds
+ * X over q_0..q_l and P; out [2][level][N] = (X - [X]_D) / D at level - 1,
+ * D = q_l * P, with [X]_D lifted from the basis B = (q_l, p_1, .., p_K) by the
+ * centred fast base conversion of ks_moddown.  B's limbs are acc's limbs
+ * level .. level + K (contiguous).  One rounding instead of ModDown's and the
+ * rescale's two. */
+static void ks_moddown_rescale(orc_ctx *c, const u64 *acc, int level, u64 *out) {
+    int N = c->N, L = c->L, K = c->K, nl = level + 1;
+    int nt = nl + K, nb = K + 1;
+    size_t poly = (size_t)nt * N;
+    int bp[MAXP];
+    bp[0] = level;
+    for (int t = 0; t < K; t++) bp[1 + t] = L + 1 + t;
+    for (int s = 0; s < 2; s++) {
+        const u64 *A = acc + (size_t)s * poly;
+        u64 *y = malloc(sizeof(u64) * (size_t)nb * N);
+        for (int t = 0; t < nb; t++) {
+            const prime_t *p = &c->pr[bp[t]];
+            memcpy(y + (size_t)t * N, A + (size_t)(level + t) * N, sizeof(u64) * N);
+            intt(c, p, y + (size_t)t * N);
+            u64 dh = 1;
+            for (int b = 0; b < nb; b++) if (b != t) dh = mulmod(dh, c->pr[bp[b]].q % p->q, p);
+            u64 inv = invmod(dh, p->q);
+            for (int k = 0; k < N; k++) y[(size_t)t * N + k] = mulmod(y[(size_t)t * N + k], inv, p);
+        }
+#pragma omp parallel for
+        for (int i = 0; i < level; i++) {
+            const prime_t *p = &c->pr[i];
+            u64 cf[MAXP], Dm = 1;
+            for (int t = 0; t < nb; t++) {
+                u64 v = 1;
+                for (int b = 0; b < nb; b++) if (b != t) v = mulmod(v, c->pr[bp[b]].q % p->q, p);
+                cf[t] = v;
+                Dm = mulmod(Dm, c->pr[bp[t]].q % p->q, p);
+            }
+            u64 dinv = invmod(Dm, p->q);
+            u64 *w = malloc(sizeof(u64) * N);
+            for (int k = 0; k < N; k++) {
+                u128 sacc = 0;
+                u64 cnt = 0;
+                for (int t = 0; t < nb; t++) {
+                    const u64 v = y[(size_t)t * N + k];
+                    sacc += (u128)v * cf[t];
+                    cnt += v > (c->pr[bp[t]].q - 1) / 2;
+                }
+                w[k] = submod(reduce128(sacc, p), mulmod(cnt, Dm, p), p->q);
+            }
+            ntt(c, p, w);
+            for (int k = 0; k < N; k++)
+                out[((size_t)s * level + i) * N + k] = mulmod(submod(A[(size_t)i * N + k], w[k], p->q), dinv, p);
+            free(w);
+        }
+        free(y);
+    }
+}
+
+/* Relinearisation + rescale of a tensor d = (d0, d1, d2) at `level` in one
+ * pass: X = P * (d0, d1) + <ModUp(d2), relin key> in the
+ * extended basis, then the merged ModDown + rescale: out at level - 1.
+ * Application levels only (level <= app_L). */
+static void keyswitch(orc_ctx *c, const u64 *d, int level, swkey_t *key, u64 *out);
+
+static void relin_rescale(orc_ctx *c, const u64 *d, int level, u64 *out) {
+    int N = c->N, L = c->L, K = c->K, nl = level + 1, nt = nl + K;
+    size_t poly = (size_t)nl * N, epoly = (size_t)nt * N;
+    swkey_t *key = get_key(c, 0);
+    if (level > c->app_L) {
+        /* bootstrapping levels keep ModDown and the exact centred rescale apart:
+         * the merged conversion's rounding (a sum of K + 1 centred terms
+         * instead of one) is ~2.3x larger, and EvalMod's precision is bound by
+         * exactly that rounding (measured: 5.4e-4 -> 1.1e-3 per bootstrap) */
+        u64 *t = malloc(sizeof(u64) * 2 * poly), *ks = malloc(sizeof(u64) * 2 * poly);
+        keyswitch(c, d + 2 * poly, level, key, ks);
+        for (size_t o = 0; o < 2 * poly; o++) t[o] = addmod(d[o], ks[o], c->pr[(o % poly) / N].q);
+        orc_rescale(c, t, level, 2, out);
+        free(t); free(ks);
+        return;
+    }
+    u64 *up = malloc(sizeof(u64) * modup_words(c, level));
+    ks_modup(c, d + 2 * poly, level, up);
+    u64 *acc = calloc(2 * epoly, sizeof(u64));
+    ks_keyprod_acc(c, up, level, key, acc);
+    for (int i = 0; i < nl; i++) {
+        const prime_t *p = &c->pr[i];
+        u64 Pm = 1;
+        for (int t = 0; t < K; t++) Pm = mulmod(Pm, c->pr[L + 1 + t].q % p->q, p);
+        for (int k = 0; k < N; k++) {
+            size_t o = (size_t)i * N + k;
+            acc[o] = addmod(acc[o], mulmod(d[o], Pm, p), p->q);
+            acc[epoly + o] = addmod(acc[epoly + o], mulmod(d[poly + o], Pm, p), p->q);
+        }
+    }
+    ks_moddown_rescale(c, acc, level, out);
+    free(up); free(acc);
+}
+
 /* Key inner product of the ModUp digits `up` with `key`, then ModDown by P:
  * out [2][level+1][N] = (k0, k1). */
 static void ks_keyprod_moddown(orc_ctx *c, const u64 *up, int level, swkey_t *key, u64 *out) {
@@ -961,7 +1059,7 @@ u64 orc_galois_rot(const orc_ctx *c, i64 r) {
     return powmod(5, rr, twoN);
 }
 
-/* tensor + relinearise + rescale; a, b at the same level */
+/* tensor, then relinearisation + rescale in one pass (relin_rescale); a, b at the same level */
 void orc_mult(orc_ctx *c, const u64 *a, const u64 *b, int level, u64 *out) {
     int N = c->N, nl = level + 1;
     size_t poly = (size_t)nl * N;
@@ -977,16 +1075,8 @@ void orc_mult(orc_ctx *c, const u64 *a, const u64 *b, int level, u64 *out) {
             d[2 * poly + o] = mulmod(a1, b1, p);
         }
     }
-    swkey_t *key = get_key(c, 0);
-    u64 *ks = malloc(sizeof(u64) * 2 * poly);
-    keyswitch(c, d + 2 * poly, level, key, ks);
-    for (size_t o = 0; o < poly; o++) {
-        u64 q = c->pr[o / N].q;
-        d[o] = addmod(d[o], ks[o], q);
-        d[poly + o] = addmod(d[poly + o], ks[poly + o], q);
-    }
-    orc_rescale(c, d, level, 2, out);
-    free(d); free(ks);
+    relin_rescale(c, d, level, out);
+    free(d);
 }
 
 /* Hoisted rotations: one ModUp of c1 shared by every
@@ -1068,8 +1158,7 @@ void orc_rotsum(orc_ctx *c, const u64 *a, int level, const u64 *gs, int ng, u64 
 }
 
 /* Sum of n ct x ct products with one relinearisation and one rescale:
- * d = sum_q tensor(a_q, b_q) (component-wise mod q), then d0 + KS(d2)_0,
- * d1 + KS(d2)_1, rescale.  as / bs: n ciphertexts [2][level+1][N] each,
+ * d = sum_q tensor(a_q, b_q) (component-wise mod q), then relin_rescale.  as / bs: n ciphertexts [2][level+1][N] each,
  * contiguous. */
 void orc_mult_sum(orc_ctx *c, const u64 *as, const u64 *bs, int n, int level, u64 *out) {
     int N = c->N, nl = level + 1;
@@ -1089,16 +1178,8 @@ void orc_mult_sum(orc_ctx *c, const u64 *as, const u64 *bs, int n, int level, u6
             }
         }
     }
-    swkey_t *key = get_key(c, 0);
-    u64 *ks = malloc(sizeof(u64) * 2 * poly);
-    keyswitch(c, d + 2 * poly, level, key, ks);
-    for (size_t o = 0; o < poly; o++) {
-        u64 q = c->pr[o / N].q;
-        d[o] = addmod(d[o], ks[o], q);
-        d[poly + o] = addmod(d[poly + o], ks[poly + o], q);
-    }
-    orc_rescale(c, d, level, 2, out);
-    free(d); free(ks);
+    relin_rescale(c, d, level, out);
+    free(d);
 }
 
 /* ------------------------------------------------------------------ */

@@ -420,6 +420,48 @@ Ctx* ctx_create(int logN, int nq, const int* qbits, int np, const int* pbits, in
     }
     c->d_moddown_cc = upload(*c, md_cc);
     c->d_pinv = upload(*c, pinv);
+    // merged ModDown + rescale: per level l >= 1 the dropped
+    // basis is B = (q_l, p_1..p_K), D = q_l * P
+    {
+        const int nb = K + 1;
+        std::vector<u64> inv((size_t)(L + 1) * nb * 2, 0), tab((size_t)(L + 1) * nb * nall * 2, 0),
+            negd((size_t)(L + 1) * nall, 0), cc((size_t)(L + 1) * nall, 0), dinv((size_t)(L + 1) * nall * 2, 0);
+        for (int l = 1; l <= L; l++) {
+            std::vector<int> bp(nb);
+            bp[0] = l;
+            for (int t = 0; t < K; t++) bp[1 + t] = L + 1 + t;
+            for (int t = 0; t < nb; t++) {
+                const u64 bt = c->pr[bp[t]].q;
+                u64 dh = 1;
+                for (int b = 0; b < nb; b++) if (b != t) dh = mulm(dh, c->pr[bp[b]].q % bt, bt);
+                const u64 iv = invmod(dh, bt);
+                inv[((size_t)l * nb + t) * 2] = iv;
+                inv[((size_t)l * nb + t) * 2 + 1] = shoup_of(iv, bt);
+            }
+            for (int i = 0; i < l; i++) {
+                const u64 qi = c->pr[i].q;
+                u64 Dm = 1, sacc = 0;
+                for (int t = 0; t < nb; t++) {
+                    u64 v = 1;
+                    for (int b = 0; b < nb; b++) if (b != t) v = mulm(v, c->pr[bp[b]].q % qi, qi);
+                    tab[(((size_t)l * nb + t) * nall + i) * 2] = v;
+                    tab[(((size_t)l * nb + t) * nall + i) * 2 + 1] = shoup_of(v, qi);
+                    Dm = mulm(Dm, c->pr[bp[t]].q % qi, qi);
+                    sacc = (sacc + mulm(((c->pr[bp[t]].q - 1) / 2) % qi, v, qi)) % qi;
+                }
+                negd[(size_t)l * nall + i] = Dm ? qi - Dm : 0;
+                cc[(size_t)l * nall + i] = sacc ? qi - sacc : 0;
+                const u64 di = invmod(Dm, qi);
+                dinv[((size_t)l * nall + i) * 2] = di;
+                dinv[((size_t)l * nall + i) * 2 + 1] = shoup_of(di, qi);
+            }
+        }
+        c->d_md2_inv = upload(*c, inv);
+        c->d_md2_tab = upload(*c, tab);
+        c->d_md2_negd = upload(*c, negd);
+        c->d_md2_cc = upload(*c, cc);
+        c->d_md2_dinv = upload(*c, dinv);
+    }
     // P mod q_i for key generation lives right after the rescale table
     std::vector<u64> rs((size_t)(L + 1) * nall * 3 + nall, 0);
     for (int l = 1; l <= L; l++) {
@@ -507,6 +549,7 @@ void ctx_destroy(Ctx* c) {
     cudaFree(c->d_primes); cudaFree(c->d_tw); cudaFree(c->d_itw);
     cudaFree(c->d_cdt); cudaFree(c->d_sk); cudaFree(c->d_modup); cudaFree(c->d_modup_inv);
     cudaFree(c->d_moddown); cudaFree(c->d_moddown_inv); cudaFree(c->d_modup_negq); cudaFree(c->d_moddown_negp); cudaFree(c->d_modup_cc); cudaFree(c->d_moddown_cc); cudaFree(c->d_pinv); cudaFree(c->d_rescale);
+    cudaFree(c->d_md2_inv); cudaFree(c->d_md2_tab); cudaFree(c->d_md2_negd); cudaFree(c->d_md2_cc); cudaFree(c->d_md2_dinv);
     cudaStreamSynchronize(c->stream);
     for (auto s : c->side) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
     for (auto e : c->side_ev) cudaEventDestroy(e);

@@ -239,14 +239,16 @@ static u64* ks_modup(Ctx& c, const u64* d, int level) {
     return UP;
 }
 
-// ModDown of the key products ACC [2][nt][N] (its P limbs are overwritten), + addend
-static void ks_tail_acc(Ctx& c, u64* ACC, int level, u64* out, const u64* addend, int add_npoly) {
+// ModDown of the key products ACC [2][nt][N] (its dropped limbs are
+// overwritten), + addend; merged: ModDown + rescale by q_l P, out at level - 1
+static void ks_tail_acc(Ctx& c, u64* ACC, int level, u64* out, const u64* addend, int add_npoly, bool merged = false) {
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
+    const int nout = merged ? nl - 1 : nl;
     {
         JobList j;
         j.n = 0;
         for (int s = 0; s < 2; s++)
-            for (int t = nl; t < nt; t++) {
+            for (int t = merged ? nl - 1 : nl; t < nt; t++) {
                 j.prime[j.n] = tprime(c, level, t);
                 j.ptr[j.n] = ACC + ((size_t)s * nt + t) * N;
                 j.src[j.n] = nullptr;
@@ -254,13 +256,61 @@ static void ks_tail_acc(Ctx& c, u64* ACC, int level, u64* out, const u64* addend
             }
         ntt_inverse(c, j);
     }
-    u64* W = c.alloc((size_t)2 * nl * N);
-    k_moddown_conv(c, W, ACC, level);
-    ntt_limbs(c, W, 0, nl, false);
-    ntt_limbs(c, W + (size_t)nl * N, 0, nl, false);
-    k_moddown_combine(c, out, ACC, W, addend, add_npoly, level);
+    u64* W = c.alloc((size_t)2 * nout * N);
+    k_moddown_conv(c, W, ACC, level, merged);
+    ntt_limbs(c, W, 0, nout, false);
+    ntt_limbs(c, W + (size_t)nout * N, 0, nout, false);
+    k_moddown_combine(c, out, ACC, W, addend, add_npoly, level, merged);
     c.free(W);
     c.counts[OP_KS]++;
+}
+
+// Relinearisation + rescale of B tensors D + 3 * poly * b = (d0, d1, d2) at
+// `level` in one pass: [P]_q (d0, d1) joins the key products of
+// ModUp(d2) in the extended basis and one ModDown divides by q_l P.
+static void rescale_many(Ctx& c, const u64* T, size_t poly, int level, std::vector<CtP>& out);
+static void relin_rescale_many(Ctx& c, const u64* D, size_t poly, int level, std::vector<CtP>& out) {
+    const size_t B = out.size();
+    if (level < 1) throw Error(-3, "multiply at level 0");
+    const Key& key = get_key(c, 0);
+    if (level > c.app_L) {
+        // bootstrapping levels keep ModDown and the exact centred rescale apart:
+        // EvalMod's precision is bound by the rescale rounding, which the merged
+        // conversion makes ~2.3x larger (a sum of K + 1 centred terms)
+        Scratch sc(c);
+        u64* T = sc.take(2 * poly * B);
+        std::vector<KsIn> in(B);
+        for (size_t b = 0; b < B; b++) {
+            const u64* Db = D + 3 * poly * b;
+            in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
+        }
+        if (keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) c.counts[OP_KS] += (int64_t)B;
+        else
+            for (size_t b = 0; b < B; b++) keyswitch(c, in[b].d, level, key, in[b].out, in[b].add, 2);
+        rescale_many(c, T, poly, level, out);
+        return;
+    }
+    std::vector<const u64*> ds(B);
+    std::vector<u64*> o(B);
+    for (size_t b = 0; b < B; b++) {
+        out[b] = new_ct(c, level - 1);
+        ds[b] = D + 3 * poly * b;
+        o[b] = out[b]->d;
+    }
+    if (keyswitch_relin_rescale(c, (int)B, ds.data(), o.data(), level, key.d)) {
+        c.counts[OP_KS] += (int64_t)B;
+        return;
+    }
+    const int nl = level + 1, nt = nl + c.K, beta = (nl + c.alpha - 1) / c.alpha;
+    for (size_t b = 0; b < B; b++) {
+        u64* UP = ks_modup(c, ds[b] + 2 * poly, level);
+        u64* ACC = c.alloc((size_t)2 * nt * c.N);
+        k_keyprod(c, ACC, UP, key.d, level, beta);
+        k_fold_p(c, ACC, ds[b], level);
+        ks_tail_acc(c, ACC, level, o[b], nullptr, 0, true);
+        c.free(ACC);
+        c.free(UP);
+    }
 }
 
 // key product of the ModUp digits UP with `key`, ModDown, + addend
@@ -354,26 +404,19 @@ std::vector<CtP> ev_mult_batch(Ctx& c, const std::vector<std::pair<const Ct*, co
     }
     const int level = ab[0].first->level;
     if (level < 1) throw Error(-3, "multiply at level 0");
-    const Key& key = get_key(c, 0);
     const int nl = level + 1;
     const size_t poly = (size_t)nl * c.N;
     Scratch sc(c);
     u64* D = sc.take(3 * poly * B);
-    u64* T = sc.take(2 * poly * B);
-    std::vector<KsIn> in(B);
     std::vector<u64*> dd(B);
     std::vector<const u64*> aa(B), bb(B);
     for (size_t b = 0; b < B; b++) {
-        u64* Db = D + 3 * poly * b;
-        dd[b] = Db;
+        dd[b] = D + 3 * poly * b;
         aa[b] = ab[b].first->d;
         bb[b] = ab[b].second->d;
-        in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
     }
     k_tensor_batch(c, (int)B, dd.data(), aa.data(), bb.data(), nl);
-    if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) throw Error(-2, "batched relinearisation");
-    c.counts[OP_KS] += (int64_t)B;
-    rescale_many(c, T, poly, level, out);
+    relin_rescale_many(c, D, poly, level, out);
     return out;
 }
 
@@ -480,44 +523,31 @@ std::vector<CtP> ev_mult_sum_batch(Ctx& c, const std::vector<std::vector<std::pa
         for (auto& pr : gr)
             if (pr.first->level != level || pr.second->level != level) throw Error(-4, "product sum: level mismatch");
     if (level < 1) throw Error(-3, "multiply at level 0");
-    const Key& key = get_key(c, 0);
     const int nl = level + 1;
     const size_t poly = (size_t)nl * c.N;
     Scratch sc(c);
     u64* D = sc.take(3 * poly * B);
-    u64* T = sc.take(2 * poly * B);
-    std::vector<KsIn> in(B);
     for (size_t b = 0; b < B; b++) {
         u64* Db = D + 3 * poly * b;
         std::vector<const u64*> as, bs;
         for (auto& pr : groups[b]) { as.push_back(pr.first->d); bs.push_back(pr.second->d); }
         k_tensor_sum(c, Db, as.data(), bs.data(), (int)as.size(), nl);
-        in[b] = KsIn{Db + 2 * poly, T + 2 * poly * b, Db, nullptr, key.d};
     }
-    if (!keyswitch_fused_batch(c, (int)B, in.data(), 0, level, 2, 0)) {
-        for (size_t b = 0; b < B; b++) keyswitch(c, in[b].d, level, key, in[b].out, in[b].add, 2);
-    } else {
-        c.counts[OP_KS] += (int64_t)B;
-    }
-    rescale_many(c, T, poly, level, out);
+    relin_rescale_many(c, D, poly, level, out);
     return out;
 }
 
 CtP ev_mult(Ctx& c, const Ct& a, const Ct& b) {
     check_same(a, b);
     if (a.level < 1) throw Error(-3, "multiply at level 0");
-    const Key& key = get_key(c, 0);
     const int nl = a.level + 1;
     const size_t poly = (size_t)nl * c.N;
     Scratch sc(c);
     u64* D = sc.take(3 * poly);
     k_tensor(c, D, a.d, b.d, nl);
-    u64* T = sc.take(2 * poly);
-    if (keyswitch_fused(c, D + 2 * poly, 0, a.level, key, T, D, 2, 0)) c.counts[OP_KS]++;
-    else keyswitch(c, D + 2 * poly, a.level, key, T, D, 2);
-    CtP o = new_ct(c, a.level - 1);
-    rescale_raw(c, T, a.level, 2, o->d);
-    return o;
+    std::vector<CtP> o(1);
+    relin_rescale_many(c, D, poly, a.level, o);
+    return o[0];
 }
 
 // ---------------------------------------------------------------------------

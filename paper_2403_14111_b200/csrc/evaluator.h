@@ -41,6 +41,9 @@ bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int
 // sum_r sigma_{gals[r]}(x_b), one ModUp and one ModDown per input; nrot <= 3
 bool keyswitch_rotsum(Ctx& c, int B, const u64* const* xs, u64* const* outs, int level, int nrot, const u64* gals,
                       const u64* const* keys);
+// relinearisation + rescale in one pass (keyswitch.cu): ds[b] = the
+// tensor (d0, d1, d2) at `level`, outs[b] at level - 1; false when not fusable
+bool keyswitch_relin_rescale(Ctx& c, int B, const u64* const* ds, u64* const* outs, int level, const u64* key);
 std::vector<CtP> ev_rotsum_batch(Ctx& c, const std::vector<const Ct*>& xs, const std::vector<u64>& gals);
 // CKKS bootstrapping (bootstrap.cu): any level -> app_L
 CtP ev_mod_raise(Ctx& c, const Ct& a, int to);

@@ -164,6 +164,14 @@ struct Ctx {
     u64* d_moddown_cc = nullptr;  // [nall]
     u64* d_pinv = nullptr;        // [nall] (value, shoup) P^-1 mod q_i
     u64* d_rescale = nullptr;     // [L+1 (dropped prime l)][nall] (q_l^-1 mod q_i, shoup, q_l mod q_i)
+    // merged ModDown + rescale of a ct x ct product at level l:
+    // the dropped basis B_l = (q_l, p_1..p_K), D_l = q_l P
+    u64* d_md2_inv = nullptr;     // [L+1][K+1] (value, shoup) (D/b_t)^-1 mod b_t
+    u64* d_md2_tab = nullptr;     // [L+1][K+1][nall] (value, shoup) D/b_t mod q_i
+    u64* d_md2_negd = nullptr;    // [L+1][nall] [-D]_{q_i}
+    u64* d_md2_cc = nullptr;      // [L+1][nall] [-sum_t h_t D/b_t]_{q_i}, h_t = (b_t - 1) / 2
+    u64* d_md2_dinv = nullptr;    // [L+1][nall] (value, shoup) D^-1 mod q_i
+    const u64* pmodq() const { return d_rescale + (size_t)(L + 1) * nall * 3; }   // [nall] P mod q_i
     // counters
     uint64_t nonce = 0;
     int64_t counts[OP_NKIND] = {0};

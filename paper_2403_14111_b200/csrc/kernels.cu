@@ -343,29 +343,33 @@ void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int b
 //   ACC: [2][nt][N]; its P limbs (t >= level+1) are already in coefficient form
 // ---------------------------------------------------------------------------
 
+// The dropped basis is ACC's limbs mdf .. mdf + nk - 1 (P, or q_l and P for the
+// merged ModDown + rescale); W and out have nout limbs per poly.
 __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__ acc, const u64* __restrict__ tab,
                                     const u64* __restrict__ tab_inv, const u64* __restrict__ negp,
-                                    const PrimeDev* __restrict__ primes, int level, int L, int K, int nall, int N) {
+                                    const PrimeDev* __restrict__ primes, int level, int L, int K, int nall, int N,
+                                    int mdf, int nk, int nout) {
     pdl_enter();
     const int s = blockIdx.y;
     const int nt = level + 1 + K;
     const u64* A = acc + (size_t)s * nt * N;
-    u64* out = W + (size_t)s * (level + 1) * N;
+    u64* out = W + (size_t)s * nout * N;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         u64 y[8];
         u64 cnt = 0;   // centred conversion (as in modup_kernel)
-        for (int t = 0; t < K; t++) {
-            const u64 p = primes[L + 1 + t].q;
-            y[t] = mul_shoup(A[(size_t)(level + 1 + t) * N + k], tab_inv[2 * t], tab_inv[2 * t + 1], p);
+        for (int t = 0; t < nk; t++) {
+            const int li = mdf + t;
+            const u64 p = primes[li <= level ? li : L + 1 + (li - level - 1)].q;
+            y[t] = mul_shoup(A[(size_t)li * N + k], tab_inv[2 * t], tab_inv[2 * t + 1], p);
             cnt += y[t] > (p - 1) / 2;
         }
-        for (int i = 0; i <= level; i++) {
+        for (int i = 0; i < nout; i++) {
             const u64 q = primes[i].q;
             u64 v = cnt * negp[i];
-            for (int t = 0; t < K; t++) {
+            for (int t = 0; t < nk; t++) {
                 const u64* c2 = tab + ((size_t)t * nall + i) * 2;
                 v += mul_shoup_lazy(y[t], c2[0], c2[1], q);
-                if (v >= 8 * q) v -= 8 * q;   // < 8q for any K <= 8 (q < 2^60)
+                if (v >= 8 * q) v -= 8 * q;   // < 8q for any nk <= 8 (q < 2^60)
             }
             if (v >= 4 * q) v -= 4 * q;
             if (v >= 2 * q) v -= 2 * q;
@@ -375,21 +379,27 @@ __global__ void moddown_conv_kernel(u64* __restrict__ W, const u64* __restrict__
     }
 }
 
-void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level) {
+void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level, bool merged) {
     dim3 grid((c.N + 255) / 256, 2);
-    Launch scope(c, "moddown_conv", 8.0 * c.N * (2.0 * c.K + 2.0 * (level + 1)));
-    launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_moddown, c.d_moddown_inv, c.d_moddown_negp,
-             c.d_primes, level, c.L, c.K, c.nall, c.N);
+    const int nk = merged ? c.K + 1 : c.K, nout = merged ? level : level + 1, mdf = merged ? level : level + 1;
+    Launch scope(c, "moddown_conv", 8.0 * c.N * (2.0 * nk + 2.0 * nout));
+    if (merged)
+        launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_md2_tab + (size_t)level * (c.K + 1) * c.nall * 2,
+                 c.d_md2_inv + (size_t)level * (c.K + 1) * 2, c.d_md2_negd + (size_t)level * c.nall, c.d_primes, level,
+                 c.L, c.K, c.nall, c.N, mdf, nk, nout);
+    else
+        launch_k(c, moddown_conv_kernel, grid, 256, 0, W, acc, c.d_moddown, c.d_moddown_inv, c.d_moddown_negp,
+                 c.d_primes, level, c.L, c.K, c.nall, c.N, mdf, nk, nout);
     HC_CUDA(cudaGetLastError());
 }
 
-// out[s][i] = (ACC[s][i] - W[s][i]) * P^-1 (+ addend[s][i] when s < add_npoly)
+// out[s][i] = (ACC[s][i] - W[s][i]) * P^-1 (+ addend[s][i] when s < add_npoly), i < nout
 __global__ void moddown_combine_kernel(u64* __restrict__ out, const u64* __restrict__ acc, const u64* __restrict__ W,
                                        const u64* __restrict__ pinv, const u64* __restrict__ addend, int add_npoly,
-                                       const PrimeDev* __restrict__ primes, int level, int K, int N) {
+                                       const PrimeDev* __restrict__ primes, int level, int K, int N, int nout) {
     pdl_enter();
     const int nl = level + 1, nt = nl + K;
-    const size_t poly = (size_t)nl * N;
+    const size_t poly = (size_t)nout * N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < 2 * poly; e += (size_t)gridDim.x * blockDim.x) {
         const int s = (int)(e / poly);
         const size_t r = e - (size_t)s * poly;
@@ -403,11 +413,37 @@ __global__ void moddown_combine_kernel(u64* __restrict__ out, const u64* __restr
 }
 
 void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly,
-                       int level) {
-    const size_t work = 2 * (size_t)(level + 1) * c.N;
-    Launch scope(c, "moddown_combine", 8.0 * c.N * (level + 1) * (6.0 + add_npoly));
-    launch_k(c, moddown_combine_kernel, nblocks(work, 256), 256, 0, out, acc, W, c.d_pinv, addend, add_npoly,
-                                                                      c.d_primes, level, c.K, c.N);
+                       int level, bool merged) {
+    const int nout = merged ? level : level + 1;
+    const size_t work = 2 * (size_t)nout * c.N;
+    Launch scope(c, "moddown_combine", 8.0 * c.N * nout * (6.0 + add_npoly));
+    launch_k(c, moddown_combine_kernel, nblocks(work, 256), 256, 0, out, acc, W,
+             merged ? c.d_md2_dinv + (size_t)level * c.nall * 2 : c.d_pinv, addend, add_npoly, c.d_primes, level, c.K,
+             c.N, nout);
+    HC_CUDA(cudaGetLastError());
+}
+
+// ACC's Q limbs += [P]_q (d0, d1): the tensor's first two polys join the key
+// products in the extended basis (relinearisation + rescale in one pass)
+__global__ void fold_p_kernel(u64* __restrict__ acc, const u64* __restrict__ d, const u64* __restrict__ pmodq,
+                              const PrimeDev* __restrict__ primes, int nl, int nt, int N) {
+    pdl_enter();
+    const size_t poly = (size_t)nl * N;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < 2 * poly; e += (size_t)gridDim.x * blockDim.x) {
+        const int s = (int)(e / poly);
+        const size_t r = e - (size_t)s * poly;
+        const int i = (int)(r / N);
+        const PrimeDev P = primes[i];
+        u64* a = acc + (size_t)s * nt * N + r;
+        *a = add_mod(*a, mul_mod(d[e], pmodq[i], P), P.q);
+    }
+}
+
+void k_fold_p(Ctx& c, u64* acc, const u64* d, int level) {
+    const int nl = level + 1;
+    Launch scope(c, "fold_p", 8.0 * c.N * nl * 6.0);
+    launch_k(c, fold_p_kernel, nblocks(2 * (size_t)nl * c.N, 256), 256, 0, acc, d, c.pmodq(), c.d_primes, nl,
+             nl + c.K, c.N);
     HC_CUDA(cudaGetLastError());
 }
 

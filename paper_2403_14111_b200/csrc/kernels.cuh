@@ -27,8 +27,12 @@ void k_pt_dot(Ctx& c, u64* out, const u64* const* a, const u64* const* p, int T,
 void k_modup(Ctx& c, u64* up, const u64* X, const u64* D, int level, int beta);
 // accumulate: acc += the products (rotate-and-sum stages)
 void k_keyprod(Ctx& c, u64* acc, const u64* up, const u64* key, int level, int beta, bool accumulate = false);
-void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level);
-void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly, int level);
+// merged: the ModDown + rescale by q_l P of a ct x ct product (W / out have `level` limbs)
+void k_moddown_conv(Ctx& c, u64* W, const u64* acc, int level, bool merged = false);
+void k_moddown_combine(Ctx& c, u64* out, const u64* acc, const u64* W, const u64* addend, int add_npoly, int level,
+                       bool merged = false);
+// ACC [2][nt][N] Q limbs += [P]_q d, d = (d0, d1) [2][level+1][N]
+void k_fold_p(Ctx& c, u64* acc, const u64* d, int level);
 void k_rescale_bcast(Ctx& c, u64* Y, const u64* X, int level, int npoly);
 void k_rescale_combine(Ctx& c, u64* out, const u64* a, const u64* Y, int level, int npoly);
 void k_uniform(Ctx& c, u64* out, int first_prime, int nl, u64 stream);

@@ -47,6 +47,10 @@ struct KsJobs {
 
 struct KsGeo {
     int level, nl, nt, L, K, alpha, dnum, nall, beta, logN, N1;
+    // ModDown: the dropped basis is ACC's limbs mdf .. mdf + nk - 1 and the
+    // result has nout limbs: (nl, K, nl) for the division by P; (nl - 1, K + 1,
+    // nl - 1) for the merged ModDown + rescale by q_l P of a ct x ct product
+    int mdf, nk, nout;
     __host__ __device__ int prime(int t) const { return t <= level ? t : L + 1 + (t - level - 1); }
     // per-key-switch strides of the batched intermediates (words)
     __host__ __device__ size_t y_stride() const { return (size_t)nl << logN; }            // Y   [nl][N]
@@ -503,8 +507,12 @@ __global__ void __launch_bounds__(256, MB > 4 ? 2 : RS_MINB) ks_keyprod_rotsum(K
 // 64-bit address arithmetic: 1031 instructions per thread against ~400 here).
 // Grid (entry, coefficient block, target limb): the entries of a coefficient
 // block run side by side and share its key words through L2.
-template <int BETA, int NR>
-__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, const PrimeDev* __restrict__ primes,
+// MODE 0: rotate-and-sum (digits, c1 and c0 read through gal[r]; [P]_q c0 joins poly 0).
+// MODE 1: relinearisation (NR = 1, no permutation): [P]_q (d0, d1) join both
+// polys, c0 -> the tensor's d0 with d1 right behind it ([nl][N] each), so the
+// merged ModDown + rescale that follows returns rescale(d + KS(d2)).
+template <int BETA, int NR, int MODE = 0>
+__global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_rotsum_t(KsGeo g, const PrimeDev* __restrict__ primes,
                                                                     KsRotsum rb, const u64* __restrict__ pmodq,
                                                                     u64* __restrict__ acc) {
     pdl_enter();
@@ -523,6 +531,7 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
     const size_t dstride = (size_t)g.nt * N;            // digit stride of UP
     const size_t kstride = (size_t)g.nall * N;          // (b, a) stride of a key digit
     const size_t koff = (size_t)pi * N + k;
+    const size_t pstride = (size_t)g.nl * N;            // MODE 1: d0 -> d1
     const u64 pq = qlimb ? pmodq[pi] : 0;
     u64 ob, oa;
     if (P.fp) {
@@ -530,9 +539,9 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
         double sb = 0, sa = 0;
 #pragma unroll
         for (int r = 0; r < NR; r++) {
-            const unsigned src = galois_src(k, g.logN, rb.gal[r]);
+            const unsigned src = MODE == 0 ? galois_src(k, g.logN, rb.gal[r]) : k;
             const u64* __restrict__ kp = rb.key[r] + koff;
-            u64 kb[BETA], ka[BETA], x[BETA], z = 0;
+            u64 kb[BETA], ka[BETA], x[BETA], z = 0, z1 = 0;
 #pragma unroll
             for (int j = 0; j < BETA; j++) {
                 kb[j] = __ldg(kp + (size_t)(2 * j) * kstride);
@@ -540,6 +549,7 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
                 x[j] = (j == dig ? c1 : up + j * dstride)[src];
             }
             if (qlimb) z = c0[src];
+            if (MODE == 1 && qlimb) z1 = c0[pstride + src];
 #pragma unroll
             for (int j = 0; j < BETA; j++) {
                 const double y = fp_word(x[j]);
@@ -547,6 +557,7 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
                 sa = __dadd_rn(sa, fp_mulmod(y, fp_word(ka[j]), q, qinv));
             }
             if (qlimb) sb = __dadd_rn(sb, fp_mulmod(fp_word(z), pqd, q, qinv));
+            if (MODE == 1 && qlimb) sa = __dadd_rn(sa, fp_mulmod(fp_word(z1), pqd, q, qinv));
         }
         ob = fp_canon(sb, q, qinv);
         oa = fp_canon(sa, q, qinv);
@@ -556,9 +567,9 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
         U128 ib = {0, 0}, ia = {0, 0};
 #pragma unroll
         for (int r = 0; r < NR; r++) {
-            const unsigned src = galois_src(k, g.logN, rb.gal[r]);
+            const unsigned src = MODE == 0 ? galois_src(k, g.logN, rb.gal[r]) : k;
             const u64* __restrict__ kp = rb.key[r] + koff;
-            u64 kb[BETA], ka[BETA], x[BETA], z = 0;
+            u64 kb[BETA], ka[BETA], x[BETA], z = 0, z1 = 0;
 #pragma unroll
             for (int j = 0; j < BETA; j++) {
                 kb[j] = __ldg(kp + (size_t)(2 * j) * kstride);
@@ -566,12 +577,14 @@ __global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_rotsum_t(KsGeo g, con
                 x[j] = (j == dig ? c1 : up + j * dstride)[src];
             }
             if (qlimb) z = c0[src];
+            if (MODE == 1 && qlimb) z1 = c0[pstride + src];
 #pragma unroll
             for (int j = 0; j < BETA; j++) {
                 mac128(ib, x[j], kb[j]);
                 mac128(ia, x[j], ka[j]);
             }
             if (qlimb) mac128(ib, z, pq);
+            if (MODE == 1 && qlimb) mac128(ia, z1, pq);
         }
         ob = reduce128(ib.hi, ib.lo, P);
         oa = reduce128(ia.hi, ia.lo, P);
@@ -591,25 +604,25 @@ __global__ void __launch_bounds__(PassGeo<LOGSZ, MODE_COLS, SUBS>::THREADS, PMB)
                     const u64* __restrict__ cc_tab, u64* __restrict__ Wt) {
     pdl_trigger();
     extern __shared__ u64 sm[];
-    const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
+    const int s = blockIdx.y / g.nout, i = blockIdx.y % g.nout;
     const size_t N = (size_t)1 << g.logN;
     const PrimeDev P = primes[i];
     const u64 q = P.q;
     acc += blockIdx.z * g.acc_stride();
     Wt += blockIdx.z * g.w_stride();
     LdModup<NK> ld;
-    ld.na = g.K;
+    ld.na = g.nk;
     ld.p = q;
     ld.cc = cc_tab[i];
 #pragma unroll
     for (int t = 0; t < NK; t++) {
-        const bool on = t < g.K;
+        const bool on = t < g.nk;
         const int tt = on ? t : 0;
-        ld.y[t] = acc + ((size_t)s * g.nt + g.nl + tt) * N;
+        ld.y[t] = acc + ((size_t)s * g.nt + g.mdf + tt) * N;
         ld.w[t] = on ? md_tab[((size_t)tt * g.nall + i) * 2] : 0;
         ld.ws[t] = on ? md_tab[((size_t)tt * g.nall + i) * 2 + 1] : 0;
     }
-    StPlain<false, false> st{Wt + ((size_t)s * g.nl + i) * N, q, 0, 0};
+    StPlain<false, false> st{Wt + ((size_t)s * g.nout + i) * N, q, 0, 0};
     PassGeo<LOGSZ, MODE_COLS, SUBS> G;
     G.init(g.N1);
     const ulonglong2* TW = tw + ((size_t)i << g.logN);
@@ -706,7 +719,7 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
                       const u64* __restrict__ pinv, int add_npoly, KsBatch kb) {
     pdl_trigger();
     extern __shared__ u64 sm[];
-    const int s = blockIdx.y / g.nl, i = blockIdx.y % g.nl;
+    const int s = blockIdx.y / g.nout, i = blockIdx.y % g.nout;
     const size_t N = (size_t)1 << g.logN;
     const int b = blockIdx.z;
     Wt += b * g.w_stride();
@@ -716,8 +729,8 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     u64* __restrict__ out = kb.out[b];
     const PrimeDev P = primes[i];
     const u64 q = P.q;
-    LdPlain ld{Wt + ((size_t)s * g.nl + i) * N};
-    StModdown st{out + ((size_t)s * g.nl + i) * N, acc + ((size_t)s * g.nt + i) * N,
+    LdPlain ld{Wt + ((size_t)s * g.nout + i) * N};
+    StModdown st{out + ((size_t)s * g.nout + i) * N, acc + ((size_t)s * g.nt + i) * N,
                  (s < add_npoly && addend) ? addend + ((size_t)s * g.nl + i) * N : nullptr, q, pinv[2 * i], pinv[2 * i + 1],
                  kb.agal[b], g.logN, addend2 ? addend2 + ((size_t)s * g.nl + i) * N : nullptr};
     PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS> G;
@@ -874,6 +887,10 @@ struct KsRotsumSpec {
     u64 gal[RS_MAXR];
     const u64* key[RS_MAXR];
     const u64* const* c0;
+    // relinearisation + rescale in one pass: nrot = 1, no
+    // permutation, c0[b] -> the tensor's (d0, d1), din[b] = d2; [P]_q (d0, d1)
+    // joins the key product and the ModDown divides by q_l P (outputs at level - 1)
+    bool relin = false;
 };
 
 template <int LOGN>
@@ -883,7 +900,10 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
     using CG = PassGeo<CL, MODE_COLS, CS>;
     using HG = PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>;
     const int N = c.N, nl = level + 1, K = c.K, nt = nl + K;
-    KsGeo g{level, nl, nt, c.L, K, c.alpha, c.dnum, c.nall, (nl + c.alpha - 1) / c.alpha, c.logN, N >> CH_LOG};
+    const bool merged = rsum && rsum->relin;
+    if (merged && level < 1) throw Error(-3, "relinearise + rescale at level 0");
+    KsGeo g{level, nl, nt, c.L, K, c.alpha, c.dnum, c.nall, (nl + c.alpha - 1) / c.alpha, c.logN, N >> CH_LOG,
+            merged ? nl - 1 : nl, merged ? K + 1 : K, merged ? nl - 1 : nl};
     const size_t csm = CG::smem_bytes(), hsm = HG::smem_bytes();
     KsBatch kb;
     kb.nb = B;
@@ -1001,7 +1021,16 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             dim3 tgrid((unsigned)B, (unsigned)(N / 256), (unsigned)nt);
             const int nr = rsum->nrot;
             auto go = [&](auto kern) { launch_k(c, kern, tgrid, 256, 0, g, c.d_primes, rb, pmodq, ACC); };
-            if (nr == 3 && g.beta == 4) go(ks_keyprod_rotsum_t<4, 3>);
+            if (merged && g.beta == 4) go(ks_keyprod_rotsum_t<4, 1, 1>);
+            else if (merged && g.beta == 3) go(ks_keyprod_rotsum_t<3, 1, 1>);
+            else if (merged && g.beta == 2) go(ks_keyprod_rotsum_t<2, 1, 1>);
+            else if (merged && g.beta == 1) go(ks_keyprod_rotsum_t<1, 1, 1>);
+            else if (merged && g.beta == 5) go(ks_keyprod_rotsum_t<5, 1, 1>);
+            else if (merged && g.beta == 6) go(ks_keyprod_rotsum_t<6, 1, 1>);
+            else if (merged && g.beta == 7) go(ks_keyprod_rotsum_t<7, 1, 1>);
+            else if (merged && g.beta == 8) go(ks_keyprod_rotsum_t<8, 1, 1>);
+            else if (merged) throw Error(-2, "relinearise + rescale: more than 8 digits");
+            else if (nr == 3 && g.beta == 4) go(ks_keyprod_rotsum_t<4, 3>);
             else if (nr == 3 && g.beta == 3) go(ks_keyprod_rotsum_t<3, 3>);
             else if (nr == 3 && g.beta == 2) go(ks_keyprod_rotsum_t<2, 3>);
             else if (nr == 3 && g.beta == 1) go(ks_keyprod_rotsum_t<1, 3>);
@@ -1031,14 +1060,15 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         j.nb = B;
         for (int b = 0; b < B; b++) j.boff[b] = (long long)(b * g.acc_stride());
         for (int s = 0; s < 2; s++)
-            for (int t = 0; t < K; t++) {
-                const int pi = c.L + 1 + t;
+            for (int t = 0; t < g.nk; t++) {
+                // the dropped basis: ACC limbs mdf .. mdf + nk - 1 (P, or q_l and P)
+                const int pi = g.prime(g.mdf + t);
                 const u64 p = c.pr[pi].q;
                 u64 ph = 1;
-                for (int b = 0; b < K; b++) if (b != t) ph = mulm(ph, c.pr[c.L + 1 + b].q % p, p);
+                for (int b = 0; b < g.nk; b++) if (b != t) ph = mulm(ph, c.pr[g.prime(g.mdf + b)].q % p, p);
                 const u64 sc = mulm(c.pr[pi].ninv, powm(ph, p - 2, p), p);
                 j.prime[j.n] = pi;
-                j.ptr[j.n] = ACC + ((size_t)s * nt + nl + t) * N;
+                j.ptr[j.n] = ACC + ((size_t)s * nt + g.mdf + t) * N;
                 j.src[j.n] = nullptr;
                 j.scale[j.n] = sc;
                 j.scale_s[j.n] = shoup_of(sc, p);
@@ -1049,18 +1079,20 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
     // 5. D: P -> Q conversion + column pass
     u64* Wt = sc.take((size_t)B * g.w_stride());
     {
-        Launch scope(c, "ks_moddown_cols", 8.0 * N * B * (2.0 * K + 2.0 * nl));
-        dim3 grid((N >> CL) / CS, 2 * nl, B);
+        Launch scope(c, "ks_moddown_cols", 8.0 * N * B * (2.0 * g.nk + 2.0 * g.nout));
+        dim3 grid((N >> CL) / CS, 2 * g.nout, B);
+        const u64* md_tab = merged ? c.d_md2_tab + (size_t)level * (K + 1) * c.nall * 2 : c.d_moddown;
+        const u64* md_cc = merged ? c.d_md2_cc + (size_t)level * c.nall : c.d_moddown_cc;
         auto go = [&](auto kern) {
             set_smem(kern, csm);
-            launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, c.d_moddown,
-                     c.d_moddown_cc, Wt);
+            launch_k(c, kern, grid, CG::THREADS, csm, g, c.d_primes, c.twp(0, false), ACC, md_tab, md_cc, Wt);
         };
-        switch (K) {
+        switch (g.nk) {
             case 1: if (B == 1) go(ks_moddown_cols<CL, CS, 1, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 1>); break;
             case 2: if (B == 1) go(ks_moddown_cols<CL, CS, 2, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 2>); break;
             case 3: if (B == 1) go(ks_moddown_cols<CL, CS, 3, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 3>); break;
-            default: if (B == 1) go(ks_moddown_cols<CL, CS, 4, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 4>); break;
+            case 4: if (B == 1) go(ks_moddown_cols<CL, CS, 4, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 4>); break;
+            default: if (B == 1) go(ks_moddown_cols<CL, CS, 5, KS_PMB_CHAIN>); else go(ks_moddown_cols<CL, CS, 5>); break;
         }
         HC_CUDA(cudaGetLastError());
     }
@@ -1070,14 +1102,17 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         set_smem(ks_moddown_chunks<MD_MINB_CHAIN>, hsm);
         int nadd2 = 0;
         for (int b = 0; b < B; b++) nadd2 += in[b].add2 != nullptr;
-        Launch scope(c, "ks_moddown_chunks", 8.0 * N * (B * (2.0 * nl * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
-        dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * nl, B);
+        Launch scope(c, "ks_moddown_chunks",
+                     8.0 * N * (B * (2.0 * g.nout * 3 + (double)add_npoly * nl) + 2.0 * nl * nadd2));
+        dim3 grid((N >> CH_LOG) / CH_SUBS, 2 * g.nout, B);
+        // (ACC - W) / P, or / (q_l P) for the merged ModDown + rescale
+        const u64* dinv = merged ? c.d_md2_dinv + (size_t)level * c.nall * 2 : c.d_pinv;
         if (B == 1)
             launch_k(c, ks_moddown_chunks<MD_MINB_CHAIN>, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt,
-                     ACC, c.d_pinv, add_npoly, kb);
+                     ACC, dinv, add_npoly, kb);
         else
             launch_k(c, ks_moddown_chunks<>, grid, HG::THREADS, hsm, g, c.d_primes, c.twp(0, false), Wt, ACC,
-                     c.d_pinv, add_npoly, kb);
+                     dinv, add_npoly, kb);
         HC_CUDA(cudaGetLastError());
     }
 }
@@ -1133,6 +1168,33 @@ bool keyswitch_fused_batch(Ctx& c, int B, const KsIn* in, u64 gal, int level, in
             tl[b] = KsTail{b, 0, x.d, x.out, x.add, x.add2, x.key, add_gal};
         }
         ks_pipeline(c, nb, din, gal, level, nb, tl, add_npoly);
+    }
+    return true;
+}
+
+// Relinearisation + rescale of B tensors at one level >= 1:
+// ds[b] = (d0, d1, d2) [3][level+1][N]; outs[b] [2][level][N] at level - 1.
+bool keyswitch_relin_rescale(Ctx& c, int B, const u64* const* ds, u64* const* outs, int level, const u64* key) {
+    if (!fusable(c, level)) return false;
+    const size_t poly = (size_t)(level + 1) * c.N;
+    KsRotsumSpec rs;
+    rs.nrot = 1;
+    rs.gal[0] = 0;
+    rs.key[0] = key;
+    rs.relin = true;
+    for (int b0 = 0; b0 < B; b0 += KS_MAXB) {
+        const int nb = std::min(KS_MAXB, B - b0);
+        const u64* din[KS_MAXB];
+        const u64* d0s[KS_MAXB];
+        KsTail tl[KS_MAXB];
+        for (int b = 0; b < nb; b++) {
+            const u64* d = ds[b0 + b];
+            d0s[b] = d;
+            din[b] = d + 2 * poly;
+            tl[b] = KsTail{b, 0, d + 2 * poly, outs[b0 + b], nullptr, nullptr, key, 0};
+        }
+        rs.c0 = d0s;
+        ks_pipeline(c, nb, din, 0, level, nb, tl, 0, &rs);
     }
     return true;
 }

@@ -449,7 +449,12 @@ def test_config3_softmax_full_size(golden):
     _same_grid(out, ref)
     assert _ledger(g) == list(golden["cfg3_led"])
     got = P.decode(out, tol=1e-3)
-    assert np.max(np.abs(got - golden["cfg3_out"])) < 1e-3          # vs the reference emulator
+    # vs the reference emulator (noise-free): CKKS noise through the inverse's
+    # ~1/y^2 conditioning; over key / encryption seeds 3..8 the worst of the
+    # 1280 outputs measured 4.5e-4 .. 1.3e-3 at an rms of 4..7e-5
+    # (scripts/softmax_noise.py), so 2e-3 bounds the tail, 2e-4 the rms
+    diff = np.abs(got - golden["cfg3_out"])
+    assert diff.max() < 2e-3 and np.sqrt((diff ** 2).mean()) < 2e-4
     assert np.max(np.abs(got - S.exact_softmax(Z))) < 0.0097         # PAPER.md:1071 (c=10)
 
 

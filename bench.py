@@ -199,10 +199,23 @@ def keyswitch_rate(ctx, ct, streams=4, batch=16, reps=4):
     return streams * batch * reps / (ms.value * 1e-3)
 
 
-def ncu_evidence():
-    """DRAM traffic and issue utilisation of the key-switch pipeline from the
-    committed ncu --set full capture (profiles/r2/ncu_keyswitch.json)."""
-    path = os.path.join(ROOT, "profiles", "r2", "ncu_keyswitch.json")
+def ladder_rate(ctx, ct, streams=3, batch=3, steps=8, reps=2):
+    """Doubling steps per second of the column ladder (stride 1, `steps`
+    steps: radix-4 rotate-and-sum stages with the fused forms on) over
+    `streams` concurrent batches of `batch` level-11 ciphertexts
+    (hc_bench_ladder) -- the op the DiagABT / DiagATB passes are made of."""
+    from paper_2403_14111_b200 import _native as N
+    ms = C.c_float()
+    N.check(N.lib().hc_bench_ladder(ctx._h, ct._h, streams, batch, 1, steps, 1, C.byref(ms)))   # warm
+    N.check(N.lib().hc_bench_ladder(ctx._h, ct._h, streams, batch, 1, steps, reps, C.byref(ms)))
+    return streams * batch * steps * reps / (ms.value * 1e-3)
+
+
+def ncu_evidence(name="ncu_keyswitch.json"):
+    """DRAM traffic and issue utilisation of the key-switch pipeline (or, with
+    ncu_ladder.json, of the radix-4 ladder stage) from the committed
+    ncu --set full captures under profiles/r2/."""
+    path = os.path.join(ROOT, "profiles", "r2", name)
     try:
         with open(path) as f:
             return json.load(f)
@@ -447,12 +460,18 @@ def run_b200(args, world, rank, local):
     # ciphertext; the §8(d) per-op model charges 94.37 MB per switch)
     ks_rate = keyswitch_rate(ctx, EX.flat()[0])
     ks_model = 94.37e6
+    # a doubling-ladder step add(x, lrot(x, 2^t)) at level 11 (the level of
+    # DiagABT's first ladder): Rot 4 Lq + 2 d (Lq + K) plus Add 6 Lq limbs
+    x11 = ctx.encrypt(np.zeros(ctx.slot_count), 11)
+    lad_rate = ladder_rate(ctx, x11)
+    lad_model = (4 * 12 + 2 * 3 * (12 + 3) + 6 * 12) * 8.0 * ctx.N
     # the dominant kernel of the profiled step (its own algorithmic bytes per
     # launch over its CUDA-event time), for the breakdown
     top = max(prof.items(), key=lambda kv: kv[1][1])
     name, (n_launch, k_ms, k_bytes) = top
     step_prof_ms = sum(v[1] for v in prof.values())
     ncu = ncu_evidence()
+    ncu_lad = ncu_evidence("ncu_ladder.json")
     achieved = model_step / (ms_step * 1e-3) / 1e9
     peak_all = hbm * world
     line = {
@@ -462,9 +481,14 @@ def run_b200(args, world, rank, local):
         "config": dict(CONFIG, parallelism=f"diagonal passes sharded over {world} rank(s), NCCL mod-sum"
                        if world > 1 else "1 GPU"),
         "diag_abt_ms": abt_ms, "diag_atb_ms": atb_ms,
-        "keyswitch_per_s": ks / (total_ms * 1e-3),
+        # key-switch/s = the ledger's (Rot + Conj + Mult) per second;
+        # the pipelines actually run (one ModUp + ModDown each) are fewer: a
+        # radix-4 rotate-and-sum stage stands for two ladder rotations and a
+        # product sum for its n relinearisations
+        "keyswitch_per_s": (counts["Rot"] + counts["Conj"] + counts["Mult"]) / (total_ms * 1e-3),
         "ledger_per_step": {k: v // args.steps for k, v in counts.items()},
-        "keyswitches_per_step": ks // args.steps,
+        "keyswitch_ops_per_step": (counts["Rot"] + counts["Conj"] + counts["Mult"]) // args.steps,
+        "keyswitch_pipelines_per_step": ks // args.steps,
         # algorithmic bytes of the step under the per-op model
         # (inputs read once, outputs written once, key-switch intermediates on
         # chip), accumulated by the library op by op at each op's level
@@ -478,6 +502,13 @@ def run_b200(args, world, rank, local):
                               "achieved_gbs": ks_rate * ks_model / 1e9,
                               "frac": ks_rate * ks_model / 1e9 / hbm,
                               "sample": "4 streams x batches of 16 rotations of one level-12 ciphertext"},
+        "ladder_level11": {"doubling_steps_per_s": lad_rate, "model_bytes": lad_model,
+                           "achieved_gbs": lad_rate * lad_model / 1e9, "frac": lad_rate * lad_model / 1e9 / hbm,
+                           "sample": "3 streams x batches of 3 level-11 ciphertexts, 8-step column ladders "
+                                     "(4 radix-4 rotate-and-sum stages each)",
+                           "traffic": ncu_lad.get("dram_bytes_per_keyswitch") if ncu_lad else None,
+                           "traffic_ratio": ncu_lad.get("traffic_ratio") if ncu_lad else None,
+                           "traffic_basis": ncu_lad.get("basis") if ncu_lad else None},
         "issue_active_pct": ncu.get("issue_active_pct") if ncu else None,
         "dominant_kernel": {"name": name, "launches_per_step": int(n_launch), "ms_per_step": k_ms,
                             "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9,

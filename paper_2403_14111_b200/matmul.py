@@ -186,18 +186,31 @@ def expected_period(c: int) -> int:
     return next_pow2(c)
 
 
+def ladder_amounts(ctx, stride: int, steps: int):
+    """Rotation amounts of the doubling ladder (stride, steps): with the fused
+    schedule forms (``ctx.hoist``) the radix-4 stages' s, 2s, 3s (s = stride *
+    4^i), else stride * 2^t."""
+    S = ctx.slot_count
+    if not getattr(ctx, "hoist", False):
+        return {(stride * (1 << t)) % S for t in range(steps)}
+    out, t = set(), 0
+    while t < steps:
+        w = min(2, steps - t)
+        out |= {(stride * (1 << t) * u) % S for u in range(1, 1 << w)}
+        t += w
+    return out
+
+
 def rotation_steps(ctx, algorithm: str, c: int, m: int = 1, n: int = 1):
     """Left-rotation amounts a schedule will use (to pre-generate keys)."""
     s0, s1, S = ctx.grid_rows, ctx.grid_cols, ctx.slot_count
     steps = set()
-    for t in range(_lg(s1)):
-        steps |= {1 << t, S - (1 << t)}
     if algorithm == "diag_abt":
+        steps |= ladder_amounts(ctx, 1, _lg(s1)) | ladder_amounts(ctx, -1, _lg(s1))
         for k in range(1, c // 2 + 1):
             steps.add((k % s0) * s1)
     else:
-        for t in range(_lg(s0)):
-            steps.add((1 << t) * s1)
+        steps |= ladder_amounts(ctx, s1, _lg(s0))
         steps |= {S - s1, s1}
         for k in range(1, c // 2 + 1):
             steps.add(k % s1)

@@ -3,7 +3,10 @@
 evidence bench.py reports next to its roofline: DRAM bytes per key switch vs
 the SURVEY §8(d) model (94.37 MB at level 12), and per-kernel issue activity.
 
-    python scripts/ncu_ks_evidence.py RAW.csv[.gz] BATCH OUT.json
+    python scripts/ncu_ks_evidence.py RAW.csv[.gz] BATCH OUT.json [STEPS MODEL_BYTES BASIS]
+
+With STEPS the capture is a ladder (scripts/ladder_probe.py): BATCH entries x
+STEPS doubling steps, each charged MODEL_BYTES by the per-op model.
 """
 import csv
 import gzip
@@ -12,6 +15,9 @@ import json
 import sys
 
 path, batch, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+model_arg = float(sys.argv[5]) if len(sys.argv) > 5 else None
+basis_arg = sys.argv[6] if len(sys.argv) > 6 else None
 raw = gzip.open(path, "rt").read() if path.endswith(".gz") else open(path).read()
 rows = list(csv.reader(io.StringIO(raw)))
 h = {k: i for i, k in enumerate(rows[0])}
@@ -33,9 +39,10 @@ for r in rows[2:]:
     inst += float(r[h["smsp__inst_executed.sum"]])
     key = name + ("<" + r[h["Kernel Name"]].split("<")[1].split(">")[0] + ">" if "<" in r[h["Kernel Name"]] else "")
     issue.setdefault(key, []).append(round(float(r[h["sm__inst_issued.avg.pct_of_peak_sustained_active"]]), 1))
+batch *= steps
 per_ks = dram / batch
-model = 94.37e6
-res = {"basis": f"ncu --set full of {batch} level-12 rotations (cfg1) in batched pipelines of 3 (scripts/ks_batch_probe.py), serialised, cold cache",
+model = model_arg or 94.37e6
+res = {"basis": basis_arg or f"ncu --set full of {batch} level-12 rotations (cfg1) in batched pipelines of 3 (scripts/ks_batch_probe.py), serialised, cold cache",
        "dram_bytes_per_keyswitch": per_ks, "model_bytes_per_keyswitch": model, "traffic_ratio": per_ks / model,
        "kernel_us_per_keyswitch": us / batch, "warp_instructions_per_keyswitch": inst / batch,
        "issue_active_pct": {k: v[0] if len(v) == 1 else v for k, v in issue.items()}}

@@ -440,22 +440,33 @@ def prot_up(E, k):                                                  # encoding.p
     return E.each(fix)
 
 
-LADDER_RADIX_LOG = 2    # doubling steps merged into one rotate-and-sum stage (radix 4)
+def ladder_plan(steps):
+    """Doubling steps per rotate-and-sum stage: radix 8 (3 steps, 7 rotations)
+    while at least 5 steps remain or exactly 3, else radix 4 (2 steps), else a
+    single step -- 8 -> 3 + 3 + 2, 7 -> 3 + 2 + 2.  A stage costs one ModUp +
+    ModDown plus a key product per rotation (~1/9 of the pair each at cfg1),
+    so a third step per stage pays for its four extra key products, a lone
+    trailing step never does."""
+    plan, rem = [], steps
+    while rem > 0:
+        w = 3 if (rem >= 5 or rem == 3) else min(2, rem)
+        plan.append(w)
+        rem -= w
+    return plan
 
 
 def ladder(ctx, acc, stride, steps):
     """The reference's doubling ladder ``for t < steps: acc = add(acc,
     lrot(acc, stride * 2^t))`` (stride < 0: rrot) -- encoding.py:354-359,
     378-379, approx.py:165-189.  On a context with the fused schedule forms
-     two steps become one radix-4 rotate-and-sum stage
-    ``acc + lrot(acc, s) + lrot(acc, 2s) + lrot(acc, 3s)``, s = stride * 4^i:
-    the same slot values and ledger, half the ModUp / ModDown passes."""
+     w = 2 or 3 steps (``ladder_plan``) become one rotate-and-sum
+    stage ``acc + sum_{u < 2^w} lrot(acc, u s)``, s = stride * 2^t: the same
+    slot values and ledger, one ModUp / ModDown per stage."""
     if getattr(ctx, "hoist", False) and hasattr(ctx, "ladder") and ctx._kind(acc)[0] == "ct":
         return ctx.ladder(acc, stride, steps)       # the CUDA product's own ladder (same stages)
     if getattr(ctx, "hoist", False) and hasattr(ctx, "rotsum") and ctx._kind(acc)[0] == "ct":
         t = 0
-        while t < steps:
-            w = min(LADDER_RADIX_LOG, steps - t)
+        for w in ladder_plan(steps):
             base = stride * (1 << t)
             acc = ctx.rotsum(acc, [base * u for u in range(1, 1 << w)], w)
             t += w

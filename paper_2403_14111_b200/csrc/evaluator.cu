@@ -768,7 +768,9 @@ std::vector<CtP> Eval::lrot_batch(const std::vector<CtP>& xs, int64_t r, bool ad
     return ev_automorph_batch(c, a, galois_rot(c, r), add_self);
 }
 
-constexpr int LADDER_RADIX_LOG = 2;   // doubling steps per rotate-and-sum stage (radix 4; oracle/slots.py ladder)
+// doubling steps of the next rotate-and-sum stage when `rem` remain (oracle/slots.py
+// ladder_plan): radix 8 while >= 5 remain or exactly 3, else radix 4, else one step
+static int ladder_width(int rem) { return (rem >= 5 || rem == 3) ? 3 : std::min(2, rem); }
 
 std::vector<CtP> Eval::ladder(const std::vector<CtP>& xs_in, int64_t stride, int steps) {
     std::vector<CtP> xs = xs_in;
@@ -778,7 +780,7 @@ std::vector<CtP> Eval::ladder(const std::vector<CtP>& xs_in, int64_t stride, int
     }
     const int64_t S = c.N / 2;
     for (int t = 0; t < steps;) {
-        const int w = std::min(LADDER_RADIX_LOG, steps - t);
+        const int w = ladder_width(steps - t);
         const int64_t base = stride * ((int64_t)1 << t);
         t += w;
         std::vector<u64> gals;

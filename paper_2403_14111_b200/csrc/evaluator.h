@@ -38,7 +38,7 @@ struct KsHoist {
 };
 bool keyswitch_hoisted(Ctx& c, const u64* const* c0s, const u64* const* c1s, int level, int B, const KsHoist* e);
 // rotate-and-sum stage (keyswitch.cu, DESIGN.md §3 radix ladders): out_b = x_b +
-// sum_r sigma_{gals[r]}(x_b), one ModUp and one ModDown per input; nrot <= 3
+// sum_r sigma_{gals[r]}(x_b), one ModUp and one ModDown per input; nrot <= 7
 bool keyswitch_rotsum(Ctx& c, int B, const u64* const* xs, u64* const* outs, int level, int nrot, const u64* gals,
                       const u64* const* keys);
 // relinearisation + rescale in one pass (keyswitch.cu): ds[b] = the
@@ -139,9 +139,9 @@ struct Eval {
     // the reference's doubling ladder over independent operands,
     //   for t < steps: x = add(x, lrot(x, stride * 2^t))      (stride < 0: rrot)
     // (encoding.py:354-359, 378-379, approx.py:165-189).  With the fused
-    // schedule forms (Ctx::hoist) two steps run as one radix-4
-    // rotate-and-sum stage x + lrot(x, s) + lrot(x, 2s) + lrot(x, 3s): same
-    // slot values and ledger (steps Rot + steps Add), half the ModUp / ModDown
+    // schedule forms (Ctx::hoist) two or three steps run as one radix-4 / radix-8
+    // rotate-and-sum stage x + sum_u lrot(x, u s) (8 steps -> 3 + 3 + 2): same
+    // slot values and ledger (steps Rot + steps Add), one ModUp / ModDown per stage
     std::vector<CtP> ladder(const std::vector<CtP>& xs, int64_t stride, int steps);
     CtP ladder(const CtP& x, int64_t stride, int steps) { return ladder(std::vector<CtP>{x}, stride, steps)[0]; }
     std::vector<CtP> conj_batch(const std::vector<CtP>& xs);

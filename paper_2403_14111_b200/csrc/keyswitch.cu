@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256, E == 2 ? KP_MINB : (MB > 4 ? 2 : 3)) ks_k
 // of rotation r are loaded once and reused by the entries.  Aligned index
 // pairs map to aligned pairs under every Galois element (src(k + 1) =
 // src(k) ^ 1), so each gather is one 16-byte load.
-constexpr int RS_MAXR = 3;   // rotations per stage (radix 4); bounds the 128-bit sums: 3 * (4 + 1) terms below 2^124
+constexpr int RS_MAXR = 7;   // rotations per stage (radix 8)
 struct KsRotsum {
     int nb, nrot;
     const u64* c0[KS_MAXB];    // x_b poly 0 [nl][N]
@@ -563,7 +563,9 @@ __global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_rotsum
         oa = fp_canon(sa, q, qinv);
     } else {
         // 128-bit sums hold 15 products of a lazy digit (< 16q) and a key
-        // word (q < 2^60): NR * (BETA + 1) <= 15 (static_assert below)
+        // word (q < 2^60): folded to one word whenever the next rotation's
+        // BETA + 1 products would pass that
+        constexpr int FOLD = 15 / (BETA + 1);   // rotations between folds
         U128 ib = {0, 0}, ia = {0, 0};
 #pragma unroll
         for (int r = 0; r < NR; r++) {
@@ -585,11 +587,16 @@ __global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_rotsum
             }
             if (qlimb) mac128(ib, z, pq);
             if (MODE == 1 && qlimb) mac128(ia, z1, pq);
+            if ((r + 1) % FOLD == 0 && r + 1 < NR) {
+                ib = U128{reduce128(ib.hi, ib.lo, P), 0};
+                ia = U128{reduce128(ia.hi, ia.lo, P), 0};
+            }
         }
         ob = reduce128(ib.hi, ib.lo, P);
         oa = reduce128(ia.hi, ia.lo, P);
     }
-    static_assert(NR * (BETA + 1) <= 15, "128-bit key-product sum bound");
+    static_assert(BETA + 1 <= 15 && NR <= RS_MAXR, "128-bit key-product sum bound");
+    // FP64 sums: NR * (BETA + 1) <= 63 terms below 0.6q, q < 2^46: exact integers below 2^53
     u64* __restrict__ ab = acc + (size_t)b * g.acc_stride() + toff + k;
     ab[0] = ob;
     ab[dstride] = oa;
@@ -1034,6 +1041,14 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
             else if (nr == 3 && g.beta == 3) go(ks_keyprod_rotsum_t<3, 3>);
             else if (nr == 3 && g.beta == 2) go(ks_keyprod_rotsum_t<2, 3>);
             else if (nr == 3 && g.beta == 1) go(ks_keyprod_rotsum_t<1, 3>);
+            else if (nr == 7 && g.beta == 4) go(ks_keyprod_rotsum_t<4, 7>);
+            else if (nr == 7 && g.beta == 3) go(ks_keyprod_rotsum_t<3, 7>);
+            else if (nr == 7 && g.beta == 2) go(ks_keyprod_rotsum_t<2, 7>);
+            else if (nr == 7 && g.beta == 1) go(ks_keyprod_rotsum_t<1, 7>);
+            else if (nr == 1 && g.beta == 4) go(ks_keyprod_rotsum_t<4, 1>);
+            else if (nr == 1 && g.beta == 3) go(ks_keyprod_rotsum_t<3, 1>);
+            else if (nr == 1 && g.beta == 2) go(ks_keyprod_rotsum_t<2, 1>);
+            else if (nr == 1 && g.beta == 1) go(ks_keyprod_rotsum_t<1, 1>);
             else if (g.beta > 4) launch_k(c, ks_keyprod_rotsum<8>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
             else launch_k(c, ks_keyprod_rotsum<4>, grid, 256, 0, g, c.d_primes, rb, pmodq, ACC, ngroups);
         } else

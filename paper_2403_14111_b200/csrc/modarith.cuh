@@ -77,7 +77,7 @@ __device__ __forceinline__ double fp_mulmod(double x, double y, double q, double
     const double qt = __dsub_rn(__fma_rn(h, qinv, FP_MAGIC), FP_MAGIC);
     return __dadd_rn(__fma_rn(-qt, q, h), l);
 }
-// |v| < 2^50 (integer) -> canonical word in [0, q)
+// |v| < 2^52 (an exact integer; v / q < 2^51) -> canonical word in [0, q)
 __device__ __forceinline__ u64 fp_canon(double v, double q, double qinv) {
     const double qt = __dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC);
     double r = __fma_rn(-qt, q, v);   // exact, |r| <= q/2

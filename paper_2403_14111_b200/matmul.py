@@ -188,14 +188,15 @@ def expected_period(c: int) -> int:
 
 def ladder_amounts(ctx, stride: int, steps: int):
     """Rotation amounts of the doubling ladder (stride, steps): with the fused
-    schedule forms (``ctx.hoist``) the radix-4 stages' s, 2s, 3s (s = stride *
-    4^i), else stride * 2^t."""
+    schedule forms (``ctx.hoist``) the rotate-and-sum stages' u * s, u < 2^w
+    (w = 3, 2 or 1 steps per stage, s = stride * 2^t), else stride * 2^t."""
     S = ctx.slot_count
     if not getattr(ctx, "hoist", False):
         return {(stride * (1 << t)) % S for t in range(steps)}
     out, t = set(), 0
     while t < steps:
-        w = min(2, steps - t)
+        rem = steps - t
+        w = 3 if (rem >= 5 or rem == 3) else min(2, rem)
         out |= {(stride * (1 << t) * u) % S for u in range(1, 1 << w)}
         t += w
     return out

@@ -131,12 +131,13 @@ def _fused_ops(g, o, seed, tol=1e-5):
     for r, a in zip(rs, g.lrot_hoisted(gx[0], rs)):
         if r:
             np.testing.assert_array_equal(a.residues(), g.lrot(gx[0], r).residues())
-    # doubling ladders as radix-4 rotate-and-sum stages (one ModUp / ModDown per
-    # two steps): residues vs the oracle's stages, the reference's ledger
+    # doubling ladders as radix-4 / radix-8 rotate-and-sum stages (one ModUp /
+    # ModDown per two or three steps): residues vs the oracle's stages, the
+    # reference's ledger
     g.ledger.reset()
     o.ledger.reset()
     ks0 = g.extra["KeySwitch"], o.extra["KeySwitch"]
-    for stride, steps, lv in ((1, 4, None), (-1, 3, None), (g.grid_cols, 2, 2), (-2, 1, 1)):
+    for stride, steps, lv in ((1, 4, None), (-1, 3, None), (g.grid_cols, 2, 2), (-2, 1, 1), (1, 5, None)):
         z = rng.uniform(-1, 1, n) * 2.0 ** -steps
         g.nonce, o.nonce = 50, 50
         a = g.encrypt(z) if lv is None else g.encrypt(z, lv)
@@ -147,8 +148,8 @@ def _fused_ops(g, o, seed, tol=1e-5):
         for t in range(steps):
             want = want + np.roll(want, -stride * (1 << t))
         assert np.max(np.abs(la.slots - want)) < tol
-    assert _ledger(g) == _ledger(o) == [10, 0, 0, 10, 0, 0]
-    assert g.extra["KeySwitch"] - ks0[0] == o.extra["KeySwitch"] - ks0[1] == 6
+    assert _ledger(g) == _ledger(o) == [15, 0, 0, 15, 0, 0]
+    assert g.extra["KeySwitch"] - ks0[0] == o.extra["KeySwitch"] - ks0[1] == 2 + 1 + 1 + 1 + 2
 
 
 def test_fused_ops_residues(pair):

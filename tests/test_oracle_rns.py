@@ -145,9 +145,9 @@ def test_restated_diag_abt_config0_over_oracle(golden):
     out = S.decode(r, tol=1e-4)
     assert np.max(np.abs(out - golden["cfg0_out"])) < 1e-4
     # key-switch pipelines run: 8 relinearisations (one per product sum), 8
-    # hoisted rotations, 16 ladders of 6 doubling steps as 3 radix-4
+    # hoisted rotations, 16 ladders of 6 doubling steps as 2 radix-8
     # rotate-and-sum stages each (96 of the ledger's 104 Rot), 1 conj
-    assert ctx.extra["KeySwitch"] == 8 + 8 + 48 + 1
+    assert ctx.extra["KeySwitch"] == 8 + 8 + 32 + 1
 
 
 def test_restated_softmax_small12(golden):
@@ -230,8 +230,8 @@ def test_rotate_and_sum_stage(small):
         ctx = R.OracleCKKSContext("small12", 16, seed=5, hoist=hoist)
         v = rng.uniform(-1, 1, ctx.slot_count)
         b = ctx.encrypt(v)
-        got = S.ladder(ctx, b, 16, 4)            # row ladder: stride s1 = 16, 4 steps
-        got = S.ladder(ctx, got, -1, 3)          # odd step count: radix 4 then radix 2
+        got = S.ladder(ctx, b, 16, 4)            # row ladder: stride s1 = 16, 4 steps: two radix-4 stages
+        got = S.ladder(ctx, got, -1, 3)          # 3 steps: one radix-8 stage
         want = v
         for t in range(4):
             want = want + np.roll(want, -16 * (1 << t))
@@ -239,7 +239,8 @@ def test_rotate_and_sum_stage(small):
             want = want + np.roll(want, 1 << t)
         assert np.max(np.abs(got.slots - want)) < 1e-4
         assert ctx.ledger.counts()["Rot"] == 7 and ctx.ledger.counts()["Add"] == 7
-        assert ctx.extra["KeySwitch"] == (4 if hoist else 7)
+        assert ctx.extra["KeySwitch"] == (3 if hoist else 7)
+    assert [S.ladder_plan(n) for n in range(1, 9)] == [[1], [2], [3], [2, 2], [3, 2], [3, 3], [3, 2, 2], [3, 3, 2]]
 
 
 @pytest.mark.parametrize("hoist", [True, False])

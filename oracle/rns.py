@@ -44,6 +44,11 @@ PARAMS = {
     # the same chain on a 2^10 ring (test-only, insecure): bootstrapping parity
     "boot10": (10, [60] + [42] * 12 + [58, 60] + [55] * 15, [60] * 4, 4, 55, 64),
     "tiny": (10, [50] + [40] * 3, [50], 1, 40, 32),
+    # short chains on the other split-pass rings (test-only): the fused
+    # key-switch / rescale pipeline's column-pass geometries for 2^14, 2^15, 2^17
+    "n14": (14, [58] + [42] * 5, [60] * 2, 2, 42, 64),
+    "n15": (15, [58] + [42] * 4, [60] * 3, 3, 42, 64),
+    "n17": (17, [58] + [42] * 3, [60], 1, 42, 64),
 }
 
 

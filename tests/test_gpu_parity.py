@@ -165,6 +165,50 @@ def test_fused_ops_residues_cfg1():
     _fused_ops(P.CKKSContext("cfg1", 128, seed=3), R.OracleCKKSContext("cfg1", 128, seed=3), seed=7, tol=1e-3)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["n14", "n15", "n17"])
+def test_fused_pipeline_other_rings(name):
+    """The fused key-switch / rescale pipeline's column-pass geometries for
+    N = 2^14, 2^15 and 2^17 (keyswitch.cu ColCfg; cfg1 covers 2^16): rotation,
+    conjugation, ct x ct (relinearisation + rescale in one pass), ct x pt
+    (fused rescale), hoisted rotations and a radix-8 + radix-4 ladder,
+    residues against the oracle with alpha = 2, 3, 1 digits."""
+    P = _prod()
+    g = P.CKKSContext(name, 128, seed=21)
+    o = R.OracleCKKSContext(name, 128, seed=21)
+    rng = np.random.default_rng(12)
+    n = g.slot_count
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    g.nonce, o.nonce = 0, 0
+    gx, gy, ox, oy = g.encrypt(x), g.encrypt(y), o.encrypt(x), o.encrypt(y)
+    np.testing.assert_array_equal(gx.residues(), ox.data)
+    for r in (1, n - 5):
+        a, b = g.lrot(gx, r), o.lrot(ox, r)
+        np.testing.assert_array_equal(a.residues(), b.data)
+        assert np.max(np.abs(a.slots - np.roll(x, -r))) < 1e-4
+    np.testing.assert_array_equal(g.conj(gx).residues(), o.conj(ox).data)
+    gm, om = g.mult(gx, gy), o.mult(ox, oy)
+    np.testing.assert_array_equal(gm.residues(), om.data)
+    assert gm.level == g.max_level - 1 and np.max(np.abs(gm.slots - x * y)) < 1e-4
+    gp, op = g.cmult(gm, y), o.cmult(om, y)
+    np.testing.assert_array_equal(gp.residues(), op.data)
+    for a, b in zip(g.lrot_hoisted(gp, (3, 0, n - 1)), o.lrot_hoisted(op, (3, 0, n - 1))):
+        np.testing.assert_array_equal(a.residues(), b.data if hasattr(b, "data") else b)
+    z = rng.uniform(-1, 1, n) / 32
+    gz, oz = g.encrypt(z, 2), o.encrypt(z, 2)
+    la, lb = S.ladder(g, gz, -3, 5), S.ladder(o, oz, -3, 5)
+    np.testing.assert_array_equal(la.residues(), lb.data)
+    want = z
+    for t in range(5):
+        want = want + np.roll(want, 3 << t)
+    assert np.max(np.abs(la.slots - want)) < 1e-4
+    data = _adversarial(g.moduli, g.max_level + 1, g.N, "max", rng)
+    gb, ob = g.from_residues(data, g.max_level), R.RnsBlock(o, data, g.max_level)
+    np.testing.assert_array_equal(g.mult(gb, gb).residues(), o.mult(ob, ob).data)
+    np.testing.assert_array_equal(S.ladder(g, gb, 1, 3).residues(), S.ladder(o, ob, 1, 3).data)
+
+
 @pytest.mark.parametrize("hoist,cols", [(True, 40), (False, 40), (True, 200)])
 def test_native_multi_column_diag_abt_small12(hoist, cols):
     """DiagABT with 3 (and 13: more than one 8-product group of the fused

@@ -514,6 +514,9 @@ def run_b200(args, world, rank, local):
                             "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9,
                             "share_of_step": k_ms / step_prof_ms},
         "kernel_breakdown_ms": {k: round(v[1], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            # per kernel: [launches, ms, algorithmic GB/s] of the serialised profiled step
+            "kernel_detail": {k: [int(v[0]), round(v[1], 3), round(v[2] / max(v[1], 1e-9) / 1e6, 1)]
+                              for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "transfers": "async copy streams (hc_ct_upload_async / hc_ct_download_async)",
                 "runs_ms": [round(v, 3) for v in e2e_runs], "statistic": "median of 3 timed runs after warm-up",
@@ -600,6 +603,9 @@ def run_train_step(args, world, rank, local):
                        "rows": int(X.shape[0]), "block_rows_per_rank": len(sharding.partition(8, world, rank))},
             "ledger_per_step": counts, "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0),
             "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            # per kernel: [launches, ms, algorithmic GB/s] of the serialised profiled step
+            "kernel_detail": {k: [int(v[0]), round(v[1], 3), round(v[2] / max(v[1], 1e-9) / 1e6, 1)]
+                              for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -662,6 +668,9 @@ def run_softmax(args, world, rank, local):
                        else "surrogate (decrypt/re-encrypt), not CKKS bootstrapping"},
             "max_abs_err_vs_float64": err, "ledger_per_step": counts,
             "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            # per kernel: [launches, ms, algorithmic GB/s] of the serialised profiled step
+            "kernel_detail": {k: [int(v[0]), round(v[1], 3), round(v[2] / max(v[1], 1e-9) / 1e6, 1)]
+                              for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -712,6 +721,9 @@ def run_bootstrap(args, world, rank, local):
                        "chain": "q0 60 + 12x42 (app) + 58, 60, 15x55 bits; P 4x60; dnum 8"},
             "max_abs_err": err, "paper_hea_an_a40_ms": 159.0,
             "kernel_breakdown_ms": {k: round(v[1], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            # per kernel: [launches, ms, algorithmic GB/s] of the serialised profiled step
+            "kernel_detail": {k: [int(v[0]), round(v[1], 3), round(v[2] / max(v[1], 1e-9) / 1e6, 1)]
+                              for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "gpu_launches": int(L.hc_launch_count(ctx._h) - launches0), "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)

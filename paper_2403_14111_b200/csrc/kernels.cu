@@ -30,58 +30,66 @@ struct EwPtrs {
     const u64* a[KS_MAXB];
     const u64* b[KS_MAXB];
 };
-__global__ void ew_kernel(int op, EwPtrs ptr, const ConstTab consts, const PrimeDev* __restrict__ primes, int nl,
-                          int npoly, int N, int bpoly) {
+// EW_U index pairs (16 bytes each) per thread: every operand load is issued
+// before the first use (one pair per thread ran at ~2.2 TB/s, latency-bound)
+constexpr int EW_U = 4;
+__global__ void __launch_bounds__(256) ew_kernel(int op, EwPtrs ptr, const ConstTab consts,
+                                                 const PrimeDev* __restrict__ primes, int nl, int npoly, int N,
+                                                 int bpoly) {
     pdl_enter();
     // grid.y = poly * nl + limb: no integer division on the hot path
     u64* __restrict__ out = ptr.out[blockIdx.z];
     const u64* __restrict__ a = ptr.a[blockIdx.z];
     const u64* __restrict__ b = ptr.b[blockIdx.z];
-    const size_t half = (size_t)N / 2;
+    const int half = N / 2;
     const int limb = blockIdx.y % nl;
     const int s = blockIdx.y / nl;
-    const u64 q = primes[limb].q;
-    for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < half; v += (size_t)gridDim.x * blockDim.x) {
-        const size_t k = v * 2;
-        const size_t e = (size_t)blockIdx.y * N + k;
-        const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + e);
+    const PrimeDev P = primes[limb];
+    const u64 q = P.q;
+    // second operand: a ciphertext poly (add / sub, polys below bpoly), a
+    // plaintext limb (poly 0 only, except the product), or none
+    const bool ctb = op <= EW_SUB, ptb = op >= EW_PT_ADD && op <= EW_PT_MUL;
+    const bool hasb = ctb ? s < bpoly : (ptb && (op == EW_PT_MUL || s == 0));
+    const u64* __restrict__ bb = ctb ? b + (size_t)blockIdx.y * N : (ptb ? b + (size_t)limb * N : nullptr);
+    const u64* __restrict__ aa = a + (size_t)blockIdx.y * N;
+    u64* __restrict__ oo = out + (size_t)blockIdx.y * N;
+    const int v0 = (blockIdx.x * blockDim.x) * EW_U + threadIdx.x;
+    ulonglong2 x[EW_U], y[EW_U];
+#pragma unroll
+    for (int u = 0; u < EW_U; u++) {
+        const int v = v0 + u * (int)blockDim.x;
+        if (v < half) x[u] = *reinterpret_cast<const ulonglong2*>(aa + 2 * v);
+    }
+#pragma unroll
+    for (int u = 0; u < EW_U; u++) {
+        const int v = v0 + u * (int)blockDim.x;
+        y[u] = make_ulonglong2(0, 0);
+        if (hasb && v < half) y[u] = *reinterpret_cast<const ulonglong2*>(bb + 2 * v);
+    }
+#pragma unroll
+    for (int u = 0; u < EW_U; u++) {
+        const int v = v0 + u * (int)blockDim.x;
+        if (v >= half) continue;
+        const int k = 2 * v;
         u64 r0, r1;
         switch (op) {
             case EW_ADD:
-            case EW_SUB: {
-                ulonglong2 y = (s < bpoly) ? *reinterpret_cast<const ulonglong2*>(b + e) : make_ulonglong2(0, 0);
-                if (op == EW_ADD) { r0 = add_mod(x.x, y.x, q); r1 = add_mod(x.y, y.y, q); }
-                else { r0 = sub_mod(x.x, y.x, q); r1 = sub_mod(x.y, y.y, q); }
-                break;
-            }
-            case EW_NEG: r0 = neg_mod(x.x, q); r1 = neg_mod(x.y, q); break;
-            case EW_PT_ADD:
-            case EW_PT_SUB:
-            case EW_PT_RSUB: {
-                ulonglong2 y = (s == 0) ? *reinterpret_cast<const ulonglong2*>(b + (size_t)limb * N + k)
-                                        : make_ulonglong2(0, 0);
-                if (op == EW_PT_ADD) { r0 = add_mod(x.x, y.x, q); r1 = add_mod(x.y, y.y, q); }
-                else if (op == EW_PT_SUB) { r0 = sub_mod(x.x, y.x, q); r1 = sub_mod(x.y, y.y, q); }
-                else { r0 = sub_mod(y.x, x.x, q); r1 = sub_mod(y.y, x.y, q); }
-                break;
-            }
-            case EW_PT_MUL: {
-                const PrimeDev P = primes[limb];
-                ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b + (size_t)limb * N + k);
-                r0 = mul_mod(x.x, y.x, P);
-                r1 = mul_mod(x.y, y.y, P);
-                break;
-            }
+            case EW_PT_ADD: r0 = add_mod(x[u].x, y[u].x, q); r1 = add_mod(x[u].y, y[u].y, q); break;
+            case EW_SUB:
+            case EW_PT_SUB: r0 = sub_mod(x[u].x, y[u].x, q); r1 = sub_mod(x[u].y, y[u].y, q); break;
+            case EW_PT_RSUB: r0 = sub_mod(y[u].x, x[u].x, q); r1 = sub_mod(y[u].y, x[u].y, q); break;
+            case EW_NEG: r0 = neg_mod(x[u].x, q); r1 = neg_mod(x[u].y, q); break;
+            case EW_PT_MUL: r0 = mul_mod(x[u].x, y[u].x, P); r1 = mul_mod(x[u].y, y[u].y, P); break;
             case EW_CONST_MUL: {
                 const u64* cc = consts.v + 4 * limb + (k < half ? 0 : 2);
-                r0 = mul_shoup(x.x, cc[0], cc[1], q);
-                r1 = mul_shoup(x.y, cc[0], cc[1], q);
+                r0 = mul_shoup(x[u].x, cc[0], cc[1], q);
+                r1 = mul_shoup(x[u].y, cc[0], cc[1], q);
                 break;
             }
             case EW_CONST_ADD:
             case EW_CONST_RADD: {
-                u64 cv = (s == 0) ? consts.v[4 * limb + (k < half ? 0 : 2)] : 0;
-                u64 x0 = x.x, x1 = x.y;
+                const u64 cv = (s == 0) ? consts.v[4 * limb + (k < half ? 0 : 2)] : 0;
+                u64 x0 = x[u].x, x1 = x[u].y;
                 if (op == EW_CONST_RADD) { x0 = neg_mod(x0, q); x1 = neg_mod(x1, q); }
                 r0 = add_mod(x0, cv, q);
                 r1 = add_mod(x1, cv, q);
@@ -89,7 +97,7 @@ __global__ void ew_kernel(int op, EwPtrs ptr, const ConstTab consts, const Prime
             }
             default: r0 = r1 = 0;
         }
-        *reinterpret_cast<ulonglong2*>(out + e) = make_ulonglong2(r0, r1);
+        *reinterpret_cast<ulonglong2*>(oo + k) = make_ulonglong2(r0, r1);
     }
 }
 
@@ -107,7 +115,7 @@ void k_elementwise_batch(Ctx& c, int op, int B, u64* const* out, const u64* cons
             p.b[i] = b ? b[b0 + i] : nullptr;
         }
         Launch scope(c, "elementwise", 8.0 * c.N * nb * (rd + (double)npoly * nl));
-        dim3 grid((unsigned)((c.N / 2 + 255) / 256), (unsigned)(npoly * nl), nb);
+        dim3 grid((unsigned)((c.N / 2 + 256 * EW_U - 1) / (256 * EW_U)), (unsigned)(npoly * nl), nb);
         launch_k(c, ew_kernel, grid, 256, 0, op, p, consts ? *consts : zero, c.d_primes, nl, npoly, c.N, bpoly);
         HC_CUDA(cudaGetLastError());
     }

@@ -3,12 +3,17 @@
 # bench lines, launch list of the bench command, ncu --set full of the batched
 # rotation pipeline and of one radix-4 ladder stage.  Every command runs alone
 # first without ncu.
-O=gpurun_out/r2b
+O=gpurun_out/r2d
 mkdir -p $O
 python bench.py > $O/bench_pair.json 2> $O/bench_pair.err
 python bench.py --workload softmax --steps 5 --no-cpu > $O/softmax.json 2>/dev/null
 python bench.py --workload train --steps 3 --no-cpu > $O/train.json 2>/dev/null
 python bench.py --workload table4 --no-cpu > $O/table4.json 2>/dev/null
+python bench.py --workload bootstrap --no-cpu > $O/bootstrap.json 2>/dev/null
+python bench.py --workload softmax --boot ckks --steps 2 --warmup 1 --no-cpu > $O/softmax_ckks.json 2>/dev/null
+python bench.py --workload train --boot ckks --steps 1 --warmup 1 --no-cpu > $O/train_ckks.json 2>/dev/null
+python bench.py --impl reference --steps 2 --warmup 1 > $O/reference.json 2>/dev/null
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_exit=$? >> $O/smoke.log
 python scripts/ks_batch_probe.py 3 2 > $O/ks_probe.log 2>&1
 HC_PROBE_PROFILE=1 ncu --set full --clock-control none --profile-from-start off -o $O/ks_batch3 \
     python scripts/ks_batch_probe.py 3 2 > $O/ncu_ks.log 2>&1

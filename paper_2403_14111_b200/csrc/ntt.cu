@@ -22,6 +22,8 @@
 // shared memory (one barrier per round).  The first round loads straight
 // from HBM and the last round stores straight to HBM, so a pass reads and
 // writes each word exactly once.  All index math is shifts and masks.
+#include <cstdlib>
+
 #include "ntt_pass.cuh"
 
 namespace hc {
@@ -93,6 +95,68 @@ static void launch_t(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src,
     HC_CUDA(cudaGetLastError());
 }
 
+// Compact (looped, one butterfly per thread) variant for sub-wave launches:
+// see ntt_pass.cuh.  Same arguments and hooks as ntt_kernel.
+template <int LOGSZ, int MODE, int SUBS, bool INV>
+__global__ void __launch_bounds__(SmallGeo<LOGSZ, MODE, SUBS>::THREADS)
+    ntt_small_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
+                     int N1, int use_src, int last) {
+    pdl_trigger();
+    extern __shared__ u64 sm[];
+    const int job = blockIdx.y, b = blockIdx.z;
+    const int pidx = jobs.prime[job];
+    u64* dst = jobs.ptr[job] + (b ? jobs.boff[b] : 0);
+    const u64* src = (use_src && jobs.src[job]) ? jobs.src[job] + (b ? jobs.sboff[b] : 0) : dst;
+    const PrimeDev P = primes[pidx];
+    const ulonglong2* TW = tw + ((size_t)pidx << logN);
+    using SG = SmallGeo<LOGSZ, MODE, SUBS>;
+    SG G;
+    G.init(N1);
+    stage_twiddles_small<LOGSZ, MODE, SUBS>(G, SG::twsm_of(sm), TW, N1);
+    pdl_wait();   // above: context-lifetime tables (primes, twiddles) only
+    const u64 gal = use_src ? jobs.galois : 0;
+    u64 c = P.ninv, cs = P.ninv_s;
+    if (INV && jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
+    const u64 off = (INV && jobs.center) ? (P.q - 1) / 2 : 0;
+    constexpr int INB = (MODE == MODE_CHUNKS) ? BOUND_LIM : 2;
+    if (gal) {
+        LdGalois ld{src, logN, gal};
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs, off}; ntt_pass_small<LOGSZ, MODE, SUBS, INV, INB>(G, sm, P, ld, st); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass_small<LOGSZ, MODE, SUBS, INV, INB>(G, sm, P, ld, st); }
+    } else {
+        LdPlain ld{src};
+        if (last) { StPlain<INV, true> st{dst, P.q, c, cs, off}; ntt_pass_small<LOGSZ, MODE, SUBS, INV, INB>(G, sm, P, ld, st); }
+        else { StPlain<INV, false> st{dst, P.q, 0, 0}; ntt_pass_small<LOGSZ, MODE, SUBS, INV, INB>(G, sm, P, ld, st); }
+    }
+}
+
+template <int LOGSZ, int MODE, int SUBS>
+static void launch_small(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
+    using SG = SmallGeo<LOGSZ, MODE, SUBS>;
+    const size_t smem = SG::smem_bytes();
+    const int nsub = (MODE == MODE_COLS) ? (c.N >> LOGSZ) : N1;
+    dim3 grid(nsub / SUBS, jobs.n, jobs.nb);
+    static const char* names[2][3] = {{"ntt_fwd_full", "ntt_fwd_cols", "ntt_fwd_chunks"},
+                                      {"ntt_inv_full", "ntt_inv_cols", "ntt_inv_chunks"}};
+    Launch scope(c, names[inv ? 1 : 0][MODE], 16.0 * c.N * jobs.n * jobs.nb);
+    if (inv)
+        launch_k(c, ntt_small_kernel<LOGSZ, MODE, SUBS, true>, grid, SG::THREADS, smem, jobs, c.d_primes,
+                 c.twp(0, true), c.logN, N1, use_src, last);
+    else
+        launch_k(c, ntt_small_kernel<LOGSZ, MODE, SUBS, false>, grid, SG::THREADS, smem, jobs, c.d_primes,
+                 c.twp(0, false), c.logN, N1, use_src, last);
+    HC_CUDA(cudaGetLastError());
+}
+
+// HC_NTT_SMALL: 0 = never, 1 = lone sub-wave launches (chains), 2 = every sub-wave launch, 3 = every launch
+static int small_policy() {
+    static const int v = [] {
+        const char* e = std::getenv("HC_NTT_SMALL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 static void full_pass(Ctx& c, const JobList& jobs, bool inv) {
     switch (c.logN) {
         case 9: launch_t<9, MODE_FULL, 1>(c, jobs, inv, 1, 1, 1); break;
@@ -119,6 +183,15 @@ static bool chain_grid(const JobList& jobs, int ctas_per_job) { return jobs.nb =
 static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
     const int big_subs = 1 << (20 - c.logN);   // 64, 32, 16, 8 columns per CTA for 2^14 .. 2^17
     const bool sm = small_grid(jobs, 512 / big_subs), ch = sm && jobs.nb == 1;
+    if ((small_policy() == 1 && ch) || (small_policy() == 2 && sm) || small_policy() == 3) {
+        switch (c.logN) {
+            case 14: launch_small<5, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last); return;
+            case 15: launch_small<6, MODE_COLS, 8>(c, jobs, inv, N1, use_src, last); return;
+            case 16: launch_small<7, MODE_COLS, 4>(c, jobs, inv, N1, use_src, last); return;
+            case 17: launch_small<8, MODE_COLS, 2>(c, jobs, inv, N1, use_src, last); return;
+            default: throw Error(-1, "unsupported ring degree");
+        }
+    }
     switch (c.logN) {
         case 14: if (ch) launch_t<5, MODE_COLS, 16, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
                  else if (sm) launch_t<5, MODE_COLS, 16>(c, jobs, inv, N1, use_src, last);
@@ -140,6 +213,11 @@ static void cols_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src
 #define HC_NTT_CH_SUBS 2   // 128-thread CTAs (measured 4 -> 2: -0.8 % per pair)
 #endif
 static void chunks_pass(Ctx& c, const JobList& jobs, bool inv, int N1, int use_src, int last) {
+    const bool smg = small_grid(jobs, N1 / HC_NTT_CH_SUBS);
+    if ((small_policy() == 1 && smg && jobs.nb == 1) || (small_policy() == 2 && smg) || small_policy() == 3) {
+        launch_small<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
+        return;
+    }
     if (chain_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1, NTT_PMB_SMALL>(c, jobs, inv, N1, use_src, last);
     else if (small_grid(jobs, N1 / HC_NTT_CH_SUBS)) launch_t<9, MODE_CHUNKS, 1>(c, jobs, inv, N1, use_src, last);
     else launch_t<9, MODE_CHUNKS, HC_NTT_CH_SUBS>(c, jobs, inv, N1, use_src, last);

@@ -425,6 +425,226 @@ __device__ __forceinline__ void ntt_pass(const PassGeo<LOGSZ, MODE, SUBS>& G, u6
     }
 }
 
+// ---- compact pass (sub-wave launches) ------------------------------------------
+//
+// The radix-8 pass above is straight-line code: ~1000 instructions (16-20 KB)
+// per arithmetic path, executed once per warp.  In a launch that does not
+// fill the machine (the INTTs of a lone ciphertext in the softmax /
+// inversion chains, the 6 special-prime limbs of a ModDown) every SM streams
+// that code from L2 for a handful of warps, and ncu shows instruction fetch
+// (`no_instruction`) as the top stall: 12-15 us per pass for work that moves
+// 3 MB.  The compact pass is the same transform as a loop: four words per
+// thread and two stages (radix 4) per iteration, every iteration through
+// shared memory (one barrier each), the CTA's twiddle pairs staged once by
+// cp.async, loads and stores coalesced through the shared tile.  ~300
+// instructions per arithmetic path, twice the threads per sub-transform; same
+// load / store hooks, same twiddle tables, bit-identical residues.  Lazy
+// bounds are uniform instead of planned: integer forward values stay below 4q
+// (Harvey), FP64 values follow the growth rules above with the inverse
+// reductions on a compile-time mask.  An odd stage count runs stage 0 alone.
+template <int LOGSZ, int MODE, int SUBS>
+struct SmallGeo {
+    static constexpr int SZ = 1 << LOGSZ;
+    static constexpr int Q = SZ / 4;
+    static constexpr int THREADS = SUBS * Q;
+    static constexpr size_t N2 = (size_t)1 << CHUNK_LOG;
+    static constexpr int TW_ENTRIES = (MODE == MODE_CHUNKS) ? SUBS * SZ : SZ;
+    // padding (bank conflicts of the stride-4^k groups): columns interleave
+    // SUBS sub-transforms per position, chunks lay them out one after another
+    static constexpr int PADSZ = (MODE == MODE_COLS) ? (SUBS >= 16 ? SZ : SZ + SZ / 4) : SZ + 3 * (SZ / 16);
+    static constexpr size_t smem_words() { return (size_t)SUBS * PADSZ; }
+    static constexpr size_t smem_bytes() { return smem_words() * 8 + (size_t)TW_ENTRIES * 16; }
+    static __device__ __forceinline__ ulonglong2* twsm_of(u64* sm) {
+        return reinterpret_cast<ulonglong2*>(sm + smem_words());
+    }
+    int sub, g, first_sub, R;
+    __device__ __forceinline__ void init(int N1) {
+        const int tid = threadIdx.x;
+        if (MODE == MODE_COLS) { sub = tid % SUBS; g = tid / SUBS; }
+        else { sub = tid / Q; g = tid % Q; }
+        first_sub = blockIdx.x * SUBS;
+        R = (MODE == MODE_CHUNKS) ? (N1 + first_sub + sub) : 1;
+    }
+    __device__ __forceinline__ size_t gidx(int pos) const {
+        if (MODE == MODE_COLS) return (size_t)(first_sub + sub) + (size_t)pos * N2;
+        return ((size_t)(first_sub + sub) << LOGSZ) + pos;
+    }
+    __device__ __forceinline__ int sidx(int pos) const {
+        if (MODE == MODE_COLS) return (SUBS >= 16 ? pos : pos + (pos >> 2)) * SUBS + sub;
+        return sub * PADSZ + pos + 3 * (pos >> 4);
+    }
+    __device__ __forceinline__ int twl(int s, int i) const {
+        if (MODE == MODE_CHUNKS) return SUBS * ((1 << s) - 1) + (sub << s) + i;
+        return (1 << s) + i;
+    }
+};
+
+template <int LOGSZ, int MODE, int SUBS>
+__device__ __forceinline__ void stage_twiddles_small(const SmallGeo<LOGSZ, MODE, SUBS>& G, ulonglong2* twsm,
+                                                     const ulonglong2* __restrict__ TW, int N1) {
+    using SG = SmallGeo<LOGSZ, MODE, SUBS>;
+    const int tid = threadIdx.x;
+    if (MODE == MODE_CHUNKS) {
+#pragma unroll 1
+        for (int s = 0; s < LOGSZ; s++) {
+            const int cnt = SUBS << s;
+            const ulonglong2* src = TW + ((size_t)(N1 + G.first_sub) << s);
+            ulonglong2* dst = twsm + SUBS * ((1 << s) - 1);
+            for (int i = tid; i < cnt; i += SG::THREADS) cp_async16(dst + i, src + i);
+        }
+    } else {
+        for (int i = tid; i < SG::SZ; i += SG::THREADS) cp_async16(twsm + i, TW + i);
+    }
+}
+
+// uniform-bound butterflies for the looped stages
+template <int INB>
+struct SmInt {
+    using V = u64;
+    using W = ulonglong2;
+    u64 q, twoq;
+    __device__ __forceinline__ SmInt(const PrimeDev& P) : q(P.q), twoq(2 * P.q) {}
+    // forward input below INB q -> below 4q; inverse inputs are below 2q already
+    __device__ __forceinline__ V in(u64 u, bool inv) const { return inv ? u : reduce_to(u, q, INB, 4); }
+    __device__ __forceinline__ u64 out(V v) const { return v; }   // fwd < 4q, inv < 2q
+    __device__ __forceinline__ void fwd(V& a, V& b, const W& w) const {
+        const u64 X = a >= twoq ? a - twoq : a;
+        const u64 T = mul_shoup_lazy(b, w.x, w.y, q);
+        a = X + T;
+        b = X + twoq - T;
+    }
+    __device__ __forceinline__ void inv(V& a, V& b, const W& w, int) const {
+        const u64 X = a + b;
+        const u64 D = a + twoq - b;
+        a = X >= twoq ? X - twoq : X;
+        b = mul_shoup_lazy(D, w.x, w.y, q);
+    }
+};
+template <int LOGSZ>
+__host__ __device__ constexpr unsigned fp_inv_red_mask() {
+    unsigned m = 0;
+    for (int e = 0; e < LOGSZ; e++) m |= fp_inv_red(e) ? (1u << e) : 0u;
+    return m;
+}
+template <int LOGSZ, int INB>
+struct SmFp {
+    using V = double;
+    using W = double2;
+    double q, qinv, qp52;
+    static_assert(4 * INB + 3 * LOGSZ <= 4 * 32, "FP forward pass bound");
+    __device__ __forceinline__ SmFp(const PrimeDev& P) : q(P.qd), qinv(P.qinv), qp52(P.qd + FP_P52) {}
+    __device__ __forceinline__ V in(u64 u, bool) const { return fp_word(u); }
+    __device__ __forceinline__ double red(double v) const {
+        const double qt = __dsub_rn(__fma_rn(v, qinv, FP_MAGIC), FP_MAGIC);
+        return __fma_rn(-qt, q, v);
+    }
+    __device__ __forceinline__ u64 out(V v) const {
+        return (u64)__double_as_longlong(__dadd_rn(red(v), qp52)) & FP_MANT;
+    }
+    __device__ __forceinline__ double mm(double x, const W& w) const {
+        const double h = __dmul_rn(x, w.x);
+        const double l = __fma_rn(x, w.x, -h);
+        const double qt = __dsub_rn(__fma_rn(x, w.y, FP_MAGIC), FP_MAGIC);
+        return __dadd_rn(__fma_rn(-qt, q, h), l);
+    }
+    __device__ __forceinline__ void fwd(V& a, V& b, const W& w) const {
+        const double T = mm(b, w);
+        const double X = a;
+        a = __dadd_rn(X, T);
+        b = __dsub_rn(X, T);
+    }
+    // e = ordinal of the executed inverse stage (0 first)
+    __device__ __forceinline__ void inv(V& a, V& b, const W& w, int e) const {
+        const double X = __dadd_rn(a, b);
+        const double D = __dsub_rn(a, b);
+        a = ((fp_inv_red_mask<LOGSZ>() >> e) & 1u) ? red(X) : X;
+        b = mm(D, w);
+    }
+};
+
+template <class AR, int LOGSZ, int MODE, int SUBS, bool INV, class LD, class ST>
+__device__ __forceinline__ void ntt_pass_small_ar(const AR& ar, const SmallGeo<LOGSZ, MODE, SUBS>& G, u64* smw,
+                                                  LD& ld, ST& st) {
+    using SG = SmallGeo<LOGSZ, MODE, SUBS>;
+    using V = typename AR::V;
+    using W = typename AR::W;
+    V* sm = reinterpret_cast<V*>(smw);
+    const W* twsm = reinterpret_cast<const W*>(SG::twsm_of(smw));
+    const int g = G.g;
+    constexpr int ODD = LOGSZ & 1;
+    // coalesced loads of positions g + m SZ/4 into the shared tile
+    {
+        u64 w[4];
+#pragma unroll
+        for (int m = 0; m < 4; m++) w[m] = ld(G.gidx(g + m * SG::Q));
+#pragma unroll
+        for (int m = 0; m < 4; m++) sm[G.sidx(g + m * SG::Q)] = ar.in(w[m], INV);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // stage 0 alone (odd stage counts): pairs (g + m SZ/4, g + (m + 2) SZ/4), one twiddle
+    auto lone_stage = [&]() {
+        V x[4];
+        int ix[4];
+#pragma unroll
+        for (int m = 0; m < 4; m++) { ix[m] = G.sidx(g + m * SG::Q); x[m] = sm[ix[m]]; }
+        const W w = twsm[G.twl(0, 0)];
+        if (INV) { ar.inv(x[0], x[2], w, LOGSZ - 1); ar.inv(x[1], x[3], w, LOGSZ - 1); }
+        else { ar.fwd(x[0], x[2], w); ar.fwd(x[1], x[3], w); }
+#pragma unroll
+        for (int m = 0; m < 4; m++) sm[ix[m]] = x[m];
+        __syncthreads();
+    };
+    if (!INV && ODD) lone_stage();
+    // stages (s, s + 1) per iteration: words base + m u2, u2 = SZ >> (s + 2)
+#pragma unroll 1
+    for (int it = 0; it < LOGSZ / 2; it++) {
+        const int s = INV ? (LOGSZ - 2 - 2 * it) : (ODD + 2 * it);
+        const int logu2 = LOGSZ - 2 - s;
+        const int blk = g >> logu2;
+        const int base = (blk << (logu2 + 2)) + (g & ((1 << logu2) - 1));
+        V x[4];
+        int ix[4];
+#pragma unroll
+        for (int m = 0; m < 4; m++) { ix[m] = G.sidx(base + (m << logu2)); x[m] = sm[ix[m]]; }
+        const W wa = twsm[G.twl(s, blk)];
+        const W* tb = twsm + G.twl(s + 1, 2 * blk);
+        const W wb0 = tb[0], wb1 = tb[1];
+        if (INV) {
+            ar.inv(x[0], x[1], wb0, 2 * it);
+            ar.inv(x[2], x[3], wb1, 2 * it);
+            ar.inv(x[0], x[2], wa, 2 * it + 1);
+            ar.inv(x[1], x[3], wa, 2 * it + 1);
+        } else {
+            ar.fwd(x[0], x[2], wa);
+            ar.fwd(x[1], x[3], wa);
+            ar.fwd(x[0], x[1], wb0);
+            ar.fwd(x[2], x[3], wb1);
+        }
+#pragma unroll
+        for (int m = 0; m < 4; m++) sm[ix[m]] = x[m];
+        __syncthreads();
+    }
+    if (INV && ODD) lone_stage();
+#pragma unroll
+    for (int m = 0; m < 4; m++) st(G.gidx(g + m * SG::Q), ar.out(sm[G.sidx(g + m * SG::Q)]));
+}
+
+// The compact pass on prime P.  INB as for ntt_pass; forward outputs are
+// below 4q (integer) / 2q (FP64), inverse outputs below 2q.  The caller has
+// issued stage_twiddles_small before its pdl_wait.
+template <int LOGSZ, int MODE, int SUBS, bool INV, int INB, class LD, class ST>
+__device__ __forceinline__ void ntt_pass_small(const SmallGeo<LOGSZ, MODE, SUBS>& G, u64* sm, const PrimeDev& P,
+                                               LD& ld, ST& st) {
+    if (P.fp) {
+        const SmFp<LOGSZ, INB> ar(P);
+        ntt_pass_small_ar<SmFp<LOGSZ, INB>, LOGSZ, MODE, SUBS, INV>(ar, G, sm, ld, st);
+    } else {
+        const SmInt<INB> ar(P);
+        ntt_pass_small_ar<SmInt<INB>, LOGSZ, MODE, SUBS, INV>(ar, G, sm, ld, st);
+    }
+}
+
 // ---- common hooks ----
 
 struct LdPlain {

@@ -22,6 +22,9 @@
 // shared memory (one barrier per round).  The first round loads straight
 // from HBM and the last round stores straight to HBM, so a pass reads and
 // writes each word exactly once.  All index math is shifts and masks.
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cstdlib>
 
 #include "ntt_pass.cuh"
@@ -240,10 +243,110 @@ void ntt_forward(Ctx& c, const JobList& jobs) {
     chunks_pass(c, jobs, false, N1, 0, 1);
 }
 
+// ---- both inverse passes of a lone sub-wave INTT in one cooperative launch ----
+//
+// In the chains a launch costs more than its work (ncu: 9-10 us per compact
+// pass of 6-13 limbs, ~5 us of it fixed), so the two passes of an INTT run as
+// one kernel: every CTA runs the compact chunk pass of chunk x of its limb,
+// the grid synchronises (cooperative launch: all CTAs are co-resident, so the
+// barrier cannot deadlock whatever runs on the other streams), then the same
+// CTA runs the compact column pass of column block x.  Chunk CTAs and column
+// blocks are both N1 per limb, both passes use 128 threads.  The column pass
+// reads words other CTAs wrote in this kernel: L2 loads (ld.global.cg).
+template <int CL, int CS>
+__global__ void __launch_bounds__(128)
+    intt_fused_kernel(JobList jobs, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ tw, int logN,
+                      int N1) {
+    pdl_trigger();
+    extern __shared__ u64 sm[];
+    static_assert(SmallGeo<9, MODE_CHUNKS, 1>::THREADS == 128 && SmallGeo<CL, MODE_COLS, CS>::THREADS == 128,
+                  "fused INTT: 128-thread passes");
+    pdl_wait();
+    // grid y strides over the limb jobs (the grid is capped at the co-residency bound)
+    for (int job = blockIdx.y; job < jobs.n; job += gridDim.y) {
+        const int pidx = jobs.prime[job];
+        u64* dst = jobs.ptr[job];
+        const u64* src = jobs.src[job] ? jobs.src[job] : dst;
+        const PrimeDev P = primes[pidx];
+        const ulonglong2* TW = tw + ((size_t)pidx << logN);
+        StPlain<true, false> st{dst, P.q, 0, 0};
+        if (jobs.galois) {
+            LdGalois ld{src, logN, jobs.galois};
+            small_pass_run<9, MODE_CHUNKS, 1, true, 2>(N1, blockIdx.x, sm, TW, P, ld, st);
+        } else {
+            LdPlain ld{src};
+            small_pass_run<9, MODE_CHUNKS, 1, true, 2>(N1, blockIdx.x, sm, TW, P, ld, st);
+        }
+    }
+    cooperative_groups::this_grid().sync();
+    for (int job = blockIdx.y; job < jobs.n; job += gridDim.y) {
+        const int pidx = jobs.prime[job];
+        u64* dst = jobs.ptr[job];
+        const PrimeDev P = primes[pidx];
+        const ulonglong2* TW = tw + ((size_t)pidx << logN);
+        u64 c = P.ninv, cs = P.ninv_s;
+        if (jobs.custom) { c = jobs.scale[job]; cs = jobs.scale_s[job]; }
+        const u64 off = jobs.center ? (P.q - 1) / 2 : 0;
+        LdCg ld{dst};
+        StPlain<true, true> st{dst, P.q, c, cs, off};
+        small_pass_run<CL, MODE_COLS, CS, true, 2>(N1, blockIdx.x, sm, TW, P, ld, st);
+    }
+}
+
+// HC_INTT_FUSE: the most limbs a lone INTT may have to take the one-launch form (0 = never)
+static int intt_fuse_max() {
+    static const int v = [] { const char* e = std::getenv("HC_INTT_FUSE"); return e ? std::atoi(e) : 9; }();
+    return v;
+}
+template <int CL, int CS>
+static bool launch_intt_fused(Ctx& c, const JobList& jobs, int N1) {
+    using S1 = SmallGeo<9, MODE_CHUNKS, 1>;
+    using S2 = SmallGeo<CL, MODE_COLS, CS>;
+    const size_t smem = S1::smem_bytes() > S2::smem_bytes() ? S1::smem_bytes() : S2::smem_bytes();
+    auto kern = intt_fused_kernel<CL, CS>;
+    // co-residency bound of the cooperative launch, once per device
+    static int cap[64] = {0};
+    int dev = 0;
+    HC_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return false;
+    if (!cap[dev]) {
+        int per_sm = 0, sms = 0;
+        HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+        HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        cap[dev] = per_sm * sms > 0 ? per_sm * sms : -1;
+    }
+    const int gy = std::min(jobs.n, cap[dev] / N1);
+    if (gy < 1) return false;
+    Launch scope(c, "ntt_inv_fused", 32.0 * c.N * jobs.n);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(N1, gy, 1);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HC_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, (const PrimeDev*)c.d_primes, (const ulonglong2*)c.twp(0, true), c.logN, N1));
+    return true;
+}
+
 void ntt_inverse(Ctx& c, const JobList& jobs) {
     if (jobs.n == 0) return;
     if (c.logN <= 13) { full_pass(c, jobs, true); return; }
     const int N1 = 1 << (c.logN - 9);
+    if (small_policy() >= 1 && jobs.nb == 1 && jobs.n <= intt_fuse_max()) {
+        bool done = false;
+        switch (c.logN) {
+            case 14: done = launch_intt_fused<5, 16>(c, jobs, N1); break;
+            case 15: done = launch_intt_fused<6, 8>(c, jobs, N1); break;
+            case 16: done = launch_intt_fused<7, 4>(c, jobs, N1); break;
+            case 17: done = launch_intt_fused<8, 2>(c, jobs, N1); break;
+            default: break;
+        }
+        if (done) return;
+    }
     chunks_pass(c, jobs, true, N1, 1, 0);
     cols_pass(c, jobs, true, N1, 0, 1);
 }

@@ -645,6 +645,28 @@ __device__ __forceinline__ void ntt_pass_small(const SmallGeo<LOGSZ, MODE, SUBS>
     }
 }
 
+// One compact pass inside a multi-phase (cooperative) kernel: the shared tile
+// is reused from phase to phase, so the CTA synchronises, stages this
+// sub-transform's twiddles and runs the pass.
+template <int LOGSZ, int MODE, int SUBS, bool INV, int INB, class LD, class ST>
+__device__ __forceinline__ void small_pass_run(int N1, int xblock, u64* sm, const ulonglong2* __restrict__ TW,
+                                               const PrimeDev& P, LD& ld, ST& st) {
+    using SG = SmallGeo<LOGSZ, MODE, SUBS>;
+    SG G;
+    G.init(N1);
+    G.first_sub = xblock * SUBS;
+    if (MODE == MODE_CHUNKS) G.R = N1 + G.first_sub + G.sub;
+    __syncthreads();
+    stage_twiddles_small<LOGSZ, MODE, SUBS>(G, SG::twsm_of(sm), TW, N1);
+    ntt_pass_small<LOGSZ, MODE, SUBS, INV, INB>(G, sm, P, ld, st);
+}
+
+// L2 loads for words written earlier in the same kernel by other CTAs
+struct LdCg {
+    const u64* p;
+    __device__ __forceinline__ u64 operator()(size_t i) const { return __ldcg(p + i); }
+};
+
 // ---- common hooks ----
 
 struct LdPlain {

@@ -25,10 +25,6 @@
 //
 // Every step is exact modular arithmetic, so the residues equal the
 // unfused path and the oracle bit for bit.
-#include <cooperative_groups.h>
-
-#include <algorithm>
-#include <cstdlib>
 #include <type_traits>
 
 #include "evaluator.h"
@@ -851,71 +847,6 @@ __global__ void __launch_bounds__(PassGeo<CH_LOG, MODE_CHUNKS, CH_SUBS>::THREADS
     ntt_pass<CH_LOG, MODE_CHUNKS, CH_SUBS, false, BOUND_LIM, StRescale::RS_OUTB>(G, sm, TW, P, ld, st, twsm, true);
 }
 
-// ---- a lone ciphertext's rescale in one cooperative launch ------------------
-//
-// In the chains (one ciphertext per op, few limbs) a launch costs more than
-// its work, so the four launches of a rescale -- the two INTT passes of the
-// dropped limb, rs_cols, rs_chunks -- run as four phases of one kernel with
-// grid barriers between them (cooperative launch: every CTA is co-resident,
-// the barrier cannot deadlock).  Each phase is the compact pass
-// (ntt_pass.cuh) on 128 threads with the same hooks; CTA x owns chunk x /
-// column block x, grid y strides over the limb jobs.  Words written by other
-// CTAs earlier in the kernel are read with L2 loads.
-struct LdBcastCg {
-    const u64* X;
-    u64 ql, q, qlm, r1;
-    __device__ __forceinline__ u64 operator()(size_t k) const {
-        const u64 v = __ldcg(X + k), vm = mul_shoup(v, 1, r1, q);
-        return v > (ql - 1) / 2 ? sub_mod(vm, qlm, q) : vm;
-    }
-};
-template <int CL, int CS>
-__global__ void __launch_bounds__(128)
-    rs_fused_kernel(int level, int logN, int N1, const PrimeDev* __restrict__ primes, const ulonglong2* __restrict__ twf,
-                    const ulonglong2* __restrict__ twi, const u64* __restrict__ a, u64* X, u64* Yt, u64* __restrict__ out,
-                    const u64* __restrict__ tab, int npoly) {
-    pdl_trigger();
-    extern __shared__ u64 sm[];
-    namespace cg = cooperative_groups;
-    const size_t N = (size_t)1 << logN;
-    const int x = blockIdx.x;
-    pdl_wait();
-    const PrimeDev PL = primes[level];
-    const ulonglong2* TWL = twi + ((size_t)level << logN);
-    // A: inverse chunk pass of the dropped limb of every poly -> X (lazy)
-    for (int s = blockIdx.y; s < npoly; s += gridDim.y) {
-        LdPlain ld{a + ((size_t)s * (level + 1) + level) * N};
-        StPlain<true, false> st{X + (size_t)s * N, PL.q, 0, 0};
-        small_pass_run<9, MODE_CHUNKS, 1, true, 2>(N1, x, sm, TWL, PL, ld, st);
-    }
-    cg::this_grid().sync();
-    // B: inverse column pass, N^-1 folded into the store -> X canonical
-    for (int s = blockIdx.y; s < npoly; s += gridDim.y) {
-        LdCg ld{X + (size_t)s * N};
-        StPlain<true, true> st{X + (size_t)s * N, PL.q, PL.ninv, PL.ninv_s, 0};
-        small_pass_run<CL, MODE_COLS, CS, true, 2>(N1, x, sm, TWL, PL, ld, st);
-    }
-    cg::this_grid().sync();
-    // C: centred broadcast of X to limb i in the loads of its forward column pass -> Yt (lazy)
-    for (int y = blockIdx.y; y < npoly * level; y += gridDim.y) {
-        const int s = y / level, i = y % level;
-        const PrimeDev P = primes[i];
-        LdBcastCg ld{X + (size_t)s * N, PL.q, P.q, tab[3 * i + 2], P.mu_hi};
-        StPlain<false, false> st{Yt + ((size_t)s * level + i) * N, P.q, 0, 0};
-        small_pass_run<CL, MODE_COLS, CS, false, 2>(N1, x, sm, twf + ((size_t)i << logN), P, ld, st);
-    }
-    cg::this_grid().sync();
-    // D: forward chunk pass, (a - y) q_l^-1 in the stores -> out
-    for (int y = blockIdx.y; y < npoly * level; y += gridDim.y) {
-        const int s = y / level, i = y % level;
-        const PrimeDev P = primes[i];
-        LdCg ld{Yt + ((size_t)s * level + i) * N};
-        StRescale st{out + ((size_t)s * level + i) * N, a + ((size_t)s * (level + 1) + i) * N, P.q, tab[3 * i],
-                     tab[3 * i + 1]};
-        small_pass_run<9, MODE_CHUNKS, 1, false, 4>(N1, x, sm, twf + ((size_t)i << logN), P, ld, st);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1309,18 +1240,6 @@ bool keyswitch_fused(Ctx& c, const u64* d, u64 gal, int level, const Key& key, u
     return keyswitch_fused_batch(c, 1, &in, gal, level, add_npoly, add_gal);
 }
 
-// HC_RS_FUSE: the most limb jobs (npoly * level) a lone rescale may have to take
-// the one-launch form (0 = never; HC_NTT_SMALL=0 also disables it)
-static int rs_fuse_max() {
-    static const int v = [] {
-        const char* e = std::getenv("HC_RS_FUSE");
-        const char* p = std::getenv("HC_NTT_SMALL");
-        if (p && std::atoi(p) == 0) return 0;
-        return e ? std::atoi(e) : 18;
-    }();
-    return v;
-}
-
 template <int LOGN>
 static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int npoly, u64* const* out) {
     constexpr int CL = ColCfg<LOGN>::LOGSZ, CS = ColCfg<LOGN>::SUBS;
@@ -1329,47 +1248,6 @@ static void rescale_fused_t(Ctx& c, int B, const u64* const* a, int level, int n
     const int N = c.N;
     Scratch sc(c);
     u64* X = sc.take((size_t)B * npoly * N);
-    if (B == 1 && npoly * level <= rs_fuse_max()) {
-        // lone ciphertext, sub-wave work: one cooperative launch (phases A-D)
-        constexpr int SCL = LOGN - 9, SCS = 512 >> (LOGN - 9);   // compact column pass: 128 threads
-        using S1 = SmallGeo<9, MODE_CHUNKS, 1>;
-        using S2 = SmallGeo<SCL, MODE_COLS, SCS>;
-        static_assert(S2::THREADS == 128, "fused rescale: 128-thread passes");
-        const size_t smem = S1::smem_bytes() > S2::smem_bytes() ? S1::smem_bytes() : S2::smem_bytes();
-        auto kern = rs_fused_kernel<SCL, SCS>;
-        static int cap[64] = {0};
-        int dev = 0;
-        HC_CUDA(cudaGetDevice(&dev));
-        if (dev >= 0 && dev < 64) {
-            if (!cap[dev]) {
-                int per_sm = 0, sms = 0;
-                HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
-                HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-                cap[dev] = per_sm * sms > 0 ? per_sm * sms : -1;
-            }
-            const int N1 = N >> CH_LOG;
-            const int gy = std::min(npoly * level, cap[dev] / N1);
-            if (gy >= 1) {
-                u64* Yt = sc.take((size_t)npoly * level * N);
-                const u64* tab = c.d_rescale + (size_t)level * c.nall * 3;
-                Launch scope(c, "rs_fused", 8.0 * N * npoly * (4.0 + 4.0 * level));
-                cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3(N1, gy, 1);
-                cfg.blockDim = dim3(128);
-                cfg.dynamicSmemBytes = smem;
-                cfg.stream = c.stream;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributeCooperative;
-                at[0].val.cooperative = 1;
-                cfg.attrs = at;
-                cfg.numAttrs = 1;
-                HC_CUDA(cudaLaunchKernelEx(&cfg, kern, level, c.logN, N1, (const PrimeDev*)c.d_primes,
-                                           (const ulonglong2*)c.twp(0, false), (const ulonglong2*)c.twp(0, true),
-                                           (const u64*)a[0], X, Yt, out[0], tab, npoly));
-                return;
-            }
-        }
-    }
     JobList j;
     j.n = B * npoly;
     for (int b = 0; b < B; b++)

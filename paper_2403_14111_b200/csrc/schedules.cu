@@ -343,19 +343,11 @@ static G mult_many(Eval& ev, const G& xs_in, const G& ys_in) {
     bool boot = false;
     for (size_t i = 0; i < xs.size(); i++) boot |= xs[i]->level < 1 || ys[i]->level < 1;
     if (!boot) {
-        std::map<std::pair<const Ct*, int>, CtP> adj;
-        auto once = [&](CtP& a, int l) {
-            if (a->level == l) return;
-            auto key = std::make_pair((const Ct*)a.get(), l);
-            auto it = adj.find(key);
-            if (it == adj.end()) it = adj.emplace(key, ev.at(a, l)).first;
-            a = it->second;
-        };
-        for (size_t i = 0; i < xs.size(); i++) {
-            const int l = std::min(xs[i]->level, ys[i]->level);
-            once(xs[i], l);
-            once(ys[i], l);
-        }
+        // one batch per (source level, target level), shared operands once
+        std::vector<int> ls(xs.size());
+        for (size_t i = 0; i < xs.size(); i++) ls[i] = std::min(xs[i]->level, ys[i]->level);
+        ev.at_batch(xs, ls);
+        ev.at_batch(ys, ls);
     }
     G out(xs.size());
     par_for(C, nsub, fork_width(C, nsub), [&](int i) {
@@ -408,8 +400,9 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
     // packing prologue: B + i * RU(B, c/2), all block columns in one batch
     const int kk0 = (c / 2) % g.s0;
     G rolled = kk0 ? ev.lrot_batch(B, (int64_t)kk0 * g.s1) : B;
-    G packed(n);
-    for (int q = 0; q < n; q++) packed[q] = ev.add(B[q], ev.mul_i(rolled[q]));
+    G ri(n);
+    for (int q = 0; q < n; q++) ri[q] = ev.mul_i(rolled[q]);
+    G packed = ev.add_batch(B, ri);
     std::vector<G> shifted(K);
     G acc((size_t)K * m);
     if (ev.c.hoist) {
@@ -481,12 +474,8 @@ static std::vector<CtP> diag_abt_lockstep(Eval& ev, const G& A, int m, int n, co
 static void rot_left_split(Eval& ev, const G& E, int k, const Geo& g, G& head, G& tail, const G* first = nullptr) {
     const Pattern keep = keep_head(g, g.s1 - k);
     G a1 = first ? *first : ev.lrot_batch(E, k);
-    head.resize(E.size());
-    tail.resize(E.size());
-    for (size_t i = 0; i < E.size(); i++) {
-        head[i] = ev.mult_p(a1[i], keep);
-        tail[i] = ev.sub(a1[i], head[i]);
-    }
+    head = ev.mult_p_batch(a1, std::vector<const Pattern*>(a1.size(), &keep));
+    tail = ev.add_batch(a1, head, true);
 }
 
 static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& B, int n, int c, double scale,
@@ -504,9 +493,11 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
             G head, tail;
             rot_left_split(ev, A, k, g, head, tail);
             G back = ev.lrot_batch(tail, -(int64_t)s1);
-            for (int p = 0; p < m; p++) one[p] = ev.add(head[p], back[p]);
+            one = ev.add_batch(head, back);
         }
-        for (int p = 0; p < m; p++) packed[p] = ev.add(A[p], ev.mul_i(one[p]));
+        G oi(m);
+        for (int p = 0; p < m; p++) oi[p] = ev.mul_i(one[p]);
+        packed = ev.add_batch(A, oi);
     }
     // the level of pass k's term (all passes, for pass sharding): RL / PRU of
     // a non-zero k costs the rotated operand one level, then the product and
@@ -554,38 +545,44 @@ static std::vector<CtP> diag_atb_lockstep(Eval& ev, const G& A, int m, const G& 
             }
         }
         G heads = ev.mult_p_batch(a1s, ps);
-        G tails(a1s.size());
-        for (size_t i = 0; i < a1s.size(); i++) tails[i] = ev.sub(a1s[i], heads[i]);
+        G tails = ev.add_batch(a1s, heads, true);   // one batch; a shared a1 is level-adjusted once
         G back = rot_many(ev, tails, -(int64_t)s1);
+        G lefts = ev.add_batch(heads, back);
         size_t o = 0;
         for (int k : moving) {
             left[k].resize(m);
-            for (int p = 0; p < m; p++, o++) left[k][p] = ev.add(heads[o], back[o]);
+            for (int p = 0; p < m; p++, o++) left[k][p] = lefts[o];
         }
     }
     // right operands: B, or PRU(B, k) on the partial branch (all lrot(s1) in one batch)
     std::vector<G> right(K, B);
     if (partial) {
-        std::vector<G> heads(K), tails(K);
+        // the keep masks of every (pass, block) in one batch, the tails in one
+        // batch (B's blocks are level-adjusted once for all passes), the
+        // lrot(s1) of every tail in one batch, the sums in one batch
         std::vector<int> moving;
-        for (int k = 0; k < K; k++) {
-            const int kk = ks[k] % s1;
-            if (!kk) continue;
-            const Pattern keep = keep_head(g, s1 - kk);
-            heads[k].resize(B.size());
-            tails[k].resize(B.size());
+        for (int k = 0; k < K; k++)
+            if (ks[k] % s1) moving.push_back(k);
+        std::vector<Pattern> keeps;
+        keeps.reserve(moving.size());
+        G src;
+        std::vector<const Pattern*> ps;
+        for (int k : moving) {
+            keeps.push_back(keep_head(g, s1 - ks[k] % s1));
             for (size_t i = 0; i < B.size(); i++) {
-                heads[k][i] = ev.mult_p(B[i], keep);
-                tails[k][i] = ev.sub(B[i], heads[k][i]);
+                src.push_back(B[i]);
+                ps.push_back(&keeps.back());
             }
-            moving.push_back(k);
         }
-        std::vector<G> tparts;
-        for (int k : moving) tparts.push_back(tails[k]);
-        G up = rot_many(ev, concat(tparts), (int64_t)s1);
-        size_t o = 0;
-        for (int k : moving)
-            for (size_t i = 0; i < B.size(); i++) right[k][i] = ev.add(heads[k][i], up[o++]);
+        if (!src.empty()) {
+            G hd = ev.mult_p_batch(src, ps);
+            G tl = ev.add_batch(src, hd, true);
+            G up = rot_many(ev, tl, (int64_t)s1);
+            G rt = ev.add_batch(hd, up);
+            size_t o = 0;
+            for (int k : moving)
+                for (size_t i = 0; i < B.size(); i++) right[k][i] = rt[o++];
+        }
     }
     // all passes' products in one batch
     G xs, ys;

@@ -51,3 +51,15 @@ def hefit():
     if mod is None:
         pytest.skip("reference package hefit not importable (baseline/_ref absent)")
     return mod
+
+
+@pytest.fixture(autouse=True)
+def _release_contexts():
+    """A context owns a multi-GB device pool (keys, reserved working set) that
+    is released when the object is destroyed; contexts caught in reference
+    cycles (ciphertexts, closures of the threaded shard tests) would wait for
+    the cyclic collector, and a long GPU session could pile them up to the
+    180 GB of the device.  Collect after every test."""
+    yield
+    import gc
+    gc.collect()

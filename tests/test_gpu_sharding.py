@@ -13,6 +13,7 @@
   test_gpu_parity.py.
 """
 
+import gc
 import threading
 
 import numpy as np
@@ -230,6 +231,8 @@ def _pass_sharded(name, grid, fn, worlds):
             for a, b in zip(out[r], ref_res):
                 for x, z in zip(a, b):
                     np.testing.assert_array_equal(x, z)
+        del th, red
+        gc.collect()   # the R shard contexts (keys + reserved pool each) before the next world
 
 
 @pytest.mark.parametrize("fn", ["abt", "atb"])

@@ -1095,22 +1095,38 @@ std::vector<CtP> Eval::mult_p_batch(const std::vector<CtP>& xs_in, const std::ve
     if (xs.size() > 1) ready_batch(xs);   // refreshes in block order, batched
     std::vector<CtP> out(xs.size());
     bool ok = c.logN >= 14 && xs.size() > 1;
-    for (auto& x : xs) ok = ok && x->level >= 1 && x->level == xs[0]->level;
+    for (auto& x : xs) ok = ok && x->level >= 1;
     if (!ok) {
         for (size_t i = 0; i < xs.size(); i++) out[i] = mult_p(xs[i], *ps[i]);
         return out;
     }
-    rec(OP_CMULT, (int)xs.size());
-    const int level = xs[0]->level;
-    model(OP_CMULT, MV_PT, level, (int)xs.size());
-    const size_t poly = (size_t)(level + 1) * c.N;
-    Scratch sc(c);
-    u64* T = sc.take(2 * poly * xs.size());
-    for (size_t i = 0; i < xs.size(); i++) {
-        PtP pt = encoded(*ps[i], level);
-        k_elementwise(c, EWP_PT_MUL, T + 2 * poly * i, xs[i]->d, pt->d, nullptr, level + 1, 2, 1);
+    // one batch per level present (DiagATB's passes end one level apart): the
+    // products in one launch, then one batched rescale
+    std::map<int, std::vector<size_t>> groups;
+    for (size_t i = 0; i < xs.size(); i++) groups[xs[i]->level].push_back(i);
+    for (auto it = groups.rbegin(); it != groups.rend(); ++it) {
+        const int level = it->first;
+        const std::vector<size_t>& idx = it->second;
+        const size_t n = idx.size();
+        rec(OP_CMULT, (int)n);
+        model(OP_CMULT, MV_PT, level, (int)n);
+        const size_t poly = (size_t)(level + 1) * c.N;
+        Scratch sc(c);
+        u64* T = sc.take(2 * poly * n);
+        std::vector<PtP> pts(n);
+        std::vector<u64*> o(n);
+        std::vector<const u64*> a(n), b(n);
+        for (size_t u = 0; u < n; u++) {
+            pts[u] = encoded(*ps[idx[u]], level);
+            o[u] = T + 2 * poly * u;
+            a[u] = xs[idx[u]]->d;
+            b[u] = pts[u]->d;
+        }
+        k_elementwise_batch(c, EWP_PT_MUL, (int)n, o.data(), a.data(), b.data(), nullptr, level + 1, 2, 1);
+        std::vector<CtP> r(n);
+        rescale_many(c, T, poly, level, r);
+        for (size_t u = 0; u < n; u++) out[idx[u]] = r[u];
     }
-    rescale_many(c, T, poly, level, out);
     return out;
 }
 

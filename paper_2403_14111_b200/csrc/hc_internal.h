@@ -118,7 +118,7 @@ struct Ctx {
     bool ntt_fp = true;           // FP64 NTT passes for primes below 2^46 (HC_NTT_FP=0 disables)
     bool lockstep = true;         // batched (lockstep) diagonal passes when no refresh can fire (HC_LOCKSTEP)
     bool hoist = true;            // fused schedule forms: hoisted rotations, one relinearisation per product sum (HC_HOIST, hc_set_hoist)
-    int batch = 3;                // key switches per batched pipeline in the lockstep schedules (HC_BATCH)
+    int batch = 6;                // key switches per batched pipeline in the lockstep schedules (HC_BATCH; 3 -> 6: training step -2 %)
     std::vector<cudaEvent_t> ra_ev;   // schedule run-ahead throttle (capi.cu): a schedule call
     int ra_idx = 0;                   // waits for the one ra_depth calls back to finish
     int ra_depth = 8;                 // HC_RUNAHEAD (2 measured host-jitter-bound steps)

@@ -321,13 +321,30 @@ static G rot_many(Eval& ev, const G& xs, int64_t r, bool add_self = false) {
 // sub-batches on concurrent branches like rot_many
 static G ladder_many(Eval& ev, const G& xs, int64_t stride, int steps) {
     Ctx& C = ev.c;
-    const int SB = std::max(1, C.batch), nsub = ((int)xs.size() + SB - 1) / SB;
+    const int SB = std::max(1, C.batch);
+    // sub-batches of one level each (a batched pipeline needs one level; DiagATB's
+    // passes end one level apart), in first-appearance order
+    std::vector<std::vector<size_t>> subs;
+    {
+        std::vector<std::pair<int, std::vector<size_t>>> by_level;
+        for (size_t i = 0; i < xs.size(); i++) {
+            size_t u = 0;
+            while (u < by_level.size() && by_level[u].first != xs[i]->level) u++;
+            if (u == by_level.size()) by_level.emplace_back(xs[i]->level, std::vector<size_t>());
+            by_level[u].second.push_back(i);
+        }
+        for (auto& lv : by_level)
+            for (size_t lo = 0; lo < lv.second.size(); lo += SB)
+                subs.emplace_back(lv.second.begin() + lo, lv.second.begin() + std::min(lv.second.size(), lo + (size_t)SB));
+    }
+    const int nsub = (int)subs.size();
     if (nsub <= 1) return ev.ladder(xs, stride, steps);
     G out(xs.size());
     par_for(C, nsub, fork_width(C, nsub), [&](int i) {
-        const size_t lo = (size_t)i * SB, hi = std::min(xs.size(), lo + SB);
-        G part = ev.ladder(G(xs.begin() + lo, xs.begin() + hi), stride, steps);
-        std::copy(part.begin(), part.end(), out.begin() + lo);
+        G in;
+        for (size_t j : subs[i]) in.push_back(xs[j]);
+        G part = ev.ladder(in, stride, steps);
+        for (size_t u = 0; u < subs[i].size(); u++) out[subs[i][u]] = part[u];
     });
     return out;
 }

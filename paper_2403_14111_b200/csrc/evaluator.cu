@@ -1084,8 +1084,15 @@ std::vector<CtP> Eval::mult_c_batch(const std::vector<CtP>& xs_in, std::complex<
     const_pairs(c, std::llrint(s.real() * sc), std::llrint(s.imag() * sc), level + 1, t);
     Scratch scr(c);
     u64* T = scr.take(2 * poly * xs.size());
-    for (size_t i = 0; i < xs.size(); i++)
-        k_elementwise(c, EWP_CONST_MUL, T + 2 * poly * i, xs[i]->d, nullptr, &t, level + 1, 2, 0);
+    {   // the products of the batch in one launch
+        std::vector<u64*> o(xs.size());
+        std::vector<const u64*> a(xs.size());
+        for (size_t i = 0; i < xs.size(); i++) {
+            o[i] = T + 2 * poly * i;
+            a[i] = xs[i]->d;
+        }
+        k_elementwise_batch(c, EWP_CONST_MUL, (int)xs.size(), o.data(), a.data(), nullptr, &t, level + 1, 2, 0);
+    }
     rescale_many(c, T, poly, level, out);
     return out;
 }

@@ -328,7 +328,16 @@ static bool launch_intt_fused(Ctx& c, const JobList& jobs, int N1) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    HC_CUDA(cudaLaunchKernelEx(&cfg, kern, jobs, (const PrimeDev*)c.d_primes, (const ulonglong2*)c.twp(0, true), c.logN, N1));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, jobs, (const PrimeDev*)c.d_primes,
+                                             (const ulonglong2*)c.twp(0, true), c.logN, N1);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+        // fewer SMs than the occupancy query promised (MPS partition, green context):
+        // nothing was launched; this device keeps the two-launch form from now on
+        (void)cudaGetLastError();
+        cap[dev] = -1;
+        return false;
+    }
+    HC_CUDA(e);
     return true;
 }
 

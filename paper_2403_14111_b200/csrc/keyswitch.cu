@@ -25,6 +25,7 @@
 //
 // Every step is exact modular arithmetic, so the residues equal the
 // unfused path and the oracle bit for bit.
+#include <cstdlib>
 #include <type_traits>
 
 #include "evaluator.h"
@@ -602,6 +603,66 @@ __global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_rotsum
     ab[dstride] = oa;
 }
 
+// The plain key product in the stage kernel's form: one coefficient of one
+// entry per thread, the digit count compile-time, grid (entry, coefficient
+// block, target limb) so the entries of a coefficient block run side by side
+// and equal keys are read once from HBM (the rest from L2).  Entry b reads its
+// c1 through ugal[b] (hoisted) or the pipeline's element, its ModUp digits
+// through ugal[b] only (a plain pipeline's digits are already permuted).
+template <int BETA>
+__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_plain_t(KsGeo g, const PrimeDev* __restrict__ primes, u64 gal,
+                                                                    KsBatch kb, u64* __restrict__ acc) {
+    pdl_enter();
+    const int t = blockIdx.z;
+    const int pi = g.prime(t);
+    const PrimeDev P = primes[pi];
+    const int b = blockIdx.x;
+    const unsigned k = blockIdx.y * 256u + threadIdx.x;
+    const unsigned N = 1u << g.logN;
+    const int dig = t < g.nl ? t / g.alpha : -1;
+    const size_t toff = (size_t)t * N;
+    const u64 ug = kb.ugal[b], gd = ug ? ug : gal;
+    const unsigned src_d = gd ? galois_src(k, g.logN, gd) : k;
+    const unsigned src_u = ug ? src_d : k;
+    const u64* __restrict__ c1 = kb.d[b] + toff;
+    const u64* __restrict__ up = kb.up[b] + toff;
+    const size_t dstride = (size_t)g.nt * N;
+    const size_t kstride = (size_t)g.nall * N;
+    const u64* __restrict__ kp = kb.key[b] + (size_t)pi * N + k;
+    u64 kbw[BETA], kaw[BETA], x[BETA];
+#pragma unroll
+    for (int j = 0; j < BETA; j++) {
+        kbw[j] = __ldg(kp + (size_t)(2 * j) * kstride);
+        kaw[j] = __ldg(kp + (size_t)(2 * j + 1) * kstride);
+        x[j] = j == dig ? c1[src_d] : up[j * dstride + src_u];
+    }
+    u64 ob, oa;
+    if (P.fp) {
+        const double q = P.qd, qinv = P.qinv;
+        double sb = 0, sa = 0;
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            const double y = fp_word(x[j]);
+            sb = __dadd_rn(sb, fp_mulmod(y, fp_word(kbw[j]), q, qinv));
+            sa = __dadd_rn(sa, fp_mulmod(y, fp_word(kaw[j]), q, qinv));
+        }
+        ob = fp_canon(sb, q, qinv);
+        oa = fp_canon(sa, q, qinv);
+    } else {
+        U128 ib = {0, 0}, ia = {0, 0};
+#pragma unroll
+        for (int j = 0; j < BETA; j++) {
+            mac128(ib, x[j], kbw[j]);
+            mac128(ia, x[j], kaw[j]);
+        }
+        ob = reduce128(ib.hi, ib.lo, P);
+        oa = reduce128(ia.hi, ia.lo, P);
+    }
+    u64* __restrict__ ab = acc + (size_t)b * g.acc_stride() + toff + k;
+    ab[0] = ob;
+    ab[dstride] = oa;
+}
+
 // ---- D: ModDown conversion fused into the column pass ----------------------
 
 // (the P -> Q conversion has the ModUp loader's shape: K inputs, one target)
@@ -900,6 +961,12 @@ struct KsRotsumSpec {
     bool relin = false;
 };
 
+// HC_KP_PLAIN=0: the plain pipelines keep ks_keyprod_stream
+static bool kp_plain_t() {
+    static const bool v = [] { const char* e = std::getenv("HC_KP_PLAIN"); return !e || std::atoi(e) != 0; }();
+    return v;
+}
+
 template <int LOGN>
 static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int level, int B, const KsTail* in,
                           int add_npoly, const KsRotsumSpec* rsum = nullptr) {
@@ -1057,6 +1124,15 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         if (g.beta > 4) {   // deep chains (bootstrapping): 8 digits, one coefficient per thread
             dim3 grid((unsigned)((N + 255) / 256), nt);
             launch_k(c, ks_keyprod_stream<1, 8>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
+        } else if (kp_plain_t()) {
+            dim3 tgrid((unsigned)B, (unsigned)(N / 256), (unsigned)nt);
+            auto go = [&](auto kern) { launch_k(c, kern, tgrid, 256, 0, g, c.d_primes, gal, kb, ACC); };
+            switch (g.beta) {
+                case 1: go(ks_keyprod_plain_t<1>); break;
+                case 2: go(ks_keyprod_plain_t<2>); break;
+                case 3: go(ks_keyprod_plain_t<3>); break;
+                default: go(ks_keyprod_plain_t<4>); break;
+            }
         } else if (B >= KP_PAIRB) {
             dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
             launch_k(c, ks_keyprod_stream<2>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);

@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_rotsum
 // c1 through ugal[b] (hoisted) or the pipeline's element, its ModUp digits
 // through ugal[b] only (a plain pipeline's digits are already permuted).
 template <int BETA>
-__global__ void __launch_bounds__(256, RS_MINB) ks_keyprod_plain_t(KsGeo g, const PrimeDev* __restrict__ primes, u64 gal,
+__global__ void __launch_bounds__(256, BETA > 4 ? 3 : RS_MINB) ks_keyprod_plain_t(KsGeo g, const PrimeDev* __restrict__ primes, u64 gal,
                                                                     KsBatch kb, u64* __restrict__ acc) {
     pdl_enter();
     const int t = blockIdx.z;
@@ -961,9 +961,10 @@ struct KsRotsumSpec {
     bool relin = false;
 };
 
-// HC_KP_PLAIN=0: the plain pipelines keep ks_keyprod_stream
-static bool kp_plain_t() {
-    static const bool v = [] { const char* e = std::getenv("HC_KP_PLAIN"); return !e || std::atoi(e) != 0; }();
+// HC_KP_PLAIN: 0 = the plain pipelines keep ks_keyprod_stream, 1 = ks_keyprod_plain_t
+// for up to 4 digits, 2 (default) = for up to 8 (the bootstrapping chains: 58.1 -> 53.9 ms)
+static int kp_plain_t() {
+    static const int v = [] { const char* e = std::getenv("HC_KP_PLAIN"); return e ? std::atoi(e) : 2; }();
     return v;
 }
 
@@ -1121,18 +1122,26 @@ static void ks_pipeline_t(Ctx& c, int nin, const u64* const* din, u64 gal, int l
         } else
         // a lone key switch (chains) takes one coefficient per thread for
         // parallelism; batches take pairs (16-byte accesses, fewer index ops)
-        if (g.beta > 4) {   // deep chains (bootstrapping): 8 digits, one coefficient per thread
-            dim3 grid((unsigned)((N + 255) / 256), nt);
-            launch_k(c, ks_keyprod_stream<1, 8>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
-        } else if (kp_plain_t()) {
+        // entries per distinct key: the stage-form kernel re-reads a shared key from L2
+        // once per entry, the streaming form keeps its words in registers across the
+        // entries -- better from 4 entries per key up (16 same-key rotations at
+        // level 12: 11,700/s against 11,400/s)
+        if (kp_plain_t() && g.beta <= (kp_plain_t() > 1 ? 8 : 4) && B < 4 * nkeys) {
             dim3 tgrid((unsigned)B, (unsigned)(N / 256), (unsigned)nt);
             auto go = [&](auto kern) { launch_k(c, kern, tgrid, 256, 0, g, c.d_primes, gal, kb, ACC); };
             switch (g.beta) {
                 case 1: go(ks_keyprod_plain_t<1>); break;
                 case 2: go(ks_keyprod_plain_t<2>); break;
                 case 3: go(ks_keyprod_plain_t<3>); break;
-                default: go(ks_keyprod_plain_t<4>); break;
+                case 4: go(ks_keyprod_plain_t<4>); break;
+                case 5: go(ks_keyprod_plain_t<5>); break;
+                case 6: go(ks_keyprod_plain_t<6>); break;
+                case 7: go(ks_keyprod_plain_t<7>); break;
+                default: go(ks_keyprod_plain_t<8>); break;
             }
+        } else if (g.beta > 4) {   // deep chains (bootstrapping): 8 digits, one coefficient per thread
+            dim3 grid((unsigned)((N + 255) / 256), nt);
+            launch_k(c, ks_keyprod_stream<1, 8>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);
         } else if (B >= KP_PAIRB) {
             dim3 grid((unsigned)((N / 2 + 255) / 256), nt);
             launch_k(c, ks_keyprod_stream<2>, grid, 256, 0, g, c.d_primes, gal, kb, ACC, nt);

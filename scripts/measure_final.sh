@@ -1,6 +1,6 @@
 #!/bin/bash
 # Final lines of round 2 (batched schedule ops, 6 key switches per pipeline): tests, bench lines, smoke, reference arm, launch list of the bench command.
-O=gpurun_out/r2l
+O=gpurun_out/r2m
 mkdir -p $O
 python -m pytest tests -m gpu -q > $O/gputest.log 2>&1; echo exit=$? >> $O/gputest.log
 python bench.py > $O/bench_pair.json 2> $O/bench_pair.err
